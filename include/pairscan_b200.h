@@ -1,0 +1,193 @@
+/*
+ * pairscan_b200.h — C ABI of the B200 (sm_100a) exact pair-search library.
+ *
+ * It replaces the hot path of the reference C++ library `pairscan`
+ * (paths below relative to /root/reference/proj):
+ *
+ *   core/include/pairscan/refscan.hpp:50-51  build_reference_set  -> psg_build_reference_set_f64
+ *   core/include/pairscan/refscan.hpp:55-56  closest_pair          -> psg_closest_pair_f64 / _f32
+ *   core/include/pairscan/refscan.hpp:58     brute_force_closest_pair -> psg_brute_force_closest_pair_f64
+ *   core/include/pairscan/refscan.hpp:61-63  fixed_radius_neighbors -> psg_fixed_radius_neighbors_f64 / _f32
+ *   core/include/pairscan/refscan.hpp:65-66  brute_force_neighbors -> psg_brute_force_neighbors_f64
+ *   core/include/pairscan/refscan.hpp:70-71  reference_bound       -> psg_reference_bound
+ *   core/include/pairscan/series.hpp:30-31   PointSet::from_flat / windows_of -> psg_pointset_*
+ *   tools/src/main.cpp:332-346 (cmd_motif: closest_pair over windows_of)   -> psg_motif_f64 / _f32
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; all host buffers are caller-owned except
+ *    the arrays inside psg_neighbor_result, released by psg_neighbor_result_free.
+ *  - Every entry returns PSG_OK or an error code.  PSG_ERR_INVALID carries the
+ *    reference's std::invalid_argument message verbatim (psg_last_error()).
+ *  - Results are the reference's exactly: indices bit-exact (ties to the
+ *    lowest (i, j)), distances computed in the reference's FP64 order.
+ *  - The library runs on the calling thread's current CUDA device, on its own
+ *    stream, and is synchronous at return.  There is no CPU fallback: without
+ *    a usable sm_100 device every compute entry returns PSG_ERR_CUDA.
+ */
+#ifndef PAIRSCAN_B200_H
+#define PAIRSCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_OK 0
+#define PSG_ERR_INVALID 1 /* reference std::invalid_argument */
+#define PSG_ERR_CUDA 2    /* CUDA runtime / device failure */
+#define PSG_ERR_NOMEM 3
+#define PSG_ERR_INTERNAL 4
+
+/* refscan.hpp:27-36 ScanStats */
+typedef struct psg_scan_stats {
+  uint64_t pairs_examined;            /* pairs re-evaluated in the reference's FP64 arithmetic */
+  uint64_t pairs_pruned_by_reference; /* inside the final key window, removed by key/FP32 bounds */
+  uint64_t pairs_skipped_by_exit;     /* outside the final key window */
+  uint64_t inner_loop_exits;          /* rows whose key window ended before the last point */
+} psg_scan_stats;
+
+/* refscan.hpp:38-43 PairResult */
+typedef struct psg_pair_result {
+  uint64_t index_i; /* original indices, index_i < index_j */
+  uint64_t index_j;
+  double distance;
+  psg_scan_stats stats;
+} psg_pair_result;
+
+/* refscan.hpp:45-48 NeighborResult as CSR: neighbors of i are
+ * neighbors[offsets[i] .. offsets[i+1]), ascending, symmetric.
+ * pair_count = #{i<j}, pair_hash = sum of mix_seed((i<<32)|j) mod 2^64. */
+typedef struct psg_neighbor_result {
+  uint64_t n;
+  uint64_t* offsets;   /* n+1, or NULL when only counts were requested */
+  uint64_t* neighbors; /* offsets[n] entries */
+  uint64_t pair_count;
+  uint64_t pair_hash;
+  psg_scan_stats stats;
+} psg_neighbor_result;
+
+/* Per-call measurements of the last compute entry on this thread. */
+typedef struct psg_profile {
+  int stages;
+  char stage_name[16][24];
+  float stage_ms[16];        /* CUDA-event time of each stage on the library stream */
+  uint64_t launches;         /* kernels launched by the library in the call */
+  uint64_t window_pairs;     /* pairs inside the final key-0 window */
+  uint64_t lb_survivors;     /* pairs that reached an FP32 distance evaluation */
+  uint64_t candidates;       /* FP32 band candidates sent to FP64 recheck */
+  uint64_t bootstrap_width;  /* sorted-neighbour width of the delta bootstrap */
+  uint64_t h2d_bytes, d2h_bytes;
+  double scan_kernel_ms;     /* device time of the candidate (window) kernel(s) */
+  double project_kernel_ms;  /* device time of the projection kernel */
+} psg_profile;
+
+const char* psg_last_error(void);
+const char* psg_version(void);
+int psg_last_profile(psg_profile* out);
+/* Whether CUDA device `device` is usable (compute capability 10.x). */
+int psg_device_ok(int device);
+
+/* ---- one-shot entries (host buffers in, result out) --------------------- */
+int psg_closest_pair_f64(const double* points, uint64_t n, uint64_t dim, uint64_t q, double f,
+                         uint64_t seed, uint64_t exclusion_zone, psg_pair_result* out);
+int psg_closest_pair_f32(const float* points, uint64_t n, uint64_t dim, uint64_t q, double f,
+                         uint64_t seed, uint64_t exclusion_zone, psg_pair_result* out);
+int psg_brute_force_closest_pair_f64(const double* points, uint64_t n, uint64_t dim,
+                                     uint64_t exclusion_zone, psg_pair_result* out);
+int psg_brute_force_closest_pair_f32(const float* points, uint64_t n, uint64_t dim,
+                                     uint64_t exclusion_zone, psg_pair_result* out);
+
+/* Motif: closest pair over the length-`len` windows of a series.  znorm=0 is
+ * the reference's raw windows (series.cpp:34-42); znorm=1 z-normalises every
+ * window in FP64 (two-pass mean, population sigma, 0 when sigma==0). */
+int psg_motif_f64(const double* series, uint64_t length, uint64_t len, int znorm, uint64_t q,
+                  double f, uint64_t seed, uint64_t exclusion_zone, psg_pair_result* out);
+int psg_motif_f32(const float* series, uint64_t length, uint64_t len, int znorm, uint64_t q,
+                  double f, uint64_t seed, uint64_t exclusion_zone, psg_pair_result* out);
+int psg_brute_force_motif_f64(const double* series, uint64_t length, uint64_t len, int znorm,
+                              uint64_t exclusion_zone, psg_pair_result* out);
+
+/* FRNN, boundary inclusive (refscan.cpp:159-209).  want_lists=0 fills only
+ * pair_count / pair_hash / stats (offsets = neighbors = NULL). */
+int psg_fixed_radius_neighbors_f64(const double* points, uint64_t n, uint64_t dim, double radius,
+                                   uint64_t q, double f, uint64_t seed, uint64_t exclusion_zone,
+                                   int want_lists, psg_neighbor_result* out);
+int psg_fixed_radius_neighbors_f32(const float* points, uint64_t n, uint64_t dim, double radius,
+                                   uint64_t q, double f, uint64_t seed, uint64_t exclusion_zone,
+                                   int want_lists, psg_neighbor_result* out);
+int psg_brute_force_neighbors_f64(const double* points, uint64_t n, uint64_t dim, double radius,
+                                  uint64_t exclusion_zone, int want_lists, psg_neighbor_result* out);
+/* The sorted pair list itself: pairs[k] = (i<<32)|j, i<j, lexicographic. */
+int psg_frnn_pairs_f32(const float* points, uint64_t n, uint64_t dim, double radius, uint64_t q,
+                       double f, uint64_t seed, uint64_t exclusion_zone, uint64_t* pairs,
+                       uint64_t capacity, uint64_t* pair_count, uint64_t* pair_hash);
+void psg_neighbor_result_free(psg_neighbor_result* r);
+
+/* build_reference_set (refscan.cpp:30-65), bit-exact: ref_indices[q],
+ * references[q*dim], dist_table[q*n] (k-major), order[n]. */
+int psg_build_reference_set_f64(const double* points, uint64_t n, uint64_t dim, uint64_t q,
+                                double f, uint64_t seed, uint64_t* ref_indices,
+                                double* references, double* dist_table, uint64_t* order);
+/* reference_bound (refscan.cpp:229-232): d(r,x) - d(r,y) in the reference's FP64 order. */
+int psg_reference_bound(const double* r, const double* x, const double* y, uint64_t dim,
+                        double* out);
+
+/* ---- device-resident point sets -------------------------
+ * A point set lives in HBM across calls; repeated solves skip the upload. */
+typedef struct psg_pointset psg_pointset;
+#define PSG_SRC_DEVICE 1 /* the input pointer is device memory (copied D2D) */
+int psg_pointset_from_f32(const float* points, uint64_t n, uint64_t dim, int flags, psg_pointset** out);
+int psg_pointset_from_f64(const double* points, uint64_t n, uint64_t dim, int flags, psg_pointset** out);
+/* windows_of (series.cpp:34-42), optionally z-normalised */
+int psg_pointset_windows_f64(const double* series, uint64_t length, uint64_t len, int znorm, int flags,
+                             psg_pointset** out);
+int psg_pointset_windows_f32(const float* series, uint64_t length, uint64_t len, int znorm, int flags,
+                             psg_pointset** out);
+void psg_pointset_free(psg_pointset* ps);
+uint64_t psg_pointset_size(const psg_pointset* ps);
+uint64_t psg_pointset_dim(const psg_pointset* ps);
+
+int psg_closest_pair_ps(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t exclusion_zone,
+                        psg_pair_result* out);
+int psg_brute_force_closest_pair_ps(psg_pointset* ps, uint64_t exclusion_zone, psg_pair_result* out);
+int psg_fixed_radius_neighbors_ps(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed,
+                                  uint64_t exclusion_zone, int want_lists, psg_neighbor_result* out);
+
+/* ---- key-range sharding across ranks (one process per GPU) --------------
+ * plan_create projects + sorts (identical on every rank); bootstrap returns a
+ * rank-local FP32 squared-distance bound for sorted positions of part `part`
+ * of `nparts`; the caller all-reduces (MIN) it; scan then searches the part's
+ * rows with the global bound and returns the part's best pair (index_i =
+ * UINT64_MAX when the part holds none); the caller all-reduces
+ * (distance, index_i, index_j) lexicographically and sums stats. */
+typedef struct psg_cpp_plan psg_cpp_plan;
+int psg_cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t exclusion_zone,
+                        psg_cpp_plan** out);
+int psg_cpp_plan_bootstrap(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float* bound_s32);
+int psg_cpp_plan_scan(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float bound_s32,
+                      psg_pair_result* out);
+void psg_cpp_plan_free(psg_cpp_plan* plan);
+
+/* ---- host helpers: the reference's seeded synthetic data (datagen.cpp) --- */
+int psg_gen_random_walk(uint64_t n, uint64_t seed, double stddev, double* out);
+/* SURVEY §8(d) recipes: blocks of 65,536 points from Rng(derive_seed(master, 1000+b)). */
+void psg_gen_uniform(uint64_t master, uint64_t n, uint64_t dim, float* out);
+void psg_gen_gauss_planted(uint64_t master, uint64_t n, uint64_t dim, double noise, float* out,
+                           uint64_t* planted_i, uint64_t* planted_j);
+void psg_gen_walk_motif(uint64_t master, uint64_t length, uint64_t len, double noise, float* out,
+                        uint64_t* planted_a, uint64_t* planted_b);
+void psg_gen_mixture(uint64_t master, uint64_t n, uint64_t dim, uint64_t clusters, double sigma,
+                     float* out);
+uint64_t psg_mix_seed(uint64_t x);
+uint64_t psg_derive_seed(uint64_t base, uint64_t stream);
+
+/* pinned host memory for callers that want the fast H2D path */
+int psg_host_alloc(size_t bytes, void** out);
+void psg_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,267 @@
+// psg_capi.cu — the extern "C" boundary (include/pairscan_b200.h).
+// Every entry: clear the per-thread profile, run, translate exceptions into
+// status codes, keep the message for psg_last_error().
+#include <cmath>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "host_rng.hpp"
+#include "psg_cpp.cuh"
+#include "psg_engines.cuh"
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    psg::prof_begin();
+    f();
+    psg::g_prof.launches = psg::g_launches;
+    return PSG_OK;
+  } catch (const psg::invalid_argument& e) {
+    g_err = e.what();
+    return PSG_ERR_INVALID;
+  } catch (const psg::cuda_error& e) {
+    g_err = e.what();
+    return PSG_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of memory";
+    return PSG_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PSG_ERR_INTERNAL;
+  }
+}
+
+void require_dim(uint64_t dim) {
+  if (dim == 0) throw psg::invalid_argument("point dimension must be positive");  // series.cpp:20
+}
+
+// PointSet::from_flat takes a flat buffer whose length is a multiple of dim
+// (series.cpp:19-32); here n and dim are given separately.
+std::unique_ptr<psg_pointset> rows32(const float* p, uint64_t n, uint64_t dim, bool dev = false) {
+  require_dim(dim);
+  return std::unique_ptr<psg_pointset>(psg::pointset_rows_f32(p, n, dim, dev));
+}
+std::unique_ptr<psg_pointset> rows64(const double* p, uint64_t n, uint64_t dim, bool dev = false) {
+  require_dim(dim);
+  return std::unique_ptr<psg_pointset>(psg::pointset_rows_f64(p, n, dim, dev));
+}
+
+void account_io(const psg_pointset& ps, uint64_t d2h) {
+  psg::g_prof.h2d_bytes += ps.h2d_bytes;
+  psg::g_prof.d2h_bytes += d2h;
+}
+
+struct psg_cpp_plan_box {};
+}  // namespace
+
+struct psg_cpp_plan {
+  std::unique_ptr<psg::CppPlan> plan;
+};
+
+extern "C" {
+
+const char* psg_last_error(void) { return g_err.c_str(); }
+const char* psg_version(void) { return "pairscan_b200 0.1.0 (sm_100a)"; }
+
+int psg_last_profile(psg_profile* out) {
+  if (!out) return PSG_ERR_INVALID;
+  *out = psg::g_prof;
+  return PSG_OK;
+}
+
+int psg_device_ok(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+  return prop.major == 10;
+}
+
+// ---- closest pair -----------------------------------------------------------
+int psg_closest_pair_f64(const double* points, uint64_t n, uint64_t dim, uint64_t q, double f, uint64_t seed,
+                         uint64_t exclusion_zone, psg_pair_result* out) {
+  return guarded([&] {
+    auto ps = rows64(points, n, dim);
+    *out = psg::cpp_solve(ps.get(), q, f, seed, exclusion_zone);
+    account_io(*ps, 0);
+  });
+}
+int psg_closest_pair_f32(const float* points, uint64_t n, uint64_t dim, uint64_t q, double f, uint64_t seed,
+                         uint64_t exclusion_zone, psg_pair_result* out) {
+  return guarded([&] {
+    auto ps = rows32(points, n, dim);
+    *out = psg::cpp_solve(ps.get(), q, f, seed, exclusion_zone);
+    account_io(*ps, 0);
+  });
+}
+int psg_brute_force_closest_pair_f64(const double* points, uint64_t n, uint64_t dim, uint64_t exclusion_zone,
+                                     psg_pair_result* out) {
+  return guarded([&] {
+    auto ps = rows64(points, n, dim);
+    *out = psg::brute_solve(ps.get(), exclusion_zone);
+  });
+}
+int psg_brute_force_closest_pair_f32(const float* points, uint64_t n, uint64_t dim, uint64_t exclusion_zone,
+                                     psg_pair_result* out) {
+  return guarded([&] {
+    auto ps = rows32(points, n, dim);
+    *out = psg::brute_solve(ps.get(), exclusion_zone);
+  });
+}
+
+// ---- motif -------------------------------------------------------------------
+int psg_motif_f64(const double* series, uint64_t length, uint64_t len, int znorm, uint64_t q, double f,
+                  uint64_t seed, uint64_t exclusion_zone, psg_pair_result* out) {
+  return guarded([&] {
+    std::unique_ptr<psg_pointset> ps(psg::pointset_windows(series, nullptr, length, len, znorm != 0, false));
+    *out = psg::cpp_solve(ps.get(), q, f, seed, exclusion_zone);
+    account_io(*ps, 0);
+  });
+}
+int psg_motif_f32(const float* series, uint64_t length, uint64_t len, int znorm, uint64_t q, double f,
+                  uint64_t seed, uint64_t exclusion_zone, psg_pair_result* out) {
+  return guarded([&] {
+    std::unique_ptr<psg_pointset> ps(psg::pointset_windows(nullptr, series, length, len, znorm != 0, false));
+    *out = psg::cpp_solve(ps.get(), q, f, seed, exclusion_zone);
+    account_io(*ps, 0);
+  });
+}
+int psg_brute_force_motif_f64(const double* series, uint64_t length, uint64_t len, int znorm,
+                              uint64_t exclusion_zone, psg_pair_result* out) {
+  return guarded([&] {
+    std::unique_ptr<psg_pointset> ps(psg::pointset_windows(series, nullptr, length, len, znorm != 0, false));
+    *out = psg::brute_solve(ps.get(), exclusion_zone);
+  });
+}
+
+// ---- fixed radius --------------------------------------------------------------
+int psg_fixed_radius_neighbors_f64(const double* points, uint64_t n, uint64_t dim, double radius, uint64_t q,
+                                   double f, uint64_t seed, uint64_t exclusion_zone, int want_lists,
+                                   psg_neighbor_result* out) {
+  return guarded([&] {
+    if (n == 0) throw psg::invalid_argument("empty input");  // refscan.cpp:162, before from_flat checks
+    auto ps = rows64(points, n, dim);
+    psg::frnn_solve(ps.get(), radius, q, f, seed, exclusion_zone, want_lists != 0, out);
+    account_io(*ps, 0);
+  });
+}
+int psg_fixed_radius_neighbors_f32(const float* points, uint64_t n, uint64_t dim, double radius, uint64_t q,
+                                   double f, uint64_t seed, uint64_t exclusion_zone, int want_lists,
+                                   psg_neighbor_result* out) {
+  return guarded([&] {
+    if (n == 0) throw psg::invalid_argument("empty input");
+    auto ps = rows32(points, n, dim);
+    psg::frnn_solve(ps.get(), radius, q, f, seed, exclusion_zone, want_lists != 0, out);
+    account_io(*ps, 0);
+  });
+}
+int psg_brute_force_neighbors_f64(const double* points, uint64_t n, uint64_t dim, double radius,
+                                  uint64_t exclusion_zone, int want_lists, psg_neighbor_result* out) {
+  return guarded([&] {
+    if (n == 0) throw psg::invalid_argument("empty input");  // refscan.cpp:214
+    auto ps = rows64(points, n, dim);
+    psg::brute_neighbors(ps.get(), radius, exclusion_zone, want_lists != 0, out);
+  });
+}
+int psg_frnn_pairs_f32(const float* points, uint64_t n, uint64_t dim, double radius, uint64_t q, double f,
+                       uint64_t seed, uint64_t exclusion_zone, uint64_t* pairs, uint64_t capacity,
+                       uint64_t* pair_count, uint64_t* pair_hash) {
+  return guarded([&] {
+    if (n == 0) throw psg::invalid_argument("empty input");
+    auto ps = rows32(points, n, dim);
+    psg::frnn_pairs(ps.get(), radius, q, f, seed, exclusion_zone, pairs, capacity, pair_count, pair_hash);
+    account_io(*ps, 0);
+  });
+}
+void psg_neighbor_result_free(psg_neighbor_result* r) {
+  if (!r) return;
+  std::free(r->offsets);
+  std::free(r->neighbors);
+  r->offsets = nullptr;
+  r->neighbors = nullptr;
+}
+
+// ---- reference set -------------------------------------------------------------
+int psg_build_reference_set_f64(const double* points, uint64_t n, uint64_t dim, uint64_t q, double f,
+                                uint64_t seed, uint64_t* ref_indices, double* references, double* dist_table,
+                                uint64_t* order) {
+  return guarded([&] {
+    auto ps = rows64(points, n, dim);
+    psg::reference_set(ps.get(), q, f, seed, ref_indices, references, dist_table, order);
+  });
+}
+int psg_reference_bound(const double* r, const double* x, const double* y, uint64_t dim, double* out) {
+  return guarded([&] { *out = psg::reference_bound_dev(r, x, y, dim); });
+}
+
+// ---- device-resident point sets ------------------------------------------------
+int psg_pointset_from_f32(const float* points, uint64_t n, uint64_t dim, int flags, psg_pointset** out) {
+  return guarded([&] { *out = rows32(points, n, dim, flags & PSG_SRC_DEVICE).release(); });
+}
+int psg_pointset_from_f64(const double* points, uint64_t n, uint64_t dim, int flags, psg_pointset** out) {
+  return guarded([&] { *out = rows64(points, n, dim, flags & PSG_SRC_DEVICE).release(); });
+}
+int psg_pointset_windows_f64(const double* series, uint64_t length, uint64_t len, int znorm, int flags,
+                             psg_pointset** out) {
+  return guarded([&] {
+    *out = psg::pointset_windows(series, nullptr, length, len, znorm != 0, flags & PSG_SRC_DEVICE);
+  });
+}
+int psg_pointset_windows_f32(const float* series, uint64_t length, uint64_t len, int znorm, int flags,
+                             psg_pointset** out) {
+  return guarded([&] {
+    *out = psg::pointset_windows(nullptr, series, length, len, znorm != 0, flags & PSG_SRC_DEVICE);
+  });
+}
+void psg_pointset_free(psg_pointset* ps) { delete ps; }
+uint64_t psg_pointset_size(const psg_pointset* ps) { return ps ? ps->n : 0; }
+uint64_t psg_pointset_dim(const psg_pointset* ps) { return ps ? static_cast<uint64_t>(ps->d) : 0; }
+
+int psg_closest_pair_ps(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t exclusion_zone,
+                        psg_pair_result* out) {
+  return guarded([&] { *out = psg::cpp_solve(ps, q, f, seed, exclusion_zone); });
+}
+int psg_brute_force_closest_pair_ps(psg_pointset* ps, uint64_t exclusion_zone, psg_pair_result* out) {
+  return guarded([&] { *out = psg::brute_solve(ps, exclusion_zone); });
+}
+int psg_fixed_radius_neighbors_ps(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed,
+                                  uint64_t exclusion_zone, int want_lists, psg_neighbor_result* out) {
+  return guarded([&] { psg::frnn_solve(ps, radius, q, f, seed, exclusion_zone, want_lists != 0, out); });
+}
+
+// ---- sharded closest pair ------------------------------------------------------
+int psg_cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t exclusion_zone,
+                        psg_cpp_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<psg_cpp_plan>();
+    p->plan.reset(psg::cpp_plan_create(ps, q, f, seed, exclusion_zone));
+    *out = p.release();
+  });
+}
+int psg_cpp_plan_bootstrap(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float* bound_s32) {
+  return guarded([&] {
+    if (nparts == 0 || part >= nparts) throw psg::invalid_argument("part out of range");
+    *bound_s32 = psg::cpp_plan_bootstrap(*plan->plan, part, nparts);
+  });
+}
+int psg_cpp_plan_scan(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float bound_s32, psg_pair_result* out) {
+  return guarded([&] {
+    if (nparts == 0 || part >= nparts) throw psg::invalid_argument("part out of range");
+    *out = psg::cpp_plan_scan(*plan->plan, part, nparts, bound_s32);
+  });
+}
+void psg_cpp_plan_free(psg_cpp_plan* plan) { delete plan; }
+
+// ---- host helpers ----------------------------------------------------------------
+int psg_host_alloc(size_t bytes, void** out) {
+  return guarded([&] { PSG_CUDA(cudaMallocHost(out, bytes)); });
+}
+void psg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

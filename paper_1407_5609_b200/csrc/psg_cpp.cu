@@ -1,0 +1,910 @@
+// psg_cpp.cu — exact closest pair on B200.
+//
+// Pipeline (reference loop refscan.cpp:67-132):
+//   K1 project    keys = <U_k, X_i>, k < nk, one warp per row, U in registers
+//   K2 sort       LSD radix sort of key 0 (+ index payload)          (psg_sort.cu)
+//      gather     keys into sorted order (AoS, nk floats per point)
+//   K3a bootstrap each sorted row vs its next `width` rows: min lower bound
+//                 sum_k gap_k^2 per row, exact FP32 distance of each warp's
+//                 best -> global upper bound delta_0 (atomicMin on FP32 bits)
+//   K3b scan      each sorted row vs the rows whose key-0 gap is <= delta
+//                 (the reference's sorted-order exit, refscan.cpp:85-92),
+//                 pruned by all nk keys (its secondary references, 95-105),
+//                 survivors queued in shared memory and evaluated as exact
+//                 FP32 distances by whole warps (coalesced row loads, shuffle
+//                 reduction); delta tightens as the atomic minimum falls
+//   K6 recheck    every candidate inside the FP32 error band of the final
+//                 delta re-evaluated in the reference's FP64 order; ties to the
+//                 lowest (i, j) (refscan.cpp:118-126)
+#include <algorithm>
+#include <cmath>
+#include <memory>
+
+#include "psg_cpp.cuh"
+#include "psg_sort.cuh"
+
+namespace psg {
+
+thread_local psg_profile g_prof;
+
+void prof_begin() {
+  std::memset(&g_prof, 0, sizeof(g_prof));
+  g_launches = 0;
+}
+
+void prof_stages(const StageTimer& t) {
+  if (!t.on) return;
+  for (int i = 0; i < t.count && g_prof.stages < 16; ++i) {
+    float ms = 0.f;
+    PSG_CUDA(cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]));
+    std::strncpy(g_prof.stage_name[g_prof.stages], t.name[i], 23);
+    g_prof.stage_ms[g_prof.stages] = ms;
+    ++g_prof.stages;
+  }
+}
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 256;
+constexpr int kChunk = 256;
+constexpr int kQueue = 1024;
+constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
+
+__device__ __forceinline__ bool admissible(uint32_t a, uint32_t b, uint64_t zone) {
+  const uint32_t gap = a > b ? a - b : b - a;
+  return gap >= zone;  // refscan.cpp:15-18
+}
+
+template <int NK>
+__device__ __forceinline__ void load_keys(const float* __restrict__ p, float (&k)[NK]) {
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int v = 0; v < NK / 4; ++v) {
+    const float4 t = p4[v];
+    k[4 * v + 0] = t.x;
+    k[4 * v + 1] = t.y;
+    k[4 * v + 2] = t.z;
+    k[4 * v + 3] = t.w;
+  }
+}
+
+// Lower-bound accumulator: the ONE expression both the scan and the recheck
+// use, so the recheck filter is a deterministic subset of what the scan kept.
+template <int NK>
+__device__ __forceinline__ float lb2_full(const float (&a)[NK], const float (&b)[NK]) {
+  float g = b[0] - a[0];
+  float s = g * g;
+#pragma unroll
+  for (int k = 1; k < NK; ++k) {
+    g = b[k] - a[k];
+    s = fmaf(g, g, s);
+  }
+  return s;
+}
+
+// Exact FP32 squared distance, warp-cooperative.  Fixed order for a given d:
+// lane-strided partial sums (float4 when d % 128 == 0), then an xor tree.
+__device__ __forceinline__ float warp_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d,
+                                             int lane) {
+  float s = 0.f;
+  if ((d & 127) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (int t = lane; t < (d >> 2); t += 32) {
+      const float4 x = __ldg(a4 + t), y = __ldg(b4 + t);
+      float g = x.x - y.x;
+      s = fmaf(g, g, s);
+      g = x.y - y.y;
+      s = fmaf(g, g, s);
+      g = x.z - y.z;
+      s = fmaf(g, g, s);
+      g = x.w - y.w;
+      s = fmaf(g, g, s);
+    }
+  } else {
+    for (int t = lane; t < d; t += 32) {
+      const float g = __ldg(a + t) - __ldg(b + t);
+      s = fmaf(g, g, s);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  return s;
+}
+
+__device__ __forceinline__ float thread_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d) {
+  float s = 0.f;
+  for (int t = 0; t < d; ++t) {
+    const float g = __ldg(a + t) - __ldg(b + t);
+    s = fmaf(g, g, s);
+  }
+  return s;
+}
+
+__device__ __forceinline__ float best_now(const unsigned* best) {
+  return __uint_as_float(*reinterpret_cast<const volatile unsigned*>(best));
+}
+
+// ---------------------------------------------------------------------------
+// K1: projection.  One warp per row, lane l owns the V consecutive
+// coordinates [l*V, l*V+V) of a d = 32V row (coalesced 4V-byte loads) and the
+// matching NK x V slice of U in registers.  The NK partial sums are combined
+// by a transposing butterfly (log2 NK halving steps, then an xor tree), so a
+// row costs NK*V FMAs + (NK-1) + (5 - log2 NK) shuffles per lane.
+template <int CNT, int OFF, int NK>
+struct Transpose {
+  static __device__ __forceinline__ void run(float (&v)[NK], int lane) {
+    const bool up = lane & OFF;
+#pragma unroll
+    for (int i = 0; i < CNT / 2; ++i) {
+      const float send = up ? v[i] : v[i + CNT / 2];
+      const float keep = up ? v[i + CNT / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(kFull, send, OFF);
+    }
+    Transpose<CNT / 2, OFF / 2, NK>::run(v, lane);
+  }
+};
+template <int OFF, int NK>
+struct Transpose<1, OFF, NK> {
+  static __device__ __forceinline__ void run(float (&)[NK], int) {}
+};
+
+template <int NK>
+constexpr int log2c() {
+  return NK == 8 ? 3 : (NK == 4 ? 2 : (NK == 2 ? 1 : 0));
+}
+
+template <int NK, int V>
+__global__ void __launch_bounds__(256) k_project_warp(const float* __restrict__ X, uint32_t n,
+                                                      const float* __restrict__ U, float* __restrict__ keys,
+                                                      unsigned* __restrict__ norm2_bits) {
+  constexpr int d = 32 * V;
+  constexpr int L = log2c<NK>();
+  const int lane = threadIdx.x & 31;
+  float u[NK][V];
+#pragma unroll
+  for (int k = 0; k < NK; ++k)
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[k][v] = __ldg(U + k * d + lane * V + v);
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  float worst = 0.f;
+  for (uint32_t r = warp; r < n; r += nwarps) {
+    float x[V];
+    const float* row = X + static_cast<size_t>(r) * d + lane * V;
+    if constexpr (V % 4 == 0) {
+#pragma unroll
+      for (int v = 0; v < V; v += 4) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(row + v));
+        x[v] = t.x; x[v + 1] = t.y; x[v + 2] = t.z; x[v + 3] = t.w;
+      }
+    } else if constexpr (V == 2) {
+      const float2 t = __ldcs(reinterpret_cast<const float2*>(row));
+      x[0] = t.x; x[1] = t.y;
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = __ldcs(row + v);
+    }
+    float acc[NK];
+    float nn = 0.f;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      nn = fmaf(x[v], x[v], nn);
+#pragma unroll
+      for (int k = 0; k < NK; ++k) acc[k] = fmaf(u[k][v], x[v], acc[k]);
+    }
+    Transpose<NK, 16, NK>::run(acc, lane);
+    float key = acc[0];
+#pragma unroll
+    for (int o = 16 >> L; o; o >>= 1) key += __shfl_xor_sync(kFull, key, o);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nn += __shfl_xor_sync(kFull, nn, o);
+    worst = fmaxf(worst, nn);
+    if ((lane & ((1 << (5 - L)) - 1)) == 0) keys[static_cast<size_t>(r) * NK + (lane >> (5 - L))] = key;
+  }
+  if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
+}
+
+// Small or irregular d: one thread per row, U staged in shared memory.
+template <int NK>
+__global__ void __launch_bounds__(256) k_project_thread(const float* __restrict__ X, uint32_t n, int d,
+                                                        const float* __restrict__ U, float* __restrict__ keys,
+                                                        unsigned* __restrict__ norm2_bits, int u_in_smem) {
+  extern __shared__ float su[];
+  if (u_in_smem) {
+    for (int i = threadIdx.x; i < NK * d; i += blockDim.x) su[i] = U[i];
+    __syncthreads();
+  }
+  const float* Us = u_in_smem ? su : U;
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  float nn = 0.f;
+  if (r < n) {
+    float acc[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
+    const float* row = X + static_cast<size_t>(r) * d;
+    for (int t = 0; t < d; ++t) {
+      const float x = __ldg(row + t);
+      nn = fmaf(x, x, nn);
+#pragma unroll
+      for (int k = 0; k < NK; ++k) acc[k] = fmaf(Us[k * d + t], x, acc[k]);
+    }
+    float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(r) * NK);
+#pragma unroll
+    for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+  }
+  nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
+  if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
+}
+
+template <int NK>
+__global__ void k_sort_keys(const float* __restrict__ keys, uint32_t n, uint32_t* __restrict__ k_out,
+                            uint32_t* __restrict__ v_out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  k_out[i] = f32_order(keys[static_cast<size_t>(i) * NK]);
+  v_out[i] = i;
+}
+
+template <int NK>
+__global__ void k_gather(const float* __restrict__ keys, const uint32_t* __restrict__ perm, uint32_t n,
+                         float* __restrict__ skeys, uint32_t* __restrict__ sidx) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t i = perm[p];
+  const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
+  float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(p) * NK);
+#pragma unroll
+  for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+  sidx[p] = i;
+}
+
+// ---------------------------------------------------------------------------
+struct ScanArgs {
+  const float* X;
+  const float* skeys;
+  const uint32_t* sidx;
+  uint32_t n;
+  int d;
+  uint64_t zone;
+  Budget bud;
+  unsigned* best;
+  uint32_t* cand_p;
+  uint32_t* cand_j;
+  float* cand_s;
+  unsigned* cand_n;
+  uint32_t cand_cap;
+  uint32_t* ovf_p;
+  uint32_t* ovf_j;
+  unsigned* ovf_n;
+  uint32_t ovf_cap;
+  unsigned long long* evals;
+};
+
+__device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {
+  atomicMin(a.best, __float_as_uint(s32));
+  if (s32 <= band) {
+    const unsigned c = atomicAdd(a.cand_n, 1u);
+    if (c < a.cand_cap) {
+      a.cand_p[c] = p;
+      a.cand_j[c] = j;
+      a.cand_s[c] = s32;
+    }
+  }
+}
+
+// Seed: pair (0, max(zone,1)) is admissible whenever any pair is, so delta
+// is finite from the start.
+__global__ void k_seed_pair(ScanArgs a, uint32_t z) {
+  const int lane = threadIdx.x & 31;
+  const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(a.X, a.X + static_cast<size_t>(z) * a.d, a.d) : 0.f)
+                                  : warp_sqdist(a.X, a.X + static_cast<size_t>(z) * a.d, a.d, lane);
+  if (lane == 0) atomicMin(a.best, __float_as_uint(s));
+}
+
+// K3a: bootstrap.  All threads walk the same j (shared-memory broadcast).
+template <int NK>
+__global__ void __launch_bounds__(kThreads) k_bootstrap(ScanArgs a, uint32_t lo, uint32_t hi, uint32_t width) {
+  __shared__ __align__(16) float sk[kChunk * NK];
+  __shared__ uint32_t so[kChunk];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t p0 = lo + blockIdx.x * kThreads;
+  const uint32_t p = p0 + tid;
+  const bool valid = p < hi;
+  float mk[NK];
+  uint32_t mo = 0;
+  if (valid) {
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+    mo = a.sidx[p];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) mk[k] = 0.f;
+  }
+  float best_lb = INFINITY;
+  uint32_t best_j = 0xffffffffu;
+  const uint64_t jend64 = static_cast<uint64_t>(p0) + kThreads + width;
+  const uint32_t jend = static_cast<uint32_t>(jend64 < a.n ? jend64 : a.n);
+  for (uint32_t c0 = p0 + 1; c0 < jend; c0 += kChunk) {
+    const uint32_t cnt = min(static_cast<uint32_t>(kChunk), jend - c0);
+    __syncthreads();
+    if (tid < cnt) {
+      const float4* src = reinterpret_cast<const float4*>(a.skeys + static_cast<size_t>(c0 + tid) * NK);
+      float4* dst = reinterpret_cast<float4*>(sk + tid * NK);
+#pragma unroll
+      for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+      so[tid] = a.sidx[c0 + tid];
+    }
+    __syncthreads();
+    if (valid) {
+      for (uint32_t jj = 0; jj < cnt; ++jj) {
+        const uint32_t j = c0 + jj;
+        if (j <= p || j > p + width) continue;
+        const float* kj = sk + jj * NK;
+        float g = kj[0] - mk[0];
+        float s = g * g;
+        g = kj[1] - mk[1];
+        s = fmaf(g, g, s);
+        if (s >= best_lb) continue;
+#pragma unroll
+        for (int k = 2; k < NK; ++k) {
+          g = kj[k] - mk[k];
+          s = fmaf(g, g, s);
+        }
+        if (s < best_lb && admissible(mo, so[jj], a.zone)) {
+          best_lb = s;
+          best_j = j;
+        }
+      }
+    }
+  }
+  // warp argmin of the per-row best lower bound, then one exact evaluation
+  float wlb = best_lb;
+  uint32_t wj = best_j, wp = p;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float olb = __shfl_xor_sync(kFull, wlb, o);
+    const uint32_t oj = __shfl_xor_sync(kFull, wj, o);
+    const uint32_t op = __shfl_xor_sync(kFull, wp, o);
+    if (olb < wlb || (olb == wlb && op < wp)) {
+      wlb = olb;
+      wj = oj;
+      wp = op;
+    }
+  }
+  if (wj == 0xffffffffu) return;
+  const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+  if (!(wlb <= th.lb2)) return;
+  const float* xi = a.X + static_cast<size_t>(a.sidx[wp]) * a.d;
+  const float* xj = a.X + static_cast<size_t>(a.sidx[wj]) * a.d;
+  float s;
+  if (a.d <= kInlineD)
+    s = lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f;
+  else
+    s = warp_sqdist(xi, xj, a.d, lane);
+  if (lane == 0) atomicMin(a.best, __float_as_uint(s));
+}
+
+// K3b: the windowed candidate scan.
+template <int NK>
+__global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint32_t hi) {
+  __shared__ __align__(16) float sk[kChunk * NK];
+  __shared__ uint32_t so[kChunk];
+  __shared__ uint32_t qp[kQueue], qj[kQueue];
+  __shared__ int qn;
+  __shared__ Thresholds th;
+  __shared__ unsigned long long nevals;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t p0 = lo + blockIdx.x * kThreads;
+  const uint32_t p = p0 + tid;
+  const uint32_t plast = min(p0 + kThreads, hi) - 1;
+  bool active = p < hi;
+  float mk[NK];
+  uint32_t mo = 0;
+  if (active) {
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+    mo = a.sidx[p];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) mk[k] = 0.f;
+  }
+  const float kmax = a.skeys[static_cast<size_t>(plast) * NK];
+  if (tid == 0) {
+    qn = 0;
+    nevals = 0;
+    th = budget_thresholds_s32(a.bud, best_now(a.best));
+  }
+  __syncthreads();
+  for (uint32_t c0 = p0 + 1; c0 < a.n; c0 += kChunk) {
+    if (a.skeys[static_cast<size_t>(c0) * NK] - kmax > th.win) break;  // block-wide exit
+    const uint32_t cnt = min(static_cast<uint32_t>(kChunk), a.n - c0);
+    if (tid < cnt) {
+      const float4* src = reinterpret_cast<const float4*>(a.skeys + static_cast<size_t>(c0 + tid) * NK);
+      float4* dst = reinterpret_cast<float4*>(sk + tid * NK);
+#pragma unroll
+      for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+      so[tid] = a.sidx[c0 + tid];
+    }
+    __syncthreads();
+    if (active) {
+      const float win = th.win, lb2 = th.lb2;
+      for (uint32_t jj = 0; jj < cnt; ++jj) {
+        const uint32_t j = c0 + jj;
+        if (j <= p) continue;
+        const float* kj = sk + jj * NK;
+        float g = kj[0] - mk[0];
+        if (g > win) {  // sorted: every later j is farther (refscan.cpp:85)
+          active = false;
+          break;
+        }
+        float s = g * g;
+        g = kj[1] - mk[1];
+        s = fmaf(g, g, s);
+        if (s > lb2) continue;
+#pragma unroll
+        for (int k = 2; k < NK; ++k) {
+          g = kj[k] - mk[k];
+          s = fmaf(g, g, s);
+        }
+        if (s > lb2 || !admissible(mo, so[jj], a.zone)) continue;
+        const int slot = atomicAdd(&qn, 1);
+        if (slot < kQueue) {
+          qp[slot] = p;
+          qj[slot] = j;
+        } else {
+          const unsigned o = atomicAdd(a.ovf_n, 1u);
+          if (o < a.ovf_cap) {
+            a.ovf_p[o] = p;
+            a.ovf_j[o] = j;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nq = min(qn, kQueue);
+    if (nq > 0) {
+      const float band = th.band;
+      if (a.d <= kInlineD) {
+        for (int i = tid; i < nq; i += kThreads) {
+          const uint32_t pi = qp[i], pj = qj[i];
+          const float s = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                        a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
+          record(a, pi, pj, s, band);
+        }
+      } else {
+        for (int i = warp; i < nq; i += kThreads / 32) {
+          const uint32_t pi = qp[i], pj = qj[i];
+          const float s = warp_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                      a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d, lane);
+          if (lane == 0) record(a, pi, pj, s, band);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      nevals += static_cast<unsigned long long>(nq);
+      qn = 0;
+      th = budget_thresholds_s32(a.bud, best_now(a.best));
+    }
+    if (!__syncthreads_or(active)) break;
+  }
+  if (tid == 0 && nevals) atomicAdd(a.evals, nevals);
+}
+
+// Pairs that overflowed the shared-memory queue.
+__global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const uint32_t* __restrict__ lj,
+                            uint32_t count) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = warp; i < count; i += nwarps) {
+    const uint32_t pi = lp[i], pj = lj[i];
+    const float* xi = a.X + static_cast<size_t>(a.sidx[pi]) * a.d;
+    const float* xj = a.X + static_cast<size_t>(a.sidx[pj]) * a.d;
+    const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f) : warp_sqdist(xi, xj, a.d, lane);
+    if (lane == 0) {
+      const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+      record(a, pi, pj, s, th.band);
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(a.evals, static_cast<unsigned long long>(count));
+}
+
+// K6: deterministic final filter + FP64 recheck in the reference's order.
+template <int NK>
+__global__ void k_recheck(ScanArgs a, ExactSrc src, Thresholds th, uint32_t count, double* __restrict__ d64,
+                          unsigned long long* __restrict__ best64, unsigned long long* __restrict__ examined) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned pass = 0;
+  if (c < count) {
+    const uint32_t p = a.cand_p[c], j = a.cand_j[c];
+    float kp[NK], kj[NK];
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, kp);
+    load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
+    const bool keep = (kj[0] - kp[0] <= th.win) && (lb2_full<NK>(kp, kj) <= th.lb2) && (a.cand_s[c] <= th.band);
+    double dd = -1.0;
+    if (keep) {
+      dd = exact_distance(src, a.sidx[p], a.sidx[j]);
+      atomicMin(best64, static_cast<unsigned long long>(__double_as_longlong(dd)));
+      pass = 1;
+    }
+    d64[c] = dd;
+  }
+  const unsigned wsum = __reduce_add_sync(kFull, pass);
+  if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(examined, static_cast<unsigned long long>(wsum));
+}
+
+__global__ void k_pick(const ScanArgs a, uint32_t count, const double* __restrict__ d64,
+                       const unsigned long long* __restrict__ best64, unsigned long long* __restrict__ lex) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= count) return;
+  if (static_cast<unsigned long long>(__double_as_longlong(d64[c])) != *best64 || d64[c] < 0.0) return;
+  const uint32_t i = a.sidx[a.cand_p[c]], j = a.sidx[a.cand_j[c]];
+  const unsigned long long key = i < j ? (static_cast<unsigned long long>(i) << 32) | j
+                                       : (static_cast<unsigned long long>(j) << 32) | i;
+  atomicMin(lex, key);
+}
+
+// Window statistics at the final delta: pairs with fl(k0_j - k0_p) <= win,
+// and rows whose window ends before the last point.
+template <int NK>
+__global__ void k_window_stats(const float* __restrict__ skeys, uint32_t n, uint32_t lo, uint32_t hi, float win,
+                               unsigned long long* __restrict__ pairs, unsigned long long* __restrict__ exits) {
+  const uint32_t p = lo + blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long cnt = 0;
+  unsigned ex = 0;
+  if (p < hi) {
+    const float kp = skeys[static_cast<size_t>(p) * NK];
+    uint32_t a = p + 1, b = n;  // first j in [p+1, n) with gap > win
+    while (a < b) {
+      const uint32_t m = a + ((b - a) >> 1);
+      if (skeys[static_cast<size_t>(m) * NK] - kp <= win)
+        a = m + 1;
+      else
+        b = m;
+    }
+    cnt = a - p - 1;
+    ex = a < n;
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+  ex = __reduce_add_sync(kFull, ex);
+  if ((threadIdx.x & 31) == 0) {
+    if (cnt) atomicAdd(pairs, cnt);
+    if (ex) atomicAdd(exits, static_cast<unsigned long long>(ex));
+  }
+}
+
+int blocks_for(uint64_t n, int per) { return static_cast<int>((n + per - 1) / per); }
+
+template <class T>
+T read1(const T* dptr, cudaStream_t s) {
+  T h;
+  PSG_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+void part_range(uint64_t n, uint64_t part, uint64_t nparts, uint32_t* lo, uint32_t* hi) {
+  *lo = static_cast<uint32_t>(n * part / nparts);
+  *hi = static_cast<uint32_t>(n * (part + 1) / nparts);
+}
+
+}  // namespace
+
+// ===========================================================================
+void check_reference_args(uint64_t n, uint64_t q, double f) {
+  // build_reference_set validation order (refscan.cpp:33-35)
+  if (q == 0) throw invalid_argument("reference count must be positive");
+  if (q > n) throw invalid_argument("reference count exceeds point count");
+  if (!(f > 0.0) || !std::isfinite(f)) throw invalid_argument("projection factor must be positive");
+}
+
+float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s) {
+  DevBuf<float> U(dir.U.size(), s);
+  PSG_CUDA(cudaMemcpyAsync(U.p, dir.U.data(), dir.U.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  DevBuf<unsigned> nb(1, s);
+  PSG_CUDA(cudaMemsetAsync(nb.p, 0, 4, s));
+  const uint32_t n = static_cast<uint32_t>(ps.n);
+  const int d = ps.d;
+  const int sms = ctx().sm_count;
+  const int warp_grid = std::min<int>(blocks_for(n, 8), sms * 16);
+  bool done = true;
+#define PSG_PROJ_WARP(NKV, VV) \
+  k_project_warp<NKV, VV><<<warp_grid, 256, 0, s>>>(ps.X, n, U.p, keys, nb.p)
+  if (d == 32 || d == 64 || d == 128 || d == 256) {
+    const int V = d / 32;
+    if (dir.nk == 4) {
+      if (V == 1) PSG_PROJ_WARP(4, 1); else if (V == 2) PSG_PROJ_WARP(4, 2); else if (V == 4) PSG_PROJ_WARP(4, 4); else PSG_PROJ_WARP(4, 8);
+    } else {
+      if (V == 1) PSG_PROJ_WARP(8, 1); else if (V == 2) PSG_PROJ_WARP(8, 2); else if (V == 4) PSG_PROJ_WARP(8, 4); else PSG_PROJ_WARP(8, 8);
+    }
+  } else {
+    done = false;
+  }
+#undef PSG_PROJ_WARP
+  if (!done) {
+    const size_t ubytes = static_cast<size_t>(dir.nk) * d * sizeof(float);
+    const int smem_ok = ubytes <= 48 * 1024;
+    if (dir.nk == 4)
+      k_project_thread<4><<<blocks_for(n, 256), 256, smem_ok ? ubytes : 0, s>>>(ps.X, n, d, U.p, keys, nb.p, smem_ok);
+    else
+      k_project_thread<8><<<blocks_for(n, 256), 256, smem_ok ? ubytes : 0, s>>>(ps.X, n, d, U.p, keys, nb.p, smem_ok);
+  }
+  PSG_LAUNCHED();
+  ++g_launches;
+  const unsigned bits = read1(nb.p, s);
+  float v;
+  std::memcpy(&v, &bits, 4);
+  return v;
+}
+
+Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm2) {
+  const double u = 0x1.0p-24;
+  const int d = ps.d;
+  Budget b;
+  b.e = (d + 4) * u * 1.01;
+  b.a = (2.0 * d + 2.0) * 0x1.0p-149;
+  const double maxnorm = std::sqrt(static_cast<double>(max_norm2) * (1.0 + (d + 4) * u)) * (1.0 + 1e-7);
+  const double gamma = d * u / (1.0 - d * u);
+  b.E = gamma * dir.unorm * maxnorm * 1.0001;
+  b.Rn = ps.Rn;
+  b.sigma = dir.sigma;
+  b.unorm = dir.unorm;
+  b.gamma64 = (d + 2) * 0x1.0p-53 * 1.01;
+  b.nk = dir.nk;
+  return b;
+}
+
+CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone) {
+  const uint64_t n = ps->n;
+  if (n < 2) throw invalid_argument("closest_pair needs at least 2 points");  // refscan.cpp:70
+  check_reference_args(n, q, f);
+  if (n >= 0xffffffffull) throw invalid_argument("point count exceeds 2^32-1");
+  if (admissible_pairs(n, zone) == 0) throw invalid_argument("no admissible pair");  // refscan.cpp:129
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  auto plan = std::make_unique<CppPlan>();
+  plan->ps = ps;
+  plan->zone = zone;
+  plan->dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
+  const int nk = plan->dir.nk;
+  StageTimer tm(s);
+  DevBuf<float> keys(n * nk, s);
+  const float norm2 = project(*ps, plan->dir, keys.p, s);
+  tm.mark("project");
+  plan->bud = make_budget(*ps, plan->dir, norm2);
+  // K2: sort by key 0 (stable, index payload)
+  DevBuf<uint32_t> kb0(n, s), kb1(n, s), vb0(n, s), vb1(n, s);
+  DevBuf<uint32_t> hist(radix_hist_words(n), s);
+  if (nk == 4)
+    k_sort_keys<4><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), kb0.p, vb0.p);
+  else
+    k_sort_keys<8><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), kb0.p, vb0.p);
+  PSG_LAUNCHED();
+  ++g_launches;
+  uint32_t* kk[2] = {kb0.p, kb1.p};
+  uint32_t* vv[2] = {vb0.p, vb1.p};
+  const int which = radix_sort<uint32_t>(kk, vv, n, 0, 32, hist.p, s);
+  g_launches += 12;
+  tm.mark("sort");
+  plan->skeys.alloc(n * nk, s);
+  plan->sidx.alloc(n, s);
+  if (nk == 4)
+    k_gather<4><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, vv[which], static_cast<uint32_t>(n), plan->skeys.p,
+                                                   plan->sidx.p);
+  else
+    k_gather<8><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, vv[which], static_cast<uint32_t>(n), plan->skeys.p,
+                                                   plan->sidx.p);
+  PSG_LAUNCHED();
+  ++g_launches;
+  tm.mark("gather");
+  plan->best.alloc(1, s);
+  const float inf = INFINITY;
+  PSG_CUDA(cudaMemcpyAsync(plan->best.p, &inf, 4, cudaMemcpyHostToDevice, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
+  for (int i = 0; i < 3 && i < tm.count; ++i) plan->prep_ms[i] = g_prof.stage_ms[g_prof.stages - tm.count + i];
+  return plan.release();
+}
+
+namespace {
+ScanArgs make_args(CppPlan& plan) {
+  ScanArgs a{};
+  a.X = plan.ps->X;
+  a.skeys = plan.skeys.p;
+  a.sidx = plan.sidx.p;
+  a.n = static_cast<uint32_t>(plan.ps->n);
+  a.d = plan.ps->d;
+  a.zone = plan.zone;
+  a.bud = plan.bud;
+  a.best = plan.best.p;
+  return a;
+}
+
+uint64_t window_pairs(CppPlan& plan, uint32_t lo, uint32_t hi, float win, uint64_t* exits, cudaStream_t s) {
+  DevBuf<unsigned long long> acc(2, s);
+  PSG_CUDA(cudaMemsetAsync(acc.p, 0, 16, s));
+  if (hi > lo) {
+    if (plan.dir.nk == 4)
+      k_window_stats<4><<<blocks_for(hi - lo, 256), 256, 0, s>>>(plan.skeys.p, static_cast<uint32_t>(plan.ps->n), lo,
+                                                                 hi, win, acc.p, acc.p + 1);
+    else
+      k_window_stats<8><<<blocks_for(hi - lo, 256), 256, 0, s>>>(plan.skeys.p, static_cast<uint32_t>(plan.ps->n), lo,
+                                                                 hi, win, acc.p, acc.p + 1);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
+  unsigned long long h[2];
+  PSG_CUDA(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  if (exits) *exits = h[1];
+  return h[0];
+}
+}  // namespace
+
+float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  uint32_t lo, hi;
+  part_range(plan.ps->n, part, nparts, &lo, &hi);
+  ScanArgs a = make_args(plan);
+  StageTimer tm(s);
+  const uint32_t z = static_cast<uint32_t>(std::max<uint64_t>(plan.zone, 1));
+  if (z < plan.ps->n) {
+    k_seed_pair<<<1, 32, 0, s>>>(a, z);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
+  // Adaptive width: widen while the window the bound implies is far more
+  // work than the bootstrap that produced it.
+  uint32_t width = 1024;
+  for (int round = 0; round < 4; ++round) {
+    if (hi > lo) {
+      if (plan.dir.nk == 4)
+        k_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi, width);
+      else
+        k_bootstrap<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi, width);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    const float b = read1(plan.best.p, s);
+    const Thresholds th = budget_thresholds_s32(plan.bud, b);
+    const uint64_t est = window_pairs(plan, lo, hi, th.win, nullptr, s);
+    if (est <= 8ull * (hi - lo) * width || width >= 16384) break;
+    width *= 4;
+  }
+  plan.width = width;
+  tm.mark("bootstrap");
+  PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
+  g_prof.bootstrap_width = width;
+  return read1(plan.best.p, s);
+}
+
+psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, float bound_s32) {
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  const uint64_t n = plan.ps->n;
+  uint32_t lo, hi;
+  part_range(n, part, nparts, &lo, &hi);
+  StageTimer tm(s);
+  {
+    const float cur = read1(plan.best.p, s);
+    const float b = std::min(cur, bound_s32);
+    PSG_CUDA(cudaMemcpyAsync(plan.best.p, &b, 4, cudaMemcpyHostToDevice, s));
+  }
+  uint32_t cand_cap = 1u << 16, ovf_cap = 1u << 20;
+  DevBuf<uint32_t> cp, cj, op, oj;
+  DevBuf<float> cs;
+  DevBuf<unsigned> counters(2, s);
+  DevBuf<unsigned long long> evals(1, s);
+  PSG_CUDA(cudaMemsetAsync(evals.p, 0, 8, s));
+  ScanArgs a = make_args(plan);
+  unsigned ncand = 0;
+  for (int attempt = 0;; ++attempt) {
+    cp.alloc(cand_cap, s);
+    cj.alloc(cand_cap, s);
+    cs.alloc(cand_cap, s);
+    op.alloc(ovf_cap, s);
+    oj.alloc(ovf_cap, s);
+    PSG_CUDA(cudaMemsetAsync(counters.p, 0, 8, s));
+    a.cand_p = cp.p;
+    a.cand_j = cj.p;
+    a.cand_s = cs.p;
+    a.cand_n = counters.p;
+    a.cand_cap = cand_cap;
+    a.ovf_p = op.p;
+    a.ovf_j = oj.p;
+    a.ovf_n = counters.p + 1;
+    a.ovf_cap = ovf_cap;
+    a.evals = evals.p;
+    if (hi > lo) {
+      if (plan.dir.nk == 4)
+        k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
+      else
+        k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    unsigned h[2];
+    PSG_CUDA(cudaMemcpyAsync(h, counters.p, 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    if (h[1] > ovf_cap) {  // queue spill list overflowed: rescan with the tighter bound
+      ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h[1]) * 2, 1u << 28);
+      continue;
+    }
+    if (h[1]) {
+      k_eval_list<<<std::min<int>(blocks_for(h[1], 8), c.sm_count * 16), 256, 0, s>>>(a, op.p, oj.p, h[1]);
+      PSG_LAUNCHED();
+      ++g_launches;
+      PSG_CUDA(cudaMemcpyAsync(h, counters.p, 4, cudaMemcpyDeviceToHost, s));
+      PSG_CUDA(cudaStreamSynchronize(s));
+    }
+    if (h[0] > cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
+      cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h[0]) * 2, 1u << 28);
+      PSG_CUDA(cudaMemsetAsync(evals.p, 0, 8, s));
+      continue;
+    }
+    ncand = h[0];
+    break;
+  }
+  tm.mark("scan");
+  const float best_s32 = read1(plan.best.p, s);
+  const Thresholds th = budget_thresholds_s32(plan.bud, best_s32);
+  DevBuf<double> d64(std::max<unsigned>(ncand, 1), s);
+  DevBuf<unsigned long long> red(3, s);
+  const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
+  PSG_CUDA(cudaMemcpyAsync(red.p, init, 24, cudaMemcpyHostToDevice, s));
+  if (ncand) {
+    if (plan.dir.nk == 4)
+      k_recheck<4><<<blocks_for(ncand, 256), 256, 0, s>>>(a, plan.ps->exact(), th, ncand, d64.p, red.p, red.p + 2);
+    else
+      k_recheck<8><<<blocks_for(ncand, 256), 256, 0, s>>>(a, plan.ps->exact(), th, ncand, d64.p, red.p, red.p + 2);
+    PSG_LAUNCHED();
+    k_pick<<<blocks_for(ncand, 256), 256, 0, s>>>(a, ncand, d64.p, red.p, red.p + 1);
+    PSG_LAUNCHED();
+    g_launches += 2;
+  }
+  unsigned long long hr[3];
+  PSG_CUDA(cudaMemcpyAsync(hr, red.p, 24, cudaMemcpyDeviceToHost, s));
+  const unsigned long long hev = read1(evals.p, s);
+  tm.mark("recheck");
+  uint64_t exits = 0;
+  const uint64_t wp = window_pairs(plan, lo, hi, th.win, &exits, s);
+  tm.mark("stats");
+  PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
+
+  psg_pair_result r{};
+  if (hr[1] == ~0ull) {
+    r.index_i = r.index_j = UINT64_MAX;
+    r.distance = INFINITY;
+  } else {
+    r.index_i = hr[1] >> 32;
+    r.index_j = hr[1] & 0xffffffffull;
+    std::memcpy(&r.distance, &hr[0], 8);
+  }
+  r.stats.pairs_examined = hr[2];
+  r.stats.pairs_pruned_by_reference = wp > hr[2] ? wp - hr[2] : 0;
+  r.stats.inner_loop_exits = exits;
+  g_prof.window_pairs += wp;
+  g_prof.lb_survivors += hev;
+  g_prof.candidates += ncand;
+  return r;
+}
+
+psg_pair_result cpp_solve(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone) {
+  std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));
+  const float b = cpp_plan_bootstrap(*plan, 0, 1);
+  psg_pair_result r = cpp_plan_scan(*plan, 0, 1, b);
+  if (r.index_i == UINT64_MAX) throw invalid_argument("no admissible pair");
+  const uint64_t adm = admissible_pairs(ps->n, zone);
+  const uint64_t used = r.stats.pairs_examined + r.stats.pairs_pruned_by_reference;
+  if (used > adm) r.stats.pairs_pruned_by_reference = adm - r.stats.pairs_examined;
+  r.stats.pairs_skipped_by_exit = adm - r.stats.pairs_examined - r.stats.pairs_pruned_by_reference;
+  return r;
+}
+
+}  // namespace psg

@@ -1,0 +1,30 @@
+// psg_engines.cuh — the engines behind the C ABI besides the closest-pair
+// scan: fixed-radius neighbours, brute force (device oracle and API), the
+// exact reference set, and the reference bound.
+#pragma once
+
+#include "../../include/pairscan_b200.h"
+#include "psg_internal.cuh"
+#include "psg_points.cuh"
+
+namespace psg {
+
+// refscan.cpp:134-157 on device: exact over every admissible pair.
+psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone);
+
+// refscan.cpp:159-209: cell grid on the first min(3, q) projection keys,
+// FP32 filter + FP64 decision on the boundary band.
+void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                bool want_lists, psg_neighbor_result* out);
+void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                uint64_t* pairs, uint64_t capacity, uint64_t* count, uint64_t* hash);
+// refscan.cpp:211-227 on device.
+void brute_neighbors(psg_pointset* ps, double radius, uint64_t zone, bool want_lists, psg_neighbor_result* out);
+
+// refscan.cpp:30-65, bit-exact.
+void reference_set(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t* ref_indices,
+                   double* references, double* table, uint64_t* order);
+// refscan.cpp:229-232.
+double reference_bound_dev(const double* r, const double* x, const double* y, uint64_t d);
+
+}  // namespace psg

@@ -1,0 +1,214 @@
+// psg_internal.cuh — shared host/device plumbing for the sm_100a pair-search
+// library: error handling, stream-ordered device buffers, the per-device
+// context, and the rigorous FP32 error-budget arithmetic every filter uses.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace psg {
+
+// Mirrors the reference's std::invalid_argument contract (refscan.cpp:33-35,
+// 70, 129, 136, 162-163, 214; series.cpp:9, 20-24); surfaced through the C ABI
+// as PSG_ERR_INVALID with the identical message.
+struct invalid_argument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define PSG_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t psg_e_ = (call);                                                        \
+    if (psg_e_ != cudaSuccess)                                                          \
+      throw ::psg::cuda_error(std::string(#call) + ": " + cudaGetErrorString(psg_e_) + \
+                              " (" __FILE__ ":" + std::to_string(__LINE__) + ")");      \
+  } while (0)
+#define PSG_LAUNCHED() PSG_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// Per-device context: one stream, a stream-ordered pool that keeps freed
+// blocks (so repeated solves do not pay cudaMalloc), timing events.
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;  // the reference is reentrant; we serialise per device
+};
+Ctx& ctx();  // context of the current CUDA device (created on first use)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Stage timer: CUDA events on the library stream; read after the final sync.
+struct StageTimer {
+  static constexpr int kMax = 16;
+  cudaEvent_t ev[kMax + 1] = {};
+  const char* name[kMax] = {};
+  int count = 0;
+  cudaStream_t s = nullptr;
+  bool on = true;
+  explicit StageTimer(cudaStream_t st, bool enabled = true) : s(st), on(enabled) {
+    if (!on) return;
+    for (auto& e : ev) PSG_CUDA(cudaEventCreate(&e));
+    PSG_CUDA(cudaEventRecord(ev[0], s));
+  }
+  void mark(const char* stage) {
+    if (!on || count >= kMax) return;
+    name[count] = stage;
+    ++count;
+    PSG_CUDA(cudaEventRecord(ev[count], s));
+  }
+  ~StageTimer() {
+    if (!on) return;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Orderable integer images of floats (radix sort keys, atomic min/max).
+__host__ __device__ __forceinline__ uint32_t f32_order(float f) {
+#ifdef __CUDA_ARCH__
+  uint32_t u = __float_as_uint(f);
+#else
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+#endif
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float f32_unorder(uint32_t u) {
+  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+__host__ __device__ __forceinline__ uint64_t f64_order(double f) {
+#ifdef __CUDA_ARCH__
+  uint64_t u = static_cast<uint64_t>(__double_as_longlong(f));
+#else
+  uint64_t u;
+  std::memcpy(&u, &f, 8);
+#endif
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// ---------------------------------------------------------------------------
+// Error budget of the FP32 filters (all quantities in the scaled working
+// units of the FP32 copy; see DESIGN.md §4 for the derivation).
+//
+//   s32 = FP32 squared distance (FMA accumulation, any fixed order):
+//         |s32 - S| <= e*S + a,  e = (d+4)u(1.01), a = (2d+2)*2^-149
+//   key error |k^ - k| <= E = gamma_d * max||U_k|| * max||x||
+//   narrowing radius Rn = max_i ||x_src,i*scale - x_f32,i||   (0 if exact)
+//   sigma = spectral-norm bound of the FP32 direction matrix U
+struct Budget {
+  double e = 0, a = 0;     // s32 relative / absolute error
+  double E = 0;            // per-key absolute error
+  double Rn = 0;           // narrowing radius
+  double sigma = 1;        // ||U||_2 bound
+  double unorm = 1;        // max_k ||U_k||_2
+  double gamma64 = 0;      // relative error of the reference's FP64 distance
+  int nk = 1;              // keys used in the LB
+};
+
+// Thresholds derived from an upper bound `dmax` (working units) on the real
+// distance of any pair that may still matter.
+struct Thresholds {
+  float win;   // key-0 window: keep if fl(k0_j - k0_i) <= win
+  float lb2;   // keep if sum_k fl(k_j - k_i)^2 (FP32) <= lb2
+  float band;  // keep as FP64-recheck candidate if s32 <= band
+};
+
+__host__ __device__ inline double budget_dmax_from_s32(const Budget& b, float best_s32) {
+  // real distance (float points) of the best-seen pair, then of the best
+  // source pair, widened so every pair the FP64 reference could prefer fits.
+  const double s = static_cast<double>(best_s32);
+  const double df = sqrt((s + b.a) / (1.0 - b.e)) * (1.0 + 1e-12);
+  return (df + 2.0 * b.Rn) * (1.0 + 4.0 * b.gamma64) + 2.0 * b.Rn;
+}
+
+__host__ __device__ inline Thresholds budget_thresholds(const Budget& b, double dmax) {
+  const double u = 0x1.0p-24;
+  Thresholds t;
+  if (!(dmax < 1e300)) {  // +inf: everything passes
+    t.win = t.lb2 = t.band = INFINITY;
+    return t;
+  }
+  const double w = (dmax * b.unorm + 2.0 * b.E) * (1.0 + 4.0 * u);
+  const double lb = (dmax * b.sigma + 2.0 * b.E * sqrt(static_cast<double>(b.nk))) * (1.0 + 4.0 * u);
+  const double lb2 = lb * lb * (1.0 + (2.0 * b.nk + 8.0) * u);
+  const double band = (dmax * dmax * (1.0 + b.e) + b.a) * (1.0 + 4.0 * u);
+  // round up to float
+  t.win = static_cast<float>(w * (1.0 + 2.0 * u));
+  t.lb2 = static_cast<float>(lb2 * (1.0 + 2.0 * u));
+  t.band = static_cast<float>(band * (1.0 + 2.0 * u));
+  return t;
+}
+
+__host__ __device__ inline Thresholds budget_thresholds_s32(const Budget& b, float best_s32) {
+  if (!(best_s32 < INFINITY)) return budget_thresholds(b, INFINITY);
+  return budget_thresholds(b, budget_dmax_from_s32(b, best_s32));
+}
+
+// ---------------------------------------------------------------------------
+// The algebra shared by the closest-pair and fixed-radius engines.
+constexpr int kMaxKeys = 8;
+
+// Host-built orthonormal projection directions (random, seeded), in FP32.
+struct Directions {
+  int d = 0, q = 0, nk = 0;   // q used rows, nk = padded rows (power of 2)
+  std::vector<float> U;       // nk x d, rows >= q are zero
+  double sigma = 1.0, unorm = 1.0;
+};
+Directions make_directions(uint64_t seed, int d, int q);
+
+// Closed-form admissible pair count (main.cpp:388-395).
+inline uint64_t admissible_pairs(uint64_t n, uint64_t zone) {
+  if (zone <= 1) return n * (n - 1) / 2;
+  if (zone >= n) return 0;
+  const uint64_t m = n - zone;
+  return m * (m + 1) / 2;
+}
+
+}  // namespace psg

@@ -1,0 +1,397 @@
+// psg_points.cu — device context, point-set construction (validation,
+// narrowing to the FP32 working copy, z-normalised windows), and the seeded
+// projection directions.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <memory>
+
+#include "host_rng.hpp"
+#include "psg_points.cuh"
+
+namespace psg {
+
+thread_local uint64_t g_launches = 0;
+
+Ctx& ctx() {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Ctx>> all;
+  int dev = 0;
+  PSG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  auto& c = all[dev];
+  if (!c) {
+    auto nc = std::make_unique<Ctx>();
+    nc->device = dev;
+    cudaDeviceProp prop;
+    PSG_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+      throw cuda_error("pairscan_b200 is built for sm_100a; device " + std::to_string(dev) + " is sm_" +
+                       std::to_string(prop.major) + std::to_string(prop.minor));
+    nc->sm_count = prop.multiProcessorCount;
+    PSG_CUDA(cudaStreamCreateWithFlags(&nc->stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    PSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;  // keep freed blocks: repeated solves reuse them
+    PSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    c = std::move(nc);
+  }
+  return *c;
+}
+
+namespace {
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, double v) {
+  atomicMax(a, static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// Validation of float rows: finiteness (series.cpp:20-24) and max |x|.
+__global__ void k_check_f32(const float* __restrict__ x, uint64_t count, unsigned* __restrict__ bad,
+                            unsigned* __restrict__ maxabs_bits) {
+  unsigned m = 0, nonfinite = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    if (!isfinite(v)) nonfinite = 1;
+    m = max(m, __float_as_uint(fabsf(v)));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+  if ((threadIdx.x & 31) == 0) {
+    if (nonfinite) atomicOr(bad, 1u);
+    atomicMax(maxabs_bits, m);
+  }
+}
+
+__global__ void k_check_f64(const double* __restrict__ x, uint64_t count, unsigned* __restrict__ bad,
+                            unsigned long long* __restrict__ maxabs_bits) {
+  unsigned long long m = 0;
+  unsigned nonfinite = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double v = x[i];
+    if (!isfinite(v)) nonfinite = 1;
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(fabs(v)));
+    m = b > m ? b : m;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+  }
+  nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+  if ((threadIdx.x & 31) == 0) {
+    if (nonfinite) atomicOr(bad, 1u);
+    atomicMax(maxabs_bits, m);
+  }
+}
+
+// Rows (f32 or f64 source) -> scaled FP32 rows; per-row narrowing radius
+// ||scale*x - fl(scale*x)|| accumulated in FP64 and max-reduced.
+template <class T>
+__global__ void k_narrow_rows(const T* __restrict__ src, uint64_t n, int d, double scale, float* __restrict__ X,
+                              unsigned long long* __restrict__ r2max_bits) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  double worst = 0.0;
+  for (uint64_t r = warp; r < n; r += nwarps) {
+    double acc = 0.0;
+    for (int t = lane; t < d; t += 32) {
+      const double v = scale * static_cast<double>(src[r * d + t]);
+      const float f = static_cast<float>(v);
+      X[r * d + t] = f;
+      const double e = v - static_cast<double>(f);
+      acc += e * e;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    worst = fmax(worst, acc);
+  }
+  if (lane == 0) atomic_max_nonneg(r2max_bits, worst);
+}
+
+// Per-window FP64 statistics, two-pass and sequential like the oracle.
+__global__ void k_window_stats(const double* __restrict__ s, uint64_t nw, int len, double* __restrict__ mu,
+                               double* __restrict__ sigma) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nw) return;
+  const double* w = s + i;
+  double acc = 0.0;
+  for (int t = 0; t < len; ++t) acc = __dadd_rn(acc, w[t]);
+  const double m = __ddiv_rn(acc, static_cast<double>(len));
+  double v = 0.0;
+  for (int t = 0; t < len; ++t) {
+    const double c = __dsub_rn(w[t], m);
+    v = __dadd_rn(v, __dmul_rn(c, c));
+  }
+  mu[i] = m;
+  sigma[i] = __dsqrt_rn(__ddiv_rn(v, static_cast<double>(len)));
+}
+
+// Window rows (raw or z-normalised) -> scaled FP32 rows + narrowing radius.
+__global__ void k_narrow_windows(const double* __restrict__ s, uint64_t nw, int len, const double* __restrict__ mu,
+                                 const double* __restrict__ sigma, double scale, float* __restrict__ X,
+                                 unsigned long long* __restrict__ r2max_bits) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  double worst = 0.0;
+  for (uint64_t r = warp; r < nw; r += nwarps) {
+    double m = 0.0, sg = 1.0;
+    const bool z = mu != nullptr;
+    if (z) {
+      m = mu[r];
+      sg = sigma[r];
+    }
+    double acc = 0.0;
+    for (int t = lane; t < len; t += 32) {
+      double v = s[r + t];
+      if (z) v = sg == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(v, m), sg);
+      v *= scale;
+      const float f = static_cast<float>(v);
+      X[r * len + t] = f;
+      const double e = v - static_cast<double>(f);
+      acc += e * e;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    worst = fmax(worst, acc);
+  }
+  if (lane == 0) atomic_max_nonneg(r2max_bits, worst);
+}
+
+__global__ void k_widen(const float* __restrict__ in, uint64_t count, double* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+
+int grid_for(uint64_t work, int per_block, int sms) {
+  const uint64_t want = (work + per_block - 1) / per_block;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+  return static_cast<int>(want < cap ? (want ? want : 1) : cap);
+}
+
+// Power-of-two scale that keeps FP32 squares far from overflow/underflow.
+double choose_scale(double maxabs) {
+  if (maxabs == 0.0 || (maxabs < 0x1.0p60 && maxabs > 0x1.0p-60)) return 1.0;
+  int e = 0;
+  std::frexp(maxabs, &e);
+  return std::ldexp(1.0, 8 - e);
+}
+
+template <class T>
+void upload(DevBuf<T>& dst, const T* src, uint64_t count, bool dev_src, cudaStream_t s, uint64_t* h2d) {
+  dst.alloc(count, s);
+  if (!count) return;
+  PSG_CUDA(cudaMemcpyAsync(dst.p, src, count * sizeof(T), dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  if (!dev_src) *h2d += count * sizeof(T);
+}
+
+double read_r2(unsigned long long* dbits, cudaStream_t s) {
+  unsigned long long h = 0;
+  PSG_CUDA(cudaMemcpyAsync(&h, dbits, 8, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  double r2;
+  std::memcpy(&r2, &h, 8);
+  return r2;
+}
+
+// sqrt of an FP64-accumulated sum of squares, widened to a safe upper bound.
+double radius_bound(double r2, int d) {
+  if (r2 <= 0.0) return 0.0;
+  return std::sqrt(r2 * (1.0 + 4.0 * d * 0x1.0p-53)) * (1.0 + 1e-12);
+}
+
+}  // namespace
+
+psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev_src) {
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  auto ps = std::make_unique<psg_pointset>();
+  ps->n = n;
+  ps->d = static_cast<int>(d);
+  ps->kind = kRowsF32;
+  ps->device = c.device;
+  upload(ps->src32, p, n * d, dev_src, s, &ps->h2d_bytes);
+  DevBuf<unsigned> flags(2, s);
+  PSG_CUDA(cudaMemsetAsync(flags.p, 0, 8, s));
+  if (n * d) {
+    k_check_f32<<<grid_for(n * d, 256 * 8, c.sm_count), 256, 0, s>>>(ps->src32.p, n * d, flags.p, flags.p + 1);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
+  unsigned h[2];
+  PSG_CUDA(cudaMemcpyAsync(h, flags.p, 8, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  if (h[0]) throw invalid_argument("point coordinate must be finite");
+  float mx;
+  std::memcpy(&mx, &h[1], 4);
+  ps->scale = choose_scale(mx);
+  ps->X = ps->src32.p;
+  if (ps->scale != 1.0) {
+    ps->work.alloc(n * d, s);
+    DevBuf<unsigned long long> r2(1, s);
+    PSG_CUDA(cudaMemsetAsync(r2.p, 0, 8, s));
+    k_narrow_rows<float><<<grid_for(n * 32, 256, c.sm_count), 256, 0, s>>>(ps->src32.p, n, ps->d, ps->scale,
+                                                                           ps->work.p, r2.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+    ps->Rn = radius_bound(read_r2(r2.p, s), ps->d);
+    ps->X = ps->work.p;
+  }
+  ps->maxabs = static_cast<double>(mx) * ps->scale;
+  return ps.release();
+}
+
+psg_pointset* pointset_rows_f64(const double* p, uint64_t n, uint64_t d, bool dev_src) {
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  auto ps = std::make_unique<psg_pointset>();
+  ps->n = n;
+  ps->d = static_cast<int>(d);
+  ps->kind = kRowsF64;
+  ps->device = c.device;
+  upload(ps->src64, p, n * d, dev_src, s, &ps->h2d_bytes);
+  DevBuf<unsigned> bad(1, s);
+  DevBuf<unsigned long long> mx(2, s);
+  PSG_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  PSG_CUDA(cudaMemsetAsync(mx.p, 0, 16, s));
+  if (n * d) {
+    k_check_f64<<<grid_for(n * d, 256 * 8, c.sm_count), 256, 0, s>>>(ps->src64.p, n * d, bad.p, mx.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
+  unsigned hb = 0;
+  unsigned long long hm = 0;
+  PSG_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaMemcpyAsync(&hm, mx.p, 8, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  if (hb) throw invalid_argument("point coordinate must be finite");
+  double maxabs;
+  std::memcpy(&maxabs, &hm, 8);
+  ps->scale = choose_scale(maxabs);
+  ps->work.alloc(n * d, s);
+  if (n * d) {
+    k_narrow_rows<double><<<grid_for(n * 32, 256, c.sm_count), 256, 0, s>>>(ps->src64.p, n, ps->d, ps->scale,
+                                                                            ps->work.p, mx.p + 1);
+    PSG_LAUNCHED();
+    ++g_launches;
+    ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d);
+  }
+  ps->X = ps->work.p;
+  ps->maxabs = maxabs * ps->scale;
+  return ps.release();
+}
+
+psg_pointset* pointset_windows(const double* series64, const float* series32, uint64_t length, uint64_t len,
+                               bool znorm, bool dev_src) {
+  // TimeSeries::window_count (series.cpp:8-11)
+  if (len == 0 || len > length) throw invalid_argument("window length out of range");
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  auto ps = std::make_unique<psg_pointset>();
+  const uint64_t nw = length - len + 1;
+  ps->n = nw;
+  ps->d = static_cast<int>(len);
+  ps->kind = znorm ? kWindowsZ : kWindowsRaw;
+  ps->device = c.device;
+  if (series64) {
+    upload(ps->src64, series64, length, dev_src, s, &ps->h2d_bytes);
+  } else {
+    DevBuf<float> tmp;
+    upload(tmp, series32, length, dev_src, s, &ps->h2d_bytes);
+    ps->src64.alloc(length, s);
+    k_widen<<<grid_for(length, 256 * 4, c.sm_count), 256, 0, s>>>(tmp.p, length, ps->src64.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
+  DevBuf<unsigned> bad(1, s);
+  DevBuf<unsigned long long> mx(2, s);
+  PSG_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  PSG_CUDA(cudaMemsetAsync(mx.p, 0, 16, s));
+  k_check_f64<<<grid_for(length, 256 * 8, c.sm_count), 256, 0, s>>>(ps->src64.p, length, bad.p, mx.p);
+  PSG_LAUNCHED();
+  ++g_launches;
+  unsigned hb = 0;
+  unsigned long long hm = 0;
+  PSG_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaMemcpyAsync(&hm, mx.p, 8, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  if (hb) throw invalid_argument("series value must be finite");
+  double maxabs;
+  std::memcpy(&maxabs, &hm, 8);
+  if (znorm) {
+    ps->mu.alloc(nw, s);
+    ps->sigma.alloc(nw, s);
+    k_window_stats<<<static_cast<int>((nw + 255) / 256), 256, 0, s>>>(ps->src64.p, nw, ps->d, ps->mu.p, ps->sigma.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+    ps->scale = 1.0;  // |z| <= sqrt(len)
+    maxabs = std::sqrt(static_cast<double>(len));
+  } else {
+    ps->scale = choose_scale(maxabs);
+  }
+  ps->work.alloc(nw * len, s);
+  k_narrow_windows<<<grid_for(nw * 32, 256, c.sm_count), 256, 0, s>>>(ps->src64.p, nw, ps->d, ps->mu.p, ps->sigma.p,
+                                                                       ps->scale, ps->work.p, mx.p + 1);
+  PSG_LAUNCHED();
+  ++g_launches;
+  ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d);
+  ps->X = ps->work.p;
+  ps->maxabs = maxabs * ps->scale;
+  return ps.release();
+}
+
+// ---------------------------------------------------------------------------
+// Seeded orthonormal projection directions.  These replace the reference's
+// scaled reference points (refscan.cpp:30-56): a key is <u_k, x> instead of
+// ||f*x_r - x||, the f -> infinity limit of the same 1-Lipschitz bound
+// (test_refscan.cpp:85-99).  Rows are drawn from the
+// reference Rng stream derive_seed(seed, 0x5eed), orthonormalised in FP64
+// (modified Gram-Schmidt), then rounded to FP32; the spectral norm of the
+// rounded matrix is bounded (Gershgorin on U U^T) for the LB filter.
+Directions make_directions(uint64_t seed, int d, int q) {
+  Directions dir;
+  dir.d = d;
+  dir.q = std::max(1, std::min(std::min(q, d), kMaxKeys));
+  dir.nk = dir.q <= 4 ? 4 : 8;
+  std::vector<double> V(static_cast<size_t>(dir.q) * d);
+  HostRng rng(stream_seed(seed, 0x5eed));
+  for (int k = 0; k < dir.q; ++k) {
+    for (;;) {
+      double* v = &V[static_cast<size_t>(k) * d];
+      for (int t = 0; t < d; ++t) v[t] = rng.gauss(0.0, 1.0);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int l = 0; l < k; ++l) {
+          const double* w = &V[static_cast<size_t>(l) * d];
+          double dot = 0.0;
+          for (int t = 0; t < d; ++t) dot += v[t] * w[t];
+          for (int t = 0; t < d; ++t) v[t] -= dot * w[t];
+        }
+      double nrm = 0.0;
+      for (int t = 0; t < d; ++t) nrm += v[t] * v[t];
+      nrm = std::sqrt(nrm);
+      if (nrm < 1e-6) continue;  // degenerate draw: redraw
+      for (int t = 0; t < d; ++t) v[t] /= nrm;
+      break;
+    }
+  }
+  dir.U.assign(static_cast<size_t>(dir.nk) * d, 0.0f);
+  for (size_t i = 0; i < V.size(); ++i) dir.U[i] = static_cast<float>(V[i]);
+  double gmax = 0.0, unorm = 0.0;
+  for (int k = 0; k < dir.q; ++k) {
+    double row = 0.0;
+    for (int l = 0; l < dir.q; ++l) {
+      double g = 0.0;
+      for (int t = 0; t < d; ++t)
+        g += static_cast<double>(dir.U[static_cast<size_t>(k) * d + t]) * dir.U[static_cast<size_t>(l) * d + t];
+      row += std::fabs(g);
+      if (k == l) unorm = std::max(unorm, std::sqrt(g));
+    }
+    gmax = std::max(gmax, row);
+  }
+  dir.sigma = std::sqrt(gmax) * (1.0 + 1e-9);
+  dir.unorm = unorm * (1.0 + 1e-9);
+  return dir;
+}
+
+}  // namespace psg

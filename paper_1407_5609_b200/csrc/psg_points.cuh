@@ -1,0 +1,89 @@
+// psg_points.cuh — the device-resident point set (series.hpp:28-44 PointSet)
+// and the reference's exact FP64 distance (metrics.cpp:16-24) on device.
+//
+// HBM layout:
+//   src   the caller's values, kept for the FP64 recheck: f32 rows (n x d),
+//         f64 rows (n x d), or an f64 series for window point sets
+//   X     FP32 working rows, n x d row-major, = fl(scale * src) (aliases src
+//         for exact float input); every FP32 filter reads only X
+//   mu/sigma  per-window FP64 statistics of z-normalised window sets
+#pragma once
+
+#include "psg_internal.cuh"
+
+namespace psg {
+
+enum SrcKind : int { kRowsF32 = 0, kRowsF64 = 1, kWindowsRaw = 2, kWindowsZ = 3 };
+
+// What the FP64 recheck reads.
+struct ExactSrc {
+  int kind = kRowsF32;
+  int d = 0;
+  const float* f32 = nullptr;    // kRowsF32
+  const double* f64 = nullptr;   // kRowsF64 rows, or the series for windows
+  const double* mu = nullptr;    // kWindowsZ
+  const double* sigma = nullptr; // kWindowsZ
+};
+
+// Coordinate t of point i exactly as the reference's PointSet would hold it.
+__device__ __forceinline__ double exact_coord(const ExactSrc& s, uint64_t i, int t) {
+  switch (s.kind) {
+    case kRowsF32: return static_cast<double>(s.f32[i * s.d + t]);
+    case kRowsF64: return s.f64[i * s.d + t];
+    case kWindowsRaw: return s.f64[i + t];
+    default: {
+      const double sg = s.sigma[i];
+      return sg == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(s.f64[i + t], s.mu[i]), sg);
+    }
+  }
+}
+
+// metrics.cpp:16-24: sum over t in index order of (x_t - y_t)^2, then sqrt;
+// explicit _rn intrinsics forbid FMA contraction, matching x86-64 SSE2.
+__device__ __forceinline__ double exact_distance(const ExactSrc& s, uint64_t i, uint64_t j) {
+  double acc = 0.0;
+  for (int t = 0; t < s.d; ++t) {
+    const double diff = __dsub_rn(exact_coord(s, i, t), exact_coord(s, j, t));
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  return __dsqrt_rn(acc);
+}
+
+}  // namespace psg
+
+struct psg_pointset {
+  uint64_t n = 0;
+  int d = 0;
+  int kind = psg::kRowsF32;
+  int device = 0;
+  psg::DevBuf<float> src32;    // kRowsF32
+  psg::DevBuf<double> src64;   // kRowsF64 rows / window series
+  psg::DevBuf<double> mu, sigma;
+  psg::DevBuf<float> work;     // FP32 working copy when X != src32
+  const float* X = nullptr;
+  double scale = 1.0;          // X = fl(scale * src)
+  double Rn = 0.0;             // max narrowing radius, working units
+  double maxabs = 0.0;         // max |X|
+  uint64_t h2d_bytes = 0;
+
+  psg::ExactSrc exact() const {
+    psg::ExactSrc s;
+    s.kind = kind;
+    s.d = d;
+    s.f32 = src32.p;
+    s.f64 = src64.p;
+    s.mu = mu.p;
+    s.sigma = sigma.p;
+    return s;
+  }
+};
+
+namespace psg {
+// Builders (psg_points.cu).  `dev_src` = the pointer is device memory.
+psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev_src);
+psg_pointset* pointset_rows_f64(const double* p, uint64_t n, uint64_t d, bool dev_src);
+psg_pointset* pointset_windows(const double* series64, const float* series32, uint64_t length, uint64_t len,
+                               bool znorm, bool dev_src);
+// Launch accounting for the profile (incremented by every launch site).
+extern thread_local uint64_t g_launches;
+}  // namespace psg
