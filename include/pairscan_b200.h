@@ -81,6 +81,9 @@ typedef struct psg_profile {
   uint64_t h2d_bytes, d2h_bytes;
   double scan_kernel_ms;     /* device time of the candidate (window) kernel(s) */
   double project_kernel_ms;  /* device time of the projection kernel */
+  double bootstrap_kernel_ms;/* device time of the delta-bootstrap kernel(s) */
+  double total_ms;           /* device span of the whole call on the library stream */
+  uint64_t scan_launches;    /* launches of the candidate kernel */
 } psg_profile;
 
 const char* psg_last_error(void);
@@ -88,6 +91,12 @@ const char* psg_version(void);
 int psg_last_profile(psg_profile* out);
 /* Whether CUDA device `device` is usable (compute capability 10.x). */
 int psg_device_ok(int device);
+/* The library's cudaStream_t on the current device (for callers that want to
+ * bracket calls with their own CUDA events); NULL on failure. */
+void* psg_stream(void);
+/* Select the CUDA device for this thread's subsequent calls (one process per
+ * GPU: pass LOCAL_RANK). */
+int psg_set_device(int device);
 
 /* ---- one-shot entries (host buffers in, result out) --------------------- */
 int psg_closest_pair_f64(const double* points, uint64_t n, uint64_t dim, uint64_t q, double f,

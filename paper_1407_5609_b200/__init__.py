@@ -74,7 +74,8 @@ class _Profile(C.Structure):
     _fields_ = [("stages", _int), ("stage_name", (C.c_char * 24) * 16), ("stage_ms", _f32 * 16),
                 ("launches", _u64), ("window_pairs", _u64), ("lb_survivors", _u64),
                 ("candidates", _u64), ("bootstrap_width", _u64), ("h2d_bytes", _u64),
-                ("d2h_bytes", _u64), ("scan_kernel_ms", _f64), ("project_kernel_ms", _f64)]
+                ("d2h_bytes", _u64), ("scan_kernel_ms", _f64), ("project_kernel_ms", _f64),
+                ("bootstrap_kernel_ms", _f64), ("total_ms", _f64), ("scan_launches", _u64)]
 
 
 _SIGS = {
@@ -82,6 +83,8 @@ _SIGS = {
     "psg_version": (C.c_char_p, []),
     "psg_last_profile": (_int, [_p]),
     "psg_device_ok": (_int, [_int]),
+    "psg_stream": (_p, []),
+    "psg_set_device": (_int, [_int]),
     "psg_closest_pair_f64": (_int, [_p, _u64, _u64, _u64, _f64, _u64, _u64, _p]),
     "psg_closest_pair_f32": (_int, [_p, _u64, _u64, _u64, _f64, _u64, _u64, _p]),
     "psg_brute_force_closest_pair_f64": (_int, [_p, _u64, _u64, _u64, _p]),
@@ -166,6 +169,8 @@ def last_profile() -> dict:
         "launches": p.launches, "window_pairs": p.window_pairs, "lb_survivors": p.lb_survivors,
         "candidates": p.candidates, "bootstrap_width": p.bootstrap_width,
         "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
+        "scan_kernel_ms": p.scan_kernel_ms, "project_kernel_ms": p.project_kernel_ms,
+        "bootstrap_kernel_ms": p.bootstrap_kernel_ms, "total_ms": p.total_ms, "scan_launches": p.scan_launches,
     }
 
 

@@ -17,7 +17,9 @@ template <class F>
 int guarded(F&& f) {
   try {
     psg::prof_begin();
+    psg::KernelSpan span(psg::ctx().stream);  // device span of the whole call
     f();
+    psg::g_prof.total_ms = span.stop();
     psg::g_prof.launches = psg::g_launches;
     return PSG_OK;
   } catch (const psg::invalid_argument& e) {
@@ -71,6 +73,24 @@ int psg_last_profile(psg_profile* out) {
   if (!out) return PSG_ERR_INVALID;
   *out = psg::g_prof;
   return PSG_OK;
+}
+
+int psg_set_device(int device) {
+  const cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return PSG_ERR_CUDA;
+  }
+  return PSG_OK;
+}
+
+void* psg_stream(void) {
+  try {
+    return static_cast<void*>(psg::ctx().stream);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
 }
 
 int psg_device_ok(int device) {

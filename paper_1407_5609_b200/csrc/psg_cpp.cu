@@ -611,6 +611,7 @@ float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaSt
   const int sms = ctx().sm_count;
   const int warp_grid = std::min<int>(blocks_for(n, 8), sms * 16);
   bool done = true;
+  KernelSpan span(s);
 #define PSG_PROJ_WARP(NKV, VV) \
   k_project_warp<NKV, VV><<<warp_grid, 256, 0, s>>>(ps.X, n, U.p, keys, nb.p)
   if (d == 32 || d == 64 || d == 128 || d == 256) {
@@ -634,6 +635,7 @@ float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaSt
   }
   PSG_LAUNCHED();
   ++g_launches;
+  g_prof.project_kernel_ms += span.stop();
   const unsigned bits = read1(nb.p, s);
   float v;
   std::memcpy(&v, &bits, 4);
@@ -762,12 +764,14 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   uint32_t width = 1024;
   for (int round = 0; round < 4; ++round) {
     if (hi > lo) {
+      KernelSpan ks(s);
       if (plan.dir.nk == 4)
         k_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi, width);
       else
         k_bootstrap<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi, width);
       PSG_LAUNCHED();
       ++g_launches;
+      g_prof.bootstrap_kernel_ms += ks.stop();
     }
     const float b = read1(plan.best.p, s);
     const Thresholds th = budget_thresholds_s32(plan.bud, b);
@@ -821,16 +825,20 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
     a.ovf_cap = ovf_cap;
     a.evals = evals.p;
     if (hi > lo) {
+      KernelSpan ks(s);
       if (plan.dir.nk == 4)
         k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
       else
         k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
       PSG_LAUNCHED();
       ++g_launches;
+      g_prof.scan_kernel_ms += ks.stop();
+      ++g_prof.scan_launches;
     }
     unsigned h[2];
     PSG_CUDA(cudaMemcpyAsync(h, counters.p, 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
+    if (attempt > 12) throw std::runtime_error("closest_pair: candidate buffers kept overflowing");
     if (h[1] > ovf_cap) {  // queue spill list overflowed: rescan with the tighter bound
       ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h[1]) * 2, 1u << 28);
       continue;

@@ -102,6 +102,29 @@ struct StageTimer {
   }
 };
 
+// Device time of one kernel (or a short launch sequence) on a stream.
+struct KernelSpan {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s = nullptr;
+  explicit KernelSpan(cudaStream_t st) : s(st) {
+    PSG_CUDA(cudaEventCreate(&a));
+    PSG_CUDA(cudaEventCreate(&b));
+    PSG_CUDA(cudaEventRecord(a, s));
+  }
+  // Records the end event, waits for it, returns milliseconds.
+  double stop() {
+    PSG_CUDA(cudaEventRecord(b, s));
+    PSG_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    PSG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  ~KernelSpan() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Orderable integer images of floats (radix sort keys, atomic min/max).
 __host__ __device__ __forceinline__ uint32_t f32_order(float f) {
