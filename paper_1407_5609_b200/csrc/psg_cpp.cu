@@ -586,6 +586,14 @@ T read1(const T* dptr, cudaStream_t s) {
   return h;
 }
 
+// The running best lives on device as FP32 bits (atomicMin on unsigned).
+float read_best(const unsigned* dptr, cudaStream_t s) {
+  const unsigned bits = read1(dptr, s);
+  float v;
+  std::memcpy(&v, &bits, 4);
+  return v;
+}
+
 void part_range(uint64_t n, uint64_t part, uint64_t nparts, uint32_t* lo, uint32_t* hi) {
   *lo = static_cast<uint32_t>(n * part / nparts);
   *hi = static_cast<uint32_t>(n * (part + 1) / nparts);
@@ -773,7 +781,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
       ++g_launches;
       g_prof.bootstrap_kernel_ms += ks.stop();
     }
-    const float b = read1(plan.best.p, s);
+    const float b = read_best(plan.best.p, s);
     const Thresholds th = budget_thresholds_s32(plan.bud, b);
     const uint64_t est = window_pairs(plan, lo, hi, th.win, nullptr, s);
     if (est <= 8ull * (hi - lo) * width || width >= 16384) break;
@@ -784,7 +792,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   PSG_CUDA(cudaStreamSynchronize(s));
   prof_stages(tm);
   g_prof.bootstrap_width = width;
-  return read1(plan.best.p, s);
+  return read_best(plan.best.p, s);
 }
 
 psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, float bound_s32) {
@@ -795,7 +803,7 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
   part_range(n, part, nparts, &lo, &hi);
   StageTimer tm(s);
   {
-    const float cur = read1(plan.best.p, s);
+    const float cur = read_best(plan.best.p, s);
     const float b = std::min(cur, bound_s32);
     PSG_CUDA(cudaMemcpyAsync(plan.best.p, &b, 4, cudaMemcpyHostToDevice, s));
   }
@@ -838,7 +846,11 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
     unsigned h[2];
     PSG_CUDA(cudaMemcpyAsync(h, counters.p, 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    if (attempt > 12) throw std::runtime_error("closest_pair: candidate buffers kept overflowing");
+    if (attempt > 12)
+      throw std::runtime_error("closest_pair: candidate buffers kept overflowing (cand " + std::to_string(h[0]) +
+                               "/" + std::to_string(cand_cap) + ", spill " + std::to_string(h[1]) + "/" +
+                               std::to_string(ovf_cap) + ", best_s32 " + std::to_string(read_best(plan.best.p, s)) +
+                               ")");
     if (h[1] > ovf_cap) {  // queue spill list overflowed: rescan with the tighter bound
       ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h[1]) * 2, 1u << 28);
       continue;
@@ -859,7 +871,7 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
     break;
   }
   tm.mark("scan");
-  const float best_s32 = read1(plan.best.p, s);
+  const float best_s32 = read_best(plan.best.p, s);
   const Thresholds th = budget_thresholds_s32(plan.bud, best_s32);
   DevBuf<double> d64(std::max<unsigned>(ncand, 1), s);
   DevBuf<unsigned long long> red(3, s);
