@@ -50,6 +50,8 @@ constexpr int kThreads = 256;
 constexpr int kChunk = 256;
 constexpr int kQueue = 1024;
 constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
+constexpr double kGridOccupancy = 0.125;  // mean points per cell over the key box
+constexpr int kGridBootCap = 256;         // candidates per point in the grid bootstrap
 
 __device__ __forceinline__ bool admissible(uint32_t a, uint32_t b, uint64_t zone) {
   const uint32_t gap = a > b ? a - b : b - a;
@@ -169,41 +171,53 @@ __global__ void __launch_bounds__(256) k_project_warp(const float* __restrict__ 
     for (int v = 0; v < V; ++v) u[k][v] = __ldg(U + k * d + lane * V + v);
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  // R rows per iteration: all R row loads are issued before any math so each
+  // warp keeps R x 4V x 32 bytes in flight (Little's law at HBM latency).
+  constexpr int R = V >= 4 ? 4 : 8;
   float worst = 0.f;
-  for (uint32_t r = warp; r < n; r += nwarps) {
-    float x[V];
-    const float* row = X + static_cast<size_t>(r) * d + lane * V;
-    if constexpr (V % 4 == 0) {
+  for (uint32_t r0 = warp; r0 < n; r0 += R * nwarps) {
+    float x[R][V];
 #pragma unroll
-      for (int v = 0; v < V; v += 4) {
-        const float4 t = __ldcs(reinterpret_cast<const float4*>(row + v));
-        x[v] = t.x; x[v + 1] = t.y; x[v + 2] = t.z; x[v + 3] = t.w;
+    for (int q = 0; q < R; ++q) {
+      const uint32_t r = r0 + q * nwarps;
+      const float* row = X + static_cast<size_t>(r < n ? r : 0) * d + lane * V;
+      if constexpr (V % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < V; v += 4) {
+          const float4 t = __ldcs(reinterpret_cast<const float4*>(row + v));
+          x[q][v] = t.x; x[q][v + 1] = t.y; x[q][v + 2] = t.z; x[q][v + 3] = t.w;
+        }
+      } else if constexpr (V == 2) {
+        const float2 t = __ldcs(reinterpret_cast<const float2*>(row));
+        x[q][0] = t.x; x[q][1] = t.y;
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) x[q][v] = __ldcs(row + v);
       }
-    } else if constexpr (V == 2) {
-      const float2 t = __ldcs(reinterpret_cast<const float2*>(row));
-      x[0] = t.x; x[1] = t.y;
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) x[v] = __ldcs(row + v);
     }
-    float acc[NK];
-    float nn = 0.f;
 #pragma unroll
-    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
+    for (int q = 0; q < R; ++q) {
+      const uint32_t r = r0 + q * nwarps;
+      if (r >= n) break;  // warp-uniform
+      float acc[NK];
+      float nn = 0.f;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      nn = fmaf(x[v], x[v], nn);
+      for (int k = 0; k < NK; ++k) acc[k] = 0.f;
 #pragma unroll
-      for (int k = 0; k < NK; ++k) acc[k] = fmaf(u[k][v], x[v], acc[k]);
+      for (int v = 0; v < V; ++v) {
+        nn = fmaf(x[q][v], x[q][v], nn);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) acc[k] = fmaf(u[k][v], x[q][v], acc[k]);
+      }
+      Transpose<NK, 16, NK>::run(acc, lane);
+      float key = acc[0];
+#pragma unroll
+      for (int o = 16 >> L; o; o >>= 1) key += __shfl_xor_sync(kFull, key, o);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) nn += __shfl_xor_sync(kFull, nn, o);
+      worst = fmaxf(worst, nn);
+      if ((lane & ((1 << (5 - L)) - 1)) == 0) keys[static_cast<size_t>(r) * NK + (lane >> (5 - L))] = key;
     }
-    Transpose<NK, 16, NK>::run(acc, lane);
-    float key = acc[0];
-#pragma unroll
-    for (int o = 16 >> L; o; o >>= 1) key += __shfl_xor_sync(kFull, key, o);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) nn += __shfl_xor_sync(kFull, nn, o);
-    worst = fmaxf(worst, nn);
-    if ((lane & ((1 << (5 - L)) - 1)) == 0) keys[static_cast<size_t>(r) * NK + (lane >> (5 - L))] = key;
   }
   if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
 }
@@ -282,6 +296,7 @@ struct ScanArgs {
   unsigned* ovf_n;
   uint32_t ovf_cap;
   unsigned long long* evals;
+  unsigned long long* visited;  // grid engine: admissible stencil pairs
 };
 
 __device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {
@@ -493,12 +508,187 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
   if (tid == 0 && nevals) atomicAdd(a.evals, nevals);
 }
 
+// ---------------------------------------------------------------------------
+// Grid engine (psg_grid.cuh): candidates of sorted position p are the later
+// positions of its own cell and every position of the forward half of the
+// 3^g cell stencil, so each unordered pair is visited exactly once.
+
+// Warp argmin of (lb, p) and one exact FP32 evaluation of the winner.
+__device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint32_t j, uint32_t p, int lane) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float olb = __shfl_xor_sync(kFull, lb, o);
+    const uint32_t oj = __shfl_xor_sync(kFull, j, o);
+    const uint32_t op = __shfl_xor_sync(kFull, p, o);
+    if (olb < lb || (olb == lb && op < p)) {
+      lb = olb;
+      j = oj;
+      p = op;
+    }
+  }
+  if (j == 0xffffffffu) return;
+  const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+  if (!(lb <= th.lb2)) return;
+  const float* xi = a.X + static_cast<size_t>(a.sidx[p]) * a.d;
+  const float* xj = a.X + static_cast<size_t>(a.sidx[j]) * a.d;
+  const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f) : warp_sqdist(xi, xj, a.d, lane);
+  if (lane == 0) atomicMin(a.best, __float_as_uint(s));
+}
+
+// K3a (grid): per position, the stencil candidate with the least key lower
+// bound (at most `cap` candidates looked at); each warp evaluates its best.
+template <int NK>
+__global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi,
+                                                             int cap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t p = lo + blockIdx.x * kThreads + threadIdx.x;
+  float best_lb = INFINITY;
+  uint32_t best_j = 0xffffffffu;
+  if (p < hi) {
+    float mk[NK];
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+    const uint32_t mo = a.sidx[p];
+    uint32_t rb[5], re[5];
+    const int nr = grid_ranges(G, p, G.scell[p], rb, re);
+    int seen = 0;
+    for (int r = 0; r < nr && seen < cap; ++r) {
+      for (uint32_t j = rb[r]; j < re[r] && seen < cap; ++j, ++seen) {
+        float kj[NK];
+        load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
+        float g = kj[0] - mk[0];
+        float sl = g * g;
+        g = kj[1] - mk[1];
+        sl = fmaf(g, g, sl);
+        if (sl >= best_lb) continue;
+#pragma unroll
+        for (int k = 2; k < NK; ++k) {
+          g = kj[k] - mk[k];
+          sl = fmaf(g, g, sl);
+        }
+        if (sl < best_lb && (a.zone <= 1 || admissible(mo, a.sidx[j], a.zone))) {
+          best_lb = sl;
+          best_j = j;
+        }
+      }
+    }
+  }
+  warp_eval_best(a, best_lb, best_j, p, lane);
+}
+
+// K3b (grid): every stencil candidate whose key lower bound is within the
+// current delta goes to the shared-memory queue; warps evaluate the queue as
+// exact FP32 distances; delta tightens as the atomic minimum falls.  Threads
+// keep a resumable cursor (stencil cell, position) and work in rounds of at
+// most kBudget candidates so the block can flush in lock step.
+constexpr int kBudget = 64;
+
+template <int NK>
+__global__ void __launch_bounds__(kThreads) k_grid_scan(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi) {
+  __shared__ uint32_t qp[kQueue], qj[kQueue];
+  __shared__ int qn;
+  __shared__ Thresholds th;
+  __shared__ unsigned long long nevals;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t p = lo + blockIdx.x * kThreads + tid;
+  bool active = p < hi;
+  float mk[NK];
+  uint32_t mo = 0, j = 0, rb[5], re[5];
+  int nr = 0, r = 0;
+  if (active) {
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+    mo = a.sidx[p];
+    nr = grid_ranges(G, p, G.scell[p], rb, re);
+    j = rb[0];
+  } else {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) mk[k] = 0.f;
+  }
+  unsigned long long visited = 0;
+  if (tid == 0) {
+    qn = 0;
+    nevals = 0;
+    th = budget_thresholds_s32(a.bud, best_now(a.best));
+  }
+  __syncthreads();
+  for (;;) {
+    const float lb2 = th.lb2;
+    int budget = kBudget;
+    while (active && budget > 0) {
+      if (j >= re[r]) {
+        if (++r >= nr) {
+          active = false;
+          break;
+        }
+        j = rb[r];
+        continue;
+      }
+      if (a.zone > 1 && !admissible(mo, a.sidx[j], a.zone)) {
+        ++j;
+        continue;
+      }
+      --budget;
+      float kj[NK];
+      load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
+      float g = kj[0] - mk[0];
+      float sl = g * g;
+      g = kj[1] - mk[1];
+      sl = fmaf(g, g, sl);
+      if (sl <= lb2) {
+#pragma unroll
+        for (int k = 2; k < NK; ++k) {
+          g = kj[k] - mk[k];
+          sl = fmaf(g, g, sl);
+        }
+        if (sl <= lb2) {
+          const int slot = atomicAdd(&qn, 1);
+          if (slot >= kQueue) break;  // queue full: retry this j next round
+          qp[slot] = p;
+          qj[slot] = j;
+        }
+      }
+      ++visited;
+      ++j;
+    }
+    __syncthreads();
+    const int nq = min(qn, kQueue);
+    if (nq > 0) {
+      const float band = th.band;
+      if (a.d <= kInlineD) {
+        for (int i = tid; i < nq; i += kThreads) {
+          const uint32_t pi = qp[i], pj = qj[i];
+          const float sd = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                         a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
+          record(a, pi, pj, sd, band);
+        }
+      } else {
+        for (int i = warp; i < nq; i += kThreads / 32) {
+          const uint32_t pi = qp[i], pj = qj[i];
+          const float sd = warp_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                       a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d, lane);
+          if (lane == 0) record(a, pi, pj, sd, band);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      nevals += static_cast<unsigned long long>(nq);
+      qn = 0;
+      th = budget_thresholds_s32(a.bud, best_now(a.best));
+    }
+    if (!__syncthreads_or(active)) break;
+  }
+  for (int o = 16; o; o >>= 1) visited += __shfl_xor_sync(kFull, visited, o);
+  if (lane == 0 && visited) atomicAdd(a.visited, visited);
+  if (tid == 0 && nevals) atomicAdd(a.evals, nevals);
+}
+
 // Pairs that overflowed the shared-memory queue.
-__global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const uint32_t* __restrict__ lj,
-                            uint32_t count) {
+// The count is read on device (min(spill count, capacity)): no host round trip.
+__global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const uint32_t* __restrict__ lj) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t count = min(*a.ovf_n, a.ovf_cap);
   for (uint32_t i = warp; i < count; i += nwarps) {
     const uint32_t pi = lp[i], pj = lj[i];
     const float* xi = a.X + static_cast<size_t>(a.sidx[pi]) * a.d;
@@ -513,17 +703,23 @@ __global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const u
 }
 
 // K6: deterministic final filter + FP64 recheck in the reference's order.
-template <int NK>
-__global__ void k_recheck(ScanArgs a, ExactSrc src, Thresholds th, uint32_t count, double* __restrict__ d64,
-                          unsigned long long* __restrict__ best64, unsigned long long* __restrict__ examined) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+// Thresholds come from the final FP32 bound on device; the candidate count is
+// min(candidates, capacity) read on device; grid-stride over candidates.
+template <int NK, bool kWindow>
+__global__ void k_recheck(ScanArgs a, ExactSrc src, double* __restrict__ d64, unsigned long long* __restrict__ best64,
+                          unsigned long long* __restrict__ examined) {
+  const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+  const uint32_t count = min(*a.cand_n, a.cand_cap);
+  for (uint32_t base = blockIdx.x * blockDim.x; base < count; base += gridDim.x * blockDim.x) {
+  const uint32_t c = base + threadIdx.x;
   unsigned pass = 0;
   if (c < count) {
     const uint32_t p = a.cand_p[c], j = a.cand_j[c];
     float kp[NK], kj[NK];
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, kp);
     load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
-    const bool keep = (kj[0] - kp[0] <= th.win) && (lb2_full<NK>(kp, kj) <= th.lb2) && (a.cand_s[c] <= th.band);
+    const bool keep = (!kWindow || kj[0] - kp[0] <= th.win) && (lb2_full<NK>(kp, kj) <= th.lb2) &&
+                      (a.cand_s[c] <= th.band);
     double dd = -1.0;
     if (keep) {
       dd = exact_distance(src, a.sidx[p], a.sidx[j]);
@@ -534,17 +730,24 @@ __global__ void k_recheck(ScanArgs a, ExactSrc src, Thresholds th, uint32_t coun
   }
   const unsigned wsum = __reduce_add_sync(kFull, pass);
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(examined, static_cast<unsigned long long>(wsum));
+  }
 }
 
-__global__ void k_pick(const ScanArgs a, uint32_t count, const double* __restrict__ d64,
-                       const unsigned long long* __restrict__ best64, unsigned long long* __restrict__ lex) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= count) return;
-  if (static_cast<unsigned long long>(__double_as_longlong(d64[c])) != *best64 || d64[c] < 0.0) return;
-  const uint32_t i = a.sidx[a.cand_p[c]], j = a.sidx[a.cand_j[c]];
-  const unsigned long long key = i < j ? (static_cast<unsigned long long>(i) << 32) | j
-                                       : (static_cast<unsigned long long>(j) << 32) | i;
-  atomicMin(lex, key);
+__global__ void k_pick(const ScanArgs a, const double* __restrict__ d64, const unsigned long long* __restrict__ best64,
+                       unsigned long long* __restrict__ lex) {
+  const uint32_t count = min(*a.cand_n, a.cand_cap);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
+    if (static_cast<unsigned long long>(__double_as_longlong(d64[c])) != *best64 || d64[c] < 0.0) continue;
+    const uint32_t i = a.sidx[a.cand_p[c]], j = a.sidx[a.cand_j[c]];
+    const unsigned long long key = i < j ? (static_cast<unsigned long long>(i) << 32) | j
+                                         : (static_cast<unsigned long long>(j) << 32) | i;
+    atomicMin(lex, key);
+  }
+}
+
+// Lower the device bound to min(current, bound) (multi-rank global bound).
+__global__ void k_min_bound(unsigned* best, float bound) {
+  if (bound >= 0.f) atomicMin(best, __float_as_uint(bound));
 }
 
 // Window statistics at the final delta: pairs with fl(k0_j - k0_p) <= win,
@@ -681,10 +884,31 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   plan->dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
   const int nk = plan->dir.nk;
   StageTimer tm(s);
+  trace("plan: directions");
   DevBuf<float> keys(n * nk, s);
   const float norm2 = project(*ps, plan->dir, keys.p, s);
+  trace("plan: project (sync)");
   tm.mark("project");
   plan->bud = make_budget(*ps, plan->dir, norm2);
+  const char* eng = std::getenv("PSG_ENGINE");
+  plan->grid = plan->dir.q >= 2 && !(eng && std::string(eng) == "window");
+  if (plan->grid) {
+    // K2 (grid): cells over the first g keys at the occupancy width, sorted
+    plan->g = std::min(3, plan->dir.q);
+    grid_sample_box(keys.p, static_cast<uint32_t>(n), nk, plan->g, plan->box_lo, plan->box_span, s);
+    const double w = grid_occupancy_width(static_cast<uint32_t>(n), plan->g, plan->box_span, kGridOccupancy);
+    build_grid(keys.p, static_cast<uint32_t>(n), nk, plan->g, w, plan->box_lo, plan->box_span, plan->gi, s);
+    plan->keys = std::move(keys);
+    tm.mark("grid");
+    trace("plan: grid built");
+    plan->best.alloc(1, s);
+    const float inf = INFINITY;
+    PSG_CUDA(cudaMemcpyAsync(plan->best.p, &inf, 4, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    trace("plan: grid synced");
+    prof_stages(tm);
+    return plan.release();
+  }
   // K2: sort by key 0 (stable, index payload)
   DevBuf<uint32_t> kb0(n, s), kb1(n, s), vb0(n, s), vb1(n, s);
   DevBuf<uint32_t> hist(radix_hist_words(n), s);
@@ -723,8 +947,8 @@ namespace {
 ScanArgs make_args(CppPlan& plan) {
   ScanArgs a{};
   a.X = plan.ps->X;
-  a.skeys = plan.skeys.p;
-  a.sidx = plan.sidx.p;
+  a.skeys = plan.grid ? plan.gi.skeys.p : plan.skeys.p;
+  a.sidx = plan.grid ? plan.gi.sidx.p : plan.sidx.p;
   a.n = static_cast<uint32_t>(plan.ps->n);
   a.d = plan.ps->d;
   a.zone = plan.zone;
@@ -767,6 +991,24 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
     PSG_LAUNCHED();
     ++g_launches;
   }
+  if (plan.grid) {
+    KernelSpan ks(s);
+    if (hi > lo) {
+      if (plan.dir.nk == 4)
+        k_grid_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi, kGridBootCap);
+      else
+        k_grid_bootstrap<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi, kGridBootCap);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    ks.end();
+    tm.mark("bootstrap");
+    const float b = read_best(plan.best.p, s);  // synchronises the stream
+    trace("bootstrap: done");
+    g_prof.bootstrap_kernel_ms += ks.ms();
+    prof_stages(tm);
+    return b;
+  }
   // Adaptive width: widen while the window the bound implies is far more
   // work than the bootstrap that produced it.
   uint32_t width = 1024;
@@ -803,18 +1045,39 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
   part_range(n, part, nparts, &lo, &hi);
   StageTimer tm(s);
   {
-    const float cur = read_best(plan.best.p, s);
-    const float b = std::min(cur, bound_s32);
-    PSG_CUDA(cudaMemcpyAsync(plan.best.p, &b, 4, cudaMemcpyHostToDevice, s));
+    // the bound handed in is the (global) minimum of what bootstrap returned,
+    // hence <= this rank's device bound: lower the device copy to it.
+    const float b = bound_s32;
+    k_min_bound<<<1, 1, 0, s>>>(plan.best.p, b);
+    PSG_LAUNCHED();
+    ++g_launches;
+    if (plan.grid) {
+      // The grid must hold every pair whose key gaps are within the window of
+      // the (global) bound: widen the cells when the occupancy width is
+      // smaller.  Every rank derives the same grid from the same bound.
+      const Thresholds th0 = budget_thresholds_s32(plan.bud, b);
+      const double need = static_cast<double>(th0.win) * (1.0 + 1e-5);
+      if (!(plan.gi.w >= need)) {
+        if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
+        build_grid(plan.keys.p, static_cast<uint32_t>(n), plan.dir.nk, plan.g, need, plan.box_lo, plan.box_span,
+                   plan.gi, s);
+        tm.mark("regrid");
+      }
+    }
   }
   uint32_t cand_cap = 1u << 16, ovf_cap = 1u << 20;
   DevBuf<uint32_t> cp, cj, op, oj;
   DevBuf<float> cs;
   DevBuf<unsigned> counters(2, s);
   DevBuf<unsigned long long> evals(1, s);
-  PSG_CUDA(cudaMemsetAsync(evals.p, 0, 8, s));
   ScanArgs a = make_args(plan);
   unsigned ncand = 0;
+  // result block read back once: [0] best64 bits, [1] lex pair, [2] examined,
+  // [3] evals, [4] visited, [5] cand count | spill count << 32
+  DevBuf<unsigned long long> red(6, s);
+  DevBuf<double> d64;
+  unsigned long long hr[6];
+  KernelSpan* scan_span = nullptr;
   for (int attempt = 0;; ++attempt) {
     cp.alloc(cand_cap, s);
     cj.alloc(cand_cap, s);
@@ -831,18 +1094,50 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
     a.ovf_j = oj.p;
     a.ovf_n = counters.p + 1;
     a.ovf_cap = ovf_cap;
-    a.evals = evals.p;
+    a.evals = red.p + 3;
+    a.visited = red.p + 4;
+    const unsigned long long init[6] = {~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull};
+    PSG_CUDA(cudaMemcpyAsync(red.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    d64.alloc(cand_cap, s);
+    delete scan_span;
+    scan_span = new KernelSpan(s);
     if (hi > lo) {
-      KernelSpan ks(s);
-      if (plan.dir.nk == 4)
+      if (plan.grid) {
+        if (plan.dir.nk == 4)
+          k_grid_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi);
+        else
+          k_grid_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi);
+      } else if (plan.dir.nk == 4)
         k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
       else
         k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
       PSG_LAUNCHED();
       ++g_launches;
-      g_prof.scan_kernel_ms += ks.stop();
       ++g_prof.scan_launches;
     }
+    scan_span->end();
+    if (!plan.grid) {  // spill list of the window engine (grid threads retry instead)
+      k_eval_list<<<c.sm_count * 8, 256, 0, s>>>(a, op.p, oj.p);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    // speculative recheck: correct whenever nothing overflowed (checked below)
+    const ExactSrc ex = plan.ps->exact();
+    const int nb = c.sm_count * 2;
+    if (plan.grid) {
+      if (plan.dir.nk == 4)
+        k_recheck<4, false><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+      else
+        k_recheck<8, false><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+    } else if (plan.dir.nk == 4)
+      k_recheck<4, true><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+    else
+      k_recheck<8, true><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+    PSG_LAUNCHED();
+    k_pick<<<nb, 256, 0, s>>>(a, d64.p, red.p, red.p + 1);
+    PSG_LAUNCHED();
+    g_launches += 2;
+    PSG_CUDA(cudaMemcpyAsync(hr, red.p, 5 * 8, cudaMemcpyDeviceToHost, s));
     unsigned h[2];
     PSG_CUDA(cudaMemcpyAsync(h, counters.p, 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
@@ -855,45 +1150,26 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h[1]) * 2, 1u << 28);
       continue;
     }
-    if (h[1]) {
-      k_eval_list<<<std::min<int>(blocks_for(h[1], 8), c.sm_count * 16), 256, 0, s>>>(a, op.p, oj.p, h[1]);
-      PSG_LAUNCHED();
-      ++g_launches;
-      PSG_CUDA(cudaMemcpyAsync(h, counters.p, 4, cudaMemcpyDeviceToHost, s));
-      PSG_CUDA(cudaStreamSynchronize(s));
-    }
     if (h[0] > cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
       cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h[0]) * 2, 1u << 28);
-      PSG_CUDA(cudaMemsetAsync(evals.p, 0, 8, s));
       continue;
     }
     ncand = h[0];
     break;
   }
-  tm.mark("scan");
-  const float best_s32 = read_best(plan.best.p, s);
-  const Thresholds th = budget_thresholds_s32(plan.bud, best_s32);
-  DevBuf<double> d64(std::max<unsigned>(ncand, 1), s);
-  DevBuf<unsigned long long> red(3, s);
-  const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
-  PSG_CUDA(cudaMemcpyAsync(red.p, init, 24, cudaMemcpyHostToDevice, s));
-  if (ncand) {
-    if (plan.dir.nk == 4)
-      k_recheck<4><<<blocks_for(ncand, 256), 256, 0, s>>>(a, plan.ps->exact(), th, ncand, d64.p, red.p, red.p + 2);
-    else
-      k_recheck<8><<<blocks_for(ncand, 256), 256, 0, s>>>(a, plan.ps->exact(), th, ncand, d64.p, red.p, red.p + 2);
-    PSG_LAUNCHED();
-    k_pick<<<blocks_for(ncand, 256), 256, 0, s>>>(a, ncand, d64.p, red.p, red.p + 1);
-    PSG_LAUNCHED();
-    g_launches += 2;
-  }
-  unsigned long long hr[3];
-  PSG_CUDA(cudaMemcpyAsync(hr, red.p, 24, cudaMemcpyDeviceToHost, s));
-  const unsigned long long hev = read1(evals.p, s);
-  tm.mark("recheck");
+  g_prof.scan_kernel_ms += scan_span->ms();
+  delete scan_span;
+  tm.mark("scan+recheck");
+  trace("scan+recheck: done");
   uint64_t exits = 0;
-  const uint64_t wp = window_pairs(plan, lo, hi, th.win, &exits, s);
-  tm.mark("stats");
+  const unsigned long long hev = hr[3];
+  uint64_t wp = hr[4];
+  if (!plan.grid) {
+    const Thresholds th = budget_thresholds_s32(plan.bud, read_best(plan.best.p, s));
+    wp = window_pairs(plan, lo, hi, th.win, &exits, s);
+    tm.mark("stats");
+  }
+  trace("stats: done");
   PSG_CUDA(cudaStreamSynchronize(s));
   prof_stages(tm);
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "../../include/pairscan_b200.h"
+#include "psg_grid.cuh"
 #include "psg_internal.cuh"
 #include "psg_points.cuh"
 
@@ -24,8 +25,15 @@ struct CppPlan {
   uint64_t zone = 0;
   Directions dir;
   Budget bud;
-  DevBuf<float> skeys;     // n x nk keys in key-0 sorted order (AoS)
-  DevBuf<uint32_t> sidx;   // sorted position -> original index
+  // engine "window": keys sorted by key 0, candidates = the key-0 window
+  // engine "grid":   keys sorted by cell of the first g keys (psg_grid.cuh)
+  bool grid = false;
+  DevBuf<float> skeys;     // window engine: n x nk keys in key-0 order (AoS)
+  DevBuf<uint32_t> sidx;   // window engine: sorted position -> original index
+  DevBuf<float> keys;      // grid engine: unsorted keys, kept for a rebuild
+  GridIndex gi;            // grid engine
+  int g = 0;
+  double box_lo[3] = {0, 0, 0}, box_span[3] = {0, 0, 0};
   DevBuf<unsigned> best;   // FP32 bits of the best squared distance seen
   uint32_t width = 0;      // bootstrap width (sorted neighbours)
   float prep_ms[3] = {0, 0, 0};

@@ -102,6 +102,9 @@ struct StageTimer {
   }
 };
 
+// Host-side trace (PSG_TRACE=1): wall time since the previous mark, stderr.
+void trace(const char* what);
+
 // Device time of one kernel (or a short launch sequence) on a stream.
 struct KernelSpan {
   cudaEvent_t a = nullptr, b = nullptr;
@@ -113,11 +116,16 @@ struct KernelSpan {
   }
   // Records the end event, waits for it, returns milliseconds.
   double stop() {
-    PSG_CUDA(cudaEventRecord(b, s));
+    end();
     PSG_CUDA(cudaEventSynchronize(b));
-    float ms = 0.f;
-    PSG_CUDA(cudaEventElapsedTime(&ms, a, b));
-    return ms;
+    return ms();
+  }
+  // Deferred form: end() now, ms() after a later stream synchronisation.
+  void end() { PSG_CUDA(cudaEventRecord(b, s)); }
+  double ms() const {
+    float v = 0.f;
+    PSG_CUDA(cudaEventElapsedTime(&v, a, b));
+    return v;
   }
   ~KernelSpan() {
     if (a) cudaEventDestroy(a);

@@ -2,9 +2,13 @@
 // narrowing to the FP32 working copy, z-normalised windows), and the seeded
 // projection directions.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
+#include <tuple>
 
 #include "host_rng.hpp"
 #include "psg_points.cuh"
@@ -12,6 +16,16 @@
 namespace psg {
 
 thread_local uint64_t g_launches = 0;
+
+void trace(const char* what) {
+  static const bool on = std::getenv("PSG_TRACE") != nullptr;
+  if (!on) return;
+  static thread_local auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[psg] %-24s %9.1f us\n", what,
+               std::chrono::duration<double, std::micro>(now - last).count());
+  last = now;
+}
 
 Ctx& ctx() {
   static std::mutex mu;
@@ -349,7 +363,24 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
 // reference Rng stream derive_seed(seed, 0x5eed), orthonormalised in FP64
 // (modified Gram-Schmidt), then rounded to FP32; the spectral norm of the
 // rounded matrix is bounded (Gershgorin on U U^T) for the LB filter.
+namespace {
+Directions make_directions_uncached(uint64_t seed, int d, int q);
+}
+
+// Cached: repeated solves with the same (seed, d, q) reuse the matrix.
 Directions make_directions(uint64_t seed, int d, int q) {
+  static std::mutex mu;
+  static std::map<std::tuple<uint64_t, int, int>, Directions> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_tuple(seed, d, q);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 64) cache.clear();
+  return cache[key] = make_directions_uncached(seed, d, q);
+}
+
+namespace {
+Directions make_directions_uncached(uint64_t seed, int d, int q) {
   Directions dir;
   dir.d = d;
   dir.q = std::max(1, std::min(std::min(q, d), kMaxKeys));
@@ -393,5 +424,6 @@ Directions make_directions(uint64_t seed, int d, int q) {
   dir.unorm = unorm * (1.0 + 1e-9);
   return dir;
 }
+}  // namespace
 
 }  // namespace psg
