@@ -97,6 +97,8 @@ class Port:
         L.orc_build_reference_set.argtypes = [_p, _u64, _u64, _u64, _f64, _u64, _p, _p, _p, _p]
         L.orc_znorm_windows.argtypes = [_p, _u64, _u64, _p]
         L.orc_motif_brute_znorm.argtypes = [_p, _u64, _u64, _u64, _p]
+        L.orc_znorm_pair_distance.restype = _f64
+        L.orc_znorm_pair_distance.argtypes = [_p, _u64, _u64, _u64]
         L.orc_gen_uniform_u24.argtypes = [_u64, _u64, _u64, _p]
         L.orc_gen_gauss_planted.argtypes = [_u64, _u64, _u64, _f64, _p, _p, _p]
         L.orc_gen_walk_motif.argtypes = [_u64, _u64, _u64, _f64, _p, _p, _p]
@@ -209,6 +211,10 @@ class Port:
         if self.lib.orc_znorm_windows(_ptr(s), s.size, l, _ptr(out)) != 0:
             raise OracleError("window length out of range")
         return out
+
+    def znorm_pair_distance(self, series: np.ndarray, l: int, i: int, j: int) -> float:
+        s = np.ascontiguousarray(series, dtype=np.float64)
+        return self.lib.orc_znorm_pair_distance(_ptr(s), l, i, j)
 
     def motif_brute_znorm(self, series: np.ndarray, l: int, zone: int) -> Pair:
         s = np.ascontiguousarray(series, dtype=np.float64)

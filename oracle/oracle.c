@@ -380,6 +380,19 @@ int orc_znorm_windows(const double* series, uint64_t N, uint64_t l, double* out)
   return 0;
 }
 
+double orc_znorm_pair_distance(const double* series, uint64_t l, uint64_t i, uint64_t j) {
+  double mi, si, mj, sj, acc = 0.0;
+  window_stats(series + i, l, &mi, &si);
+  window_stats(series + j, l, &mj, &sj);
+  for (uint64_t t = 0; t < l; ++t) {
+    const double a = si == 0.0 ? 0.0 : (series[i + t] - mi) / si;
+    const double b = sj == 0.0 ? 0.0 : (series[j + t] - mj) / sj;
+    const double diff = a - b;
+    acc += diff * diff;
+  }
+  return sqrt(acc);
+}
+
 int orc_motif_brute_znorm(const double* series, uint64_t N, uint64_t l, uint64_t zone,
                           orc_pair* out) {
   if (l == 0 || l > N) return -1;

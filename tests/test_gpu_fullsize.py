@@ -1,0 +1,63 @@
+"""GPU parity at BASELINE.json's full sizes, through size-independent checks.
+
+At full size the CPU oracle cannot enumerate every pair (hours to
+days), so each config is pinned by properties that do not depend on n:
+  C2/C3  the answer is the planted pair, its distance equals the oracle's FP64
+         value for that pair, and the device all-pairs engine (an independent
+         kernel: tiled brute force + FP64 band recheck) returns the same pair;
+  C4     count and order-independent hash equal the oracle's exact cell-grid
+         restatement of brute_force_neighbors; the pair list is sorted, i<j;
+  C5     (n = 2^17 of the recipe) scan == device all-pairs engine.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c2_full(psg, orc):
+    n, d = 1 << 20, 128
+    pts, (pi, pj) = psg.gen.gauss_planted(2, n, d)
+    ps = psg.PointSet.from_flat(pts, d)
+    got = psg.closest_pair(ps, 10, 10.0, 1, 0)
+    i, j = sorted((pi, pj))
+    assert (got.index_i, got.index_j) == (i, j)
+    assert got.distance == orc.euclidean(pts[i].astype(np.float64), pts[j].astype(np.float64))
+    assert abs(got.distance - 0.0113) < 0.002
+    bf = psg.brute_force_closest_pair(ps, 0)
+    assert (bf.index_i, bf.index_j, bf.distance) == (got.index_i, got.index_j, got.distance)
+
+
+def test_c3_full(psg, orc):
+    N, l = 1 << 20, 256
+    s, (a, b) = psg.gen.walk_motif(3, N, l)
+    got = psg.motif(s, l, znorm=True)
+    i, j = min(a, b), max(a, b)
+    assert (got.index_i, got.index_j) == (i, j)
+    assert got.distance == orc.znorm_pair_distance(s.astype(np.float64), l, i, j)
+    out = psg._Pair()
+    s64 = s.astype(np.float64)
+    psg._check(psg.lib().psg_brute_force_motif_f64(s64.ctypes.data, N, l, 1, l, ctypes.byref(out)))
+    assert (out.index_i, out.index_j, out.distance) == (got.index_i, got.index_j, got.distance)
+
+
+def test_c4_full(psg, orc):
+    n = 1 << 22
+    cube = psg.gen.uniform(4, n, 3)
+    pairs, cnt, h = psg.frnn_pairs(cube, oracle.R_C4)
+    assert (cnt, h) == orc.frnn_grid(cube, oracle.R_C4)
+    assert 60_000_000 < cnt < 72_000_000  # ~32 expected neighbours per point
+    assert np.all(pairs[1:] > pairs[:-1])
+    assert np.all((pairs >> np.uint64(32)) < (pairs & np.uint64(0xFFFFFFFF)))
+
+
+def test_c5_recipe_n2_17(psg):
+    pts = psg.gen.mixture(5, 1 << 17, 64, 1024, 0.05)
+    ps = psg.PointSet.from_flat(pts, 64)
+    got = psg.closest_pair(ps, 10, 10.0, 1, 0)
+    bf = psg.brute_force_closest_pair(ps, 0)
+    assert (got.index_i, got.index_j, got.distance) == (bf.index_i, bf.index_j, bf.distance)
