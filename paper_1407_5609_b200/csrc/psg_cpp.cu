@@ -222,6 +222,117 @@ __global__ void __launch_bounds__(256) k_project_warp(const float* __restrict__ 
   if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
 }
 
+// K1 (d in {32, 64, 128, 256}): each warp stages 32 consecutive rows through
+// padded shared memory with coalesced row loads (all 32 loads in flight per
+// lane), then lane l computes row l's NK keys alone.  U arrives as a
+// __grid_constant__ kernel parameter, so every FMA takes its U operand from
+// the constant bank (uniform across the warp): no shared-memory traffic for
+// U and no cross-lane reduction.  Per row: D FMAs per key + D for the norm.
+template <int NK, int D>
+struct UParam {
+  float u[NK][D];
+};
+
+template <int NK, int D>
+__global__ void __launch_bounds__(128) k_project_smem(const float* __restrict__ X, uint32_t n,
+                                                      const __grid_constant__ UParam<NK, D> U, float* __restrict__ keys,
+                                                      unsigned* __restrict__ norm2_bits) {
+  constexpr int V = D / 32;        // floats per lane per row
+  constexpr int STRIDE = D + 4;    // padded row stride (floats): conflict-free 16 B lane reads
+  constexpr int TILE = 32 * STRIDE;
+  extern __shared__ __align__(16) float tile[];  // (blockDim/32) x 2 buffers x 32 x STRIDE
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* bufs = tile + static_cast<size_t>(w) * 2 * TILE;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  // cp.async of one 32-row tile: lane copies its V floats of every row
+  auto stage = [&](uint32_t r0, float* dst) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t row = r0 + r < n ? r0 + r : n - 1;
+      const float* src = X + static_cast<size_t>(row) * D + lane * V;
+      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + r * STRIDE + lane * V));
+      if constexpr (V >= 4) {
+#pragma unroll
+        for (int v = 0; v < V; v += 4)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + 4 * v), "l"(src + v));
+      } else if constexpr (V == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src));
+      } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  float worst = 0.f;
+  uint32_t r0 = warp * 32;
+  if (r0 < n) stage(r0, bufs);
+  for (int it = 0; r0 < n; ++it, r0 += nwarps * 32) {
+    float* buf = bufs + (it & 1) * TILE;
+    const uint32_t next = r0 + nwarps * 32;
+    if (next < n) {
+      stage(next, bufs + ((it + 1) & 1) * TILE);  // next tile streams while this one computes
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncwarp();
+    // lane computes its own row
+    float acc[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
+    float nn = 0.f;
+    const float* mine = buf + lane * STRIDE;
+#pragma unroll
+    for (int t = 0; t < D; t += 4) {
+      const float4 xv = *reinterpret_cast<const float4*>(mine + t);
+      nn = fmaf(xv.x, xv.x, nn);
+      nn = fmaf(xv.y, xv.y, nn);
+      nn = fmaf(xv.z, xv.z, nn);
+      nn = fmaf(xv.w, xv.w, nn);
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        acc[k] = fmaf(U.u[k][t], xv.x, acc[k]);
+        acc[k] = fmaf(U.u[k][t + 1], xv.y, acc[k]);
+        acc[k] = fmaf(U.u[k][t + 2], xv.z, acc[k]);
+        acc[k] = fmaf(U.u[k][t + 3], xv.w, acc[k]);
+      }
+    }
+    const uint32_t row = r0 + lane;
+    if (row < n) {
+      worst = fmaxf(worst, nn);
+      float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(row) * NK);
+#pragma unroll
+      for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+    }
+    __syncwarp();
+  }
+  worst = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(worst)));
+  if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
+}
+
+template <int NK, int D>
+void launch_project_smem(const float* X, uint32_t n, const Directions& dir, float* keys, unsigned* nb, int sms,
+                         cudaStream_t s) {
+  constexpr size_t kWarpBytes = 2ull * 32 * (D + 4) * sizeof(float);  // double-buffered tile
+  constexpr int kWarpsPerBlock = kWarpBytes * 4 <= 100 * 1024 ? 4 : (kWarpBytes * 2 <= 100 * 1024 ? 2 : 1);
+  constexpr size_t kSmem = kWarpsPerBlock * kWarpBytes;
+  static bool configured = false;
+  if (!configured) {
+    PSG_CUDA(cudaFuncSetAttribute(k_project_smem<NK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmem)));
+    configured = true;
+  }
+  UParam<NK, D> u;
+  for (int k = 0; k < NK; ++k)
+    for (int t = 0; t < D; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * D + t];
+  const int per_sm = static_cast<int>((200 * 1024) / kSmem);
+  const uint32_t tiles = (n + 31) / 32;
+  const int grid = static_cast<int>(std::min<uint64_t>((tiles + kWarpsPerBlock - 1) / kWarpsPerBlock,
+                                                       static_cast<uint64_t>(sms) * std::max(per_sm, 1)));
+  k_project_smem<NK, D><<<grid, 32 * kWarpsPerBlock, kSmem, s>>>(X, n, u, keys, nb);
+}
+
 // Small or irregular d: one thread per row, U staged in shared memory.
 template <int NK>
 __global__ void __launch_bounds__(256) k_project_thread(const float* __restrict__ X, uint32_t n, int d,
@@ -822,20 +933,22 @@ float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaSt
   const int sms = ctx().sm_count;
   const int warp_grid = std::min<int>(blocks_for(n, 8), sms * 16);
   bool done = true;
+  (void)warp_grid;
   KernelSpan span(s);
-#define PSG_PROJ_WARP(NKV, VV) \
-  k_project_warp<NKV, VV><<<warp_grid, 256, 0, s>>>(ps.X, n, U.p, keys, nb.p)
   if (d == 32 || d == 64 || d == 128 || d == 256) {
-    const int V = d / 32;
-    if (dir.nk == 4) {
-      if (V == 1) PSG_PROJ_WARP(4, 1); else if (V == 2) PSG_PROJ_WARP(4, 2); else if (V == 4) PSG_PROJ_WARP(4, 4); else PSG_PROJ_WARP(4, 8);
-    } else {
-      if (V == 1) PSG_PROJ_WARP(8, 1); else if (V == 2) PSG_PROJ_WARP(8, 2); else if (V == 4) PSG_PROJ_WARP(8, 4); else PSG_PROJ_WARP(8, 8);
+    switch (dir.nk * 1000 + d) {
+      case 4032: launch_project_smem<4, 32>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 4064: launch_project_smem<4, 64>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 4128: launch_project_smem<4, 128>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 4256: launch_project_smem<4, 256>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 8032: launch_project_smem<8, 32>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 8064: launch_project_smem<8, 64>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 8128: launch_project_smem<8, 128>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      default: launch_project_smem<8, 256>(ps.X, n, dir, keys, nb.p, sms, s); break;
     }
   } else {
     done = false;
   }
-#undef PSG_PROJ_WARP
   if (!done) {
     const size_t ubytes = static_cast<size_t>(dir.nk) * d * sizeof(float);
     const int smem_ok = ubytes <= 48 * 1024;
