@@ -395,7 +395,7 @@ struct ScanArgs {
   uint32_t n;
   int d;
   uint64_t zone;
-  Budget bud;
+  const Budget* bud;  // device (DevState::bud)
   unsigned* best;
   uint32_t* cand_p;
   uint32_t* cand_j;
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kThreads) k_bootstrap(ScanArgs a, uint32_t lo,
     }
   }
   if (wj == 0xffffffffu) return;
-  const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+  const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
   if (!(wlb <= th.lb2)) return;
   const float* xi = a.X + static_cast<size_t>(a.sidx[wp]) * a.d;
   const float* xj = a.X + static_cast<size_t>(a.sidx[wj]) * a.d;
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
   if (tid == 0) {
     qn = 0;
     nevals = 0;
-    th = budget_thresholds_s32(a.bud, best_now(a.best));
+    th = budget_thresholds_s32(*a.bud,best_now(a.best));
   }
   __syncthreads();
   for (uint32_t c0 = p0 + 1; c0 < a.n; c0 += kChunk) {
@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
     if (tid == 0) {
       nevals += static_cast<unsigned long long>(nq);
       qn = 0;
-      th = budget_thresholds_s32(a.bud, best_now(a.best));
+      th = budget_thresholds_s32(*a.bud,best_now(a.best));
     }
     if (!__syncthreads_or(active)) break;
   }
@@ -638,7 +638,7 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
     }
   }
   if (j == 0xffffffffu) return;
-  const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+  const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
   if (!(lb <= th.lb2)) return;
   const float* xi = a.X + static_cast<size_t>(a.sidx[p]) * a.d;
   const float* xj = a.X + static_cast<size_t>(a.sidx[j]) * a.d;
@@ -659,11 +659,12 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
     float mk[NK];
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
     const uint32_t mo = a.sidx[p];
-    uint32_t rb[5], re[5];
-    const int nr = grid_ranges(G, p, G.scell[p], rb, re);
+    const GridParams P = *G.gp;
+    const GridRanges R = grid_ranges(G.cfirst, P, p, G.scell[p]);
     int seen = 0;
-    for (int r = 0; r < nr && seen < cap; ++r) {
-      for (uint32_t j = rb[r]; j < re[r] && seen < cap; ++j, ++seen) {
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      for (uint32_t j = R.b(r); j < R.e(r) && seen < cap; ++j, ++seen) {
         float kj[NK];
         load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
         float g = kj[0] - mk[0];
@@ -703,13 +704,16 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan(ScanArgs a, GridDev G, u
   const uint32_t p = lo + blockIdx.x * kThreads + tid;
   bool active = p < hi;
   float mk[NK];
-  uint32_t mo = 0, j = 0, rb[5], re[5];
-  int nr = 0, r = 0;
+  uint32_t mo = 0, j = 0, je = 0;
+  GridRanges R{};
+  int r = 0;
   if (active) {
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
     mo = a.sidx[p];
-    nr = grid_ranges(G, p, G.scell[p], rb, re);
-    j = rb[0];
+    const GridParams P = *G.gp;
+    R = grid_ranges(G.cfirst, P, p, G.scell[p]);
+    j = R.b0;
+    je = R.e0;
   } else {
 #pragma unroll
     for (int k = 0; k < NK; ++k) mk[k] = 0.f;
@@ -718,19 +722,20 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan(ScanArgs a, GridDev G, u
   if (tid == 0) {
     qn = 0;
     nevals = 0;
-    th = budget_thresholds_s32(a.bud, best_now(a.best));
+    th = budget_thresholds_s32(*a.bud,best_now(a.best));
   }
   __syncthreads();
   for (;;) {
     const float lb2 = th.lb2;
     int budget = kBudget;
     while (active && budget > 0) {
-      if (j >= re[r]) {
-        if (++r >= nr) {
+      if (j >= je) {
+        if (++r >= 5) {
           active = false;
           break;
         }
-        j = rb[r];
+        j = R.b(r);
+        je = R.e(r);
         continue;
       }
       if (a.zone > 1 && !admissible(mo, a.sidx[j], a.zone)) {
@@ -784,7 +789,7 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan(ScanArgs a, GridDev G, u
     if (tid == 0) {
       nevals += static_cast<unsigned long long>(nq);
       qn = 0;
-      th = budget_thresholds_s32(a.bud, best_now(a.best));
+      th = budget_thresholds_s32(*a.bud,best_now(a.best));
     }
     if (!__syncthreads_or(active)) break;
   }
@@ -806,7 +811,7 @@ __global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const u
     const float* xj = a.X + static_cast<size_t>(a.sidx[pj]) * a.d;
     const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f) : warp_sqdist(xi, xj, a.d, lane);
     if (lane == 0) {
-      const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+      const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
       record(a, pi, pj, s, th.band);
     }
   }
@@ -819,7 +824,7 @@ __global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const u
 template <int NK, bool kWindow>
 __global__ void k_recheck(ScanArgs a, ExactSrc src, double* __restrict__ d64, unsigned long long* __restrict__ best64,
                           unsigned long long* __restrict__ examined) {
-  const Thresholds th = budget_thresholds_s32(a.bud, best_now(a.best));
+  const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
   const uint32_t count = min(*a.cand_n, a.cand_cap);
   for (uint32_t base = blockIdx.x * blockDim.x; base < count; base += gridDim.x * blockDim.x) {
   const uint32_t c = base + threadIdx.x;
@@ -913,6 +918,105 @@ void part_range(uint64_t n, uint64_t part, uint64_t nparts, uint32_t* lo, uint32
   *hi = static_cast<uint32_t>(n * (part + 1) / nparts);
 }
 
+// ---------------------------------------------------------------------------
+// Device-side solve state (DevState): initialised, filled and read back once.
+__global__ void k_state_init(DevState* st) {
+  st->norm2_bits = 0;
+  st->best = 0x7f800000u;  // +inf
+  st->cand_n = st->ovf_n = 0;
+  st->best64 = ~0ull;
+  st->lex = ~0ull;
+  st->examined = st->evals = st->visited = 0;
+}
+
+__global__ void k_scan_reset(DevState* st) {
+  st->cand_n = st->ovf_n = 0;
+  st->best64 = ~0ull;
+  st->lex = ~0ull;
+  st->examined = st->evals = st->visited = 0;
+}
+
+struct SetupArgs {
+  int d, nk, g;
+  double unorm, sigma, Rn, occupancy;
+  uint32_t n, m;
+};
+
+// The error budget from the projection's max norm (same formula as the host
+// make_budget), then — grid engine — the key box from the sample moments
+// (mean +- 3 sd clipped to the sample range) and the grid parameters for the
+// occupancy width.  One block; nothing returns to the host.
+__global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, const float* __restrict__ sample,
+                                               SetupArgs sa) {
+  __shared__ double red[4][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const double u = 0x1.0p-24;
+    Budget b;
+    b.e = (sa.d + 4) * u * 1.01;
+    b.a = (2.0 * sa.d + 2.0) * 0x1.0p-149;
+    const double nn = static_cast<double>(__uint_as_float(st->norm2_bits));
+    const double maxnorm = sqrt(nn * (1.0 + (sa.d + 4) * u)) * (1.0 + 1e-7);
+    const double gamma = sa.d * u / (1.0 - sa.d * u);
+    b.E = gamma * sa.unorm * maxnorm * 1.0001;
+    b.Rn = sa.Rn;
+    b.sigma = sa.sigma;
+    b.unorm = sa.unorm;
+    b.gamma64 = (sa.d + 2) * 0x1.0p-53 * 1.01;
+    b.nk = sa.nk;
+    st->bud = b;
+  }
+  if (sa.g == 0) return;
+  double lo[3] = {0, 0, 0}, span[3] = {0, 0, 0};
+  for (int t = 0; t < sa.g; ++t) {
+    const float* v = sample + static_cast<size_t>(t) * sa.m;
+    double s1 = 0, s2 = 0, mn = 1e300, mx = -1e300;
+    for (uint32_t i = tid; i < sa.m; i += blockDim.x) {
+      const double x = v[i];
+      s1 += x;
+      s2 += x * x;
+      mn = fmin(mn, x);
+      mx = fmax(mx, x);
+    }
+    for (int o = 16; o; o >>= 1) {
+      s1 += __shfl_xor_sync(kFull, s1, o);
+      s2 += __shfl_xor_sync(kFull, s2, o);
+      mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+    }
+    __syncthreads();
+    if (lane == 0) {
+      red[0][warp] = s1;
+      red[1][warp] = s2;
+      red[2][warp] = mn;
+      red[3][warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < 8; ++w) {
+        s1 += red[0][w];
+        s2 += red[1][w];
+        mn = fmin(mn, red[2][w]);
+        mx = fmax(mx, red[3][w]);
+      }
+      const double mean = s1 / sa.m, sd = sqrt(fmax(s2 / sa.m - mean * mean, 0.0));
+      const double a = fmax(mn, mean - 3 * sd), b = fmin(mx, mean + 3 * sd);
+      lo[t] = a;
+      span[t] = fmax(b - a, 1e-30);
+    }
+  }
+  if (tid == 0) {
+    for (int t = 0; t < 3; ++t) {
+      st->box_lo[t] = lo[t];
+      st->box_span[t] = span[t];
+    }
+    const double w = grid_occupancy_width(sa.n, sa.g, span, sa.occupancy);
+    GridParams P;
+    grid_params_for(P, sa.g, w, lo, span);
+    *gp = P;
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -923,42 +1027,44 @@ void check_reference_args(uint64_t n, uint64_t q, double f) {
   if (!(f > 0.0) || !std::isfinite(f)) throw invalid_argument("projection factor must be positive");
 }
 
-float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s) {
-  DevBuf<float> U(dir.U.size(), s);
-  PSG_CUDA(cudaMemcpyAsync(U.p, dir.U.data(), dir.U.size() * sizeof(float), cudaMemcpyHostToDevice, s));
-  DevBuf<unsigned> nb(1, s);
-  PSG_CUDA(cudaMemsetAsync(nb.p, 0, 4, s));
+void project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
+                   cudaStream_t s) {
   const uint32_t n = static_cast<uint32_t>(ps.n);
   const int d = ps.d;
   const int sms = ctx().sm_count;
-  const int warp_grid = std::min<int>(blocks_for(n, 8), sms * 16);
-  bool done = true;
-  (void)warp_grid;
-  KernelSpan span(s);
   if (d == 32 || d == 64 || d == 128 || d == 256) {
     switch (dir.nk * 1000 + d) {
-      case 4032: launch_project_smem<4, 32>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      case 4064: launch_project_smem<4, 64>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      case 4128: launch_project_smem<4, 128>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      case 4256: launch_project_smem<4, 256>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      case 8032: launch_project_smem<8, 32>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      case 8064: launch_project_smem<8, 64>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      case 8128: launch_project_smem<8, 128>(ps.X, n, dir, keys, nb.p, sms, s); break;
-      default: launch_project_smem<8, 256>(ps.X, n, dir, keys, nb.p, sms, s); break;
+      case 4032: launch_project_smem<4, 32>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 4064: launch_project_smem<4, 64>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 4128: launch_project_smem<4, 128>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 4256: launch_project_smem<4, 256>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 8032: launch_project_smem<8, 32>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 8064: launch_project_smem<8, 64>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 8128: launch_project_smem<8, 128>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      default: launch_project_smem<8, 256>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
     }
   } else {
-    done = false;
-  }
-  if (!done) {
+    // small or irregular d: thread per row, U staged in shared memory
+    DevBuf<float> U(dir.U.size(), s);  // freed stream-ordered after the launch
+    PSG_CUDA(cudaMemcpyAsync(U.p, dir.U.data(), dir.U.size() * sizeof(float), cudaMemcpyHostToDevice, s));
     const size_t ubytes = static_cast<size_t>(dir.nk) * d * sizeof(float);
     const int smem_ok = ubytes <= 48 * 1024;
     if (dir.nk == 4)
-      k_project_thread<4><<<blocks_for(n, 256), 256, smem_ok ? ubytes : 0, s>>>(ps.X, n, d, U.p, keys, nb.p, smem_ok);
+      k_project_thread<4><<<blocks_for(n, 256), 256, smem_ok ? ubytes : 0, s>>>(ps.X, n, d, U.p, keys, norm2_bits,
+                                                                               smem_ok);
     else
-      k_project_thread<8><<<blocks_for(n, 256), 256, smem_ok ? ubytes : 0, s>>>(ps.X, n, d, U.p, keys, nb.p, smem_ok);
+      k_project_thread<8><<<blocks_for(n, 256), 256, smem_ok ? ubytes : 0, s>>>(ps.X, n, d, U.p, keys, norm2_bits,
+                                                                               smem_ok);
   }
   PSG_LAUNCHED();
   ++g_launches;
+}
+
+float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s) {
+  DevBuf<unsigned> nb(1, s);
+  PSG_CUDA(cudaMemsetAsync(nb.p, 0, 4, s));
+  KernelSpan span(s);
+  project_async(ps, dir, keys, nb.p, s);
   g_prof.project_kernel_ms += span.stop();
   const unsigned bits = read1(nb.p, s);
   float v;
@@ -983,6 +1089,89 @@ Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm
   return b;
 }
 
+CppWork::~CppWork() {
+  if (host_st) cudaFreeHost(host_st);
+}
+
+namespace {
+
+std::shared_ptr<CppWork> get_work(psg_pointset* ps, int nk, cudaStream_t s) {
+  std::shared_ptr<void>& slot = ps->cpp_work[nk == 8 ? 1 : 0];
+  std::shared_ptr<CppWork> w = std::static_pointer_cast<CppWork>(slot);
+  if (!w) {
+    w = std::make_shared<CppWork>();
+    w->n = static_cast<uint32_t>(ps->n);
+    w->nk = nk;
+    w->keys.alloc(ps->n * nk, s);
+    w->st.alloc(1, s);
+    PSG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->host_st), sizeof(DevState)));
+    slot = w;
+  }
+  return w;
+}
+
+// One synchronisation: DevState (and the grid parameters) back to the host.
+void read_state(CppPlan& plan, cudaStream_t s) {
+  CppWork& W = *plan.work;
+  PSG_CUDA(cudaMemcpyAsync(W.host_st, W.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  if (plan.grid) PSG_CUDA(cudaMemcpyAsync(&plan.gp, W.gi.gp.p, sizeof(GridParams), cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  plan.bud = W.host_st->bud;
+}
+
+float bits_to_float(unsigned b) {
+  float v;
+  std::memcpy(&v, &b, 4);
+  return v;
+}
+
+ScanArgs make_args(CppPlan& plan) {
+  CppWork& W = *plan.work;
+  ScanArgs a{};
+  a.X = plan.ps->X;
+  a.skeys = plan.grid ? W.gi.skeys.p : W.wskeys.p;
+  a.sidx = plan.grid ? W.gi.sidx.p : W.wsidx.p;
+  a.n = static_cast<uint32_t>(plan.ps->n);
+  a.d = plan.ps->d;
+  a.zone = plan.zone;
+  DevState* st = W.st.p;
+  a.bud = &st->bud;
+  a.best = &st->best;
+  a.cand_p = W.cand_p.p;
+  a.cand_j = W.cand_j.p;
+  a.cand_s = W.cand_s.p;
+  a.cand_n = &st->cand_n;
+  a.cand_cap = W.cand_cap;
+  a.ovf_p = W.ovf_p.p;
+  a.ovf_j = W.ovf_j.p;
+  a.ovf_n = &st->ovf_n;
+  a.ovf_cap = W.ovf_cap;
+  a.evals = &st->evals;
+  a.visited = &st->visited;
+  return a;
+}
+
+uint64_t window_pairs(CppPlan& plan, uint32_t lo, uint32_t hi, float win, uint64_t* exits, cudaStream_t s) {
+  CppWork& W = *plan.work;
+  DevBuf<unsigned long long> acc(2, s);
+  PSG_CUDA(cudaMemsetAsync(acc.p, 0, 16, s));
+  if (hi > lo) {
+    if (plan.dir.nk == 4)
+      k_window_stats<4><<<blocks_for(hi - lo, 256), 256, 0, s>>>(W.wskeys.p, W.n, lo, hi, win, acc.p, acc.p + 1);
+    else
+      k_window_stats<8><<<blocks_for(hi - lo, 256), 256, 0, s>>>(W.wskeys.p, W.n, lo, hi, win, acc.p, acc.p + 1);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
+  unsigned long long h[2];
+  PSG_CUDA(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  if (exits) *exits = h[1];
+  return h[0];
+}
+
+}  // namespace
+
 CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone) {
   const uint64_t n = ps->n;
   if (n < 2) throw invalid_argument("closest_pair needs at least 2 points");  // refscan.cpp:70
@@ -996,98 +1185,76 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   plan->zone = zone;
   plan->dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
   const int nk = plan->dir.nk;
-  StageTimer tm(s);
-  trace("plan: directions");
-  DevBuf<float> keys(n * nk, s);
-  const float norm2 = project(*ps, plan->dir, keys.p, s);
-  trace("plan: project (sync)");
-  tm.mark("project");
-  plan->bud = make_budget(*ps, plan->dir, norm2);
+  plan->work = get_work(ps, nk, s);
+  CppWork& W = *plan->work;
   const char* eng = std::getenv("PSG_ENGINE");
   plan->grid = plan->dir.q >= 2 && !(eng && std::string(eng) == "window");
-  if (plan->grid) {
-    // K2 (grid): cells over the first g keys at the occupancy width, sorted
-    plan->g = std::min(3, plan->dir.q);
-    grid_sample_box(keys.p, static_cast<uint32_t>(n), nk, plan->g, plan->box_lo, plan->box_span, s);
-    const double w = grid_occupancy_width(static_cast<uint32_t>(n), plan->g, plan->box_span, kGridOccupancy);
-    build_grid(keys.p, static_cast<uint32_t>(n), nk, plan->g, w, plan->box_lo, plan->box_span, plan->gi, s);
-    plan->keys = std::move(keys);
-    tm.mark("grid");
-    trace("plan: grid built");
-    plan->best.alloc(1, s);
-    const float inf = INFINITY;
-    PSG_CUDA(cudaMemcpyAsync(plan->best.p, &inf, 4, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaStreamSynchronize(s));
-    trace("plan: grid synced");
-    prof_stages(tm);
-    return plan.release();
+  plan->g = plan->grid ? std::min(3, plan->dir.q) : 0;
+  plan->prep_tm = std::make_unique<StageTimer>(s);
+  StageTimer& tm = *plan->prep_tm;
+  k_state_init<<<1, 1, 0, s>>>(W.st.p);
+  PSG_LAUNCHED();
+  {
+    plan->proj_span = std::make_unique<KernelSpan>(s);
+    project_async(*ps, plan->dir, W.keys.p, &W.st.p->norm2_bits, s);
+    plan->proj_span->end();
+    tm.mark("project");
+    SetupArgs sa{ps->d, nk, plan->g, plan->dir.unorm, plan->dir.sigma, ps->Rn, kGridOccupancy,
+                 static_cast<uint32_t>(n), 0};
+    if (plan->grid) {
+      // K2 (grid): cells over the first g keys at the occupancy width, sorted;
+      // parameters computed on device, no host round trip
+      W.gi.ensure(static_cast<uint32_t>(n), nk, s);
+      sa.m = grid_sample(W.keys.p, static_cast<uint32_t>(n), nk, plan->g, W.gi, s);
+      k_setup<<<1, 256, 0, s>>>(W.st.p, W.gi.gp.p, W.gi.sample.p, sa);
+      PSG_LAUNCHED();
+      build_grid(W.keys.p, static_cast<uint32_t>(n), nk, W.gi, 24, s);
+      g_launches += 3;
+      tm.mark("grid");
+    } else {
+      k_setup<<<1, 256, 0, s>>>(W.st.p, nullptr, nullptr, sa);
+      PSG_LAUNCHED();
+      // K2 (window): sort by key 0 (stable, index payload)
+      if (W.wsidx.n != n) {
+        W.wskeys.alloc(n * nk, s);
+        W.wsidx.alloc(n, s);
+        W.wk0.alloc(n, s);
+        W.wk1.alloc(n, s);
+        W.wv0.alloc(n, s);
+        W.wv1.alloc(n, s);
+        W.whist.alloc(radix_hist_words(n), s);
+      }
+      if (nk == 4)
+        k_sort_keys<4><<<blocks_for(n, 256), 256, 0, s>>>(W.keys.p, static_cast<uint32_t>(n), W.wk0.p, W.wv0.p);
+      else
+        k_sort_keys<8><<<blocks_for(n, 256), 256, 0, s>>>(W.keys.p, static_cast<uint32_t>(n), W.wk0.p, W.wv0.p);
+      PSG_LAUNCHED();
+      uint32_t* kk[2] = {W.wk0.p, W.wk1.p};
+      uint32_t* vv[2] = {W.wv0.p, W.wv1.p};
+      const int which = radix_sort<uint32_t>(kk, vv, n, 0, 32, W.whist.p, s);
+      if (nk == 4)
+        k_gather<4><<<blocks_for(n, 256), 256, 0, s>>>(W.keys.p, vv[which], static_cast<uint32_t>(n), W.wskeys.p,
+                                                       W.wsidx.p);
+      else
+        k_gather<8><<<blocks_for(n, 256), 256, 0, s>>>(W.keys.p, vv[which], static_cast<uint32_t>(n), W.wskeys.p,
+                                                       W.wsidx.p);
+      PSG_LAUNCHED();
+      g_launches += 16;
+      tm.mark("sort");
+      read_state(*plan, s);  // the window engine's adaptive bootstrap needs the budget on the host
+    }
+    trace("plan: enqueued");  // timings are collected at the bootstrap's synchronisation
   }
-  // K2: sort by key 0 (stable, index payload)
-  DevBuf<uint32_t> kb0(n, s), kb1(n, s), vb0(n, s), vb1(n, s);
-  DevBuf<uint32_t> hist(radix_hist_words(n), s);
-  if (nk == 4)
-    k_sort_keys<4><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), kb0.p, vb0.p);
-  else
-    k_sort_keys<8><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), kb0.p, vb0.p);
-  PSG_LAUNCHED();
-  ++g_launches;
-  uint32_t* kk[2] = {kb0.p, kb1.p};
-  uint32_t* vv[2] = {vb0.p, vb1.p};
-  const int which = radix_sort<uint32_t>(kk, vv, n, 0, 32, hist.p, s);
-  g_launches += 12;
-  tm.mark("sort");
-  plan->skeys.alloc(n * nk, s);
-  plan->sidx.alloc(n, s);
-  if (nk == 4)
-    k_gather<4><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, vv[which], static_cast<uint32_t>(n), plan->skeys.p,
-                                                   plan->sidx.p);
-  else
-    k_gather<8><<<blocks_for(n, 256), 256, 0, s>>>(keys.p, vv[which], static_cast<uint32_t>(n), plan->skeys.p,
-                                                   plan->sidx.p);
-  PSG_LAUNCHED();
-  ++g_launches;
-  tm.mark("gather");
-  plan->best.alloc(1, s);
-  const float inf = INFINITY;
-  PSG_CUDA(cudaMemcpyAsync(plan->best.p, &inf, 4, cudaMemcpyHostToDevice, s));
-  PSG_CUDA(cudaStreamSynchronize(s));
-  prof_stages(tm);
-  for (int i = 0; i < 3 && i < tm.count; ++i) plan->prep_ms[i] = g_prof.stage_ms[g_prof.stages - tm.count + i];
   return plan.release();
 }
 
 namespace {
-ScanArgs make_args(CppPlan& plan) {
-  ScanArgs a{};
-  a.X = plan.ps->X;
-  a.skeys = plan.grid ? plan.gi.skeys.p : plan.skeys.p;
-  a.sidx = plan.grid ? plan.gi.sidx.p : plan.sidx.p;
-  a.n = static_cast<uint32_t>(plan.ps->n);
-  a.d = plan.ps->d;
-  a.zone = plan.zone;
-  a.bud = plan.bud;
-  a.best = plan.best.p;
-  return a;
-}
-
-uint64_t window_pairs(CppPlan& plan, uint32_t lo, uint32_t hi, float win, uint64_t* exits, cudaStream_t s) {
-  DevBuf<unsigned long long> acc(2, s);
-  PSG_CUDA(cudaMemsetAsync(acc.p, 0, 16, s));
-  if (hi > lo) {
-    if (plan.dir.nk == 4)
-      k_window_stats<4><<<blocks_for(hi - lo, 256), 256, 0, s>>>(plan.skeys.p, static_cast<uint32_t>(plan.ps->n), lo,
-                                                                 hi, win, acc.p, acc.p + 1);
-    else
-      k_window_stats<8><<<blocks_for(hi - lo, 256), 256, 0, s>>>(plan.skeys.p, static_cast<uint32_t>(plan.ps->n), lo,
-                                                                 hi, win, acc.p, acc.p + 1);
-    PSG_LAUNCHED();
-    ++g_launches;
-  }
-  unsigned long long h[2];
-  PSG_CUDA(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, s));
-  PSG_CUDA(cudaStreamSynchronize(s));
-  if (exits) *exits = h[1];
-  return h[0];
+// Stage/kernel times of plan_create, read once the stream has synchronised.
+void collect_prep(CppPlan& plan) {
+  if (plan.proj_span) g_prof.project_kernel_ms += plan.proj_span->ms();
+  if (plan.prep_tm) prof_stages(*plan.prep_tm);
+  plan.proj_span.reset();
+  plan.prep_tm.reset();
 }
 }  // namespace
 
@@ -1108,22 +1275,26 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
     KernelSpan ks(s);
     if (hi > lo) {
       if (plan.dir.nk == 4)
-        k_grid_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi, kGridBootCap);
+        k_grid_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, lo, hi,
+                                                                             kGridBootCap);
       else
-        k_grid_bootstrap<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi, kGridBootCap);
+        k_grid_bootstrap<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, lo, hi,
+                                                                             kGridBootCap);
       PSG_LAUNCHED();
       ++g_launches;
     }
     ks.end();
     tm.mark("bootstrap");
-    const float b = read_best(plan.best.p, s);  // synchronises the stream
+    read_state(plan, s);  // synchronises the stream
+    collect_prep(plan);
     trace("bootstrap: done");
     g_prof.bootstrap_kernel_ms += ks.ms();
     prof_stages(tm);
-    return b;
+    return bits_to_float(plan.work->host_st->best);
   }
-  // Adaptive width: widen while the window the bound implies is far more
-  // work than the bootstrap that produced it.
+  // Window engine.  Adaptive width: widen while the window the bound implies
+  // is far more work than the bootstrap that produced it.
+  collect_prep(plan);
   uint32_t width = 1024;
   for (int round = 0; round < 4; ++round) {
     if (hi > lo) {
@@ -1136,7 +1307,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
       ++g_launches;
       g_prof.bootstrap_kernel_ms += ks.stop();
     }
-    const float b = read_best(plan.best.p, s);
+    const float b = read_best(a.best, s);
     const Thresholds th = budget_thresholds_s32(plan.bud, b);
     const uint64_t est = window_pairs(plan, lo, hi, th.win, nullptr, s);
     if (est <= 8ull * (hi - lo) * width || width >= 16384) break;
@@ -1147,159 +1318,142 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   PSG_CUDA(cudaStreamSynchronize(s));
   prof_stages(tm);
   g_prof.bootstrap_width = width;
-  return read_best(plan.best.p, s);
+  return read_best(a.best, s);
 }
 
 psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, float bound_s32) {
   Ctx& c = ctx();
   cudaStream_t s = c.stream;
   const uint64_t n = plan.ps->n;
+  CppWork& W = *plan.work;
   uint32_t lo, hi;
   part_range(n, part, nparts, &lo, &hi);
   StageTimer tm(s);
-  {
-    // the bound handed in is the (global) minimum of what bootstrap returned,
-    // hence <= this rank's device bound: lower the device copy to it.
-    const float b = bound_s32;
-    k_min_bound<<<1, 1, 0, s>>>(plan.best.p, b);
-    PSG_LAUNCHED();
-    ++g_launches;
-    if (plan.grid) {
-      // The grid must hold every pair whose key gaps are within the window of
-      // the (global) bound: widen the cells when the occupancy width is
-      // smaller.  Every rank derives the same grid from the same bound.
-      const Thresholds th0 = budget_thresholds_s32(plan.bud, b);
-      const double need = static_cast<double>(th0.win) * (1.0 + 1e-5);
-      if (!(plan.gi.w >= need)) {
-        if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
-        build_grid(plan.keys.p, static_cast<uint32_t>(n), plan.dir.nk, plan.g, need, plan.box_lo, plan.box_span,
-                   plan.gi, s);
-        tm.mark("regrid");
-      }
+  // The bound handed in is the (global) minimum of what the bootstraps
+  // returned; lower the device copy to it.
+  k_min_bound<<<1, 1, 0, s>>>(&W.st.p->best, bound_s32);
+  PSG_LAUNCHED();
+  ++g_launches;
+  if (plan.grid) {
+    // The grid must hold every pair whose key gaps are within the window of
+    // the bound: widen the cells when the occupancy width is smaller.  Every
+    // rank derives the same grid from the same bound.
+    const float b = std::min(bound_s32, bits_to_float(W.host_st->best));
+    const Thresholds th0 = budget_thresholds_s32(plan.bud, b);
+    const double need = static_cast<double>(th0.win) * (1.0 + 1e-5);
+    if (!(plan.gp.w >= need)) {
+      if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
+      grid_params_for(plan.gp, plan.g, need, W.host_st->box_lo, W.host_st->box_span);
+      PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
+      build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
+      tm.mark("regrid");
     }
   }
-  uint32_t cand_cap = 1u << 16, ovf_cap = 1u << 20;
-  DevBuf<uint32_t> cp, cj, op, oj;
-  DevBuf<float> cs;
-  DevBuf<unsigned> counters(2, s);
-  DevBuf<unsigned long long> evals(1, s);
-  ScanArgs a = make_args(plan);
+  if (W.cand_cap == 0) {
+    W.cand_cap = 1u << 16;
+    W.ovf_cap = plan.grid ? 1 : (1u << 20);
+  }
   unsigned ncand = 0;
-  // result block read back once: [0] best64 bits, [1] lex pair, [2] examined,
-  // [3] evals, [4] visited, [5] cand count | spill count << 32
-  DevBuf<unsigned long long> red(6, s);
-  DevBuf<double> d64;
-  unsigned long long hr[6];
   KernelSpan* scan_span = nullptr;
   for (int attempt = 0;; ++attempt) {
-    cp.alloc(cand_cap, s);
-    cj.alloc(cand_cap, s);
-    cs.alloc(cand_cap, s);
-    op.alloc(ovf_cap, s);
-    oj.alloc(ovf_cap, s);
-    PSG_CUDA(cudaMemsetAsync(counters.p, 0, 8, s));
-    a.cand_p = cp.p;
-    a.cand_j = cj.p;
-    a.cand_s = cs.p;
-    a.cand_n = counters.p;
-    a.cand_cap = cand_cap;
-    a.ovf_p = op.p;
-    a.ovf_j = oj.p;
-    a.ovf_n = counters.p + 1;
-    a.ovf_cap = ovf_cap;
-    a.evals = red.p + 3;
-    a.visited = red.p + 4;
-    const unsigned long long init[6] = {~0ull, ~0ull, 0ull, 0ull, 0ull, 0ull};
-    PSG_CUDA(cudaMemcpyAsync(red.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    d64.alloc(cand_cap, s);
+    if (W.cand_p.n < W.cand_cap) {
+      W.cand_p.alloc(W.cand_cap, s);
+      W.cand_j.alloc(W.cand_cap, s);
+      W.cand_s.alloc(W.cand_cap, s);
+      W.d64.alloc(W.cand_cap, s);
+    }
+    if (W.ovf_p.n < W.ovf_cap) {
+      W.ovf_p.alloc(W.ovf_cap, s);
+      W.ovf_j.alloc(W.ovf_cap, s);
+    }
+    ScanArgs a = make_args(plan);
+    k_scan_reset<<<1, 1, 0, s>>>(W.st.p);
+    PSG_LAUNCHED();
     delete scan_span;
     scan_span = new KernelSpan(s);
     if (hi > lo) {
       if (plan.grid) {
         if (plan.dir.nk == 4)
-          k_grid_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi);
+          k_grid_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi);
         else
-          k_grid_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.gi.dev, lo, hi);
+          k_grid_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi);
       } else if (plan.dir.nk == 4)
         k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
       else
         k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
       PSG_LAUNCHED();
-      ++g_launches;
+      g_launches += 2;
       ++g_prof.scan_launches;
     }
     scan_span->end();
     if (!plan.grid) {  // spill list of the window engine (grid threads retry instead)
-      k_eval_list<<<c.sm_count * 8, 256, 0, s>>>(a, op.p, oj.p);
+      k_eval_list<<<c.sm_count * 8, 256, 0, s>>>(a, W.ovf_p.p, W.ovf_j.p);
       PSG_LAUNCHED();
       ++g_launches;
     }
     // speculative recheck: correct whenever nothing overflowed (checked below)
     const ExactSrc ex = plan.ps->exact();
     const int nb = c.sm_count * 2;
+    DevState* st = W.st.p;
     if (plan.grid) {
       if (plan.dir.nk == 4)
-        k_recheck<4, false><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+        k_recheck<4, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
       else
-        k_recheck<8, false><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+        k_recheck<8, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
     } else if (plan.dir.nk == 4)
-      k_recheck<4, true><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+      k_recheck<4, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
     else
-      k_recheck<8, true><<<nb, 256, 0, s>>>(a, ex, d64.p, red.p, red.p + 2);
+      k_recheck<8, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
     PSG_LAUNCHED();
-    k_pick<<<nb, 256, 0, s>>>(a, d64.p, red.p, red.p + 1);
+    k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
     PSG_LAUNCHED();
     g_launches += 2;
-    PSG_CUDA(cudaMemcpyAsync(hr, red.p, 5 * 8, cudaMemcpyDeviceToHost, s));
-    unsigned h[2];
-    PSG_CUDA(cudaMemcpyAsync(h, counters.p, 8, cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaStreamSynchronize(s));
+    read_state(plan, s);
+    const DevState& h = *W.host_st;
     if (attempt > 12)
-      throw std::runtime_error("closest_pair: candidate buffers kept overflowing (cand " + std::to_string(h[0]) +
-                               "/" + std::to_string(cand_cap) + ", spill " + std::to_string(h[1]) + "/" +
-                               std::to_string(ovf_cap) + ", best_s32 " + std::to_string(read_best(plan.best.p, s)) +
-                               ")");
-    if (h[1] > ovf_cap) {  // queue spill list overflowed: rescan with the tighter bound
-      ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h[1]) * 2, 1u << 28);
+      throw std::runtime_error("closest_pair: candidate buffers kept overflowing (cand " + std::to_string(h.cand_n) +
+                               "/" + std::to_string(W.cand_cap) + ", spill " + std::to_string(h.ovf_n) + "/" +
+                               std::to_string(W.ovf_cap) + ")");
+    if (!plan.grid && h.ovf_n > W.ovf_cap) {  // spill list overflowed: rescan with the tighter bound
+      W.ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h.ovf_n) * 2, 1u << 28);
       continue;
     }
-    if (h[0] > cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
-      cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h[0]) * 2, 1u << 28);
+    if (h.cand_n > W.cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
+      W.cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h.cand_n) * 2, 1u << 28);
       continue;
     }
-    ncand = h[0];
+    ncand = h.cand_n;
     break;
   }
   g_prof.scan_kernel_ms += scan_span->ms();
   delete scan_span;
   tm.mark("scan+recheck");
   trace("scan+recheck: done");
+  const DevState h = *W.host_st;
   uint64_t exits = 0;
-  const unsigned long long hev = hr[3];
-  uint64_t wp = hr[4];
+  uint64_t wp = h.visited;
   if (!plan.grid) {
-    const Thresholds th = budget_thresholds_s32(plan.bud, read_best(plan.best.p, s));
+    const Thresholds th = budget_thresholds_s32(plan.bud, bits_to_float(h.best));
     wp = window_pairs(plan, lo, hi, th.win, &exits, s);
     tm.mark("stats");
   }
-  trace("stats: done");
   PSG_CUDA(cudaStreamSynchronize(s));
   prof_stages(tm);
 
   psg_pair_result r{};
-  if (hr[1] == ~0ull) {
+  if (h.lex == ~0ull) {
     r.index_i = r.index_j = UINT64_MAX;
     r.distance = INFINITY;
   } else {
-    r.index_i = hr[1] >> 32;
-    r.index_j = hr[1] & 0xffffffffull;
-    std::memcpy(&r.distance, &hr[0], 8);
+    r.index_i = h.lex >> 32;
+    r.index_j = h.lex & 0xffffffffull;
+    std::memcpy(&r.distance, &h.best64, 8);
   }
-  r.stats.pairs_examined = hr[2];
-  r.stats.pairs_pruned_by_reference = wp > hr[2] ? wp - hr[2] : 0;
+  r.stats.pairs_examined = h.examined;
+  r.stats.pairs_pruned_by_reference = wp > h.examined ? wp - h.examined : 0;
   r.stats.inner_loop_exits = exits;
   g_prof.window_pairs += wp;
-  g_prof.lb_survivors += hev;
+  g_prof.lb_survivors += h.evals;
   g_prof.candidates += ncand;
   return r;
 }

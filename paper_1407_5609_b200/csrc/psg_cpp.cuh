@@ -2,6 +2,8 @@
 // the pieces the fixed-radius engine shares with it.
 #pragma once
 
+#include <memory>
+
 #include "../../include/pairscan_b200.h"
 #include "psg_grid.cuh"
 #include "psg_internal.cuh"
@@ -15,28 +17,58 @@ void prof_begin();
 void prof_stages(const StageTimer& t);
 
 // Projection of the FP32 working rows onto the seeded directions:
-// keys[i*nk + k] = <U_k, X_i>.  Returns max ||X_i||^2 (FP32 upper bound).
+// keys[i*nk + k] = <U_k, X_i>; max ||X_i||^2 (FP32 bits) is atomically maxed
+// into *norm2_bits (device).  Enqueued only.
+void project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
+                   cudaStream_t s);
+// Host-synchronous variant: returns max ||X_i||^2.
 float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s);
-// Error budget for the keys of `ps` under `dir`.
+// Error budget for the keys of `ps` under `dir` (host).
 Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm2);
+
+// Device-resident solve state: every threshold and counter the kernels need,
+// so a solve is enqueued with two host synchronisations (after the bootstrap,
+// at the end).
+struct DevState {
+  unsigned norm2_bits;  // max ||x||^2 (FP32 bits), from the projection
+  unsigned best;        // FP32 bits of the best squared distance seen
+  unsigned cand_n, ovf_n;
+  unsigned long long best64, lex, examined, evals, visited;
+  Budget bud;
+  double box_lo[3], box_span[3];
+};
+
+// Buffers reused by every solve on one point set (per key count).
+struct CppWork {
+  uint32_t n = 0;
+  int nk = 0;
+  DevBuf<float> keys;      // n x nk, original order
+  GridIndex gi;            // grid engine
+  DevBuf<float> wskeys;    // window engine: keys in key-0 order
+  DevBuf<uint32_t> wsidx, wk0, wk1, wv0, wv1, whist;
+  DevBuf<DevState> st;
+  DevState* host_st = nullptr;  // pinned mirror
+  DevBuf<uint32_t> cand_p, cand_j, ovf_p, ovf_j;
+  DevBuf<float> cand_s;
+  DevBuf<double> d64;
+  uint32_t cand_cap = 0, ovf_cap = 0;
+  ~CppWork();
+};
 
 struct CppPlan {
   psg_pointset* ps = nullptr;
   uint64_t zone = 0;
   Directions dir;
-  Budget bud;
+  Budget bud;              // host copy (valid after the first readback)
+  GridParams gp;           // host copy of the grid parameters
   // engine "window": keys sorted by key 0, candidates = the key-0 window
   // engine "grid":   keys sorted by cell of the first g keys (psg_grid.cuh)
   bool grid = false;
-  DevBuf<float> skeys;     // window engine: n x nk keys in key-0 order (AoS)
-  DevBuf<uint32_t> sidx;   // window engine: sorted position -> original index
-  DevBuf<float> keys;      // grid engine: unsorted keys, kept for a rebuild
-  GridIndex gi;            // grid engine
   int g = 0;
-  double box_lo[3] = {0, 0, 0}, box_span[3] = {0, 0, 0};
-  DevBuf<unsigned> best;   // FP32 bits of the best squared distance seen
-  uint32_t width = 0;      // bootstrap width (sorted neighbours)
-  float prep_ms[3] = {0, 0, 0};
+  std::shared_ptr<CppWork> work;
+  uint32_t width = 0;      // window engine: bootstrap width (sorted neighbours)
+  std::unique_ptr<StageTimer> prep_tm;   // plan_create's stages, read at the first sync
+  std::unique_ptr<KernelSpan> proj_span;
 };
 
 CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone);

@@ -1,5 +1,6 @@
-// psg_grid.cu — build the cell grid (psg_grid.cuh): sample box, cell ids,
-// stable radix sort by cell, key gather, dense cell ranges.
+// psg_grid.cu — build the cell grid (psg_grid.cuh): cell ids from the device
+// GridParams, per-cell counts -> cfirst (exclusive scan), stable radix sort by
+// cell, key gather.  Everything is enqueued; nothing waits on the host.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -12,6 +13,7 @@ namespace psg {
 namespace {
 
 unsigned blocks(uint64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
+constexpr uint32_t kSample = 4096;
 
 __global__ void k_sample_keys(const float* __restrict__ keys, uint32_t n, int nk, int g, uint32_t m,
                               float* __restrict__ out) {
@@ -21,19 +23,30 @@ __global__ void k_sample_keys(const float* __restrict__ keys, uint32_t n, int nk
   for (int t = 0; t < g; ++t) out[static_cast<size_t>(t) * m + k] = keys[static_cast<size_t>(i) * nk + t];
 }
 
+__global__ void k_zero_counts(uint32_t* __restrict__ counts, const GridParams* __restrict__ gp) {
+  const uint64_t count = gp->cells + 1;
+  for (uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; c < count;
+       c += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    counts[c] = 0;
+}
+
 template <int NK>
-__global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, GridDev G, uint32_t* __restrict__ cid,
-                           uint32_t* __restrict__ idx) {
+__global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, const GridParams* __restrict__ gpp,
+                           uint32_t* __restrict__ cid, uint32_t* __restrict__ idx, uint32_t* __restrict__ counts) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const GridParams P = *gpp;
   uint32_t c = 0;
-  for (int t = 0; t < G.g; ++t) {
-    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - G.lo[t]) * G.inv_w;
-    uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(G.dims[t] - 1) ? G.dims[t] - 1 : static_cast<uint32_t>(v));
-    c = c * G.dims[t] + ct;
+  for (int t = 0; t < P.g; ++t) {
+    const double lo = t == 0 ? P.lo[0] : (t == 1 ? P.lo[1] : P.lo[2]);
+    const uint32_t dim = t == 0 ? P.dims[0] : (t == 1 ? P.dims[1] : P.dims[2]);
+    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - lo) * P.inv_w;
+    const uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(dim - 1) ? dim - 1 : static_cast<uint32_t>(v));
+    c = c * dim + ct;
   }
   cid[i] = c;
   idx[i] = i;
+  atomicAdd(counts + c, 1u);
 }
 
 template <int NK>
@@ -49,33 +62,43 @@ __global__ void k_gather_sorted(const float* __restrict__ keys, const uint32_t* 
   sidx[p] = i;
 }
 
-// cfirst[c] = lower_bound(scell, c) for c in [0, cells]: position p (0..n)
-// writes p into every cell id in (scell[p-1], scell[p]] — each entry exactly
-// once, total work cells + n.
-__global__ void k_cell_first(const uint32_t* __restrict__ scell, uint32_t n, uint64_t cells,
-                             uint32_t* __restrict__ cfirst) {
-  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (p > n) return;
-  const int64_t prev = p == 0 ? -1 : static_cast<int64_t>(scell[p - 1]);
-  const int64_t cur = p == n ? static_cast<int64_t>(cells) : static_cast<int64_t>(scell[p]);
-  for (int64_t c = prev + 1; c <= cur; ++c) cfirst[c] = static_cast<uint32_t>(p);
-}
-
 }  // namespace
 
-void grid_sample_box(const float* keys, uint32_t n, int nk, int g, double lo[3], double span[3], cudaStream_t s) {
-  const uint32_t m = std::min<uint32_t>(n, 4096);
-  DevBuf<float> smp(static_cast<size_t>(m) * g, s);
-  k_sample_keys<<<blocks(m, 256), 256, 0, s>>>(keys, n, nk, g, m, smp.p);
+void GridIndex::ensure(uint32_t n_, int nk_, cudaStream_t s) {
+  if (n == n_ && nk == nk_ && skeys.p) return;
+  n = n_;
+  nk = nk_;
+  skeys.alloc(static_cast<size_t>(n) * nk, s);
+  sidx.alloc(n, s);
+  cid0.alloc(n, s);
+  cid1.alloc(n, s);
+  idx0.alloc(n, s);
+  idx1.alloc(n, s);
+  hist.alloc(radix_hist_words(n), s);
+  counts.alloc(kMaxCells + 1, s);
+  cfirst.alloc(kMaxCells + 1, s);
+  stmp.alloc(scan_temp_words(kMaxCells + 1), s);
+  sample.alloc(3 * kSample, s);
+  gp.alloc(1, s);
+}
+
+uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s) {
+  const uint32_t m = std::min<uint32_t>(n, kSample);
+  k_sample_keys<<<blocks(m, 256), 256, 0, s>>>(keys, n, nk, g, m, gi.sample.p);
   PSG_LAUNCHED();
   ++g_launches;
-  std::vector<float> h(static_cast<size_t>(m) * g);
-  PSG_CUDA(cudaMemcpyAsync(h.data(), smp.p, h.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
-  PSG_CUDA(cudaStreamSynchronize(s));
-  trace("grid: sample d2h");
-  // box = [mean - 3 sd, mean + 3 sd] clipped to the sample range (one pass)
+  return m;
+}
+
+// box = [mean - 3 sd, mean + 3 sd] clipped to the sample range (a tuning
+// input only: clamping keeps any box exact).
+void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double span[3]) {
+  for (int t = 0; t < 3; ++t) {
+    lo[t] = 0;
+    span[t] = 0;
+  }
   for (int t = 0; t < g; ++t) {
-    const float* v = h.data() + static_cast<size_t>(t) * m;
+    const float* v = sample + static_cast<size_t>(t) * m;
     double s1 = 0, s2 = 0, mn = v[0], mx = v[0];
     for (uint32_t i = 0; i < m; ++i) {
       s1 += v[i];
@@ -88,74 +111,34 @@ void grid_sample_box(const float* keys, uint32_t n, int nk, int g, double lo[3],
     lo[t] = a;
     span[t] = std::max(b - a, 1e-30);
   }
-  trace("grid: quantiles");
-  for (int t = g; t < 3; ++t) {
-    lo[t] = 0;
-    span[t] = 0;
-  }
 }
 
-double grid_occupancy_width(uint32_t n, int g, const double span[3], double occupancy) {
-  double vol = 1.0;
-  for (int t = 0; t < g; ++t) vol *= span[t];
-  return std::pow(vol * occupancy / std::max<double>(n, 1), 1.0 / g);
-}
-
-void build_grid(const float* keys, uint32_t n, int nk, int g, double w, const double lo[3], const double span[3],
-                GridIndex& gi, cudaStream_t s) {
-  gi.nk = nk;
-  GridDev G;
-  G.n = n;
-  G.g = g;
-  for (;;) {
-    double cells = 1.0;
-    for (int t = 0; t < g; ++t) cells *= std::floor(span[t] / w) + 1.0;
-    if (cells <= static_cast<double>(1u << 24)) break;
-    w *= 1.25;
-  }
-  gi.w = w;
-  G.inv_w = 1.0 / w;
-  gi.cells = 1;
-  for (int t = 0; t < g; ++t) {
-    G.lo[t] = lo[t];
-    G.dims[t] = static_cast<uint32_t>(std::floor(span[t] / w)) + 1;
-    gi.cells *= G.dims[t];
-  }
-  trace("grid: params");
-  DevBuf<uint32_t> k0(n, s), k1(n, s), v0(n, s), v1(n, s), hist(radix_hist_words(n), s);
-  trace("grid: alloc");
-  if (nk == 4)
-    k_cell_ids<4><<<blocks(n, 256), 256, 0, s>>>(keys, n, G, k0.p, v0.p);
-  else
-    k_cell_ids<8><<<blocks(n, 256), 256, 0, s>>>(keys, n, G, k0.p, v0.p);
+void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s) {
+  k_zero_counts<<<1024, 256, 0, s>>>(gi.counts.p, gi.gp.p);
   PSG_LAUNCHED();
-  ++g_launches;
-  uint32_t* kk[2] = {k0.p, k1.p};
-  uint32_t* vv[2] = {v0.p, v1.p};
-  int bits = 1;
-  while ((1ull << bits) < gi.cells) ++bits;
-  const int passes = (bits + 7) / 8;
-  const int which = radix_sort<uint32_t>(kk, vv, n, 0, passes * 8, hist.p, s);
-  g_launches += 3 * passes;
-  trace("grid: sort launched");
-  gi.skeys.alloc(static_cast<size_t>(n) * nk, s);
-  gi.sidx.alloc(n, s);
+  if (nk == 4)
+    k_cell_ids<4><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p, gi.counts.p);
+  else
+    k_cell_ids<8><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p, gi.counts.p);
+  PSG_LAUNCHED();
+  // cfirst = exclusive prefix sum of the per-cell counts (cfirst[cells] = n)
+  exclusive_scan_u32_dev(gi.counts.p, gi.cfirst.p, kMaxCells + 1, &gi.gp.p->cells, gi.stmp.p, s);
+  uint32_t* kk[2] = {gi.cid0.p, gi.cid1.p};
+  uint32_t* vv[2] = {gi.idx0.p, gi.idx1.p};
+  const int passes = (sort_bits + 7) / 8;
+  const int which = radix_sort<uint32_t>(kk, vv, n, 0, passes * 8, gi.hist.p, s);
   if (nk == 4)
     k_gather_sorted<4><<<blocks(n, 256), 256, 0, s>>>(keys, vv[which], n, gi.skeys.p, gi.sidx.p);
   else
     k_gather_sorted<8><<<blocks(n, 256), 256, 0, s>>>(keys, vv[which], n, gi.skeys.p, gi.sidx.p);
   PSG_LAUNCHED();
-  gi.scell = std::move(which == 0 ? k0 : k1);
-  gi.cfirst.alloc(gi.cells + 1, s);
-  k_cell_first<<<blocks(static_cast<uint64_t>(n) + 1, 256), 256, 0, s>>>(gi.scell.p, n, gi.cells, gi.cfirst.p);
-  PSG_LAUNCHED();
-  g_launches += 2;
-  trace("grid: ranges launched");
-  G.skeys = gi.skeys.p;
-  G.sidx = gi.sidx.p;
-  G.scell = gi.scell.p;
-  G.cfirst = gi.cfirst.p;
-  gi.dev = G;
+  g_launches += 6 + 3 * passes;
+  gi.dev.skeys = gi.skeys.p;
+  gi.dev.sidx = gi.sidx.p;
+  gi.dev.scell = kk[which];
+  gi.dev.cfirst = gi.cfirst.p;
+  gi.dev.gp = gi.gp.p;
+  gi.dev.n = n;
 }
 
 }  // namespace psg

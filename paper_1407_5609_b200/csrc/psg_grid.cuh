@@ -3,36 +3,133 @@
 //
 // Points are radix-sorted by cell id (stable, so a cell lists its points in
 // original-index order) and keys are gathered into that order, so every cell
-// is a contiguous window of sorted positions [cstart[c], cend[c]).  A pair
+// is a contiguous window of sorted positions [cfirst[c], cfirst[c+1]).  A pair
 // whose key gaps are all <= w lies in the same or an adjacent cell; cell
 // coordinates are clamped to [0, dims-1], which is monotone and contracting,
 // so far-out points merge into border cells without breaking that property.
+//
+// The grid parameters live in device memory (GridParams) so the whole build
+// can be enqueued without a host round trip; kernels copy them to registers.
 #pragma once
 
 #include "psg_internal.cuh"
 
 namespace psg {
 
+constexpr uint64_t kMaxCells = 1ull << 24;
+
+// q = x / d for x < 2^31 by multiply-high (CUTLASS-style FastDivmod).
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+  __host__ __device__ static FastDiv make(uint32_t divisor) {
+    FastDiv f;
+    f.d = divisor;
+    if (divisor > 1) {
+      int l = 0;
+      while ((1u << l) < divisor) ++l;  // ceil(log2)
+      const int p = 31 + l;
+      f.m = static_cast<uint32_t>(((1ull << p) + divisor - 1) / divisor);
+      f.s = static_cast<uint32_t>(p - 32);
+    }
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const { return d == 1 ? x : (__umulhi(x, m) >> s); }
+};
+
+struct GridParams {
+  int g = 1;
+  uint32_t dims[3] = {1, 1, 1};
+  double lo[3] = {0, 0, 0};
+  double w = 1.0, inv_w = 1.0;
+  uint64_t cells = 1;
+  FastDiv fD, f1;  // division by the last dim and by dims[1]
+};
+
+// Fill dims/cells/divisors for width >= w over the box (widened until the dense
+// cell table fits kMaxCells).  Host and device.
+__host__ __device__ inline void grid_params_for(GridParams& gp, int g, double w, const double lo[3],
+                                                const double span[3]) {
+  gp.g = g;
+  for (;;) {
+    double cells = 1.0;
+    for (int t = 0; t < g; ++t) cells *= floor(span[t] / w) + 1.0;
+    if (cells <= static_cast<double>(kMaxCells)) break;
+    w *= 1.25;
+  }
+  gp.w = w;
+  gp.inv_w = 1.0 / w;
+  gp.cells = 1;
+  for (int t = 0; t < 3; ++t) {
+    gp.lo[t] = t < g ? lo[t] : 0.0;
+    gp.dims[t] = t < g ? static_cast<uint32_t>(floor(span[t] / w)) + 1 : 1;
+    gp.cells *= gp.dims[t];
+  }
+  gp.fD = FastDiv::make(gp.dims[g - 1]);
+  gp.f1 = FastDiv::make(gp.dims[1]);
+}
+
 struct GridDev {  // POD view passed to kernels
   const float* skeys = nullptr;   // n x nk keys, sorted by cell
   const uint32_t* sidx = nullptr; // sorted position -> original index
   const uint32_t* scell = nullptr;
   const uint32_t* cfirst = nullptr;  // cells+1: first sorted position with cell id >= c
+  const GridParams* gp = nullptr;    // device
   uint32_t n = 0;
-  int g = 1;
-  uint32_t dims[3] = {1, 1, 1};
-  double lo[3] = {0, 0, 0};
-  double inv_w = 1.0;
 };
 
+// Persistent buffers of one grid (reused across solves on the same point set).
 struct GridIndex {
   int nk = 4;
-  double w = 0.0;
-  uint64_t cells = 1;
+  uint32_t n = 0;
   DevBuf<float> skeys;
-  DevBuf<uint32_t> sidx, scell, cfirst;
+  DevBuf<uint32_t> sidx, cid0, cid1, idx0, idx1, hist, counts, cfirst, stmp;
+  DevBuf<float> sample;
+  DevBuf<GridParams> gp;
   GridDev dev;
+  void ensure(uint32_t n_, int nk_, cudaStream_t s);
 };
+
+// Enqueue the build (no host synchronisation): cell ids from *G.gp, counts ->
+// cfirst (exclusive scan), stable radix sort by cell (sort_bits), gather.
+void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s);
+// Strided sample of the first g keys into gi.sample (g x m floats); returns m.
+uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s);
+// Host-side box from a host copy of the sample (mean +- 3 sd, clipped).
+void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double span[3]);
+// Cell width giving about `occupancy` points per cell over the box.
+__host__ __device__ inline double grid_occupancy_width(uint32_t n, int g, const double span[3], double occupancy) {
+  double vol = 1.0;
+  for (int t = 0; t < g; ++t) vol *= span[t];
+  return pow(vol * occupancy / (n > 0 ? static_cast<double>(n) : 1.0), 1.0 / g);
+}
+
+struct GridRanges {  // five ranges held in registers; empty ranges have b == e
+  uint32_t b0, e0, b1, e1, b2, e2, b3, e3, b4, e4;
+  __device__ __forceinline__ uint32_t b(int r) const {
+    return r == 0 ? b0 : r == 1 ? b1 : r == 2 ? b2 : r == 3 ? b3 : b4;
+  }
+  __device__ __forceinline__ uint32_t e(int r) const {
+    return r == 0 ? e0 : r == 1 ? e1 : r == 2 ? e2 : r == 3 ? e3 : e4;
+  }
+};
+
+// Row (prefix) range of cells [lo_last, hi_last]; empty when the row is outside the grid.
+__device__ __forceinline__ void grid_row(const uint32_t* __restrict__ cfirst, const GridParams& P, int64_t a0,
+                                         int64_t a1, uint32_t D, uint32_t lo_last, uint32_t hi_last, uint32_t& b,
+                                         uint32_t& e) {
+  b = e = 0;
+  uint32_t prefix;
+  if (P.g == 2) {
+    if (a0 < 0 || a0 >= P.dims[0]) return;
+    prefix = static_cast<uint32_t>(a0);
+  } else {
+    if (a0 < 0 || a0 >= P.dims[0] || a1 < 0 || a1 >= P.dims[1]) return;
+    prefix = static_cast<uint32_t>(a0) * P.dims[1] + static_cast<uint32_t>(a1);
+  }
+  const uint32_t base = prefix * D;
+  b = cfirst[base + lo_last];
+  e = cfirst[base + hi_last + 1];
+}
 
 // The forward half of the 3^g stencil of sorted position p as at most five
 // contiguous position ranges.  Cells of one "row" (all coordinates but the
@@ -42,84 +139,27 @@ struct GridIndex {
 //              spans cells c_last-1 .. c_last+1
 // Each unordered pair within the stencil appears in exactly one range of
 // exactly one of its two points.
-__device__ __forceinline__ int grid_ranges(const GridDev& G, uint32_t p, uint32_t cell, uint32_t rb[5],
-                                           uint32_t re[5]) {
-  uint32_t cc[3] = {0, 0, 0};
-  {
-    uint32_t c = cell;
-    for (int t = G.g - 1; t >= 0; --t) {
-      cc[t] = c % G.dims[t];
-      c /= G.dims[t];
-    }
+__device__ __forceinline__ GridRanges grid_ranges(const uint32_t* __restrict__ cfirst, const GridParams& P,
+                                                  uint32_t p, uint32_t cell) {
+  GridRanges R{};
+  const uint32_t D = P.g == 1 ? P.dims[0] : (P.g == 2 ? P.dims[1] : P.dims[2]);  // no dynamic indexing
+  const uint32_t prefix = P.fD.div(cell);
+  const uint32_t c_last = cell - prefix * D;
+  const uint32_t lo_last = c_last > 0 ? c_last - 1 : 0;
+  const uint32_t hi_last = c_last + 1 < D ? c_last + 1 : D - 1;
+  R.b0 = p + 1;
+  R.e0 = cfirst[cell - c_last + hi_last + 1];
+  if (P.g == 2) {
+    grid_row(cfirst, P, static_cast<int64_t>(prefix) + 1, 0, D, lo_last, hi_last, R.b1, R.e1);
+  } else if (P.g == 3) {
+    const uint32_t q1 = P.f1.div(prefix);
+    const int64_t c0 = q1, c1 = prefix - q1 * P.dims[1];
+    grid_row(cfirst, P, c0, c1 + 1, D, lo_last, hi_last, R.b1, R.e1);
+    grid_row(cfirst, P, c0 + 1, c1 - 1, D, lo_last, hi_last, R.b2, R.e2);
+    grid_row(cfirst, P, c0 + 1, c1, D, lo_last, hi_last, R.b3, R.e3);
+    grid_row(cfirst, P, c0 + 1, c1 + 1, D, lo_last, hi_last, R.b4, R.e4);
   }
-  const int last = G.g - 1;
-  const uint32_t D = G.dims[last];
-  const uint32_t lo_last = cc[last] > 0 ? cc[last] - 1 : 0;
-  const uint32_t hi_last = cc[last] + 1 < D ? cc[last] + 1 : D - 1;
-  // own row
-  int k = 0;
-  rb[k] = p + 1;
-  re[k] = G.cfirst[cell - cc[last] + hi_last + 1];
-  ++k;
-  if (G.g == 1) return k;
-  // rows are identified by the prefix (c0[, c1]); row base id = prefix * D
-  auto add_row = [&](int64_t a0, int64_t a1) {
-    uint32_t prefix;
-    if (G.g == 2) {
-      if (a0 < 0 || a0 >= G.dims[0]) return;
-      prefix = static_cast<uint32_t>(a0);
-    } else {
-      if (a0 < 0 || a0 >= G.dims[0] || a1 < 0 || a1 >= G.dims[1]) return;
-      prefix = static_cast<uint32_t>(a0) * G.dims[1] + static_cast<uint32_t>(a1);
-    }
-    const uint32_t base = prefix * D;
-    rb[k] = G.cfirst[base + lo_last];
-    re[k] = G.cfirst[base + hi_last + 1];
-    ++k;
-  };
-  if (G.g == 2) {
-    add_row(static_cast<int64_t>(cc[0]) + 1, 0);
-  } else {
-    add_row(cc[0], static_cast<int64_t>(cc[1]) + 1);
-    add_row(static_cast<int64_t>(cc[0]) + 1, static_cast<int64_t>(cc[1]) - 1);
-    add_row(static_cast<int64_t>(cc[0]) + 1, cc[1]);
-    add_row(static_cast<int64_t>(cc[0]) + 1, static_cast<int64_t>(cc[1]) + 1);
-  }
-  return k;
+  return R;
 }
-
-// The 0.1%..99.9% quantile box of the first g keys, from a deterministic
-// strided sample (a tuning input only: clamping keeps any box exact).
-void grid_sample_box(const float* keys, uint32_t n, int nk, int g, double lo[3], double span[3], cudaStream_t s);
-// Cell width giving about `occupancy` points per cell over the box.
-double grid_occupancy_width(uint32_t n, int g, const double span[3], double occupancy);
-// (Re)build `gi` over `keys` (n x nk, original order) with cell width >= w
-// (widened if the dense cell table would exceed 2^24 cells).
-void build_grid(const float* keys, uint32_t n, int nk, int g, double w, const double lo[3], const double span[3],
-                GridIndex& gi, cudaStream_t s);
-
-// Decode a cell id, then the s-th cell of the 3^g stencil around it.
-__device__ __forceinline__ void grid_coords(const GridDev& G, uint32_t c, uint32_t cc[3]) {
-  for (int t = G.g - 1; t >= 0; --t) {
-    cc[t] = c % G.dims[t];
-    c /= G.dims[t];
-  }
-}
-__device__ __forceinline__ bool grid_stencil(const GridDev& G, const uint32_t cc[3], int s, uint32_t* nc) {
-  int off[3] = {0, 0, 0};
-  for (int t = G.g - 1; t >= 0; --t) {
-    off[t] = s % 3 - 1;
-    s /= 3;
-  }
-  uint32_t c = 0;
-  for (int t = 0; t < G.g; ++t) {
-    const int64_t v = static_cast<int64_t>(cc[t]) + off[t];
-    if (v < 0 || v >= static_cast<int64_t>(G.dims[t])) return false;
-    c = c * G.dims[t] + static_cast<uint32_t>(v);
-  }
-  *nc = c;
-  return true;
-}
-__host__ __device__ __forceinline__ int grid_stencil_size(int g) { return g == 1 ? 3 : (g == 2 ? 9 : 27); }
 
 }  // namespace psg

@@ -9,6 +9,8 @@
 //   mu/sigma  per-window FP64 statistics of z-normalised window sets
 #pragma once
 
+#include <memory>
+
 #include "psg_internal.cuh"
 
 namespace psg {
@@ -65,6 +67,9 @@ struct psg_pointset {
   double Rn = 0.0;             // max narrowing radius, working units
   double maxabs = 0.0;         // max |X|
   uint64_t h2d_bytes = 0;
+  // solve workspaces reused across calls on this point set (nk = 4 / 8);
+  // type-erased here, owned by the closest-pair engine (psg_cpp.cu)
+  std::shared_ptr<void> cpp_work[2];
 
   psg::ExactSrc exact() const {
     psg::ExactSrc s;

@@ -172,7 +172,124 @@ int sort_impl(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bi
   return cur;
 }
 
+// ---- exclusive scan ---------------------------------------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+
+// Block-wide exclusive scan of one value per thread; returns the block total.
+__device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* warp_sums, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = warp_sums[lane];
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    warp_sums[lane] = wi - w;
+    if (lane == 31) warp_sums[32] = wi;
+  }
+  __syncthreads();
+  total = warp_sums[32];
+  return warp_sums[warp] + incl - v;
+}
+
+// count = *dcells + 1 when dcells is given (device-side size), else count.
+__device__ __forceinline__ size_t scan_count(size_t count, const uint64_t* dcells) {
+  return dcells ? static_cast<size_t>(*dcells) + 1 : count;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint32_t* __restrict__ in, size_t count,
+                                                             const uint64_t* __restrict__ dcells,
+                                                             uint32_t* __restrict__ sums) {
+  __shared__ uint32_t ws[33];
+  count = scan_count(count, dcells);
+  if (static_cast<size_t>(blockIdx.x) * kScanTile >= count) return;
+  const size_t base = static_cast<size_t>(blockIdx.x) * kScanTile + static_cast<size_t>(threadIdx.x) * kScanItems;
+  uint32_t v = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v += base + i < count ? in[base + i] : 0u;
+  uint32_t total;
+  block_exclusive(v, ws, total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(uint32_t* __restrict__ sums, size_t count,
+                                                           const uint64_t* __restrict__ dcells) {
+  __shared__ uint32_t ws[33];
+  count = scan_count(count, dcells);
+  const int nb = static_cast<int>((count + kScanTile - 1) / kScanTile);
+  constexpr int kPer = 8;  // up to 8192 tiles
+  uint32_t v[kPer], s = 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int k = threadIdx.x * kPer + i;
+    v[i] = k < nb ? sums[k] : 0u;
+    s += v[i];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive(s, ws, total);
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int k = threadIdx.x * kPer + i;
+    if (k < nb) sums[k] = run;
+    run += v[i];
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __restrict__ in, size_t count,
+                                                             const uint64_t* __restrict__ dcells,
+                                                             const uint32_t* __restrict__ sums,
+                                                             uint32_t* __restrict__ out) {
+  __shared__ uint32_t ws[33];
+  count = scan_count(count, dcells);
+  if (static_cast<size_t>(blockIdx.x) * kScanTile >= count) return;
+  const size_t base = static_cast<size_t>(blockIdx.x) * kScanTile + static_cast<size_t>(threadIdx.x) * kScanItems;
+  uint32_t v[kScanItems], s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < count ? in[base + i] : 0u;
+    s += v[i];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive(s, ws, total) + sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < count) out[base + i] = run;
+    run += v[i];
+  }
+}
+
 }  // namespace
+
+size_t scan_temp_words(size_t count) { return (count + kScanTile - 1) / kScanTile + 1; }
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_t* temp, cudaStream_t s) {
+  exclusive_scan_u32_dev(in, out, count, nullptr, temp, s);
+}
+
+void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count, const uint64_t* dcells,
+                            uint32_t* temp, cudaStream_t s) {
+  if (max_count == 0) return;
+  const int nb = static_cast<int>((max_count + kScanTile - 1) / kScanTile);
+  if (nb > 8 * kScanThreads) throw std::runtime_error("exclusive_scan_u32: input too large");
+  k_scan_tiles<<<nb, kScanThreads, 0, s>>>(in, max_count, dcells, temp);
+  PSG_LAUNCHED();
+  k_scan_top<<<1, kScanThreads, 0, s>>>(temp, max_count, dcells);
+  PSG_LAUNCHED();
+  k_scan_apply<<<nb, kScanThreads, 0, s>>>(in, max_count, dcells, temp, out);
+  PSG_LAUNCHED();
+}
 
 size_t radix_hist_words(size_t n) {
   const size_t t = static_cast<size_t>(kThreads) * items_for(n);

@@ -15,6 +15,15 @@ namespace psg {
 // buffer holding the result.  vals may be {nullptr, nullptr}.  `hist` needs
 // radix_hist_words(n) u32 words.
 size_t radix_hist_words(size_t n);
+
+// out[i] = in[0] + ... + in[i-1] (u32), count <= 2^25; `temp` needs
+// scan_temp_words(count) words.  Three kernels: tile sums, scan of the tile
+// sums (one block), tile scans with the carried-in offset.
+size_t scan_temp_words(size_t count);
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_t* temp, cudaStream_t s);
+// Same with the length read on device: count = *dcells + 1 (<= max_count).
+void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count, const uint64_t* dcells,
+                            uint32_t* temp, cudaStream_t s);
 template <class K>
 int radix_sort(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bit, uint32_t* hist,
                cudaStream_t s);
