@@ -17,7 +17,9 @@ template <class F>
 int guarded(F&& f) {
   try {
     psg::prof_begin();
-    psg::KernelSpan span(psg::ctx().stream);  // device span of the whole call
+    psg::Ctx& c = psg::ctx();
+    std::lock_guard<std::mutex> lock(c.mu);  // one call at a time per device (shared workspaces)
+    psg::KernelSpan span(c.stream);          // device span of the whole call
     f();
     psg::g_prof.total_ms = span.stop();
     psg::g_prof.launches = psg::g_launches;

@@ -333,6 +333,37 @@ void launch_project_smem(const float* X, uint32_t n, const Directions& dir, floa
   k_project_smem<NK, D><<<grid, 32 * kWarpsPerBlock, kSmem, s>>>(X, n, u, keys, nb);
 }
 
+// d < 32 (C1 d=2, C4 d=3, ...): one thread per row, U by value in the
+// constant bank (so the launch carries no host-side buffer: graph-safe).
+struct USmall {
+  float u[kMaxKeys][32];
+};
+
+template <int NK>
+__global__ void __launch_bounds__(256) k_project_small(const float* __restrict__ X, uint32_t n, int d,
+                                                       const __grid_constant__ USmall U, float* __restrict__ keys,
+                                                       unsigned* __restrict__ norm2_bits) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  float nn = 0.f;
+  if (r < n) {
+    float acc[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
+    const float* row = X + static_cast<size_t>(r) * d;
+    for (int t = 0; t < d; ++t) {
+      const float x = __ldg(row + t);
+      nn = fmaf(x, x, nn);
+#pragma unroll
+      for (int k = 0; k < NK; ++k) acc[k] = fmaf(U.u[k][t], x, acc[k]);
+    }
+    float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(r) * NK);
+#pragma unroll
+    for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+  }
+  nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
+  if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
+}
+
 // Small or irregular d: one thread per row, U staged in shared memory.
 template <int NK>
 __global__ void __launch_bounds__(256) k_project_thread(const float* __restrict__ X, uint32_t n, int d,
@@ -660,26 +691,24 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
     const uint32_t mo = a.sidx[p];
     const GridParams P = *G.gp;
-    const GridRanges R = grid_ranges(G.cfirst, P, p, G.scell[p]);
-    int seen = 0;
+    const GridFlat F = grid_flat(grid_ranges(G.cfirst, P, p, G.scell[p]));
+    const uint32_t L = min(F.total, static_cast<uint32_t>(cap));
+    // four candidates per step: all key loads in flight before any math
+    for (uint32_t t0 = 0; t0 < L; t0 += 4) {
+      uint32_t jj[4];
+      float kk[4][NK];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      for (uint32_t j = R.b(r); j < R.e(r) && seen < cap; ++j, ++seen) {
-        float kj[NK];
-        load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
-        float g = kj[0] - mk[0];
-        float sl = g * g;
-        g = kj[1] - mk[1];
-        sl = fmaf(g, g, sl);
-        if (sl >= best_lb) continue;
+      for (int u = 0; u < 4; ++u) {
+        jj[u] = t0 + u < L ? F.at(t0 + u) : p;
+        load_keys<NK>(a.skeys + static_cast<size_t>(jj[u]) * NK, kk[u]);
+      }
 #pragma unroll
-        for (int k = 2; k < NK; ++k) {
-          g = kj[k] - mk[k];
-          sl = fmaf(g, g, sl);
-        }
-        if (sl < best_lb && (a.zone <= 1 || admissible(mo, a.sidx[j], a.zone))) {
+      for (int u = 0; u < 4; ++u) {
+        if (t0 + u >= L) break;
+        const float sl = lb2_full<NK>(mk, kk[u]);
+        if (sl < best_lb && (a.zone <= 1 || admissible(mo, a.sidx[jj[u]], a.zone))) {
           best_lb = sl;
-          best_j = j;
+          best_j = jj[u];
         }
       }
     }
@@ -796,6 +825,101 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan(ScanArgs a, GridDev G, u
   for (int o = 16; o; o >>= 1) visited += __shfl_xor_sync(kFull, visited, o);
   if (lane == 0 && visited) atomicAdd(a.visited, visited);
   if (tid == 0 && nevals) atomicAdd(a.evals, nevals);
+}
+
+// Before the scan: the grid must hold every pair whose key gaps are within
+// the window of the bound reached by the bootstrap; otherwise flag a rebuild
+// (the host widens the cells and reruns the scan).  One thread, so every
+// block of the scan sees the same decision.
+__global__ void k_check_grid(unsigned* best, const Budget* bud, const GridParams* gp, unsigned* regrid,
+                             unsigned* check_best, Thresholds* th_out) {
+  const unsigned b = *best;
+  const Thresholds th = budget_thresholds_s32(*bud, __uint_as_float(b));
+  *check_best = b;
+  *th_out = th;  // the scan's starting thresholds, computed once
+  *regrid = gp ? !(gp->w >= static_cast<double>(th.win) * (1.0 + 1e-5)) : 0u;
+}
+
+// K3b (grid): one pass per sorted position over its (at most five) stencil
+// ranges with the key lower bound at the threshold it read at start (the
+// bound only tightens, so a stale threshold only admits more); survivors go to
+// a shared-memory queue (global spill list when full) and whole warps evaluate
+// them as exact FP32 distances at the end of the block.
+template <int NK>
+__global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi,
+                                                         const unsigned* __restrict__ regrid,
+                                                         const Thresholds* __restrict__ th0) {
+  __shared__ uint32_t qp[kQueue], qj[kQueue];
+  __shared__ int qn;
+  if (*regrid) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) qn = 0;
+  __syncthreads();
+  const uint32_t p = lo + blockIdx.x * kThreads + tid;
+  unsigned long long visited = 0;
+  if (p < hi) {
+    float mk[NK];
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+    const uint32_t mo = a.sidx[p];
+    const GridParams P = *G.gp;
+    const GridFlat F = grid_flat(grid_ranges(G.cfirst, P, p, G.scell[p]));
+    const float lb2 = th0->lb2;
+    const bool zoned = a.zone > 1;
+    // four candidates per step: all loads in flight before any math
+    for (uint32_t t0 = 0; t0 < F.total; t0 += 4) {
+      uint32_t jj[4], oo[4];
+      float kk[4][NK];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        jj[u] = t0 + u < F.total ? F.at(t0 + u) : p;
+        load_keys<NK>(a.skeys + static_cast<size_t>(jj[u]) * NK, kk[u]);
+        oo[u] = zoned ? a.sidx[jj[u]] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t0 + u >= F.total) break;
+        if (zoned && !admissible(mo, oo[u], a.zone)) continue;
+        ++visited;
+        const uint32_t j = jj[u];
+        const float sl = lb2_full<NK>(mk, kk[u]);
+        if (sl > lb2) continue;
+        const int slot = atomicAdd(&qn, 1);
+        if (slot < kQueue) {
+          qp[slot] = p;
+          qj[slot] = j;
+        } else {
+          const unsigned o = atomicAdd(a.ovf_n, 1u);
+          if (o < a.ovf_cap) {
+            a.ovf_p[o] = p;
+            a.ovf_j[o] = j;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int nq = min(qn, kQueue);
+  if (nq > 0) {
+    const float band = th0->band;  // >= the band of any tighter bound: a superset, refiltered by k_recheck
+    if (a.d <= kInlineD) {
+      for (int i = tid; i < nq; i += kThreads) {
+        const uint32_t pi = qp[i], pj = qj[i];
+        const float sd = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                       a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
+        record(a, pi, pj, sd, band);
+      }
+    } else {
+      for (int i = warp; i < nq; i += kThreads / 32) {
+        const uint32_t pi = qp[i], pj = qj[i];
+        const float sd = warp_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                     a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d, lane);
+        if (lane == 0) record(a, pi, pj, sd, band);
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) visited += __shfl_xor_sync(kFull, visited, o);
+  if (lane == 0 && visited) atomicAdd(a.visited, visited);
+  if (tid == 0 && nq) atomicAdd(a.evals, static_cast<unsigned long long>(nq));
 }
 
 // Pairs that overflowed the shared-memory queue.
@@ -1043,8 +1167,17 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
       case 8128: launch_project_smem<8, 128>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
       default: launch_project_smem<8, 256>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
     }
+  } else if (d < 32) {
+    USmall u{};
+    for (int k = 0; k < dir.nk; ++k)
+      for (int t = 0; t < d; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * d + t];
+    if (dir.nk == 4)
+      k_project_small<4><<<blocks_for(n, 256), 256, 0, s>>>(ps.X, n, d, u, keys, norm2_bits);
+    else
+      k_project_small<8><<<blocks_for(n, 256), 256, 0, s>>>(ps.X, n, d, u, keys, norm2_bits);
   } else {
-    // small or irregular d: thread per row, U staged in shared memory
+    // irregular d: thread per row, U staged in shared memory (not graph-safe:
+    // solve_graph skips these)
     DevBuf<float> U(dir.U.size(), s);  // freed stream-ordered after the launch
     PSG_CUDA(cudaMemcpyAsync(U.p, dir.U.data(), dir.U.size() * sizeof(float), cudaMemcpyHostToDevice, s));
     const size_t ubytes = static_cast<size_t>(dir.nk) * d * sizeof(float);
@@ -1091,6 +1224,9 @@ Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm
 
 CppWork::~CppWork() {
   if (host_st) cudaFreeHost(host_st);
+  if (gexec) cudaGraphExecDestroy(gexec);
+  for (cudaEvent_t e : gev)
+    if (e) cudaEventDestroy(e);
 }
 
 namespace {
@@ -1249,11 +1385,14 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
 }
 
 namespace {
-// Stage/kernel times of plan_create, read once the stream has synchronised.
+// Stage/kernel times of plan_create and the bootstrap, read once the stream
+// has synchronised.
 void collect_prep(CppPlan& plan) {
   if (plan.proj_span) g_prof.project_kernel_ms += plan.proj_span->ms();
+  if (plan.boot_span) g_prof.bootstrap_kernel_ms += plan.boot_span->ms();
   if (plan.prep_tm) prof_stages(*plan.prep_tm);
   plan.proj_span.reset();
+  plan.boot_span.reset();
   plan.prep_tm.reset();
 }
 }  // namespace
@@ -1272,7 +1411,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
     ++g_launches;
   }
   if (plan.grid) {
-    KernelSpan ks(s);
+    plan.boot_span = std::make_unique<KernelSpan>(s);
     if (hi > lo) {
       if (plan.dir.nk == 4)
         k_grid_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, lo, hi,
@@ -1283,13 +1422,11 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
       PSG_LAUNCHED();
       ++g_launches;
     }
-    ks.end();
-    tm.mark("bootstrap");
+    plan.boot_span->end();
+    if (!plan.sync_bootstrap) return INFINITY;  // single-part solve: no host round trip here
     read_state(plan, s);  // synchronises the stream
     collect_prep(plan);
     trace("bootstrap: done");
-    g_prof.bootstrap_kernel_ms += ks.ms();
-    prof_stages(tm);
     return bits_to_float(plan.work->host_st->best);
   }
   // Window engine.  Adaptive width: widen while the window the bound implies
@@ -1321,125 +1458,92 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   return read_best(a.best, s);
 }
 
-psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, float bound_s32) {
-  Ctx& c = ctx();
-  cudaStream_t s = c.stream;
-  const uint64_t n = plan.ps->n;
-  CppWork& W = *plan.work;
-  uint32_t lo, hi;
-  part_range(n, part, nparts, &lo, &hi);
-  StageTimer tm(s);
-  // The bound handed in is the (global) minimum of what the bootstraps
-  // returned; lower the device copy to it.
-  k_min_bound<<<1, 1, 0, s>>>(&W.st.p->best, bound_s32);
-  PSG_LAUNCHED();
-  ++g_launches;
-  if (plan.grid) {
-    // The grid must hold every pair whose key gaps are within the window of
-    // the bound: widen the cells when the occupancy width is smaller.  Every
-    // rank derives the same grid from the same bound.
-    const float b = std::min(bound_s32, bits_to_float(W.host_st->best));
-    const Thresholds th0 = budget_thresholds_s32(plan.bud, b);
-    const double need = static_cast<double>(th0.win) * (1.0 + 1e-5);
-    if (!(plan.gp.w >= need)) {
-      if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
-      grid_params_for(plan.gp, plan.g, need, W.host_st->box_lo, W.host_st->box_span);
-      PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
-      build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
-      tm.mark("regrid");
-    }
-  }
+namespace {
+
+void ensure_candidates(CppWork& W, cudaStream_t s) {
   if (W.cand_cap == 0) {
     W.cand_cap = 1u << 16;
-    W.ovf_cap = plan.grid ? 1 : (1u << 20);
+    W.ovf_cap = 1u << 20;
   }
-  unsigned ncand = 0;
-  KernelSpan* scan_span = nullptr;
-  for (int attempt = 0;; ++attempt) {
-    if (W.cand_p.n < W.cand_cap) {
-      W.cand_p.alloc(W.cand_cap, s);
-      W.cand_j.alloc(W.cand_cap, s);
-      W.cand_s.alloc(W.cand_cap, s);
-      W.d64.alloc(W.cand_cap, s);
-    }
-    if (W.ovf_p.n < W.ovf_cap) {
-      W.ovf_p.alloc(W.ovf_cap, s);
-      W.ovf_j.alloc(W.ovf_cap, s);
-    }
-    ScanArgs a = make_args(plan);
-    k_scan_reset<<<1, 1, 0, s>>>(W.st.p);
+  if (W.cand_p.n < W.cand_cap) {
+    W.cand_p.alloc(W.cand_cap, s);
+    W.cand_j.alloc(W.cand_cap, s);
+    W.cand_s.alloc(W.cand_cap, s);
+    W.d64.alloc(W.cand_cap, s);
+  }
+  if (W.ovf_p.n < W.ovf_cap) {
+    W.ovf_p.alloc(W.ovf_cap, s);
+    W.ovf_j.alloc(W.ovf_cap, s);
+  }
+}
+
+// Grow the candidate / spill buffers after an overflow; true = rescan needed.
+bool grow_on_overflow(CppWork& W, const DevState& h) {
+  if (h.ovf_n > W.ovf_cap) {  // spill list overflowed: rescan with the tighter bound
+    W.ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h.ovf_n) * 2, 1u << 28);
+    return true;
+  }
+  if (h.cand_n > W.cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
+    W.cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h.cand_n) * 2, 1u << 28);
+    return true;
+  }
+  return false;
+}
+
+// One scan attempt, enqueued only (no host synchronisation): reset, grid
+// check, candidate scan, spill-list evaluation, speculative FP64 recheck
+// (correct whenever nothing overflowed; the caller checks), pick, and the
+// state copy to the pinned host mirror.  Returns the scan kernel's span.
+KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, cudaStream_t s) {
+  Ctx& c = ctx();
+  CppWork& W = *plan.work;
+  DevState* st = W.st.p;
+  ScanArgs a = make_args(plan);
+  k_scan_reset<<<1, 1, 0, s>>>(st);
+  PSG_LAUNCHED();
+  if (plan.grid) {
+    // The grid must hold every pair whose key gaps are within the window of
+    // the bound; decided on device from the bound every rank shares.
+    k_check_grid<<<1, 1, 0, s>>>(&st->best, &st->bud, W.gi.gp.p, &st->regrid, &st->check_best, &st->th);
     PSG_LAUNCHED();
-    delete scan_span;
-    scan_span = new KernelSpan(s);
-    if (hi > lo) {
-      if (plan.grid) {
-        if (plan.dir.nk == 4)
-          k_grid_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi);
-        else
-          k_grid_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi);
-      } else if (plan.dir.nk == 4)
-        k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
-      else
-        k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
-      PSG_LAUNCHED();
-      g_launches += 2;
-      ++g_prof.scan_launches;
-    }
-    scan_span->end();
-    if (!plan.grid) {  // spill list of the window engine (grid threads retry instead)
-      k_eval_list<<<c.sm_count * 8, 256, 0, s>>>(a, W.ovf_p.p, W.ovf_j.p);
-      PSG_LAUNCHED();
-      ++g_launches;
-    }
-    // speculative recheck: correct whenever nothing overflowed (checked below)
-    const ExactSrc ex = plan.ps->exact();
-    const int nb = c.sm_count * 2;
-    DevState* st = W.st.p;
+  }
+  KernelSpan* span = new KernelSpan(s);
+  if (hi > lo) {
     if (plan.grid) {
       if (plan.dir.nk == 4)
-        k_recheck<4, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+        k_grid_scan2<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th);
       else
-        k_recheck<8, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+        k_grid_scan2<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th);
     } else if (plan.dir.nk == 4)
-      k_recheck<4, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+      k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
     else
-      k_recheck<8, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+      k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
     PSG_LAUNCHED();
-    k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
-    PSG_LAUNCHED();
-    g_launches += 2;
-    read_state(plan, s);
-    const DevState& h = *W.host_st;
-    if (attempt > 12)
-      throw std::runtime_error("closest_pair: candidate buffers kept overflowing (cand " + std::to_string(h.cand_n) +
-                               "/" + std::to_string(W.cand_cap) + ", spill " + std::to_string(h.ovf_n) + "/" +
-                               std::to_string(W.ovf_cap) + ")");
-    if (!plan.grid && h.ovf_n > W.ovf_cap) {  // spill list overflowed: rescan with the tighter bound
-      W.ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h.ovf_n) * 2, 1u << 28);
-      continue;
-    }
-    if (h.cand_n > W.cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
-      W.cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h.cand_n) * 2, 1u << 28);
-      continue;
-    }
-    ncand = h.cand_n;
-    break;
+    ++g_prof.scan_launches;
   }
-  g_prof.scan_kernel_ms += scan_span->ms();
-  delete scan_span;
-  tm.mark("scan+recheck");
-  trace("scan+recheck: done");
-  const DevState h = *W.host_st;
-  uint64_t exits = 0;
-  uint64_t wp = h.visited;
-  if (!plan.grid) {
-    const Thresholds th = budget_thresholds_s32(plan.bud, bits_to_float(h.best));
-    wp = window_pairs(plan, lo, hi, th.win, &exits, s);
-    tm.mark("stats");
-  }
-  PSG_CUDA(cudaStreamSynchronize(s));
-  prof_stages(tm);
+  span->end();
+  k_eval_list<<<c.sm_count * 8, 256, 0, s>>>(a, W.ovf_p.p, W.ovf_j.p);  // queue spill list
+  PSG_LAUNCHED();
+  const ExactSrc ex = plan.ps->exact();
+  const int nb = c.sm_count * 2;
+  if (plan.grid) {
+    if (plan.dir.nk == 4)
+      k_recheck<4, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+    else
+      k_recheck<8, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+  } else if (plan.dir.nk == 4)
+    k_recheck<4, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+  else
+    k_recheck<8, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+  PSG_LAUNCHED();
+  k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
+  PSG_LAUNCHED();
+  PSG_CUDA(cudaMemcpyAsync(W.host_st, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  g_launches += plan.grid ? 7 : 6;
+  return span;
+}
 
+psg_pair_result result_from(const DevState& h, uint64_t wp, uint64_t exits) {
   psg_pair_result r{};
   if (h.lex == ~0ull) {
     r.index_i = r.index_j = UINT64_MAX;
@@ -1454,20 +1558,177 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
   r.stats.inner_loop_exits = exits;
   g_prof.window_pairs += wp;
   g_prof.lb_survivors += h.evals;
-  g_prof.candidates += ncand;
+  g_prof.candidates += h.cand_n;
   return r;
 }
 
-psg_pair_result cpp_solve(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone) {
-  std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));
-  const float b = cpp_plan_bootstrap(*plan, 0, 1);
-  psg_pair_result r = cpp_plan_scan(*plan, 0, 1, b);
+}  // namespace
+
+psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, float bound_s32) {
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  const uint64_t n = plan.ps->n;
+  CppWork& W = *plan.work;
+  uint32_t lo, hi;
+  part_range(n, part, nparts, &lo, &hi);
+  StageTimer tm(s);
+  // The bound handed in is the (global) minimum of what the bootstraps
+  // returned; lower the device copy to it.
+  k_min_bound<<<1, 1, 0, s>>>(&W.st.p->best, bound_s32);
+  PSG_LAUNCHED();
+  ++g_launches;
+  KernelSpan* scan_span = nullptr;
+  for (int attempt = 0;; ++attempt) {
+    ensure_candidates(W, s);
+    delete scan_span;
+    scan_span = scan_enqueue(plan, lo, hi, s);
+    PSG_CUDA(cudaStreamSynchronize(s));
+    plan.bud = W.host_st->bud;
+    if (plan.grid) PSG_CUDA(cudaMemcpy(&plan.gp, W.gi.gp.p, sizeof(GridParams), cudaMemcpyDeviceToHost));
+    collect_prep(plan);
+    const DevState& h = *W.host_st;
+    if (plan.grid && h.regrid) {
+      // widen the cells to the key window of the bound the check saw, rebuild, rescan
+      const Thresholds th0 = budget_thresholds_s32(plan.bud, bits_to_float(h.check_best));
+      const double need = static_cast<double>(th0.win) * (1.0 + 2e-5);
+      if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
+      grid_params_for(plan.gp, plan.g, need, h.box_lo, h.box_span);
+      PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
+      build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
+      tm.mark("regrid");
+      continue;
+    }
+    if (attempt > 12)
+      throw std::runtime_error("closest_pair: candidate buffers kept overflowing (cand " + std::to_string(h.cand_n) +
+                               "/" + std::to_string(W.cand_cap) + ", spill " + std::to_string(h.ovf_n) + "/" +
+                               std::to_string(W.ovf_cap) + ")");
+    if (grow_on_overflow(W, h)) continue;
+    break;
+  }
+  g_prof.scan_kernel_ms += scan_span->ms();
+  delete scan_span;
+  tm.mark("scan+recheck");
+  trace("scan+recheck: done");
+  const DevState h = *W.host_st;
+  uint64_t exits = 0, wp = h.visited;
+  if (!plan.grid) {
+    const Thresholds th = budget_thresholds_s32(plan.bud, bits_to_float(h.best));
+    wp = window_pairs(plan, lo, hi, th.win, &exits, s);
+    tm.mark("stats");
+  }
+  PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
+  return result_from(h, wp, exits);
+}
+
+namespace {
+
+psg_pair_result finalize(psg_pair_result r, uint64_t n, uint64_t zone) {
   if (r.index_i == UINT64_MAX) throw invalid_argument("no admissible pair");
-  const uint64_t adm = admissible_pairs(ps->n, zone);
+  const uint64_t adm = admissible_pairs(n, zone);
   const uint64_t used = r.stats.pairs_examined + r.stats.pairs_pruned_by_reference;
   if (used > adm) r.stats.pairs_pruned_by_reference = adm - r.stats.pairs_examined;
   r.stats.pairs_skipped_by_exit = adm - r.stats.pairs_examined - r.stats.pairs_pruned_by_reference;
   return r;
+}
+
+bool graphs_enabled() {
+  static const bool off = std::getenv("PSG_NO_GRAPH") != nullptr;
+  return !off;
+}
+
+// The single-part grid solve as one CUDA graph: plan (projection, grid
+// build), bootstrap and one scan attempt, all device-resident, ending with the
+// state copy to pinned host memory.  Captured on first use per (q, seed, zone)
+// and replayed afterwards: one launch per solve instead of ~30.  Returns false
+// when the replay's state asks for a regrid / bigger buffers (the caller then
+// runs the regular path, which handles those).
+bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone, psg_pair_result* out) {
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  const Directions dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
+  const char* eng = std::getenv("PSG_ENGINE");
+  if (dir.q < 2 || (eng && std::string(eng) == "window")) return false;
+  const int d = ps->d;
+  if (!(d < 32 || d == 32 || d == 64 || d == 128 || d == 256)) return false;  // projection needs a host buffer
+  std::shared_ptr<CppWork> work = get_work(ps, dir.nk, s);
+  CppWork& W = *work;
+  if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone) {
+    if (W.gexec) {
+      cudaGraphExecDestroy(W.gexec);
+      W.gexec = nullptr;
+    }
+    // every allocation happens before capture
+    W.gi.ensure(static_cast<uint32_t>(ps->n), dir.nk, s);
+    ensure_candidates(W, s);
+    for (cudaEvent_t& e : W.gev)
+      if (!e) PSG_CUDA(cudaEventCreate(&e));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    cudaGraph_t graph = nullptr;
+    const uint64_t launches0 = g_launches;
+    PSG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    g_capturing = true;
+    g_cap_ev = W.gev;
+    g_cap_next = 0;
+    g_cap_max = 6;
+    try {
+      std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));
+      plan->sync_bootstrap = false;
+      cpp_plan_bootstrap(*plan, 0, 1);
+      delete scan_enqueue(*plan, 0, static_cast<uint32_t>(ps->n), s);
+    } catch (...) {
+      g_capturing = false;
+      g_cap_ev = nullptr;
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    g_capturing = false;
+    g_cap_ev = nullptr;
+    PSG_CUDA(cudaStreamEndCapture(s, &graph));
+    const cudaError_t ie = cudaGraphInstantiate(&W.gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    PSG_CUDA(ie);
+    W.gq = q;
+    W.gseed = seed;
+    W.gzone = zone;
+    W.glaunches = g_launches - launches0;
+    g_launches = launches0;
+  }
+  PSG_CUDA(cudaGraphLaunch(W.gexec, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  g_launches += W.glaunches;
+  const DevState h = *W.host_st;
+  if (h.regrid || h.cand_n > W.cand_cap || h.ovf_n > W.ovf_cap) {
+    grow_on_overflow(W, h);
+    return false;
+  }
+  float ms = 0.f;
+  PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[0], W.gev[1]));
+  g_prof.project_kernel_ms += ms;
+  PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[2], W.gev[3]));
+  g_prof.bootstrap_kernel_ms += ms;
+  PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[4], W.gev[5]));
+  g_prof.scan_kernel_ms += ms;
+  ++g_prof.scan_launches;
+  *out = result_from(h, h.visited, 0);
+  return true;
+}
+
+}  // namespace
+
+psg_pair_result cpp_solve(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone) {
+  // validation first (same order as the reference), then the graph path
+  if (ps->n < 2) throw invalid_argument("closest_pair needs at least 2 points");
+  check_reference_args(ps->n, q, f);
+  if (admissible_pairs(ps->n, zone) == 0) throw invalid_argument("no admissible pair");
+  psg_pair_result r;
+  if (graphs_enabled() && ps->n < 0xffffffffull && solve_graph(ps, q, f, seed, zone, &r))
+    return finalize(r, ps->n, zone);
+  std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));
+  plan->sync_bootstrap = false;  // the bound stays on device between bootstrap and scan
+  const float b = cpp_plan_bootstrap(*plan, 0, 1);
+  return finalize(cpp_plan_scan(*plan, 0, 1, b), ps->n, zone);
 }
 
 }  // namespace psg

@@ -33,6 +33,9 @@ struct DevState {
   unsigned norm2_bits;  // max ||x||^2 (FP32 bits), from the projection
   unsigned best;        // FP32 bits of the best squared distance seen
   unsigned cand_n, ovf_n;
+  unsigned regrid;      // set by k_check_grid: cells narrower than the bound's key window
+  unsigned check_best;  // FP32 bits of the bound k_check_grid tested
+  Thresholds th;        // the scan's starting thresholds (from check_best)
   unsigned long long best64, lex, examined, evals, visited;
   Budget bud;
   double box_lo[3], box_span[3];
@@ -52,6 +55,12 @@ struct CppWork {
   DevBuf<float> cand_s;
   DevBuf<double> d64;
   uint32_t cand_cap = 0, ovf_cap = 0;
+  // The whole single-part grid solve captured once as a CUDA graph and
+  // replayed by later solves with the same (q, seed, zone) on this point set.
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t gq = 0, gseed = 0, gzone = 0;
+  uint64_t glaunches = 0;
+  cudaEvent_t gev[6] = {};  // project / bootstrap / scan spans recorded inside the graph
   ~CppWork();
 };
 
@@ -68,7 +77,8 @@ struct CppPlan {
   std::shared_ptr<CppWork> work;
   uint32_t width = 0;      // window engine: bootstrap width (sorted neighbours)
   std::unique_ptr<StageTimer> prep_tm;   // plan_create's stages, read at the first sync
-  std::unique_ptr<KernelSpan> proj_span;
+  std::unique_ptr<KernelSpan> proj_span, boot_span;
+  bool sync_bootstrap = true;  // false inside cpp_solve: bootstrap -> scan without a host round trip
 };
 
 CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone);

@@ -113,17 +113,27 @@ struct GridRanges {  // five ranges held in registers; empty ranges have b == e
   }
 };
 
+// The five ranges as one flattened candidate index space t in [0, total):
+// lets a thread issue several candidates' loads before using any of them.
+struct GridFlat {
+  uint32_t b0, b1, b2, b3, b4;  // range starts
+  uint32_t o1, o2, o3, o4;      // prefix offsets of ranges 1..4
+  uint32_t total;
+  __device__ __forceinline__ uint32_t at(uint32_t t) const {
+    return t < o1 ? b0 + t : t < o2 ? b1 + (t - o1) : t < o3 ? b2 + (t - o2) : t < o4 ? b3 + (t - o3) : b4 + (t - o4);
+  }
+};
+
 // Row (prefix) range of cells [lo_last, hi_last]; empty when the row is outside the grid.
-__device__ __forceinline__ void grid_row(const uint32_t* __restrict__ cfirst, const GridParams& P, int64_t a0,
-                                         int64_t a1, uint32_t D, uint32_t lo_last, uint32_t hi_last, uint32_t& b,
-                                         uint32_t& e) {
+__device__ __forceinline__ void grid_row(const uint32_t* __restrict__ cfirst, const GridParams& P, int a0, int a1,
+                                         uint32_t D, uint32_t lo_last, uint32_t hi_last, uint32_t& b, uint32_t& e) {
   b = e = 0;
   uint32_t prefix;
   if (P.g == 2) {
-    if (a0 < 0 || a0 >= P.dims[0]) return;
+    if (a0 < 0 || a0 >= static_cast<int>(P.dims[0])) return;
     prefix = static_cast<uint32_t>(a0);
   } else {
-    if (a0 < 0 || a0 >= P.dims[0] || a1 < 0 || a1 >= P.dims[1]) return;
+    if (a0 < 0 || a0 >= static_cast<int>(P.dims[0]) || a1 < 0 || a1 >= static_cast<int>(P.dims[1])) return;
     prefix = static_cast<uint32_t>(a0) * P.dims[1] + static_cast<uint32_t>(a1);
   }
   const uint32_t base = prefix * D;
@@ -150,16 +160,31 @@ __device__ __forceinline__ GridRanges grid_ranges(const uint32_t* __restrict__ c
   R.b0 = p + 1;
   R.e0 = cfirst[cell - c_last + hi_last + 1];
   if (P.g == 2) {
-    grid_row(cfirst, P, static_cast<int64_t>(prefix) + 1, 0, D, lo_last, hi_last, R.b1, R.e1);
+    grid_row(cfirst, P, static_cast<int>(prefix) + 1, 0, D, lo_last, hi_last, R.b1, R.e1);
   } else if (P.g == 3) {
     const uint32_t q1 = P.f1.div(prefix);
-    const int64_t c0 = q1, c1 = prefix - q1 * P.dims[1];
+    const int c0 = static_cast<int>(q1), c1 = static_cast<int>(prefix - q1 * P.dims[1]);
     grid_row(cfirst, P, c0, c1 + 1, D, lo_last, hi_last, R.b1, R.e1);
     grid_row(cfirst, P, c0 + 1, c1 - 1, D, lo_last, hi_last, R.b2, R.e2);
     grid_row(cfirst, P, c0 + 1, c1, D, lo_last, hi_last, R.b3, R.e3);
     grid_row(cfirst, P, c0 + 1, c1 + 1, D, lo_last, hi_last, R.b4, R.e4);
   }
   return R;
+}
+
+__device__ __forceinline__ GridFlat grid_flat(const GridRanges& R) {
+  GridFlat F;
+  F.b0 = R.b0;
+  F.b1 = R.b1;
+  F.b2 = R.b2;
+  F.b3 = R.b3;
+  F.b4 = R.b4;
+  F.o1 = R.e0 > R.b0 ? R.e0 - R.b0 : 0;
+  F.o2 = F.o1 + (R.e1 - R.b1);
+  F.o3 = F.o2 + (R.e2 - R.b2);
+  F.o4 = F.o3 + (R.e3 - R.b3);
+  F.total = F.o4 + (R.e4 - R.b4);
+  return F;
 }
 
 }  // namespace psg

@@ -41,6 +41,18 @@ struct Ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   std::mutex mu;  // the reference is reentrant; we serialise per device
+  std::vector<cudaEvent_t> events;  // pool: creating events per call costs microseconds each
+  cudaEvent_t get_event() {
+    if (events.empty()) {
+      cudaEvent_t e;
+      PSG_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = events.back();
+    events.pop_back();
+    return e;
+  }
+  void put_event(cudaEvent_t e) { events.push_back(e); }
 };
 Ctx& ctx();  // context of the current CUDA device (created on first use)
 
@@ -77,6 +89,14 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// True while the calling thread is capturing a CUDA graph: stage timers stay
+// out of the captured work (their events are pooled and reused); KernelSpans
+// take dedicated events from g_cap_ev (owned by the graph's workspace), in
+// creation order, so kernel times can still be read after each replay.
+extern thread_local bool g_capturing;
+extern thread_local cudaEvent_t* g_cap_ev;
+extern thread_local int g_cap_next, g_cap_max;
+
 // Stage timer: CUDA events on the library stream; read after the final sync.
 struct StageTimer {
   static constexpr int kMax = 16;
@@ -85,20 +105,22 @@ struct StageTimer {
   int count = 0;
   cudaStream_t s = nullptr;
   bool on = true;
-  explicit StageTimer(cudaStream_t st, bool enabled = true) : s(st), on(enabled) {
+  explicit StageTimer(cudaStream_t st, bool enabled = true) : s(st), on(enabled && !g_capturing) {
     if (!on) return;
-    for (auto& e : ev) PSG_CUDA(cudaEventCreate(&e));
+    ev[0] = ctx().get_event();
     PSG_CUDA(cudaEventRecord(ev[0], s));
   }
   void mark(const char* stage) {
     if (!on || count >= kMax) return;
     name[count] = stage;
     ++count;
+    ev[count] = ctx().get_event();
     PSG_CUDA(cudaEventRecord(ev[count], s));
   }
   ~StageTimer() {
     if (!on) return;
-    for (auto& e : ev) cudaEventDestroy(e);
+    Ctx& c = ctx();
+    for (int i = 0; i <= count; ++i) c.put_event(ev[i]);
   }
 };
 
@@ -109,27 +131,45 @@ void trace(const char* what);
 struct KernelSpan {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s = nullptr;
+  bool pooled = true;
   explicit KernelSpan(cudaStream_t st) : s(st) {
-    PSG_CUDA(cudaEventCreate(&a));
-    PSG_CUDA(cudaEventCreate(&b));
-    PSG_CUDA(cudaEventRecord(a, s));
+    if (g_capturing) {
+      pooled = false;
+      if (!g_cap_ev || g_cap_next + 1 >= g_cap_max) return;
+      a = g_cap_ev[g_cap_next++];
+      b = g_cap_ev[g_cap_next++];
+    } else {
+      a = ctx().get_event();
+      b = ctx().get_event();
+    }
+    record(a);
+  }
+  // Inside a capture, an external record is needed to become a graph node.
+  void record(cudaEvent_t e) {
+    PSG_CUDA(cudaEventRecordWithFlags(e, s, pooled ? cudaEventRecordDefault : cudaEventRecordExternal));
   }
   // Records the end event, waits for it, returns milliseconds.
   double stop() {
     end();
+    if (!b) return 0.0;
     PSG_CUDA(cudaEventSynchronize(b));
     return ms();
   }
   // Deferred form: end() now, ms() after a later stream synchronisation.
-  void end() { PSG_CUDA(cudaEventRecord(b, s)); }
+  void end() {
+    if (b) record(b);
+  }
   double ms() const {
+    if (!a || !b) return 0.0;
     float v = 0.f;
     PSG_CUDA(cudaEventElapsedTime(&v, a, b));
     return v;
   }
   ~KernelSpan() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
+    if (!pooled) return;
+    Ctx& c = ctx();
+    if (a) c.put_event(a);
+    if (b) c.put_event(b);
   }
 };
 

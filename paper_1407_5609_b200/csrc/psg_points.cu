@@ -16,6 +16,9 @@
 namespace psg {
 
 thread_local uint64_t g_launches = 0;
+thread_local bool g_capturing = false;
+thread_local cudaEvent_t* g_cap_ev = nullptr;
+thread_local int g_cap_next = 0, g_cap_max = 0;
 
 void trace(const char* what) {
   static const bool on = std::getenv("PSG_TRACE") != nullptr;
