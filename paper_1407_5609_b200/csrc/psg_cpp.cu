@@ -18,9 +18,12 @@
 //                 lowest (i, j) (refscan.cpp:118-126)
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 
 #include "psg_cpp.cuh"
+#include "psg_scan.cuh"
 #include "psg_sort.cuh"
 
 namespace psg {
@@ -45,88 +48,13 @@ void prof_stages(const StageTimer& t) {
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
 constexpr int kChunk = 256;
 constexpr int kQueue = 1024;
 constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
 constexpr double kGridOccupancy = 0.125;  // mean points per cell over the key box
 constexpr int kGridBootCap = 256;         // candidates per point in the grid bootstrap
-
-__device__ __forceinline__ bool admissible(uint32_t a, uint32_t b, uint64_t zone) {
-  const uint32_t gap = a > b ? a - b : b - a;
-  return gap >= zone;  // refscan.cpp:15-18
-}
-
-template <int NK>
-__device__ __forceinline__ void load_keys(const float* __restrict__ p, float (&k)[NK]) {
-  const float4* p4 = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int v = 0; v < NK / 4; ++v) {
-    const float4 t = p4[v];
-    k[4 * v + 0] = t.x;
-    k[4 * v + 1] = t.y;
-    k[4 * v + 2] = t.z;
-    k[4 * v + 3] = t.w;
-  }
-}
-
-// Lower-bound accumulator: the ONE expression both the scan and the recheck
-// use, so the recheck filter is a deterministic subset of what the scan kept.
-template <int NK>
-__device__ __forceinline__ float lb2_full(const float (&a)[NK], const float (&b)[NK]) {
-  float g = b[0] - a[0];
-  float s = g * g;
-#pragma unroll
-  for (int k = 1; k < NK; ++k) {
-    g = b[k] - a[k];
-    s = fmaf(g, g, s);
-  }
-  return s;
-}
-
-// Exact FP32 squared distance, warp-cooperative.  Fixed order for a given d:
-// lane-strided partial sums (float4 when d % 128 == 0), then an xor tree.
-__device__ __forceinline__ float warp_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d,
-                                             int lane) {
-  float s = 0.f;
-  if ((d & 127) == 0) {
-    const float4* a4 = reinterpret_cast<const float4*>(a);
-    const float4* b4 = reinterpret_cast<const float4*>(b);
-    for (int t = lane; t < (d >> 2); t += 32) {
-      const float4 x = __ldg(a4 + t), y = __ldg(b4 + t);
-      float g = x.x - y.x;
-      s = fmaf(g, g, s);
-      g = x.y - y.y;
-      s = fmaf(g, g, s);
-      g = x.z - y.z;
-      s = fmaf(g, g, s);
-      g = x.w - y.w;
-      s = fmaf(g, g, s);
-    }
-  } else {
-    for (int t = lane; t < d; t += 32) {
-      const float g = __ldg(a + t) - __ldg(b + t);
-      s = fmaf(g, g, s);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  return s;
-}
-
-__device__ __forceinline__ float thread_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d) {
-  float s = 0.f;
-  for (int t = 0; t < d; ++t) {
-    const float g = __ldg(a + t) - __ldg(b + t);
-    s = fmaf(g, g, s);
-  }
-  return s;
-}
-
-__device__ __forceinline__ float best_now(const unsigned* best) {
-  return __uint_as_float(*reinterpret_cast<const volatile unsigned*>(best));
-}
+constexpr uint64_t kDenseFactor = 512;    // mean stencil candidates per point above which cells go dense
 
 // ---------------------------------------------------------------------------
 // K1: projection.  One warp per row, lane l owns the V consecutive
@@ -418,41 +346,6 @@ __global__ void k_gather(const float* __restrict__ keys, const uint32_t* __restr
   sidx[p] = i;
 }
 
-// ---------------------------------------------------------------------------
-struct ScanArgs {
-  const float* X;
-  const float* skeys;
-  const uint32_t* sidx;
-  uint32_t n;
-  int d;
-  uint64_t zone;
-  const Budget* bud;  // device (DevState::bud)
-  unsigned* best;
-  uint32_t* cand_p;
-  uint32_t* cand_j;
-  float* cand_s;
-  unsigned* cand_n;
-  uint32_t cand_cap;
-  uint32_t* ovf_p;
-  uint32_t* ovf_j;
-  unsigned* ovf_n;
-  uint32_t ovf_cap;
-  unsigned long long* evals;
-  unsigned long long* visited;  // grid engine: admissible stencil pairs
-};
-
-__device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {
-  atomicMin(a.best, __float_as_uint(s32));
-  if (s32 <= band) {
-    const unsigned c = atomicAdd(a.cand_n, 1u);
-    if (c < a.cand_cap) {
-      a.cand_p[c] = p;
-      a.cand_j[c] = j;
-      a.cand_s[c] = s32;
-    }
-  }
-}
-
 // Seed: pair (0, max(zone,1)) is admissible whenever any pair is, so delta
 // is finite from the start.
 __global__ void k_seed_pair(ScanArgs a, uint32_t z) {
@@ -610,12 +503,9 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
         if (slot < kQueue) {
           qp[slot] = p;
           qj[slot] = j;
-        } else {
-          const unsigned o = atomicAdd(a.ovf_n, 1u);
-          if (o < a.ovf_cap) {
-            a.ovf_p[o] = p;
-            a.ovf_j[o] = j;
-          }
+        } else {  // queue full: evaluate here (canonical order, bounded memory)
+          record(a, p, j, thread_sqdist(a.X + static_cast<size_t>(mo) * a.d, a.X + static_cast<size_t>(so[jj]) * a.d, a.d),
+                 th.band);
         }
       }
     }
@@ -623,20 +513,11 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
     const int nq = min(qn, kQueue);
     if (nq > 0) {
       const float band = th.band;
-      if (a.d <= kInlineD) {
-        for (int i = tid; i < nq; i += kThreads) {
-          const uint32_t pi = qp[i], pj = qj[i];
-          const float s = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                        a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
-          record(a, pi, pj, s, band);
-        }
-      } else {
-        for (int i = warp; i < nq; i += kThreads / 32) {
-          const uint32_t pi = qp[i], pj = qj[i];
-          const float s = warp_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                      a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d, lane);
-          if (lane == 0) record(a, pi, pj, s, band);
-        }
+      for (int i = tid; i < nq; i += kThreads) {  // one queued pair per thread
+        const uint32_t pi = qp[i], pj = qj[i];
+        const float s = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                      a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
+        record(a, pi, pj, s, band);
       }
     }
     __syncthreads();
@@ -669,11 +550,21 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
     }
   }
   if (j == 0xffffffffu) return;
-  const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
-  if (!(lb <= th.lb2)) return;
   const float* xi = a.X + static_cast<size_t>(a.sidx[p]) * a.d;
   const float* xj = a.X + static_cast<size_t>(a.sidx[j]) * a.d;
-  const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f) : warp_sqdist(xi, xj, a.d, lane);
+  // Warp-parallel sum (not the canonical order), rounded up by (2d+8) ulps
+  // relative: two FP32 orders of a sum of d non-negative terms differ by at
+  // most 2d*2^-24 relative, so this stays >= the canonical value the scan
+  // computes for the same pair (the final bound is always a canonical value),
+  // and any value >= a computed one is a valid bound for the thresholds.
+  float s = 0.f;
+  for (int t = lane; t < a.d; t += 32) {
+    const float g = __ldg(xi + t) - __ldg(xj + t);
+    s = fmaf(g, g, s);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  s = __fmul_ru(s, 1.0f + static_cast<float>(2 * a.d + 8) * 0x1.0p-24f);
   if (lane == 0) atomicMin(a.best, __float_as_uint(s));
 }
 
@@ -682,7 +573,10 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
 template <int NK>
 __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi,
                                                              int cap) {
+  __shared__ GridParams sP;  // one copy per block, not per thread (registers)
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) sP = *G.gp;
+  __syncthreads();
   const uint32_t p = lo + blockIdx.x * kThreads + threadIdx.x;
   float best_lb = INFINITY;
   uint32_t best_j = 0xffffffffu;
@@ -690,20 +584,24 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
     float mk[NK];
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
     const uint32_t mo = a.sidx[p];
-    const GridParams P = *G.gp;
-    const GridFlat F = grid_flat(grid_ranges(G.cfirst, P, p, G.scell[p]));
+    const GridFlat F = grid_flat(grid_ranges(G.cfirst, sP, p, G.scell[p]));
     const uint32_t L = min(F.total, static_cast<uint32_t>(cap));
+    // more candidates than the cap: a uniform stride over all of them (a
+    // cell lists its points in index order, which can correlate with
+    // structure in the data, e.g. cluster = index mod k)
+    const uint32_t stride = F.total > L ? F.total / L : 1u;
     // four candidates per step: all key loads in flight before any math
-    for (uint32_t t0 = 0; t0 < L; t0 += 4) {
-      uint32_t jj[4];
-      float kk[4][NK];
+    constexpr int B = 2;  // candidates in flight per step (registers vs latency)
+    for (uint32_t t0 = 0; t0 < L; t0 += B) {
+      uint32_t jj[B];
+      float kk[B][NK];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        jj[u] = t0 + u < L ? F.at(t0 + u) : p;
+      for (int u = 0; u < B; ++u) {
+        jj[u] = t0 + u < L ? F.at((t0 + u) * stride) : p;
         load_keys<NK>(a.skeys + static_cast<size_t>(jj[u]) * NK, kk[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < B; ++u) {
         if (t0 + u >= L) break;
         const float sl = lb2_full<NK>(mk, kk[u]);
         if (sl < best_lb && (a.zone <= 1 || admissible(mo, a.sidx[jj[u]], a.zone))) {
@@ -714,117 +612,6 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
     }
   }
   warp_eval_best(a, best_lb, best_j, p, lane);
-}
-
-// K3b (grid): every stencil candidate whose key lower bound is within the
-// current delta goes to the shared-memory queue; warps evaluate the queue as
-// exact FP32 distances; delta tightens as the atomic minimum falls.  Threads
-// keep a resumable cursor (stencil cell, position) and work in rounds of at
-// most kBudget candidates so the block can flush in lock step.
-constexpr int kBudget = 64;
-
-template <int NK>
-__global__ void __launch_bounds__(kThreads) k_grid_scan(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi) {
-  __shared__ uint32_t qp[kQueue], qj[kQueue];
-  __shared__ int qn;
-  __shared__ Thresholds th;
-  __shared__ unsigned long long nevals;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t p = lo + blockIdx.x * kThreads + tid;
-  bool active = p < hi;
-  float mk[NK];
-  uint32_t mo = 0, j = 0, je = 0;
-  GridRanges R{};
-  int r = 0;
-  if (active) {
-    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
-    mo = a.sidx[p];
-    const GridParams P = *G.gp;
-    R = grid_ranges(G.cfirst, P, p, G.scell[p]);
-    j = R.b0;
-    je = R.e0;
-  } else {
-#pragma unroll
-    for (int k = 0; k < NK; ++k) mk[k] = 0.f;
-  }
-  unsigned long long visited = 0;
-  if (tid == 0) {
-    qn = 0;
-    nevals = 0;
-    th = budget_thresholds_s32(*a.bud,best_now(a.best));
-  }
-  __syncthreads();
-  for (;;) {
-    const float lb2 = th.lb2;
-    int budget = kBudget;
-    while (active && budget > 0) {
-      if (j >= je) {
-        if (++r >= 5) {
-          active = false;
-          break;
-        }
-        j = R.b(r);
-        je = R.e(r);
-        continue;
-      }
-      if (a.zone > 1 && !admissible(mo, a.sidx[j], a.zone)) {
-        ++j;
-        continue;
-      }
-      --budget;
-      float kj[NK];
-      load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
-      float g = kj[0] - mk[0];
-      float sl = g * g;
-      g = kj[1] - mk[1];
-      sl = fmaf(g, g, sl);
-      if (sl <= lb2) {
-#pragma unroll
-        for (int k = 2; k < NK; ++k) {
-          g = kj[k] - mk[k];
-          sl = fmaf(g, g, sl);
-        }
-        if (sl <= lb2) {
-          const int slot = atomicAdd(&qn, 1);
-          if (slot >= kQueue) break;  // queue full: retry this j next round
-          qp[slot] = p;
-          qj[slot] = j;
-        }
-      }
-      ++visited;
-      ++j;
-    }
-    __syncthreads();
-    const int nq = min(qn, kQueue);
-    if (nq > 0) {
-      const float band = th.band;
-      if (a.d <= kInlineD) {
-        for (int i = tid; i < nq; i += kThreads) {
-          const uint32_t pi = qp[i], pj = qj[i];
-          const float sd = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                         a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
-          record(a, pi, pj, sd, band);
-        }
-      } else {
-        for (int i = warp; i < nq; i += kThreads / 32) {
-          const uint32_t pi = qp[i], pj = qj[i];
-          const float sd = warp_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                       a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d, lane);
-          if (lane == 0) record(a, pi, pj, sd, band);
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      nevals += static_cast<unsigned long long>(nq);
-      qn = 0;
-      th = budget_thresholds_s32(*a.bud,best_now(a.best));
-    }
-    if (!__syncthreads_or(active)) break;
-  }
-  for (int o = 16; o; o >>= 1) visited += __shfl_xor_sync(kFull, visited, o);
-  if (lane == 0 && visited) atomicAdd(a.visited, visited);
-  if (tid == 0 && nevals) atomicAdd(a.evals, nevals);
 }
 
 // Before the scan: the grid must hold every pair whose key gaps are within
@@ -851,32 +638,36 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
                                                          const Thresholds* __restrict__ th0) {
   __shared__ uint32_t qp[kQueue], qj[kQueue];
   __shared__ int qn;
+  __shared__ GridParams sP;  // one copy per block, not per thread (registers)
   if (*regrid) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) qn = 0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    qn = 0;
+    sP = *G.gp;
+  }
   __syncthreads();
   const uint32_t p = lo + blockIdx.x * kThreads + tid;
-  unsigned long long visited = 0;
+  unsigned long long visited = 0, inline_evals = 0;
   if (p < hi) {
     float mk[NK];
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
     const uint32_t mo = a.sidx[p];
-    const GridParams P = *G.gp;
-    const GridFlat F = grid_flat(grid_ranges(G.cfirst, P, p, G.scell[p]));
+    const GridFlat F = grid_flat(grid_ranges(G.cfirst, sP, p, G.scell[p]));
     const float lb2 = th0->lb2;
     const bool zoned = a.zone > 1;
     // four candidates per step: all loads in flight before any math
-    for (uint32_t t0 = 0; t0 < F.total; t0 += 4) {
-      uint32_t jj[4], oo[4];
-      float kk[4][NK];
+    constexpr int B = 2;  // candidates in flight per step (registers vs latency)
+    for (uint32_t t0 = 0; t0 < F.total; t0 += B) {
+      uint32_t jj[B], oo[B];
+      float kk[B][NK];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < B; ++u) {
         jj[u] = t0 + u < F.total ? F.at(t0 + u) : p;
         load_keys<NK>(a.skeys + static_cast<size_t>(jj[u]) * NK, kk[u]);
         oo[u] = zoned ? a.sidx[jj[u]] : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < B; ++u) {
         if (t0 + u >= F.total) break;
         if (zoned && !admissible(mo, oo[u], a.zone)) continue;
         ++visited;
@@ -887,12 +678,11 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
         if (slot < kQueue) {
           qp[slot] = p;
           qj[slot] = j;
-        } else {
-          const unsigned o = atomicAdd(a.ovf_n, 1u);
-          if (o < a.ovf_cap) {
-            a.ovf_p[o] = p;
-            a.ovf_j[o] = j;
-          }
+        } else {  // queue full: evaluate here (canonical order, bounded memory)
+          record(a, p, j,
+                 thread_sqdist(a.X + static_cast<size_t>(mo) * a.d, a.X + static_cast<size_t>(a.sidx[j]) * a.d, a.d),
+                 th0->band);
+          ++inline_evals;
         }
       }
     }
@@ -901,24 +691,19 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
   const int nq = min(qn, kQueue);
   if (nq > 0) {
     const float band = th0->band;  // >= the band of any tighter bound: a superset, refiltered by k_recheck
-    if (a.d <= kInlineD) {
-      for (int i = tid; i < nq; i += kThreads) {
-        const uint32_t pi = qp[i], pj = qj[i];
-        const float sd = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                       a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
-        record(a, pi, pj, sd, band);
-      }
-    } else {
-      for (int i = warp; i < nq; i += kThreads / 32) {
-        const uint32_t pi = qp[i], pj = qj[i];
-        const float sd = warp_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                     a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d, lane);
-        if (lane == 0) record(a, pi, pj, sd, band);
-      }
+    for (int i = tid; i < nq; i += kThreads) {  // one queued pair per thread
+      const uint32_t pi = qp[i], pj = qj[i];
+      const float sd = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
+                                     a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
+      record(a, pi, pj, sd, band);
     }
   }
-  for (int o = 16; o; o >>= 1) visited += __shfl_xor_sync(kFull, visited, o);
+  for (int o = 16; o; o >>= 1) {
+    visited += __shfl_xor_sync(kFull, visited, o);
+    inline_evals += __shfl_xor_sync(kFull, inline_evals, o);
+  }
   if (lane == 0 && visited) atomicAdd(a.visited, visited);
+  if (lane == 0 && inline_evals) atomicAdd(a.evals, inline_evals);
   if (tid == 0 && nq) atomicAdd(a.evals, static_cast<unsigned long long>(nq));
 }
 
@@ -1061,7 +846,7 @@ __global__ void k_scan_reset(DevState* st) {
 }
 
 struct SetupArgs {
-  int d, nk, g;
+  int d, nk, g, gbox;  // gbox: keys sampled for boxes (>= g)
   double unorm, sigma, Rn, occupancy;
   uint32_t n, m;
 };
@@ -1091,8 +876,10 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
     st->bud = b;
   }
   if (sa.g == 0) return;
-  double lo[3] = {0, 0, 0}, span[3] = {0, 0, 0};
-  for (int t = 0; t < sa.g; ++t) {
+  // boxes of every key a grid may use (the sparse grid takes the first g,
+  // the dense engine up to kMaxGridKeys)
+  double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
+  for (int t = 0; t < sa.gbox; ++t) {
     const float* v = sample + static_cast<size_t>(t) * sa.m;
     double s1 = 0, s2 = 0, mn = 1e300, mx = -1e300;
     for (uint32_t i = tid; i < sa.m; i += blockDim.x) {
@@ -1130,7 +917,7 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
     }
   }
   if (tid == 0) {
-    for (int t = 0; t < 3; ++t) {
+    for (int t = 0; t < kMaxGridKeys; ++t) {
       st->box_lo[t] = lo[t];
       st->box_span[t] = span[t];
     }
@@ -1335,13 +1122,15 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
     project_async(*ps, plan->dir, W.keys.p, &W.st.p->norm2_bits, s);
     plan->proj_span->end();
     tm.mark("project");
-    SetupArgs sa{ps->d, nk, plan->g, plan->dir.unorm, plan->dir.sigma, ps->Rn, kGridOccupancy,
+    static const double occupancy = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : kGridOccupancy;
+    const int gbox = std::min(plan->dir.q, kMaxGridKeys);
+    SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy,
                  static_cast<uint32_t>(n), 0};
     if (plan->grid) {
       // K2 (grid): cells over the first g keys at the occupancy width, sorted;
       // parameters computed on device, no host round trip
       W.gi.ensure(static_cast<uint32_t>(n), nk, s);
-      sa.m = grid_sample(W.keys.p, static_cast<uint32_t>(n), nk, plan->g, W.gi, s);
+      sa.m = grid_sample(W.keys.p, static_cast<uint32_t>(n), nk, gbox, W.gi, s);
       k_setup<<<1, 256, 0, s>>>(W.st.p, W.gi.gp.p, W.gi.sample.p, sa);
       PSG_LAUNCHED();
       build_grid(W.keys.p, static_cast<uint32_t>(n), nk, W.gi, 24, s);
@@ -1494,7 +1283,7 @@ bool grow_on_overflow(CppWork& W, const DevState& h) {
 // check, candidate scan, spill-list evaluation, speculative FP64 recheck
 // (correct whenever nothing overflowed; the caller checks), pick, and the
 // state copy to the pinned host mirror.  Returns the scan kernel's span.
-KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, cudaStream_t s) {
+KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part, uint32_t nparts, cudaStream_t s) {
   Ctx& c = ctx();
   CppWork& W = *plan.work;
   DevState* st = W.st.p;
@@ -1508,7 +1297,16 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, cudaStream_t s
     PSG_LAUNCHED();
   }
   KernelSpan* span = new KernelSpan(s);
-  if (hi > lo) {
+  if (plan.grid && plan.dense) {
+    // dense cells: cell-pair tiles (the caller decided after the grid check
+    // passed on the host, so the cells are wide enough for the bound)
+    unsigned regrid = 0;
+    PSG_CUDA(cudaMemcpyAsync(&regrid, &st->regrid, 4, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    if (!regrid)
+      dense_scan(a, W.gi, plan.gp.cells, plan.ps->X, static_cast<uint32_t>(plan.ps->n), plan.ps->d, plan.dir.nk,
+                 &st->th, W.dense, part, nparts, s);
+  } else if (hi > lo) {
     if (plan.grid) {
       if (plan.dir.nk == 4)
         k_grid_scan2<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th);
@@ -1580,22 +1378,64 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
   KernelSpan* scan_span = nullptr;
   for (int attempt = 0;; ++attempt) {
     ensure_candidates(W, s);
+    if (plan.grid) {
+      // dense cells (clustered data): cell-pair tiles beat per-point lists
+      PSG_CUDA(cudaMemcpyAsync(&plan.gp, W.gi.gp.p, sizeof(GridParams), cudaMemcpyDeviceToHost, s));
+      PSG_CUDA(cudaMemcpyAsync(W.host_st, W.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+      const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
+      plan.dense = est > kDenseFactor * n;
+      const int gd = std::min(plan.dir.q, kMaxGridKeys);
+      if (plan.dense && plan.g < gd) {
+        // Dense: rebuild the cells on more keys at the same width (still >=
+        // the bound's key window): in 3 projected keys clusters overlap, in 6
+        // they separate, so cell pairs stop mixing clusters.
+        grid_params_for(plan.gp, gd, plan.gp.w, W.host_st->box_lo, W.host_st->box_span);
+        PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
+        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
+        plan.g = gd;
+        tm.mark("dense grid");
+      }
+    }
     delete scan_span;
-    scan_span = scan_enqueue(plan, lo, hi, s);
+    scan_span = scan_enqueue(plan, lo, hi, static_cast<uint32_t>(part), static_cast<uint32_t>(nparts), s);
     PSG_CUDA(cudaStreamSynchronize(s));
     plan.bud = W.host_st->bud;
     if (plan.grid) PSG_CUDA(cudaMemcpy(&plan.gp, W.gi.gp.p, sizeof(GridParams), cudaMemcpyDeviceToHost));
     collect_prep(plan);
     const DevState& h = *W.host_st;
     if (plan.grid && h.regrid) {
-      // widen the cells to the key window of the bound the check saw, rebuild, rescan
-      const Thresholds th0 = budget_thresholds_s32(plan.bud, bits_to_float(h.check_best));
-      const double need = static_cast<double>(th0.win) * (1.0 + 2e-5);
-      if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
-      grid_params_for(plan.gp, plan.g, need, h.box_lo, h.box_span);
-      PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
-      build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
-      tm.mark("regrid");
+      // Widen the cells to the key window of the bound the check saw and
+      // rebuild.  Single part: the wider cells hold far better partners, so
+      // re-bootstrap on them and shrink again while the bound keeps falling
+      // (clustered data: the occupancy grid's bootstrap bound is poor).
+      float bound = bits_to_float(h.check_best);
+      for (int round = 0; round < 4; ++round) {
+        const double need =
+            static_cast<double>(budget_thresholds_s32(plan.bud, bound).win) * (1.0 + 2e-5);
+        if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
+        grid_params_for(plan.gp, plan.g, need, h.box_lo, h.box_span);
+        PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
+        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
+        tm.mark("regrid");
+        if (nparts != 1) break;  // every rank must derive the same grid from the shared bound
+        ScanArgs a = make_args(plan);
+        if (plan.dir.nk == 4)
+          k_grid_bootstrap<4><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, W.gi.dev, 0, static_cast<uint32_t>(n),
+                                                                           kGridBootCap);
+        else
+          k_grid_bootstrap<8><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, W.gi.dev, 0, static_cast<uint32_t>(n),
+                                                                           kGridBootCap);
+        PSG_LAUNCHED();
+        g_launches += 1;
+        const float nb = read_best(&W.st.p->best, s);
+        const double next = static_cast<double>(budget_thresholds_s32(plan.bud, nb).win) * (1.0 + 2e-5);
+        if (std::getenv("PSG_TRACE"))
+          std::fprintf(stderr, "[psg] regrid %d: bound %.6g need %.6g cells %llu -> rebootstrap bound %.6g need %.6g\n",
+                       round, static_cast<double>(bound), need, static_cast<unsigned long long>(plan.gp.cells),
+                       static_cast<double>(nb), next);
+        if (!(next < need / 1.25)) break;  // converged: keep these cells
+        bound = nb;
+      }
       continue;
     }
     if (attempt > 12)
@@ -1675,7 +1515,7 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
       std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));
       plan->sync_bootstrap = false;
       cpp_plan_bootstrap(*plan, 0, 1);
-      delete scan_enqueue(*plan, 0, static_cast<uint32_t>(ps->n), s);
+      delete scan_enqueue(*plan, 0, static_cast<uint32_t>(ps->n), 0, 1, s);
     } catch (...) {
       g_capturing = false;
       g_cap_ev = nullptr;

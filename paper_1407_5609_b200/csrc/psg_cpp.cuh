@@ -5,6 +5,7 @@
 #include <memory>
 
 #include "../../include/pairscan_b200.h"
+#include "psg_dense.cuh"
 #include "psg_grid.cuh"
 #include "psg_internal.cuh"
 #include "psg_points.cuh"
@@ -38,7 +39,7 @@ struct DevState {
   Thresholds th;        // the scan's starting thresholds (from check_best)
   unsigned long long best64, lex, examined, evals, visited;
   Budget bud;
-  double box_lo[3], box_span[3];
+  double box_lo[kMaxGridKeys], box_span[kMaxGridKeys];
 };
 
 // Buffers reused by every solve on one point set (per key count).
@@ -55,6 +56,7 @@ struct CppWork {
   DevBuf<float> cand_s;
   DevBuf<double> d64;
   uint32_t cand_cap = 0, ovf_cap = 0;
+  DenseWork dense;         // dense cell-pair engine (clustered data)
   // The whole single-part grid solve captured once as a CUDA graph and
   // replayed by later solves with the same (q, seed, zone) on this point set.
   cudaGraphExec_t gexec = nullptr;
@@ -73,6 +75,7 @@ struct CppPlan {
   // engine "window": keys sorted by key 0, candidates = the key-0 window
   // engine "grid":   keys sorted by cell of the first g keys (psg_grid.cuh)
   bool grid = false;
+  bool dense = false;      // grid engine: cell-pair tiles instead of per-point candidates
   int g = 0;
   std::shared_ptr<CppWork> work;
   uint32_t width = 0;      // window engine: bootstrap width (sorted neighbours)

@@ -19,7 +19,9 @@ __global__ void k_sample_keys(const float* __restrict__ keys, uint32_t n, int nk
                               float* __restrict__ out) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
-  const uint32_t i = static_cast<uint32_t>((static_cast<uint64_t>(k) * n) / m);
+  // multiplicative hash, not a stride: a strided sample aliases with periodic
+  // structure in the index order (e.g. cluster = index mod 1024)
+  const uint32_t i = static_cast<uint32_t>((static_cast<uint64_t>(k) * 2654435761ull + 12345) % n);
   for (int t = 0; t < g; ++t) out[static_cast<size_t>(t) * m + k] = keys[static_cast<size_t>(i) * nk + t];
 }
 
@@ -37,10 +39,11 @@ __global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, const Gri
   if (i >= n) return;
   const GridParams P = *gpp;
   uint32_t c = 0;
-  for (int t = 0; t < P.g; ++t) {
-    const double lo = t == 0 ? P.lo[0] : (t == 1 ? P.lo[1] : P.lo[2]);
-    const uint32_t dim = t == 0 ? P.dims[0] : (t == 1 ? P.dims[1] : P.dims[2]);
-    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - lo) * P.inv_w;
+#pragma unroll
+  for (int t = 0; t < (NK < kMaxGridKeys ? NK : kMaxGridKeys); ++t) {
+    if (t >= P.g) break;
+    const uint32_t dim = P.dims[t];
+    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - P.lo[t]) * P.inv_w;
     const uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(dim - 1) ? dim - 1 : static_cast<uint32_t>(v));
     c = c * dim + ct;
   }
@@ -78,7 +81,7 @@ void GridIndex::ensure(uint32_t n_, int nk_, cudaStream_t s) {
   counts.alloc(kMaxCells + 1, s);
   cfirst.alloc(kMaxCells + 1, s);
   stmp.alloc(scan_temp_words(kMaxCells + 1), s);
-  sample.alloc(3 * kSample, s);
+  sample.alloc(kMaxKeys * kSample, s);
   gp.alloc(1, s);
 }
 

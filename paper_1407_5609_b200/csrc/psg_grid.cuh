@@ -36,19 +36,21 @@ struct FastDiv {
   __device__ __forceinline__ uint32_t div(uint32_t x) const { return d == 1 ? x : (__umulhi(x, m) >> s); }
 };
 
+constexpr int kMaxGridKeys = 6;  // sparse engine uses g <= 3; the dense engine up to 6
+
 struct GridParams {
   int g = 1;
-  uint32_t dims[3] = {1, 1, 1};
-  double lo[3] = {0, 0, 0};
+  uint32_t dims[kMaxGridKeys] = {1, 1, 1, 1, 1, 1};
+  double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
   double w = 1.0, inv_w = 1.0;
   uint64_t cells = 1;
-  FastDiv fD, f1;  // division by the last dim and by dims[1]
+  FastDiv fD, f1;  // division by the last dim and by dims[1] (g <= 3)
 };
 
 // Fill dims/cells/divisors for width >= w over the box (widened until the dense
-// cell table fits kMaxCells).  Host and device.
-__host__ __device__ inline void grid_params_for(GridParams& gp, int g, double w, const double lo[3],
-                                                const double span[3]) {
+// cell table fits kMaxCells).  Host and device.  lo/span have >= g entries.
+__host__ __device__ inline void grid_params_for(GridParams& gp, int g, double w, const double* lo,
+                                                const double* span) {
   gp.g = g;
   for (;;) {
     double cells = 1.0;
@@ -59,7 +61,7 @@ __host__ __device__ inline void grid_params_for(GridParams& gp, int g, double w,
   gp.w = w;
   gp.inv_w = 1.0 / w;
   gp.cells = 1;
-  for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < kMaxGridKeys; ++t) {
     gp.lo[t] = t < g ? lo[t] : 0.0;
     gp.dims[t] = t < g ? static_cast<uint32_t>(floor(span[t] / w)) + 1 : 1;
     gp.cells *= gp.dims[t];

@@ -1,0 +1,120 @@
+// psg_scan.cuh — device helpers shared by the candidate engines (sparse
+// grid / window scans in psg_cpp.cu, dense cell-pair tiles in psg_dense.cu).
+#pragma once
+
+#include "psg_internal.cuh"
+
+namespace psg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ bool admissible(uint32_t a, uint32_t b, uint64_t zone) {
+  const uint32_t gap = a > b ? a - b : b - a;
+  return gap >= zone;  // refscan.cpp:15-18
+}
+
+template <int NK>
+__device__ __forceinline__ void load_keys(const float* __restrict__ p, float (&k)[NK]) {
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int v = 0; v < NK / 4; ++v) {
+    const float4 t = p4[v];
+    k[4 * v + 0] = t.x;
+    k[4 * v + 1] = t.y;
+    k[4 * v + 2] = t.z;
+    k[4 * v + 3] = t.w;
+  }
+}
+
+// Lower-bound accumulator: the ONE expression both the scan and the recheck
+// use, so the recheck filter is a deterministic subset of what the scan kept.
+template <int NK>
+__device__ __forceinline__ float lb2_full(const float (&a)[NK], const float (&b)[NK]) {
+  float g = b[0] - a[0];
+  float s = g * g;
+#pragma unroll
+  for (int k = 1; k < NK; ++k) {
+    g = b[k] - a[k];
+    s = fmaf(g, g, s);
+  }
+  return s;
+}
+
+// The canonical FP32 squared distance: one thread, fmaf accumulated in
+// coordinate order t = 0..d-1 — the same order as the all-pairs kernel
+// (psg_brute.cu), so every engine and every code path (queue flush, inline
+// evaluation on a full queue, bootstrap, brute force) produces the same bits
+// for a pair.  float4 loads when rows are 16-byte aligned (d % 4 == 0).
+__device__ __forceinline__ float thread_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d) {
+  float s = 0.f;
+  if ((d & 3) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (int t = 0; t < (d >> 2); ++t) {
+      const float4 x = __ldg(a4 + t), y = __ldg(b4 + t);
+      float g = x.x - y.x;
+      s = fmaf(g, g, s);
+      g = x.y - y.y;
+      s = fmaf(g, g, s);
+      g = x.z - y.z;
+      s = fmaf(g, g, s);
+      g = x.w - y.w;
+      s = fmaf(g, g, s);
+    }
+  } else {
+    for (int t = 0; t < d; ++t) {
+      const float g = __ldg(a + t) - __ldg(b + t);
+      s = fmaf(g, g, s);
+    }
+  }
+  return s;
+}
+
+// Warp-level call site of the canonical distance (lane 0 computes, broadcast).
+__device__ __forceinline__ float warp_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d,
+                                             int lane) {
+  float s = 0.f;
+  if (lane == 0) s = thread_sqdist(a, b, d);
+  return __shfl_sync(kFull, s, 0);
+}
+
+__device__ __forceinline__ float best_now(const unsigned* best) {
+  return __uint_as_float(*reinterpret_cast<const volatile unsigned*>(best));
+}
+
+// ---------------------------------------------------------------------------
+struct ScanArgs {
+  const float* X;
+  const float* skeys;
+  const uint32_t* sidx;
+  uint32_t n;
+  int d;
+  uint64_t zone;
+  const Budget* bud;  // device (DevState::bud)
+  unsigned* best;
+  uint32_t* cand_p;
+  uint32_t* cand_j;
+  float* cand_s;
+  unsigned* cand_n;
+  uint32_t cand_cap;
+  uint32_t* ovf_p;
+  uint32_t* ovf_j;
+  unsigned* ovf_n;
+  uint32_t ovf_cap;
+  unsigned long long* evals;
+  unsigned long long* visited;  // grid engine: admissible stencil pairs
+};
+
+__device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {
+  atomicMin(a.best, __float_as_uint(s32));
+  if (s32 <= band) {
+    const unsigned c = atomicAdd(a.cand_n, 1u);
+    if (c < a.cand_cap) {
+      a.cand_p[c] = p;
+      a.cand_j[c] = j;
+      a.cand_s[c] = s32;
+    }
+  }
+}
+
+}  // namespace psg
