@@ -52,7 +52,8 @@ constexpr int kThreads = 256;
 constexpr int kChunk = 256;
 constexpr int kQueue = 1024;
 constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
-constexpr double kGridOccupancy = 0.125;  // mean points per cell over the key box
+constexpr double kGridOccupancy = 0.15;   // mean points per cell over the key box
+constexpr double kGridBoxSd = 2.5;        // key box: mean +- kGridBoxSd sd (clipped to the sample range)
 constexpr int kGridBootCap = 256;         // candidates per point in the grid bootstrap
 constexpr uint64_t kDenseFactor = 512;    // mean stencil candidates per point above which cells go dense
 
@@ -150,101 +151,129 @@ __global__ void __launch_bounds__(256) k_project_warp(const float* __restrict__ 
   if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
 }
 
-// K1 (d in {32, 64, 128, 256}): each warp stages 32 consecutive rows through
-// padded shared memory with coalesced row loads (all 32 loads in flight per
-// lane), then lane l computes row l's NK keys alone.  U arrives as a
-// __grid_constant__ kernel parameter, so every FMA takes its U operand from
-// the constant bank (uniform across the warp): no shared-memory traffic for
-// U and no cross-lane reduction.  Per row: D FMAs per key + D for the norm.
+// K1 (d in {32, 64, 128, 256}).  A warp owns 32-row tiles; lane l = 8g + r
+// computes keys [g*NK/4, (g+1)*NK/4) of rows r, r+8, r+16, r+24, so no
+// cross-lane reduction is needed and every shared-memory read is one
+// wavefront (the 8 rows a load instruction touches sit in distinct banks; the
+// four key groups read the same row float4 = broadcast).  The tile streams
+// through shared memory in 32-row x 32-column chunks (128 B per row: 8 lanes x
+// 16 B, four rows per cp.async instruction) over a ring of kProjStages chunk
+// buffers per warp with kProjStages-1 chunks in flight: 18 KB of shared memory
+// per warp, ten warps per SM.  U (NK x D, padded rows) sits in shared memory
+// once per block.  FMAs are packed FP32x2 (FFMA2): each key keeps two partial
+// sums (even / odd coordinates) added at the end — any summation order is
+// inside the key error budget (psg_internal.cuh Budget::E).  The row norms the
+// budget needs are a per-set invariant (psg_pointset::norm2max, computed when
+// the set is created); block 0 folds it into *norm2_bits.
 template <int NK, int D>
 struct UParam {
   float u[NK][D];
 };
 
+constexpr int kProjCols = 32;    // columns per chunk
+constexpr int kProjStride = 36;  // padded chunk row stride (floats): 8 rows -> 32 distinct banks
+constexpr int kProjStages = 4;   // chunk ring depth per warp
+constexpr int kProjChunk = 32 * kProjStride;  // floats per chunk buffer
+
 template <int NK, int D>
-__global__ void __launch_bounds__(128) k_project_smem(const float* __restrict__ X, uint32_t n,
+__global__ void __launch_bounds__(256) k_project_smem(const float* __restrict__ X, uint32_t n,
                                                       const __grid_constant__ UParam<NK, D> U, float* __restrict__ keys,
-                                                      unsigned* __restrict__ norm2_bits) {
-  constexpr int V = D / 32;        // floats per lane per row
-  constexpr int STRIDE = D + 4;    // padded row stride (floats): conflict-free 16 B lane reads
-  constexpr int TILE = 32 * STRIDE;
-  extern __shared__ __align__(16) float tile[];  // (blockDim/32) x 2 buffers x 32 x STRIDE
+                                                      unsigned* __restrict__ norm2_bits, unsigned set_norm2_bits) {
+  constexpr int NC = D / kProjCols;  // chunks per tile
+  constexpr int KPG = NK / 4;        // keys per lane group
+  constexpr int US = D + 4;          // padded U row stride: the NK rows start in distinct banks
+  extern __shared__ __align__(16) float smem[];  // U (NK x US), then per warp kProjStages chunk buffers
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* bufs = tile + static_cast<size_t>(w) * 2 * TILE;
+  const int rl = lane & 7, g = lane >> 3;
+  float* Us = smem;
+  for (int i = threadIdx.x; i < NK * D; i += blockDim.x) Us[(i / D) * US + i % D] = (&U.u[0][0])[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(norm2_bits, set_norm2_bits);
+  __syncthreads();
+  float* ring = smem + NK * US + static_cast<size_t>(w) * kProjStages * kProjChunk;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  // cp.async of one 32-row tile: lane copies its V floats of every row
-  auto stage = [&](uint32_t r0, float* dst) {
+  const uint32_t ntiles = (n + 31) / 32;
+  const uint32_t my_tiles = warp < ntiles ? (ntiles - warp + nwarps - 1) / nwarps : 0;
+  const uint32_t chunks = my_tiles * NC;
+  // copy pattern: lane -> (row rq within a group of 4 rows, 16 B column slot cq)
+  const int rq = lane >> 3, cq = (lane & 7) * 4;
+  const uint32_t ring_sa = static_cast<uint32_t>(__cvta_generic_to_shared(ring + rq * kProjStride + cq));
+  auto stage = [&](uint32_t j) {  // chunk j of this warp -> ring slot j % kProjStages
+    const uint32_t tile = warp + (j / NC) * nwarps, c = j % NC;
+    const uint32_t r0 = tile * 32;
+    const uint32_t sa = ring_sa + (j % kProjStages) * kProjChunk * sizeof(float);
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const uint32_t row = r0 + r < n ? r0 + r : n - 1;
-      const float* src = X + static_cast<size_t>(row) * D + lane * V;
-      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + r * STRIDE + lane * V));
-      if constexpr (V >= 4) {
-#pragma unroll
-        for (int v = 0; v < V; v += 4)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + 4 * v), "l"(src + v));
-      } else if constexpr (V == 2) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src));
-      } else {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src));
-      }
+    for (int q = 0; q < 8; ++q) {  // 8 groups of 4 rows
+      uint32_t row = r0 + q * 4 + rq;
+      row = row < n ? row : n - 1;  // tail tile: clamp (results of clamped rows are not stored)
+      const float* src = X + static_cast<size_t>(row) * D + c * kProjCols + cq;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + q * 4 * kProjStride * 4), "l"(src));
     }
-    asm volatile("cp.async.commit_group;\n" ::);
   };
-  float worst = 0.f;
-  uint32_t r0 = warp * 32;
-  if (r0 < n) stage(r0, bufs);
-  for (int it = 0; r0 < n; ++it, r0 += nwarps * 32) {
-    float* buf = bufs + (it & 1) * TILE;
-    const uint32_t next = r0 + nwarps * 32;
-    if (next < n) {
-      stage(next, bufs + ((it + 1) & 1) * TILE);  // next tile streams while this one computes
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
+#pragma unroll
+  for (int j = 0; j < kProjStages - 1; ++j) {
+    if (static_cast<uint32_t>(j) < chunks) stage(j);
+    asm volatile("cp.async.commit_group;\n" ::);  // empty groups keep the wait count uniform
+  }
+  float2 acc[4][KPG];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < KPG; ++k) acc[i][k] = make_float2(0.f, 0.f);
+  for (uint32_t j = 0; j < chunks; ++j) {
+    if (j + kProjStages - 1 < chunks) stage(j + kProjStages - 1);  // overwrites the slot computed at j-1
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kProjStages - 1));  // chunk j has landed
     __syncwarp();
-    // lane computes its own row
-    float acc[NK];
+    const uint32_t c = j % NC;
+    const float* xs = ring + (j % kProjStages) * kProjChunk + rl * kProjStride;
+    const float* us = Us + (g * KPG) * US + c * kProjCols;
 #pragma unroll
-    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
-    float nn = 0.f;
-    const float* mine = buf + lane * STRIDE;
+    for (int t = 0; t < kProjCols; t += 4) {
+      float4 xv[4], uv[KPG];
 #pragma unroll
-    for (int t = 0; t < D; t += 4) {
-      const float4 xv = *reinterpret_cast<const float4*>(mine + t);
-      nn = fmaf(xv.x, xv.x, nn);
-      nn = fmaf(xv.y, xv.y, nn);
-      nn = fmaf(xv.z, xv.z, nn);
-      nn = fmaf(xv.w, xv.w, nn);
+      for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const float4*>(xs + i * 8 * kProjStride + t);
 #pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        acc[k] = fmaf(U.u[k][t], xv.x, acc[k]);
-        acc[k] = fmaf(U.u[k][t + 1], xv.y, acc[k]);
-        acc[k] = fmaf(U.u[k][t + 2], xv.z, acc[k]);
-        acc[k] = fmaf(U.u[k][t + 3], xv.w, acc[k]);
+      for (int k = 0; k < KPG; ++k) uv[k] = *reinterpret_cast<const float4*>(us + k * US + t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < KPG; ++k) {
+          acc[i][k] = __ffma2_rn(make_float2(xv[i].x, xv[i].y), make_float2(uv[k].x, uv[k].y), acc[i][k]);
+          acc[i][k] = __ffma2_rn(make_float2(xv[i].z, xv[i].w), make_float2(uv[k].z, uv[k].w), acc[i][k]);
+        }
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    if (c == NC - 1) {  // tile complete: keys of the lane's rows
+      const uint32_t r0 = (warp + (j / NC) * nwarps) * 32;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t row = r0 + rl + 8 * i;
+        if (row < n) {
+          float* out = keys + static_cast<size_t>(row) * NK + g * KPG;
+          if constexpr (KPG == 2)
+            *reinterpret_cast<float2*>(out) = make_float2(acc[i][0].x + acc[i][0].y, acc[i][1].x + acc[i][1].y);
+          else
+            *out = acc[i][0].x + acc[i][0].y;
+        }
+#pragma unroll
+        for (int k = 0; k < KPG; ++k) acc[i][k] = make_float2(0.f, 0.f);
       }
     }
-    const uint32_t row = r0 + lane;
-    if (row < n) {
-      worst = fmaxf(worst, nn);
-      float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(row) * NK);
-#pragma unroll
-      for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
-    }
-    __syncwarp();
   }
-  worst = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(worst)));
-  if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
+  asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 template <int NK, int D>
-void launch_project_smem(const float* X, uint32_t n, const Directions& dir, float* keys, unsigned* nb, int sms,
+void launch_project_smem(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* nb, int sms,
                          cudaStream_t s) {
-  constexpr size_t kWarpBytes = 2ull * 32 * (D + 4) * sizeof(float);  // double-buffered tile
-  constexpr int kWarpsPerBlock = kWarpBytes * 4 <= 100 * 1024 ? 4 : (kWarpBytes * 2 <= 100 * 1024 ? 2 : 1);
-  constexpr size_t kSmem = kWarpsPerBlock * kWarpBytes;
+  const uint32_t n = static_cast<uint32_t>(ps.n);
+  constexpr size_t kWarpBytes = kProjStages * kProjChunk * sizeof(float);  // 18 KB chunk ring
+  constexpr size_t kUBytes = NK * (D + 4) * sizeof(float);
+  constexpr int kBlocksPerSM = 2;
+  constexpr int kWarpsPerBlock = static_cast<int>((110 * 1024 - kUBytes) / kWarpBytes);
+  static_assert(kWarpsPerBlock >= 1 && kWarpsPerBlock <= 8, "projection block shape (launch bounds 256)");
+  constexpr size_t kSmem = kWarpsPerBlock * kWarpBytes + kUBytes;
   static bool configured = false;
   if (!configured) {
     PSG_CUDA(cudaFuncSetAttribute(k_project_smem<NK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -254,11 +283,12 @@ void launch_project_smem(const float* X, uint32_t n, const Directions& dir, floa
   UParam<NK, D> u;
   for (int k = 0; k < NK; ++k)
     for (int t = 0; t < D; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * D + t];
-  const int per_sm = static_cast<int>((200 * 1024) / kSmem);
+  unsigned nbits;
+  std::memcpy(&nbits, &ps.norm2max, 4);
   const uint32_t tiles = (n + 31) / 32;
   const int grid = static_cast<int>(std::min<uint64_t>((tiles + kWarpsPerBlock - 1) / kWarpsPerBlock,
-                                                       static_cast<uint64_t>(sms) * std::max(per_sm, 1)));
-  k_project_smem<NK, D><<<grid, 32 * kWarpsPerBlock, kSmem, s>>>(X, n, u, keys, nb);
+                                                       static_cast<uint64_t>(sms) * kBlocksPerSM));
+  k_project_smem<NK, D><<<std::max(grid, 1), 32 * kWarpsPerBlock, kSmem, s>>>(ps.X, n, u, keys, nb, nbits);
 }
 
 // d < 32 (C1 d=2, C4 d=3, ...): one thread per row, U by value in the
@@ -847,9 +877,11 @@ __global__ void k_scan_reset(DevState* st) {
 
 struct SetupArgs {
   int d, nk, g, gbox;  // gbox: keys sampled for boxes (>= g)
-  double unorm, sigma, Rn, occupancy;
+  double unorm, sigma, Rn, occupancy, box_sd;
   uint32_t n, m;
 };
+constexpr int kSetupPer = 16;  // sample elements per thread
+static_assert(kSetupPer * 256 >= kGridSample, "k_setup covers the whole sample");
 
 // The error budget from the projection's max norm (same formula as the host
 // make_budget), then — grid engine — the key box from the sample moments
@@ -880,14 +912,24 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
   // the dense engine up to kMaxGridKeys)
   double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
   for (int t = 0; t < sa.gbox; ++t) {
+    // every load of this key in flight before any arithmetic (m <= kGridSample
+    // = 16 x 256): one memory round trip per key, not one per element
     const float* v = sample + static_cast<size_t>(t) * sa.m;
+    float x[kSetupPer];
+#pragma unroll
+    for (int r = 0; r < kSetupPer; ++r) {
+      const uint32_t i = tid + r * 256u;
+      x[r] = i < sa.m ? v[i] : v[0];
+    }
     double s1 = 0, s2 = 0, mn = 1e300, mx = -1e300;
-    for (uint32_t i = tid; i < sa.m; i += blockDim.x) {
-      const double x = v[i];
-      s1 += x;
-      s2 += x * x;
-      mn = fmin(mn, x);
-      mx = fmax(mx, x);
+#pragma unroll
+    for (int r = 0; r < kSetupPer; ++r) {
+      if (tid + r * 256u >= sa.m) break;
+      const double y = x[r];
+      s1 += y;
+      s2 += y * y;
+      mn = fmin(mn, y);
+      mx = fmax(mx, y);
     }
     for (int o = 16; o; o >>= 1) {
       s1 += __shfl_xor_sync(kFull, s1, o);
@@ -911,7 +953,7 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
         mx = fmax(mx, red[3][w]);
       }
       const double mean = s1 / sa.m, sd = sqrt(fmax(s2 / sa.m - mean * mean, 0.0));
-      const double a = fmax(mn, mean - 3 * sd), b = fmin(mx, mean + 3 * sd);
+      const double a = fmax(mn, mean - sa.box_sd * sd), b = fmin(mx, mean + sa.box_sd * sd);
       lo[t] = a;
       span[t] = fmax(b - a, 1e-30);
     }
@@ -945,14 +987,14 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
   const int sms = ctx().sm_count;
   if (d == 32 || d == 64 || d == 128 || d == 256) {
     switch (dir.nk * 1000 + d) {
-      case 4032: launch_project_smem<4, 32>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      case 4064: launch_project_smem<4, 64>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      case 4128: launch_project_smem<4, 128>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      case 4256: launch_project_smem<4, 256>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      case 8032: launch_project_smem<8, 32>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      case 8064: launch_project_smem<8, 64>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      case 8128: launch_project_smem<8, 128>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
-      default: launch_project_smem<8, 256>(ps.X, n, dir, keys, norm2_bits, sms, s); break;
+      case 4032: launch_project_smem<4, 32>(ps, dir, keys, norm2_bits, sms, s); break;
+      case 4064: launch_project_smem<4, 64>(ps, dir, keys, norm2_bits, sms, s); break;
+      case 4128: launch_project_smem<4, 128>(ps, dir, keys, norm2_bits, sms, s); break;
+      case 4256: launch_project_smem<4, 256>(ps, dir, keys, norm2_bits, sms, s); break;
+      case 8032: launch_project_smem<8, 32>(ps, dir, keys, norm2_bits, sms, s); break;
+      case 8064: launch_project_smem<8, 64>(ps, dir, keys, norm2_bits, sms, s); break;
+      case 8128: launch_project_smem<8, 128>(ps, dir, keys, norm2_bits, sms, s); break;
+      default: launch_project_smem<8, 256>(ps, dir, keys, norm2_bits, sms, s); break;
     }
   } else if (d < 32) {
     USmall u{};
@@ -1124,7 +1166,8 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
     tm.mark("project");
     static const double occupancy = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : kGridOccupancy;
     const int gbox = std::min(plan->dir.q, kMaxGridKeys);
-    SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy,
+    static const double box_sd = std::getenv("PSG_BOXSD") ? std::atof(std::getenv("PSG_BOXSD")) : kGridBoxSd;
+    SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy, box_sd,
                  static_cast<uint32_t>(n), 0};
     if (plan->grid) {
       // K2 (grid): cells over the first g keys at the occupancy width, sorted;

@@ -1,7 +1,9 @@
 // psg_grid.cu — build the cell grid (psg_grid.cuh): cell ids from the device
-// GridParams, per-cell counts -> cfirst (exclusive scan), stable radix sort by
-// cell, key gather.  Everything is enqueued; nothing waits on the host.
+// GridParams, stable radix sort by cell, cfirst by a warp-parallel search of
+// the sorted cell ids, key gather.  Everything is enqueued; nothing waits on
+// the host.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <vector>
 
@@ -12,8 +14,9 @@
 namespace psg {
 namespace {
 
+constexpr unsigned kGridFull = 0xffffffffu;
+
 unsigned blocks(uint64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
-constexpr uint32_t kSample = 4096;
 
 __global__ void k_sample_keys(const float* __restrict__ keys, uint32_t n, int nk, int g, uint32_t m,
                               float* __restrict__ out) {
@@ -25,16 +28,9 @@ __global__ void k_sample_keys(const float* __restrict__ keys, uint32_t n, int nk
   for (int t = 0; t < g; ++t) out[static_cast<size_t>(t) * m + k] = keys[static_cast<size_t>(i) * nk + t];
 }
 
-__global__ void k_zero_counts(uint32_t* __restrict__ counts, const GridParams* __restrict__ gp) {
-  const uint64_t count = gp->cells + 1;
-  for (uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; c < count;
-       c += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    counts[c] = 0;
-}
-
 template <int NK>
 __global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, const GridParams* __restrict__ gpp,
-                           uint32_t* __restrict__ cid, uint32_t* __restrict__ idx, uint32_t* __restrict__ counts) {
+                           uint32_t* __restrict__ cid, uint32_t* __restrict__ idx) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const GridParams P = *gpp;
@@ -49,8 +45,93 @@ __global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, const Gri
   }
   cid[i] = c;
   idx[i] = i;
-  atomicAdd(counts + c, 1u);
 }
+
+// cfirst[c] = first sorted position whose cell id is >= c, for c = 0..cells.
+// A warp owns kCfirstWarpCells consecutive cells: one binary search for the
+// first, then groups of 32 cells (one per lane) walk forward through windows
+// of 32 sorted cell ids, each lane ranking its cell in the window with a
+// 5-step shuffle search.  Work ~ (cells + n) / 32 per warp-step, writes
+// coalesced; no per-cell counters, atomics or scans.
+constexpr uint32_t kCfirstWarpCells = 1024;
+
+__global__ void __launch_bounds__(256) k_cfirst(const uint32_t* __restrict__ scell, uint32_t n,
+                                                const GridParams* __restrict__ gp, uint32_t* __restrict__ cfirst) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t last = static_cast<uint32_t>(gp->cells);  // entries 0..last
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t c0 = warp * kCfirstWarpCells; c0 <= last; c0 += nwarps * kCfirstWarpCells) {
+    // pos = lower_bound(scell, c0): lanes split the range 32 ways per step
+    uint32_t lo = 0, hi = n;  // answer in [lo, hi]
+    while (hi - lo > 32) {
+      const uint32_t step = (hi - lo + 31) / 32;
+      const uint32_t probe = min(lo + lane * step, hi - 1);
+      const unsigned below = __ballot_sync(kGridFull, scell[probe] < c0);  // prefix of lanes (sorted)
+      const int k = __popc(below);  // probes 0..k-1 are < c0
+      const uint32_t nlo = k == 0 ? lo : min(lo + (k - 1) * step + 1, hi);
+      const uint32_t nhi = k == 32 ? hi : min(lo + k * step, hi);
+      lo = nlo;
+      hi = nhi;
+    }
+    {
+      const uint32_t probe = lo + lane;
+      const bool lt = probe < hi && scell[probe] < c0;
+      lo += __popc(__ballot_sync(kGridFull, lt));
+    }
+    uint32_t pos = lo;
+    const uint32_t cend = min(c0 + kCfirstWarpCells - 1, last);
+    for (uint32_t cb = c0; cb <= cend; cb += 32) {
+      const uint32_t c = cb + lane;
+      uint32_t res = 0;
+      bool done = c > cend;  // lanes past the range have nothing to write
+      uint32_t base = pos;
+      while (!__all_sync(kGridFull, done)) {
+        const uint32_t v = base + lane < n ? scell[base + lane] : 0xffffffffu;
+        // r = #(window values < c); the window is ascending across lanes
+        // (every shuffle is executed by all lanes: no shuffle under a branch)
+        const uint32_t v31 = __shfl_sync(kGridFull, v, 31);
+        int r = 0;
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const uint32_t probe = __shfl_sync(kGridFull, v, r + st - 1);
+          if (probe < c) r += st;
+        }
+        if (r == 31 && v31 < c) r = 32;
+        if (!done && (r < 32 || base + 32 >= n)) {
+          res = min(base + r, n);
+          done = true;
+        }
+        base += 32;
+      }
+      if (c <= cend) cfirst[c] = res;
+      pos = __shfl_sync(kGridFull, res, min(cend - cb, 31u));  // lb of the group's last cell
+    }
+  }
+}
+
+#ifdef PSG_DEBUG_SYNC
+__global__ void k_verify_cfirst(const uint32_t* __restrict__ scell, uint32_t n, const GridParams* __restrict__ gp,
+                                const uint32_t* __restrict__ cfirst) {
+  const uint32_t last = static_cast<uint32_t>(gp->cells);
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= last; c += gridDim.x * blockDim.x) {
+    const uint32_t p = cfirst[c];
+    const bool ok = p <= n && (p == n || scell[p] >= c) && (p == 0 || scell[p - 1] < c);
+    if (!ok) {
+      uint32_t a = 0, b = n;  // true lower bound
+      while (a < b) {
+        const uint32_t m = (a + b) / 2;
+        if (scell[m] < c) a = m + 1; else b = m;
+      }
+      printf("cfirst[%u] = %u want %u (c%%32 %u c%%1024 %u) prev %u next %u\n", c, p, a, c % 32, c % 1024,
+             c > 0 ? cfirst[c - 1] : 0u, c < last ? cfirst[c + 1] : 0u);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint32_t i = 1; i < n; i += 997)
+      if (scell[i] < scell[i - 1]) { printf("scell not sorted at %u\n", i); __trap(); }
+}
+#endif
 
 template <int NK>
 __global__ void k_gather_sorted(const float* __restrict__ keys, const uint32_t* __restrict__ perm, uint32_t n,
@@ -78,15 +159,13 @@ void GridIndex::ensure(uint32_t n_, int nk_, cudaStream_t s) {
   idx0.alloc(n, s);
   idx1.alloc(n, s);
   hist.alloc(radix_hist_words(n), s);
-  counts.alloc(kMaxCells + 1, s);
   cfirst.alloc(kMaxCells + 1, s);
-  stmp.alloc(scan_temp_words(kMaxCells + 1), s);
-  sample.alloc(kMaxKeys * kSample, s);
+  sample.alloc(kMaxKeys * kGridSample, s);
   gp.alloc(1, s);
 }
 
 uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s) {
-  const uint32_t m = std::min<uint32_t>(n, kSample);
+  const uint32_t m = std::min<uint32_t>(n, kGridSample);
   k_sample_keys<<<blocks(m, 256), 256, 0, s>>>(keys, n, nk, g, m, gi.sample.p);
   PSG_LAUNCHED();
   ++g_launches;
@@ -117,25 +196,28 @@ void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double 
 }
 
 void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s) {
-  k_zero_counts<<<1024, 256, 0, s>>>(gi.counts.p, gi.gp.p);
-  PSG_LAUNCHED();
   if (nk == 4)
-    k_cell_ids<4><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p, gi.counts.p);
+    k_cell_ids<4><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p);
   else
-    k_cell_ids<8><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p, gi.counts.p);
+    k_cell_ids<8><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p);
   PSG_LAUNCHED();
-  // cfirst = exclusive prefix sum of the per-cell counts (cfirst[cells] = n)
-  exclusive_scan_u32_dev(gi.counts.p, gi.cfirst.p, kMaxCells + 1, &gi.gp.p->cells, gi.stmp.p, s);
   uint32_t* kk[2] = {gi.cid0.p, gi.cid1.p};
   uint32_t* vv[2] = {gi.idx0.p, gi.idx1.p};
   const int passes = (sort_bits + 7) / 8;
   const int which = radix_sort<uint32_t>(kk, vv, n, 0, passes * 8, gi.hist.p, s);
+  // every warp resident at once: the binary searches overlap
+  k_cfirst<<<2 * 148 * 8, 256, 0, s>>>(kk[which], n, gi.gp.p, gi.cfirst.p);
+  PSG_LAUNCHED();
+#ifdef PSG_DEBUG_SYNC
+  k_verify_cfirst<<<1024, 256, 0, s>>>(kk[which], n, gi.gp.p, gi.cfirst.p);
+  PSG_LAUNCHED();
+#endif
   if (nk == 4)
     k_gather_sorted<4><<<blocks(n, 256), 256, 0, s>>>(keys, vv[which], n, gi.skeys.p, gi.sidx.p);
   else
     k_gather_sorted<8><<<blocks(n, 256), 256, 0, s>>>(keys, vv[which], n, gi.skeys.p, gi.sidx.p);
   PSG_LAUNCHED();
-  g_launches += 6 + 3 * passes;
+  g_launches += 3 + 3 * passes;
   gi.dev.skeys = gi.skeys.p;
   gi.dev.sidx = gi.sidx.p;
   gi.dev.scell = kk[which];

@@ -17,6 +17,7 @@
 namespace psg {
 
 constexpr uint64_t kMaxCells = 1ull << 24;
+constexpr uint32_t kGridSample = 4096;  // keys sampled (hashed positions) for the key box
 
 // q = x / d for x < 2^31 by multiply-high (CUTLASS-style FastDivmod).
 struct FastDiv {
@@ -84,15 +85,15 @@ struct GridIndex {
   int nk = 4;
   uint32_t n = 0;
   DevBuf<float> skeys;
-  DevBuf<uint32_t> sidx, cid0, cid1, idx0, idx1, hist, counts, cfirst, stmp;
+  DevBuf<uint32_t> sidx, cid0, cid1, idx0, idx1, hist, cfirst;
   DevBuf<float> sample;
   DevBuf<GridParams> gp;
   GridDev dev;
   void ensure(uint32_t n_, int nk_, cudaStream_t s);
 };
 
-// Enqueue the build (no host synchronisation): cell ids from *G.gp, counts ->
-// cfirst (exclusive scan), stable radix sort by cell (sort_bits), gather.
+// Enqueue the build (no host synchronisation): cell ids from *G.gp, stable
+// radix sort by cell (sort_bits), cfirst by search of the sorted ids, gather.
 void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s);
 // Strided sample of the first g keys into gi.sample (g x m floats); returns m.
 uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s);

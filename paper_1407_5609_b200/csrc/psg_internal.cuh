@@ -31,7 +31,17 @@ struct cuda_error : std::runtime_error {
       throw ::psg::cuda_error(std::string(#call) + ": " + cudaGetErrorString(psg_e_) + \
                               " (" __FILE__ ":" + std::to_string(__LINE__) + ")");      \
   } while (0)
+// PSG_DEBUG_SYNC builds synchronise after every launch so a faulting kernel
+// is named by the failing check (there is no compute-sanitizer on the pool).
+#ifdef PSG_DEBUG_SYNC
+#define PSG_LAUNCHED()                 \
+  do {                                 \
+    PSG_CUDA(cudaGetLastError());      \
+    PSG_CUDA(cudaDeviceSynchronize()); \
+  } while (0)
+#else
 #define PSG_LAUNCHED() PSG_CUDA(cudaGetLastError())
+#endif
 
 // ---------------------------------------------------------------------------
 // Per-device context: one stream, a stream-ordered pool that keeps freed

@@ -80,6 +80,34 @@ __global__ void k_check_f32(const float* __restrict__ x, uint64_t count, unsigne
   }
 }
 
+// max over rows of the FP32 sum of squares of a row (a per-set invariant the
+// closest-pair error budget needs; computed once here, not per solve).  A warp
+// per row for d >= 32, a thread per row below.
+__global__ void k_row_norm2max(const float* __restrict__ X, uint64_t n, int d, unsigned* __restrict__ out) {
+  float worst = 0.f;
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  if (d >= 32) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r = tid >> 5; r < n; r += nth >> 5) {
+      const float* row = X + r * d;
+      float s = 0.f;
+      for (int t = lane; t < d; t += 32) s = fmaf(row[t], row[t], s);
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      worst = fmaxf(worst, s);
+    }
+  } else {
+    for (uint64_t r = tid; r < n; r += nth) {
+      const float* row = X + r * d;
+      float s = 0.f;
+      for (int t = 0; t < d; ++t) s = fmaf(row[t], row[t], s);
+      worst = fmaxf(worst, s);
+    }
+  }
+  worst = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(worst)));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(worst));
+}
+
 __global__ void k_check_f64(const double* __restrict__ x, uint64_t count, unsigned* __restrict__ bad,
                             unsigned long long* __restrict__ maxabs_bits) {
   unsigned long long m = 0;
@@ -213,6 +241,21 @@ double read_r2(unsigned long long* dbits, cudaStream_t s) {
 }
 
 // sqrt of an FP64-accumulated sum of squares, widened to a safe upper bound.
+float row_norm2max(const float* X, uint64_t n, int d, cudaStream_t s, int sms) {
+  if (n == 0 || d == 0) return 0.f;
+  DevBuf<unsigned> out(1, s);
+  PSG_CUDA(cudaMemsetAsync(out.p, 0, 4, s));
+  k_row_norm2max<<<grid_for(d >= 32 ? n * 32 : n, 256, sms), 256, 0, s>>>(X, n, d, out.p);
+  PSG_LAUNCHED();
+  ++g_launches;
+  unsigned h = 0;
+  PSG_CUDA(cudaMemcpyAsync(&h, out.p, 4, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  float v;
+  std::memcpy(&v, &h, 4);
+  return v;
+}
+
 double radius_bound(double r2, int d) {
   if (r2 <= 0.0) return 0.0;
   return std::sqrt(r2 * (1.0 + 4.0 * d * 0x1.0p-53)) * (1.0 + 1e-12);
@@ -256,6 +299,7 @@ psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev
     ps->X = ps->work.p;
   }
   ps->maxabs = static_cast<double>(mx) * ps->scale;
+  ps->norm2max = row_norm2max(ps->X, n, ps->d, s, c.sm_count);
   return ps.release();
 }
 
@@ -296,6 +340,7 @@ psg_pointset* pointset_rows_f64(const double* p, uint64_t n, uint64_t d, bool de
   }
   ps->X = ps->work.p;
   ps->maxabs = maxabs * ps->scale;
+  ps->norm2max = row_norm2max(ps->X, ps->n, ps->d, s, c.sm_count);
   return ps.release();
 }
 
@@ -355,6 +400,7 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
   ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d);
   ps->X = ps->work.p;
   ps->maxabs = maxabs * ps->scale;
+  ps->norm2max = row_norm2max(ps->X, ps->n, ps->d, s, c.sm_count);
   return ps.release();
 }
 

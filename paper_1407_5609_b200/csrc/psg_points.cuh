@@ -66,6 +66,7 @@ struct psg_pointset {
   double scale = 1.0;          // X = fl(scale * src)
   double Rn = 0.0;             // max narrowing radius, working units
   double maxabs = 0.0;         // max |X|
+  float norm2max = 0.f;        // max over rows of the FP32 sum of squares of X (any order)
   uint64_t h2d_bytes = 0;
   // solve workspaces reused across calls on this point set (nk = 4 / 8);
   // type-erased here, owned by the closest-pair engine (psg_cpp.cu)
