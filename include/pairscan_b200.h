@@ -179,6 +179,14 @@ int psg_cpp_plan_scan(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float 
                       psg_pair_result* out);
 void psg_cpp_plan_free(psg_cpp_plan* plan);
 
+/* ---- inspection (tests): the projection keys of a point set ---------------
+ * keys[i*nk + k] = <U_k, X_i> as the solve computes them (tensor cores for
+ * d in {32,64,128,256}), the directions U (nk x dim, FP32), the charged key
+ * error bound E (working units) and the working-unit scale
+ * (X = fl(scale * points)).  nk = 4 or 8 for q clamped to [1, 8]. */
+int psg_debug_projection(psg_pointset* ps, uint64_t q, uint64_t seed, int* nk, float* keys, float* dirs,
+                         double* key_error, double* scale);
+
 /* ---- host helpers: the reference's seeded synthetic data (datagen.cpp) --- */
 int psg_gen_random_walk(uint64_t n, uint64_t seed, double stddev, double* out);
 /* SURVEY §8(d) recipes: blocks of 65,536 points from Rng(derive_seed(master, 1000+b)). */

@@ -122,6 +122,7 @@ _SIGS = {
     "psg_derive_seed": (_u64, [_u64, _u64]),
     "psg_host_alloc": (_int, [C.c_size_t, _p]),
     "psg_host_free": (None, [_p]),
+    "psg_debug_projection": (_int, [_p, _u64, _u64, _p, _p, _p, _p, _p]),
 }
 
 _lib = None
@@ -488,3 +489,20 @@ class gen:
     @staticmethod
     def derive_seed(base: int, stream: int) -> int:
         return lib().psg_derive_seed(base, stream)
+
+
+def debug_projection(points: "PointSet", q: int = 10, seed: int = 1):
+    """Test hook: the projection keys of `points` as a solve computes them,
+    the directions, the charged key-error bound E and the working-unit scale
+    (keys approximate <U_k, scale * x_i>; |key - exact| <= E is the filter's
+    assumption)."""
+    n, d = points.size(), points.dim()
+    nk = C.c_int(0)
+    probe = lib().psg_debug_projection(points._device(), q, seed, C.byref(nk), None, None, None, None)
+    _check(probe)
+    keys = np.empty((n, nk.value), dtype=np.float32)
+    dirs = np.empty((nk.value, d), dtype=np.float32)
+    E, scale = C.c_double(0), C.c_double(0)
+    _check(lib().psg_debug_projection(points._device(), q, seed, C.byref(nk), keys.ctypes.data, dirs.ctypes.data,
+                                      C.byref(E), C.byref(scale)))
+    return keys, dirs, E.value, scale.value

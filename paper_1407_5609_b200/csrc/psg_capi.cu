@@ -1,6 +1,7 @@
 // psg_capi.cu — the extern "C" boundary (include/pairscan_b200.h).
 // Every entry: clear the per-thread profile, run, translate exceptions into
 // status codes, keep the message for psg_last_error().
+#include <algorithm>
 #include <cmath>
 #include <memory>
 #include <new>
@@ -287,3 +288,23 @@ void psg_host_free(void* p) {
 }
 
 }  // extern "C"
+
+// ---- inspection (tests) -----------------------------------------------------------
+int psg_debug_projection(psg_pointset* ps, uint64_t q, uint64_t seed, int* nk, float* keys, float* dirs,
+                         double* key_error, double* scale) {
+  return guarded([&] {
+    if (!ps || !nk) throw psg::invalid_argument("null argument");
+    const psg::Directions dir =
+        psg::make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(q, 1), 1u << 20)));
+    *nk = dir.nk;
+    cudaStream_t s = psg::ctx().stream;
+    psg::DevBuf<float> k(ps->n * dir.nk, s);
+    const float norm2 = psg::project(*ps, dir, k.p, s);
+    const psg::Budget b = psg::make_budget(*ps, dir, norm2);
+    if (keys) PSG_CUDA(cudaMemcpyAsync(keys, k.p, ps->n * dir.nk * sizeof(float), cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    if (dirs) std::copy(dir.U.begin(), dir.U.end(), dirs);
+    if (key_error) *key_error = b.E;
+    if (scale) *scale = ps->scale;
+  });
+}

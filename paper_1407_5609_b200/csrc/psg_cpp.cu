@@ -58,239 +58,8 @@ constexpr int kGridBootCap = 256;         // candidates per point in the grid bo
 constexpr uint64_t kDenseFactor = 512;    // mean stencil candidates per point above which cells go dense
 
 // ---------------------------------------------------------------------------
-// K1: projection.  One warp per row, lane l owns the V consecutive
-// coordinates [l*V, l*V+V) of a d = 32V row (coalesced 4V-byte loads) and the
-// matching NK x V slice of U in registers.  The NK partial sums are combined
-// by a transposing butterfly (log2 NK halving steps, then an xor tree), so a
-// row costs NK*V FMAs + (NK-1) + (5 - log2 NK) shuffles per lane.
-template <int CNT, int OFF, int NK>
-struct Transpose {
-  static __device__ __forceinline__ void run(float (&v)[NK], int lane) {
-    const bool up = lane & OFF;
-#pragma unroll
-    for (int i = 0; i < CNT / 2; ++i) {
-      const float send = up ? v[i] : v[i + CNT / 2];
-      const float keep = up ? v[i + CNT / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(kFull, send, OFF);
-    }
-    Transpose<CNT / 2, OFF / 2, NK>::run(v, lane);
-  }
-};
-template <int OFF, int NK>
-struct Transpose<1, OFF, NK> {
-  static __device__ __forceinline__ void run(float (&)[NK], int) {}
-};
-
-template <int NK>
-constexpr int log2c() {
-  return NK == 8 ? 3 : (NK == 4 ? 2 : (NK == 2 ? 1 : 0));
-}
-
-template <int NK, int V>
-__global__ void __launch_bounds__(256) k_project_warp(const float* __restrict__ X, uint32_t n,
-                                                      const float* __restrict__ U, float* __restrict__ keys,
-                                                      unsigned* __restrict__ norm2_bits) {
-  constexpr int d = 32 * V;
-  constexpr int L = log2c<NK>();
-  const int lane = threadIdx.x & 31;
-  float u[NK][V];
-#pragma unroll
-  for (int k = 0; k < NK; ++k)
-#pragma unroll
-    for (int v = 0; v < V; ++v) u[k][v] = __ldg(U + k * d + lane * V + v);
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  // R rows per iteration: all R row loads are issued before any math so each
-  // warp keeps R x 4V x 32 bytes in flight (Little's law at HBM latency).
-  constexpr int R = V >= 4 ? 4 : 8;
-  float worst = 0.f;
-  for (uint32_t r0 = warp; r0 < n; r0 += R * nwarps) {
-    float x[R][V];
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const uint32_t r = r0 + q * nwarps;
-      const float* row = X + static_cast<size_t>(r < n ? r : 0) * d + lane * V;
-      if constexpr (V % 4 == 0) {
-#pragma unroll
-        for (int v = 0; v < V; v += 4) {
-          const float4 t = __ldcs(reinterpret_cast<const float4*>(row + v));
-          x[q][v] = t.x; x[q][v + 1] = t.y; x[q][v + 2] = t.z; x[q][v + 3] = t.w;
-        }
-      } else if constexpr (V == 2) {
-        const float2 t = __ldcs(reinterpret_cast<const float2*>(row));
-        x[q][0] = t.x; x[q][1] = t.y;
-      } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v) x[q][v] = __ldcs(row + v);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const uint32_t r = r0 + q * nwarps;
-      if (r >= n) break;  // warp-uniform
-      float acc[NK];
-      float nn = 0.f;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) acc[k] = 0.f;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        nn = fmaf(x[q][v], x[q][v], nn);
-#pragma unroll
-        for (int k = 0; k < NK; ++k) acc[k] = fmaf(u[k][v], x[q][v], acc[k]);
-      }
-      Transpose<NK, 16, NK>::run(acc, lane);
-      float key = acc[0];
-#pragma unroll
-      for (int o = 16 >> L; o; o >>= 1) key += __shfl_xor_sync(kFull, key, o);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) nn += __shfl_xor_sync(kFull, nn, o);
-      worst = fmaxf(worst, nn);
-      if ((lane & ((1 << (5 - L)) - 1)) == 0) keys[static_cast<size_t>(r) * NK + (lane >> (5 - L))] = key;
-    }
-  }
-  if (lane == 0) atomicMax(norm2_bits, __float_as_uint(worst));
-}
-
-// K1 (d in {32, 64, 128, 256}).  A warp owns 32-row tiles; lane l = 8g + r
-// computes keys [g*NK/4, (g+1)*NK/4) of rows r, r+8, r+16, r+24, so no
-// cross-lane reduction is needed and every shared-memory read is one
-// wavefront (the 8 rows a load instruction touches sit in distinct banks; the
-// four key groups read the same row float4 = broadcast).  The tile streams
-// through shared memory in 32-row x 32-column chunks (128 B per row: 8 lanes x
-// 16 B, four rows per cp.async instruction) over a ring of kProjStages chunk
-// buffers per warp with kProjStages-1 chunks in flight: 18 KB of shared memory
-// per warp, ten warps per SM.  U (NK x D, padded rows) sits in shared memory
-// once per block.  FMAs are packed FP32x2 (FFMA2): each key keeps two partial
-// sums (even / odd coordinates) added at the end — any summation order is
-// inside the key error budget (psg_internal.cuh Budget::E).  The row norms the
-// budget needs are a per-set invariant (psg_pointset::norm2max, computed when
-// the set is created); block 0 folds it into *norm2_bits.
-template <int NK, int D>
-struct UParam {
-  float u[NK][D];
-};
-
-constexpr int kProjCols = 32;    // columns per chunk
-constexpr int kProjStride = 36;  // padded chunk row stride (floats): 8 rows -> 32 distinct banks
-constexpr int kProjStages = 4;   // chunk ring depth per warp
-constexpr int kProjChunk = 32 * kProjStride;  // floats per chunk buffer
-
-template <int NK, int D>
-__global__ void __launch_bounds__(256) k_project_smem(const float* __restrict__ X, uint32_t n,
-                                                      const __grid_constant__ UParam<NK, D> U, float* __restrict__ keys,
-                                                      unsigned* __restrict__ norm2_bits, unsigned set_norm2_bits) {
-  constexpr int NC = D / kProjCols;  // chunks per tile
-  constexpr int KPG = NK / 4;        // keys per lane group
-  constexpr int US = D + 4;          // padded U row stride: the NK rows start in distinct banks
-  extern __shared__ __align__(16) float smem[];  // U (NK x US), then per warp kProjStages chunk buffers
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int rl = lane & 7, g = lane >> 3;
-  float* Us = smem;
-  for (int i = threadIdx.x; i < NK * D; i += blockDim.x) Us[(i / D) * US + i % D] = (&U.u[0][0])[i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(norm2_bits, set_norm2_bits);
-  __syncthreads();
-  float* ring = smem + NK * US + static_cast<size_t>(w) * kProjStages * kProjChunk;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t ntiles = (n + 31) / 32;
-  const uint32_t my_tiles = warp < ntiles ? (ntiles - warp + nwarps - 1) / nwarps : 0;
-  const uint32_t chunks = my_tiles * NC;
-  // copy pattern: lane -> (row rq within a group of 4 rows, 16 B column slot cq)
-  const int rq = lane >> 3, cq = (lane & 7) * 4;
-  const uint32_t ring_sa = static_cast<uint32_t>(__cvta_generic_to_shared(ring + rq * kProjStride + cq));
-  auto stage = [&](uint32_t j) {  // chunk j of this warp -> ring slot j % kProjStages
-    const uint32_t tile = warp + (j / NC) * nwarps, c = j % NC;
-    const uint32_t r0 = tile * 32;
-    const uint32_t sa = ring_sa + (j % kProjStages) * kProjChunk * sizeof(float);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {  // 8 groups of 4 rows
-      uint32_t row = r0 + q * 4 + rq;
-      row = row < n ? row : n - 1;  // tail tile: clamp (results of clamped rows are not stored)
-      const float* src = X + static_cast<size_t>(row) * D + c * kProjCols + cq;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + q * 4 * kProjStride * 4), "l"(src));
-    }
-  };
-#pragma unroll
-  for (int j = 0; j < kProjStages - 1; ++j) {
-    if (static_cast<uint32_t>(j) < chunks) stage(j);
-    asm volatile("cp.async.commit_group;\n" ::);  // empty groups keep the wait count uniform
-  }
-  float2 acc[4][KPG];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int k = 0; k < KPG; ++k) acc[i][k] = make_float2(0.f, 0.f);
-  for (uint32_t j = 0; j < chunks; ++j) {
-    if (j + kProjStages - 1 < chunks) stage(j + kProjStages - 1);  // overwrites the slot computed at j-1
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(kProjStages - 1));  // chunk j has landed
-    __syncwarp();
-    const uint32_t c = j % NC;
-    const float* xs = ring + (j % kProjStages) * kProjChunk + rl * kProjStride;
-    const float* us = Us + (g * KPG) * US + c * kProjCols;
-#pragma unroll
-    for (int t = 0; t < kProjCols; t += 4) {
-      float4 xv[4], uv[KPG];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const float4*>(xs + i * 8 * kProjStride + t);
-#pragma unroll
-      for (int k = 0; k < KPG; ++k) uv[k] = *reinterpret_cast<const float4*>(us + k * US + t);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int k = 0; k < KPG; ++k) {
-          acc[i][k] = __ffma2_rn(make_float2(xv[i].x, xv[i].y), make_float2(uv[k].x, uv[k].y), acc[i][k]);
-          acc[i][k] = __ffma2_rn(make_float2(xv[i].z, xv[i].w), make_float2(uv[k].z, uv[k].w), acc[i][k]);
-        }
-    }
-    __syncwarp();  // every lane is done with this slot before it is refilled
-    if (c == NC - 1) {  // tile complete: keys of the lane's rows
-      const uint32_t r0 = (warp + (j / NC) * nwarps) * 32;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t row = r0 + rl + 8 * i;
-        if (row < n) {
-          float* out = keys + static_cast<size_t>(row) * NK + g * KPG;
-          if constexpr (KPG == 2)
-            *reinterpret_cast<float2*>(out) = make_float2(acc[i][0].x + acc[i][0].y, acc[i][1].x + acc[i][1].y);
-          else
-            *out = acc[i][0].x + acc[i][0].y;
-        }
-#pragma unroll
-        for (int k = 0; k < KPG; ++k) acc[i][k] = make_float2(0.f, 0.f);
-      }
-    }
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-}
-
-template <int NK, int D>
-void launch_project_smem(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* nb, int sms,
-                         cudaStream_t s) {
-  const uint32_t n = static_cast<uint32_t>(ps.n);
-  constexpr size_t kWarpBytes = kProjStages * kProjChunk * sizeof(float);  // 18 KB chunk ring
-  constexpr size_t kUBytes = NK * (D + 4) * sizeof(float);
-  constexpr int kBlocksPerSM = 2;
-  constexpr int kWarpsPerBlock = static_cast<int>((110 * 1024 - kUBytes) / kWarpBytes);
-  static_assert(kWarpsPerBlock >= 1 && kWarpsPerBlock <= 8, "projection block shape (launch bounds 256)");
-  constexpr size_t kSmem = kWarpsPerBlock * kWarpBytes + kUBytes;
-  static bool configured = false;
-  if (!configured) {
-    PSG_CUDA(cudaFuncSetAttribute(k_project_smem<NK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmem)));
-    configured = true;
-  }
-  UParam<NK, D> u;
-  for (int k = 0; k < NK; ++k)
-    for (int t = 0; t < D; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * D + t];
-  unsigned nbits;
-  std::memcpy(&nbits, &ps.norm2max, 4);
-  const uint32_t tiles = (n + 31) / 32;
-  const int grid = static_cast<int>(std::min<uint64_t>((tiles + kWarpsPerBlock - 1) / kWarpsPerBlock,
-                                                       static_cast<uint64_t>(sms) * kBlocksPerSM));
-  k_project_smem<NK, D><<<std::max(grid, 1), 32 * kWarpsPerBlock, kSmem, s>>>(ps.X, n, u, keys, nb, nbits);
-}
-
+// K1: projection on CUDA cores for the shapes the tensor-core kernel does not
+// take (psg_project_tc.cu handles d in {32, 64, 128, 256}).
 // d < 32 (C1 d=2, C4 d=3, ...): one thread per row, U by value in the
 // constant bank (so the launch carries no host-side buffer: graph-safe).
 struct USmall {
@@ -898,8 +667,7 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
     b.a = (2.0 * sa.d + 2.0) * 0x1.0p-149;
     const double nn = static_cast<double>(__uint_as_float(st->norm2_bits));
     const double maxnorm = sqrt(nn * (1.0 + (sa.d + 4) * u)) * (1.0 + 1e-7);
-    const double gamma = sa.d * u / (1.0 - sa.d * u);
-    b.E = gamma * sa.unorm * maxnorm * 1.0001;
+    b.E = key_gamma(sa.d, sa.n) * sa.unorm * maxnorm * 1.0001 + key_abs(sa.d, sa.n);
     b.Rn = sa.Rn;
     b.sigma = sa.sigma;
     b.unorm = sa.unorm;
@@ -985,17 +753,8 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
   const uint32_t n = static_cast<uint32_t>(ps.n);
   const int d = ps.d;
   const int sms = ctx().sm_count;
-  if (d == 32 || d == 64 || d == 128 || d == 256) {
-    switch (dir.nk * 1000 + d) {
-      case 4032: launch_project_smem<4, 32>(ps, dir, keys, norm2_bits, sms, s); break;
-      case 4064: launch_project_smem<4, 64>(ps, dir, keys, norm2_bits, sms, s); break;
-      case 4128: launch_project_smem<4, 128>(ps, dir, keys, norm2_bits, sms, s); break;
-      case 4256: launch_project_smem<4, 256>(ps, dir, keys, norm2_bits, sms, s); break;
-      case 8032: launch_project_smem<8, 32>(ps, dir, keys, norm2_bits, sms, s); break;
-      case 8064: launch_project_smem<8, 64>(ps, dir, keys, norm2_bits, sms, s); break;
-      case 8128: launch_project_smem<8, 128>(ps, dir, keys, norm2_bits, sms, s); break;
-      default: launch_project_smem<8, 256>(ps, dir, keys, norm2_bits, sms, s); break;
-    }
+  if (tc_projection(d, ps.n)) {
+    project_tc(ps, dir, keys, norm2_bits, s);  // psg_project_tc.cu
   } else if (d < 32) {
     USmall u{};
     for (int k = 0; k < dir.nk; ++k)
@@ -1041,8 +800,7 @@ Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm
   b.e = (d + 4) * u * 1.01;
   b.a = (2.0 * d + 2.0) * 0x1.0p-149;
   const double maxnorm = std::sqrt(static_cast<double>(max_norm2) * (1.0 + (d + 4) * u)) * (1.0 + 1e-7);
-  const double gamma = d * u / (1.0 - d * u);
-  b.E = gamma * dir.unorm * maxnorm * 1.0001;
+  b.E = key_gamma(d, ps.n) * dir.unorm * maxnorm * 1.0001 + key_abs(d, ps.n);
   b.Rn = ps.Rn;
   b.sigma = dir.sigma;
   b.unorm = dir.unorm;

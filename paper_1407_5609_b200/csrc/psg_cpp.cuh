@@ -22,6 +22,8 @@ void prof_stages(const StageTimer& t);
 // into *norm2_bits (device).  Enqueued only.
 void project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
                    cudaStream_t s);
+// The tensor-core projection (psg_project_tc.cu): tc_projection(d, n) shapes.
+void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s);
 // Host-synchronous variant: returns max ||X_i||^2.
 float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s);
 // Error budget for the keys of `ps` under `dir` (host).

@@ -233,6 +233,27 @@ struct Budget {
   int nk = 1;              // keys used in the LB
 };
 
+// The projection runs on the tensor cores (tcgen05 kind::tf32, psg_project_tc.cu)
+// for d in {32, 64, 128, 256}; elsewhere on FP32 CUDA cores.
+__host__ __device__ inline bool tc_projection(int d, uint64_t n) {
+  return (d == 32 || d == 64 || d == 128 || d == 256) && n < (1ull << 31);
+}
+// Relative key-error factor gamma (|k^ - k| <= gamma * sum_t |u_t x_t| + abs):
+//   CUDA cores: FP32 FMA chain, any order: d u / (1 - d u);
+//   tensor cores (psg_project_tc.cu): U is an exact TF32 operand, x = hi + lo
+//   exactly with hi exact TF32 and lo losing <= 2^-10 |lo| <= 2^-20 |x| to the
+//   TF32 conversion; products are exact in FP32.  The FP32 accumulation inside
+//   and across the 2d/8 MMAs is charged 4 ulps (2^-22) per product term, 4x an
+//   every-addition-truncates model, plus 2^-19 for lo.  tests/test_gpu_keys.py
+//   measures the realised error against FP64 projections.  Values the tensor
+//   core may flush (|x| < 2^-126) add at most d 2^-126 (key_abs).
+__host__ __device__ inline double key_gamma(int d, uint64_t n) {
+  const double u = 0x1.0p-24;
+  if (tc_projection(d, n)) return (0x1.0p-19 + 2.0 * d * 0x1.0p-22) * 1.01;
+  return d * u / (1.0 - d * u);
+}
+__host__ __device__ inline double key_abs(int d, uint64_t n) { return tc_projection(d, n) ? d * 0x1.0p-120 : 0.0; }
+
 // Thresholds derived from an upper bound `dmax` (working units) on the real
 // distance of any pair that may still matter.
 struct Thresholds {

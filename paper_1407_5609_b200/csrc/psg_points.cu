@@ -456,7 +456,19 @@ Directions make_directions_uncached(uint64_t seed, int d, int q) {
     }
   }
   dir.U.assign(static_cast<size_t>(dir.nk) * d, 0.0f);
-  for (size_t i = 0; i < V.size(); ++i) dir.U[i] = static_cast<float>(V[i]);
+  // tensor-core projection shapes take U as an exact TF32 operand: round to
+  // 10 mantissa bits here, so sigma / unorm below describe the matrix used
+  const bool tf32 = d == 32 || d == 64 || d == 128 || d == 256;
+  for (size_t i = 0; i < V.size(); ++i) {
+    float v = static_cast<float>(V[i]);
+    if (tf32) {
+      uint32_t b;
+      std::memcpy(&b, &v, 4);
+      b = (b + 0x1000u) & ~0x1fffu;  // nearest, ties away (|v| <= 1: no overflow)
+      std::memcpy(&v, &b, 4);
+    }
+    dir.U[i] = v;
+  }
   double gmax = 0.0, unorm = 0.0;
   for (int k = 0; k < dir.q; ++k) {
     double row = 0.0;

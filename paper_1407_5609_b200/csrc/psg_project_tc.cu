@@ -1,0 +1,381 @@
+// psg_project_tc.cu — K1, the projection keys[i][k] = <U_k, X_i>, as a
+// TMA-fed tcgen05 GEMM (BASELINE.json north_star item 1; the reference's
+// counterpart is the reference-distance table of build_reference_set,
+// refscan.cpp:30-65, whose role the projection keys take over).
+//
+// D = X (n x d, FP32 rows) . U^T (d x 16): M = 128 rows per tile, N = 16 (the
+// nk <= 8 directions zero-padded), K = d in 32-float chunks.  X is split
+// exactly into two TF32 terms, x = hi + lo (hi = x with its 13 low mantissa
+// bits cleared, lo = x - hi), and both are multiplied: near-FP32 keys.
+//
+//   warp 0 (one thread)  TMA producer: one 128-row x 32-float box (16 KB, 128 B
+//                        swizzle) per smem stage, kTcStages in flight; the
+//                        tail tile's OOB rows are zero-filled
+//   warps 4-7, 12-15     split (two groups, alternate chunks): lane = row; each thread reads its row's 32
+//                        floats of a stage (conflict-free through the swizzle),
+//                        frees the stage, and writes hi | lo to a TMEM slot
+//                        (tcgen05.st 32x32b, 64 columns per slot, kTcSlots)
+//   warp 1 (one thread)  MMA issuer: per slot 2 x 4 tcgen05.mma.kind::tf32
+//                        (A = hi / lo from TMEM, B = U from smem, K = 8 each)
+//                        into two TMEM accumulator chains (hi, lo: 2 x 16
+//                        columns, double buffered across tiles, summed by the
+//                        epilogue); tcgen05.commit frees the slot
+//                        and, after a tile's last chunk, hands it to the epilogue
+//   warps 8-11           epilogue: tcgen05.ld 32x32b (lane = row) -> nk keys
+//                        per row, 32 B coalesced stores
+//   warp 2               TMEM allocation / release (all 512 columns)
+//
+// Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...  Shared
+// memory carries only the TMA stream (read once by the split warps); the
+// operand traffic of the MMAs is TMEM's.
+//
+// Precision: U is rounded to TF32 when the directions are made
+// (psg_points.cu), so it is an exact operand; hi is exact TF32, lo enters as
+// TF32 (<= 2^-10 |lo| <= 2^-20 |x| lost), products are exact in FP32 and the
+// accumulation is FP32 in the tensor core.  key_gamma/key_abs
+// (psg_internal.cuh) charge this, with margin, as the key error E of the
+// filter budget — the "explicit rounding slack on the filter bound"; every
+// decision is still taken by the FP64 recheck, so answers stay exact, and
+// tests/test_gpu_keys.py checks the charged E against FP64 projections.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+
+#include "psg_cpp.cuh"
+
+namespace psg {
+namespace {
+
+constexpr int kTcM = 128;         // rows per tile (UMMA M)
+constexpr int kTcN = 16;          // UMMA N: directions padded to 16
+constexpr int kTcKChunk = 32;     // floats per 128 B swizzle row = one pipeline stage
+constexpr int kTcStages = 8;      // smem stages: 8 x 16 KB in flight per SM
+constexpr int kTcSlots = 7;       // TMEM A slots (64 columns: hi | lo) after the accumulators
+constexpr uint32_t kStageBytes = kTcM * kTcKChunk * 4;  // 16 KB
+constexpr uint32_t kBChunkBytes = kTcN * 128;            // 2 KB: 16 rows x 128 B
+constexpr int kTcThreads = 512;
+constexpr uint32_t kTmemCols = 512;  // [0, 64) 2 x (hi, lo) accumulators, [64, 64 + 64 kTcSlots) A slots
+constexpr uint32_t kSlotBase = 64;
+
+// tcgen05 instruction descriptor: D F32, A/B TF32, both K-major, N = 16, M = 128.
+constexpr uint32_t kIdesc = (1u << 4)             // c_format F32
+                            | (2u << 7)           // a_format TF32
+                            | (2u << 10)          // b_format TF32
+                            | ((kTcN >> 3) << 17) // n_dim
+                            | ((kTcM >> 4) << 24);// m_dim
+
+template <int D>
+struct UTc {
+  float u[8][D];  // rows >= nk are zero
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128 B swizzle, 8-row groups 1024 B
+// apart (SBO), version 1 (sm_100).  The start address advances by 32 B per
+// K = 8 step inside a swizzle row.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+template <int NK, int D>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_project_tc(const __grid_constant__ CUtensorMap xmap, uint32_t n, const __grid_constant__ UTc<D> U,
+                 float* __restrict__ keys, unsigned* __restrict__ norm2_bits, unsigned set_norm2_bits) {
+  constexpr int NC = D / kTcKChunk;  // K chunks (stages) per tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                             // kTcStages x 16 KB (A stages)
+  uint8_t* sb = smem + kTcStages * kStageBytes;   // NC x 2 KB (B = U, SW128 K-major)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + NC * kBChunkBytes);  // TMA -> split   (tx)
+  uint64_t* sfree = full + kTcStages;                                     // split -> TMA   (4 warps)
+  uint64_t* tready = sfree + kTcStages;                                   // split -> MMA   (4 warps)
+  uint64_t* tslot = tready + kTcSlots;                                    // MMA -> split   (commit)
+  uint64_t* tfull = tslot + kTcSlots;                                     // MMA -> epilogue (commit)
+  uint64_t* tempty = tfull + 2;                                           // epilogue -> MMA (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // B operand once per CTA: row r (direction), float kk of chunk c lands in
+  // 16 B unit (kk/4) ^ (r%8) of the row's 128 B (the 128 B swizzle pattern)
+  for (int i = threadIdx.x; i < kTcN * D; i += kTcThreads) {
+    const int r = i / D, k = i % D, c = k / kTcKChunk, kk = k % kTcKChunk;
+    const float v = r < NK ? U.u[r][k] : 0.f;
+    const uint32_t off = c * kBChunkBytes + r * 128 + ((((kk >> 2) ^ (r & 7)) & 7) << 4) + (kk & 3) * 4;
+    *reinterpret_cast<float*>(sb + off) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> visible to the MMA (async proxy)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(sfree + s, 4);
+    }
+    for (int s = 0; s < kTcSlots; ++s) {
+      mbar_init(tready + s, 4);
+      mbar_init(tslot + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x == 0) atomicMax(norm2_bits, set_norm2_bits);  // the set's row norms (psg_pointset::norm2max)
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t ntiles = (n + kTcM - 1) / kTcM;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int c = 0; c < NC; ++c) {
+          mbar_wait(sfree + stage, phase ^ 1);
+          mbar_arrive_expect_tx(full + stage, kStageBytes);
+          tma_load_2d(sa + stage * kStageBytes, &xmap, full + stage, c * kTcKChunk, static_cast<int>(t * kTcM));
+          if (++stage == kTcStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+    }
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
+    // split: two groups of four warps take alternate chunks; warp w owns rows /
+    // TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 (the tcgen05 lane-quarter rule)
+    const uint32_t e = warp & 3, grp = warp >= 12, r = 32 * e + lane;
+    const uint32_t lane_addr = tmem + ((32u * e) << 16) + kSlotBase;
+    const uint32_t nchunks = (ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0) * NC;
+    for (uint32_t j = grp; j < nchunks; j += 2) {
+      const uint32_t stage = j % kTcStages, phase = (j / kTcStages) & 1;
+      const uint32_t slot = j % kTcSlots, sphase = (j / kTcSlots) & 1;
+      mbar_wait(full + stage, phase);
+      const uint8_t* rowp = sa + stage * kStageBytes + r * 128;
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(rowp + ((q ^ (r & 7)) << 4));
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t h = __float_as_uint(x[w]) & ~0x1fffu;
+          hi[4 * q + w] = h;
+          lo[4 * q + w] = __float_as_uint(x[w] - __uint_as_float(h));  // exact
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sfree + stage);  // the TMA may refill this stage
+      mbar_wait(tslot + slot, sphase ^ 1);        // the MMAs have consumed this slot's previous chunk
+      tc_fence_after();
+      tmem_st32(lane_addr + slot * 64, hi);
+      tmem_st32(lane_addr + slot * 64 + 32, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tready + slot);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      uint32_t slot = 0, sphase = 0, it = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const uint32_t acc = it & 1, aphase = (it >> 1) & 1;
+        mbar_wait(tempty + acc, aphase ^ 1);  // the epilogue has drained this accumulator
+        tc_fence_after();
+        const uint32_t dcol = tmem + acc * 2 * kTcN;  // two chains of 16 columns
+        for (int c = 0; c < NC; ++c) {
+          mbar_wait(tready + slot, sphase);  // hi | lo of this chunk are in TMEM
+          tc_fence_after();
+          const uint32_t a = tmem + kSlotBase + slot * 64;
+          const uint64_t bd = sw128_desc(smem_u32(sb + c * kBChunkBytes));
+          // hi products accumulate in chain 0, lo products in chain 1 (adjacent
+          // MMAs are independent, so the tensor pipe overlaps them)
+#pragma unroll
+          for (int k = 0; k < kTcKChunk / 8; ++k) {
+            umma_tf32_ts(dcol, a + 8 * k, bd + 2 * k, (c | k) != 0);
+            umma_tf32_ts(dcol + kTcN, a + 32 + 8 * k, bd + 2 * k, (c | k) != 0);
+          }
+          umma_commit(tslot + slot);  // slot reusable once these MMAs have read it
+          if (++slot == kTcSlots) {
+            slot = 0;
+            sphase ^= 1;
+          }
+        }
+        umma_commit(tfull + acc);  // accumulator complete
+      }
+    }
+  } else if (warp >= 8) {  // epilogue: warp (8 + e) owns TMEM lanes 32e .. 32e+31
+    const uint32_t e = warp - 8;
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const uint32_t acc = it & 1, aphase = (it >> 1) & 1;
+      mbar_wait(tfull + acc, aphase);
+      tc_fence_after();
+      uint32_t r[8], r2[8];
+      const uint32_t taddr = tmem + ((32u * e) << 16) + acc * 2 * kTcN;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(taddr));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=r"(r2[0]), "=r"(r2[1]), "=r"(r2[2]), "=r"(r2[3]), "=r"(r2[4]), "=r"(r2[5]), "=r"(r2[6]),
+                     "=r"(r2[7])
+                   : "r"(taddr + kTcN));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));  // hi + lo
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      const uint32_t row = t * kTcM + 32 * e + lane;
+      if (row < n) {
+        float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(row) * NK);
+        out[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
+        if constexpr (NK == 8)
+          out[1] =
+              make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    PSG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("pairscan_b200: cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+template <int NK, int D>
+void launch(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* nb, cudaStream_t s) {
+  const uint32_t n = static_cast<uint32_t>(ps.n);
+  if (n == 0) return;
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(n)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(D) * sizeof(float)};
+  const cuuint32_t box[2] = {kTcKChunk, kTcM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ps.X), gdim, gstride, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("pairscan_b200: cuTensorMapEncodeTiled failed");
+  UTc<D> u{};
+  for (int k = 0; k < NK; ++k)
+    for (int t = 0; t < D; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * D + t];
+  constexpr size_t kSmem = 1024 + kTcStages * kStageBytes + (D / kTcKChunk) * kBChunkBytes + 512;
+  static bool configured = false;
+  if (!configured) {
+    PSG_CUDA(cudaFuncSetAttribute(k_project_tc<NK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmem)));
+    configured = true;
+  }
+  unsigned nbits;
+  std::memcpy(&nbits, &ps.norm2max, 4);
+  const uint32_t ntiles = (n + kTcM - 1) / kTcM;
+  const int grid = static_cast<int>(std::min<uint32_t>(ntiles, static_cast<uint32_t>(ctx().sm_count)));
+  k_project_tc<NK, D><<<grid, kTcThreads, kSmem, s>>>(map, n, u, keys, nb, nbits);
+  PSG_LAUNCHED();
+}
+
+}  // namespace
+
+void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s) {
+  switch (dir.nk * 1000 + ps.d) {
+    case 4032: launch<4, 32>(ps, dir, keys, norm2_bits, s); break;
+    case 4064: launch<4, 64>(ps, dir, keys, norm2_bits, s); break;
+    case 4128: launch<4, 128>(ps, dir, keys, norm2_bits, s); break;
+    case 4256: launch<4, 256>(ps, dir, keys, norm2_bits, s); break;
+    case 8032: launch<8, 32>(ps, dir, keys, norm2_bits, s); break;
+    case 8064: launch<8, 64>(ps, dir, keys, norm2_bits, s); break;
+    case 8128: launch<8, 128>(ps, dir, keys, norm2_bits, s); break;
+    case 8256: launch<8, 256>(ps, dir, keys, norm2_bits, s); break;
+    default: throw std::logic_error("project_tc: unsupported shape");
+  }
+}
+
+}  // namespace psg
