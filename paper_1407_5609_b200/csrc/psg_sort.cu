@@ -1,14 +1,17 @@
-// psg_sort.cu — LSD radix sort, 8 bits per pass, three kernels per pass:
-//   rs_hist    per-tile digit histogram (shared-memory atomics) -> digit-major
-//              table hist[digit][tile]
-//   rs_scan    one block per digit: exclusive scan along the tiles, digit total
-//   rs_scatter stable scatter: the block first turns the 256 digit totals into
-//              digit offsets (shared-memory scan), then ranks its tile with
-//              warp-contiguous sub-tiles, __match_any_sync ranks inside 32-item
-//              rounds, per-warp digit counters and a cross-warp scan
-// Tiles are 256 x ITEMS elements; small inputs use ITEMS = 4 so a 1M-key pass
-// still launches 1024 blocks (>= 6 per SM).  Per pass each element is read
-// twice and written once, so the sort is HBM/latency bound.
+// psg_sort.cu — LSD radix sort, 8-bit digits, one pass = ONE kernel:
+//   os_hist     once per sort: the digit histograms of every pass (one read
+//               of the keys, shared-memory counters, global atomics)
+//   os_scatter  per pass: a block takes the next tile (atomic ticket, so
+//               tiles are claimed in order), ranks its 2048 keys stably
+//               (warp __match_any_sync inside 32-key rounds, per-warp digit
+//               counters, a cross-warp scan), publishes its digit counts and
+//               resolves its global offsets by decoupled look-back over the
+//               tiles before it (flag+value words tagged with the pass, so
+//               one memset per sort serves every pass), then stages the tile
+//               in shared memory in digit order and writes it out in
+//               contiguous per-digit runs (coalesced)
+// Stable: ties keep input order, so sorting (key, index) with the identity
+// payload reproduces std::sort by (key, index).
 #include "psg_internal.cuh"
 #include "psg_sort.cuh"
 
@@ -18,154 +21,203 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRadix = 256;
+// keys per thread: 16 for u32 keys (4096-key tiles), 8 for u64 (2048) —
+// fewer, larger tiles shorten the look-back chains
+template <class K>
+constexpr int items() {
+  return sizeof(K) == 4 ? 16 : 8;
+}
+template <class K>
+constexpr int tile_keys() {
+  return kThreads * items<K>();
+}
+constexpr int kMaxPasses = 8;
+constexpr uint64_t kValMask = (1ull << 56) - 1;
+constexpr uint64_t kFlagAgg = 1ull << 56;     // tile's own digit count
+constexpr uint64_t kFlagPre = 2ull << 56;     // inclusive prefix over tiles 0..t
 
-template <int ITEMS>
-constexpr int tile() {
-  return kThreads * ITEMS;
+__device__ __forceinline__ uint64_t status_word(int pass, uint64_t flag, uint64_t v) {
+  return (static_cast<uint64_t>(pass + 1) << 58) | flag | v;
 }
 
-int items_for(size_t n) { return n <= (size_t(1) << 22) ? 4 : 16; }
-
-template <class K, int ITEMS>
-__global__ void __launch_bounds__(kThreads) rs_hist(const K* __restrict__ keys, size_t n, int shift,
-                                                    uint32_t* __restrict__ hist, int nblocks) {
-  __shared__ uint32_t h[kRadix];
-  h[threadIdx.x] = 0;
+template <class K>
+__global__ void __launch_bounds__(kThreads) os_hist(const K* __restrict__ keys, size_t n, int begin_bit, int passes,
+                                                    uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kThreads) (&h[0][0])[i] = 0;
   __syncthreads();
-  const size_t base = static_cast<size_t>(blockIdx.x) * tile<ITEMS>();
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const size_t idx = base + static_cast<size_t>(r) * kThreads + threadIdx.x;
-    if (idx < n) atomicAdd(&h[static_cast<uint32_t>(keys[idx] >> shift) & 0xffu], 1u);
+  for (size_t i = blockIdx.x * static_cast<size_t>(kThreads) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * kThreads) {
+    const K k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][static_cast<uint32_t>(k >> (begin_bit + 8 * p)) & 0xffu], 1u);
   }
   __syncthreads();
-  hist[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x] = h[threadIdx.x];
-}
-
-// Block `digit`: exclusive scan of hist[digit][0..nblocks), total -> totals[digit].
-__global__ void __launch_bounds__(kThreads) rs_scan(uint32_t* __restrict__ hist, int nblocks,
-                                                    uint32_t* __restrict__ totals) {
-  __shared__ uint32_t warp_sums[kWarps];
-  __shared__ uint32_t carry;
-  uint32_t* row = hist + static_cast<size_t>(blockIdx.x) * nblocks;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nblocks; base += kThreads) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < nblocks ? row[i] : 0u;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) warp_sums[warp] = incl;
-    __syncthreads();
-    uint32_t wpre = 0, chunk = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t s = warp_sums[w];
-      if (w < warp) wpre += s;
-      chunk += s;
-    }
-    const uint32_t c = carry;
-    if (i < nblocks) row[i] = c + wpre + incl - v;
-    __syncthreads();
-    if (threadIdx.x == 0) carry = c + chunk;
-    __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += kThreads) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(ghist + i, v);
   }
-  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
-template <class K, bool kVals, int ITEMS>
-__global__ void __launch_bounds__(kThreads) rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+template <class K, bool kVals>
+__global__ void __launch_bounds__(kThreads, 2) os_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                        K* __restrict__ kout, uint32_t* __restrict__ vout, size_t n,
-                                                       int shift, const uint32_t* __restrict__ hist,
-                                                       const uint32_t* __restrict__ totals, int nblocks) {
-  __shared__ uint32_t whist[kWarps][kRadix];
-  __shared__ uint32_t base[kRadix];
+                                                       int shift, int pass, const uint32_t* __restrict__ ghist,
+                                                       unsigned long long* __restrict__ status,
+                                                       uint32_t* __restrict__ ticket) {
+  __shared__ uint32_t whist[kWarps][kRadix];  // per-warp digit counts -> exclusive offsets
+  __shared__ uint32_t bexcl[kRadix];          // digit start inside the tile
+  __shared__ unsigned long long gbase[kRadix];  // global position of the tile's first key of each digit
   __shared__ uint32_t wsum[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&whist[0][0])[i] = 0;
-  {  // digit offsets = exclusive scan of the digit totals
-    const uint32_t t = totals[threadIdx.x];
-    uint32_t incl = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    uint32_t pre = 0;
-    for (int w = 0; w < warp; ++w) pre += wsum[w];
-    base[threadIdx.x] = pre + incl - t + hist[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x];
-  }
+  __shared__ uint32_t s_tile;
+  constexpr int kItems = items<K>(), kTile = tile_keys<K>();
+  __shared__ K skeys[kTile];
+  __shared__ uint32_t svals[kVals ? kTile : 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&whist[0][0])[i] = 0;
   __syncthreads();
+  const uint32_t tile = s_tile;
+  const size_t base = static_cast<size_t>(tile) * kTile;
+  const uint32_t tile_n = static_cast<uint32_t>(min(static_cast<size_t>(kTile), n - base));
 
-  const size_t wbase =
-      static_cast<size_t>(blockIdx.x) * tile<ITEMS>() + static_cast<size_t>(warp) * (32 * ITEMS);
+  // stable ranks: warp w owns keys [w*32*kItems, (w+1)*32*kItems) of the tile in rounds of 32
+  const size_t wbase = base + static_cast<size_t>(warp) * (32 * kItems);
   const unsigned lt_mask = (1u << lane) - 1u;
-  K key[ITEMS];
-  uint32_t val[ITEMS];
-  uint32_t rank[ITEMS];
+  K key[kItems];
+  uint32_t val[kItems], rank[kItems], dg[kItems];
 #pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
+  for (int r = 0; r < kItems; ++r) {  // every load in flight before any ranking
     const size_t idx = wbase + static_cast<size_t>(r) * 32 + lane;
     const bool ok = idx < n;
     key[r] = ok ? kin[idx] : K(0);
     if (kVals) val[r] = ok ? vin[idx] : 0u;
-    const uint32_t dgt = ok ? (static_cast<uint32_t>(key[r] >> shift) & 0xffu) : 0x100u;
-    const unsigned peers = __match_any_sync(0xffffffffu, dgt);
-    const uint32_t before = __popc(peers & lt_mask);
-    const uint32_t seen = ok ? whist[warp][dgt] : 0u;
+    dg[r] = ok ? 0u : 0x100u;
+  }
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const bool ok = dg[r] == 0u;
+    if (ok) dg[r] = static_cast<uint32_t>(key[r] >> shift) & 0xffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
+    const uint32_t seen = ok ? whist[warp][dg[r]] : 0u;
     __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) whist[warp][dgt] = seen + __popc(peers);
+    if (ok && lane == __ffs(peers) - 1) whist[warp][dg[r]] = seen + __popc(peers);
     __syncwarp();
-    rank[r] = seen + before;
+    rank[r] = seen + __popc(peers & lt_mask);
   }
   __syncthreads();
-  {
-    const int dgt = threadIdx.x;
-    uint32_t run = 0;
+  // thread = digit: counts over warps, tile total, publish, look back
+  const int d = tid;
+  uint32_t count = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = whist[w][dgt];
-      whist[w][dgt] = run;
-      run += c;
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t c = whist[w][d];
+    whist[w][d] = count;
+    count += c;
+  }
+  unsigned long long* mine = status + static_cast<size_t>(tile) * kRadix + d;
+  if (tile == 0) {
+    atomicExch(mine, status_word(pass, kFlagPre, count));
+  } else {
+    atomicExch(mine, status_word(pass, kFlagAgg, count));
+  }
+  // look back in windows of kLook predecessors: their status words are
+  // loaded together (independent loads in flight), then summed from the
+  // nearest tile until one carries an inclusive prefix
+  constexpr int kLook = 16;
+  uint64_t excl = 0;
+  bool done = tile == 0;
+  for (int64_t t0 = static_cast<int64_t>(tile) - 1; !done; t0 -= kLook) {
+    uint64_t v[kLook];
+#pragma unroll
+    for (int w = 0; w < kLook; ++w)
+      v[w] = t0 - w >= 0 ? *(reinterpret_cast<const volatile unsigned long long*>(status) +
+                             static_cast<size_t>(t0 - w) * kRadix + d)
+                         : status_word(pass, kFlagPre, 0);
+#pragma unroll
+    for (int w = 0; w < kLook; ++w) {
+      if (done) break;
+      while ((v[w] >> 58) != static_cast<uint64_t>(pass + 1))  // not yet published in this pass
+        v[w] = *(reinterpret_cast<const volatile unsigned long long*>(status) + static_cast<size_t>(t0 - w) * kRadix + d);
+      excl += v[w] & kValMask;
+      if (v[w] & kFlagPre) done = true;
+    }
+  }
+  if (tile > 0) atomicExch(mine, status_word(pass, kFlagPre, excl + count));
+  // global digit start: exclusive scan of the pass histogram (every block, 256 values)
+  const uint32_t hcount = ghist[d];
+  uint32_t incl = hcount, inclb = count;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    const uint32_t tb = __shfl_up_sync(0xffffffffu, inclb, o);
+    if (lane >= o) {
+      incl += t;
+      inclb += tb;
+    }
+  }
+  __shared__ uint32_t wsum_b[kWarps];
+  if (lane == 31) {
+    wsum[warp] = incl;
+    wsum_b[warp] = inclb;
+  }
+  __syncthreads();
+  uint32_t pre = 0, preb = 0;
+  for (int w = 0; w < warp; ++w) {
+    pre += wsum[w];
+    preb += wsum_b[w];
+  }
+  gbase[d] = static_cast<unsigned long long>(pre + incl - hcount) + excl;
+  bexcl[d] = preb + inclb - count;
+  __syncthreads();
+  // stage the tile in digit order
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    if (dg[r] < 0x100u) {
+      const uint32_t local = bexcl[dg[r]] + whist[warp][dg[r]] + rank[r];
+      skeys[local] = key[r];
+      if (kVals) svals[local] = val[r];
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const size_t idx = wbase + static_cast<size_t>(r) * 32 + lane;
-    if (idx < n) {
-      const uint32_t dgt = static_cast<uint32_t>(key[r] >> shift) & 0xffu;
-      const size_t pos = static_cast<size_t>(base[dgt]) + whist[warp][dgt] + rank[r];
-      kout[pos] = key[r];
-      if (kVals) vout[pos] = val[r];
-    }
+  // contiguous per-digit runs out
+  for (uint32_t i = tid; i < tile_n; i += kThreads) {
+    const K k = skeys[i];
+    const uint32_t dd = static_cast<uint32_t>(k >> shift) & 0xffu;
+    const size_t pos = gbase[dd] + (i - bexcl[dd]);
+    kout[pos] = k;
+    if (kVals) vout[pos] = svals[i];
   }
 }
 
-template <class K, int ITEMS>
-int sort_impl(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bit, uint32_t* hist,
-              cudaStream_t s) {
-  const int nblocks = static_cast<int>((n + tile<ITEMS>() - 1) / tile<ITEMS>());
-  uint32_t* totals = hist + static_cast<size_t>(nblocks) * kRadix;
+template <class K>
+size_t tiles_for(size_t n) {
+  return (n + tile_keys<K>() - 1) / tile_keys<K>();
+}
+
+// hist layout (u32 words): [kMaxPasses x 256 histograms][kMaxPasses tickets][pad][tiles x 256 u64 status]
+size_t status_offset_words() { return ((kMaxPasses * kRadix + kMaxPasses) + 1) & ~size_t(1); }
+
+template <class K>
+int sort_impl(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bit, uint32_t* hist, cudaStream_t s) {
+  const int passes = (end_bit - begin_bit + 7) / 8;
+  if (passes > kMaxPasses) throw std::runtime_error("radix_sort: too many passes");
+  const size_t tiles = tiles_for<K>(n);
+  uint32_t* ghist = hist;
+  uint32_t* tickets = hist + kMaxPasses * kRadix;
+  auto* status = reinterpret_cast<unsigned long long*>(hist + status_offset_words());
+  PSG_CUDA(cudaMemsetAsync(hist, 0, (status_offset_words() + 2 * tiles * kRadix) * sizeof(uint32_t), s));
+  const int hb = static_cast<int>(std::min<size_t>((n + kThreads * 16 - 1) / (kThreads * 16), 148 * 8));
+  os_hist<K><<<std::max(hb, 1), kThreads, 0, s>>>(keys[0], n, begin_bit, passes, ghist);
+  PSG_LAUNCHED();
   int cur = 0;
-  for (int shift = begin_bit; shift < end_bit; shift += 8) {
-    rs_hist<K, ITEMS><<<nblocks, kThreads, 0, s>>>(keys[cur], n, shift, hist, nblocks);
-    PSG_LAUNCHED();
-    rs_scan<<<kRadix, kThreads, 0, s>>>(hist, nblocks, totals);
-    PSG_LAUNCHED();
+  for (int p = 0; p < passes; ++p) {
+    const int shift = begin_bit + 8 * p;
     if (vals[0])
-      rs_scatter<K, true, ITEMS><<<nblocks, kThreads, 0, s>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
-                                                              shift, hist, totals, nblocks);
+      os_scatter<K, true><<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(
+          keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, shift, p, ghist + p * kRadix, status, tickets + p);
     else
-      rs_scatter<K, false, ITEMS><<<nblocks, kThreads, 0, s>>>(keys[cur], nullptr, keys[cur ^ 1], nullptr, n, shift,
-                                                               hist, totals, nblocks);
+      os_scatter<K, false><<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(
+          keys[cur], nullptr, keys[cur ^ 1], nullptr, n, shift, p, ghist + p * kRadix, status, tickets + p);
     PSG_LAUNCHED();
     cur ^= 1;
   }
@@ -291,18 +343,13 @@ void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count,
   PSG_LAUNCHED();
 }
 
-size_t radix_hist_words(size_t n) {
-  const size_t t = static_cast<size_t>(kThreads) * items_for(n);
-  const size_t blocks = (n + t - 1) / t;
-  return (blocks ? blocks : 1) * kRadix + kRadix;
-}
+size_t radix_hist_words(size_t n) { return status_offset_words() + 2 * tiles_for<uint64_t>(n) * kRadix; }
 
 template <class K>
 int radix_sort(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bit, uint32_t* hist,
                cudaStream_t s) {
   if (n <= 1) return 0;
-  if (items_for(n) == 4) return sort_impl<K, 4>(keys, vals, n, begin_bit, end_bit, hist, s);
-  return sort_impl<K, 16>(keys, vals, n, begin_bit, end_bit, hist, s);
+  return sort_impl<K>(keys, vals, n, begin_bit, end_bit, hist, s);
 }
 
 template int radix_sort<uint32_t>(uint32_t* [2], uint32_t* [2], size_t, int, int, uint32_t*, cudaStream_t);
