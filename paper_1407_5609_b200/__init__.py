@@ -385,9 +385,31 @@ def brute_force_neighbors(points: PointSet, radius: float, exclusion_zone: int =
     return _neigh(out, True).neighbors
 
 
+class PinnedBuffer:
+    """Page-locked host memory (psg_host_alloc) viewed as a numpy array: the
+    device writes into it at full PCIe rate.  Freed with the object."""
+
+    def __init__(self, count: int, dtype=np.uint64):
+        self.dtype = np.dtype(dtype)
+        self.count = int(count)
+        p = _p()
+        _check(lib().psg_host_alloc(max(self.count, 1) * self.dtype.itemsize, C.byref(p)))
+        self._p = p
+        self.array = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)),
+                                           shape=(max(self.count, 1) * self.dtype.itemsize,)).view(self.dtype)[:self.count]
+
+    def __del__(self):
+        if getattr(self, "_p", None):
+            lib().psg_host_free(self._p)
+            self._p = None
+
+
 def frnn_pairs(points: np.ndarray, radius: float, q: int = 10, f: float = 10.0, seed: int = 1,
-               exclusion_zone: int = 0, want_pairs: bool = True):
-    """Sorted i<j pair list ((i<<32)|j), count and order-independent hash."""
+               exclusion_zone: int = 0, want_pairs: bool = True, out: np.ndarray | None = None):
+    """Sorted i<j pair list ((i<<32)|j), count and order-independent hash.
+
+    `out` (optional, uint64, e.g. PinnedBuffer(...).array) receives the list;
+    when it is too small only the count and hash are returned."""
     pts = np.ascontiguousarray(points, dtype=np.float32)
     n, d = pts.shape
     cnt, h = _u64(), _u64()
@@ -395,9 +417,13 @@ def frnn_pairs(points: np.ndarray, radius: float, q: int = 10, f: float = 10.0, 
         _check(lib().psg_frnn_pairs_f32(_ptr(pts), n, d, radius, q, f, seed, exclusion_zone, None, 0,
                                         C.byref(cnt), C.byref(h)))
         return None, cnt.value, h.value
-    cap = max(64 * n, 1 << 16)
+    if out is not None:
+        _check(lib().psg_frnn_pairs_f32(_ptr(pts), n, d, radius, q, f, seed, exclusion_zone, _ptr(out), out.size,
+                                        C.byref(cnt), C.byref(h)))
+        return (out[: cnt.value] if cnt.value <= out.size else None), cnt.value, h.value
+    cap = max(40 * n, 1 << 16)
     while True:
-        buf = np.zeros(cap, np.uint64)
+        buf = np.empty(cap, np.uint64)
         _check(lib().psg_frnn_pairs_f32(_ptr(pts), n, d, radius, q, f, seed, exclusion_zone, _ptr(buf), cap,
                                         C.byref(cnt), C.byref(h)))
         if cnt.value <= cap:

@@ -1,16 +1,23 @@
 // psg_frnn.cu — exact fixed-radius neighbours (refscan.cpp:159-209).
 //
-//   K1 project    keys = <U_k, X_i>                         (psg_cpp.cu)
-//      grid       cell = floor((k_t - min_t) / w), t < g = min(3, q), w >= the
-//                 key window implied by R (+ rounding slack), so every pair
-//                 within R sits in the same or an adjacent cell
-//   K2 sort       radix sort by cell id (stable: original index inside a cell)
-//   K4 scan       one thread per point, half stencil of neighbour cells; all
-//                 nk keys prune (lower bound), then the FP32 distance decides
-//                 outside the rounding band and the reference's FP64
-//                 arithmetic decides inside it (boundary inclusive, <= R);
-//                 pairs emitted as (min(i,j)<<32)|max(i,j), hashed in-kernel
-//   lists         both directions radix-sorted -> CSR, ascending per row
+//   K1 project    keys = <U_k, X_i>                         (psg_cpp.cu / psg_project_tc.cu)
+//   K2 grid       the closest-pair engine's cell grid (psg_grid.cuh) over the
+//                 first g = min(3, q) keys with cell width >= the key window
+//                 implied by R (+ rounding slack): every pair within R sits in
+//                 the same or an adjacent cell; stable radix sort by cell, so a
+//                 point's forward half-stencil is <= 5 contiguous position ranges
+//   K4 scan       one thread per sorted position, warps iterate in lockstep over
+//                 their lanes' flattened ranges; d <= 4: coordinates gathered
+//                 into cell order (one float4 per point) and the FP32 distance
+//                 is the only filter; d > 4: all nk keys prune (lower bound) first.
+//                 The FP32 distance decides outside the rounding band, the
+//                 reference's FP64 arithmetic inside it (boundary inclusive,
+//                 <= R).  Pairs (min(i,j)<<32)|max(i,j) are appended through a
+//                 per-warp shared-memory buffer (one global atomic per 32
+//                 pairs) and hashed in-kernel (order-independent sum)
+//   lists         CSR without a global sort: per-row counts (atomics), scan,
+//                 scatter, then each row sorted by one warp (bitonic in
+//                 registers); the (i<j) pair list is the same with one direction
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -18,6 +25,8 @@
 
 #include "psg_cpp.cuh"
 #include "psg_engines.cuh"
+#include "psg_grid.cuh"
+#include "psg_scan.cuh"
 #include "psg_sort.cuh"
 
 namespace psg {
@@ -27,14 +36,14 @@ uint64_t brute_emit_pairs(psg_pointset* ps, double radius, uint64_t zone, DevBuf
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
-
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.cpp:46-51
   x += 0x9e3779b97f4a7c15ull;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
   return x ^ (x >> 31);
 }
+
+unsigned blocks(uint64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
 
 template <int NK>
 __global__ void k_key_range(const float* __restrict__ keys, uint32_t n, int g, unsigned* __restrict__ mn,
@@ -55,65 +64,28 @@ __global__ void k_key_range(const float* __restrict__ keys, uint32_t n, int g, u
   }
 }
 
-struct Grid {
-  int g = 1;
-  double lo[3] = {0, 0, 0};
-  double inv_w = 1.0;
-  uint32_t dims[3] = {1, 1, 1};
-  uint64_t cells = 1;
-};
-
-template <int NK>
-__global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, Grid gr, uint32_t* __restrict__ cid,
-                           uint32_t* __restrict__ idx) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint32_t c = 0;
-  for (int t = 0; t < gr.g; ++t) {
-    double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - gr.lo[t]) * gr.inv_w;
-    uint32_t ct = v <= 0.0 ? 0u : static_cast<uint32_t>(v);
-    if (ct >= gr.dims[t]) ct = gr.dims[t] - 1;
-    c = c * gr.dims[t] + ct;
-  }
-  cid[i] = c;
-  idx[i] = i;
-}
-
-template <int NK>
-__global__ void k_gather_cells(const float* __restrict__ keys, const uint32_t* __restrict__ perm, uint32_t n,
-                               float* __restrict__ skeys, uint32_t* __restrict__ sidx) {
+// d <= 4: the coordinates in cell order, one float4 per sorted position
+__global__ void k_gather_rows4(const float* __restrict__ X, const uint32_t* __restrict__ sidx, uint32_t n, int d,
+                               float4* __restrict__ sx) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const uint32_t i = perm[p];
-  const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
-  float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(p) * NK);
-#pragma unroll
-  for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
-  sidx[p] = i;
-}
-
-__global__ void k_cell_ranges(const uint32_t* __restrict__ scell, uint32_t n, uint32_t* __restrict__ cstart,
-                              uint32_t* __restrict__ cend) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const uint32_t c = scell[p];
-  if (p == 0 || scell[p - 1] != c) cstart[c] = p;
-  if (p == n - 1 || scell[p + 1] != c) cend[c] = p + 1;
+  const float* r = X + static_cast<size_t>(sidx[p]) * d;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int t = 0; t < d; ++t) v[t] = r[t];
+  sx[p] = make_float4(v[0], v[1], v[2], v[3]);
 }
 
 struct FrnnArgs {
   const float* X;
   const float* skeys;
+  const float4* sx;  // d <= 4
   const uint32_t* sidx;
-  const uint32_t* scell;
-  const uint32_t* cstart;
-  const uint32_t* cend;
+  GridDev grid;
   uint32_t n;
   int d;
   uint64_t zone;
-  Grid gr;
   Thresholds th;
-  float lo;
+  float lo;  // s32 <= lo: inside R for certain
   double R;
   ExactSrc src;
   uint64_t* out;
@@ -121,103 +93,221 @@ struct FrnnArgs {
   unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined
 };
 
-template <int NK>
-__device__ __forceinline__ void load_keys(const float* __restrict__ p, float (&k)[NK]) {
-  const float4* p4 = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int v = 0; v < NK / 4; ++v) {
-    const float4 t = p4[v];
-    k[4 * v] = t.x;
-    k[4 * v + 1] = t.y;
-    k[4 * v + 2] = t.z;
-    k[4 * v + 3] = t.w;
-  }
-}
+constexpr int kFrnnThreads = 256;
 
-template <int NK>
-__global__ void __launch_bounds__(256) k_frnn_scan(FrnnArgs a) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+// One thread per sorted position; the warp walks its lanes' flattened ranges
+// in lockstep (lane predicate t < total), so emission is warp-converged.
+template <int NK, bool kSmallD>
+__global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
+  __shared__ GridParams sP;
+  __shared__ uint64_t wbuf[kFrnnThreads / 32][64];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) sP = *a.grid.gp;
+  __syncthreads();
+  const uint32_t p = blockIdx.x * kFrnnThreads + tid;
+  const bool valid = p < a.n;
   uint64_t visited = 0, examined = 0, hsum = 0;
-  if (p < a.n) {
-    float mk[NK];
-    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
-    const uint32_t mi = a.sidx[p];
-    const float* xi = a.X + static_cast<size_t>(mi) * a.d;
-    const uint32_t c = a.scell[p];
-    uint32_t cc[3] = {0, 0, 0};
-    {
-      uint32_t r = c;
-      for (int t = a.gr.g - 1; t >= 0; --t) {
-        cc[t] = r % a.gr.dims[t];
-        r /= a.gr.dims[t];
-      }
-    }
-    int nst = 1;
-    for (int t = 0; t < a.gr.g; ++t) nst *= 3;
-    // offsets o in {-1,0,1}^g; visit o == 0 (j > p) and o lexicographically > 0
-    for (int s = nst / 2; s < nst; ++s) {
-      int rem = s;
-      int off[3] = {0, 0, 0};
-      for (int t = a.gr.g - 1; t >= 0; --t) {
-        off[t] = rem % 3 - 1;
-        rem /= 3;
-      }
-      uint32_t nc = 0;
-      bool ok = true;
-      for (int t = 0; t < a.gr.g; ++t) {
-        const int64_t v = static_cast<int64_t>(cc[t]) + off[t];
-        if (v < 0 || v >= a.gr.dims[t]) {
-          ok = false;
-          break;
-        }
-        nc = nc * a.gr.dims[t] + static_cast<uint32_t>(v);
-      }
-      if (!ok) continue;
-      uint32_t jb = a.cstart[nc], je = a.cend[nc];
-      if (s == nst / 2) jb = p + 1;  // own cell: later positions only
-      for (uint32_t j = jb; j < je; ++j) {
-        const uint32_t mj = a.sidx[j];
-        const uint32_t gap = mi > mj ? mi - mj : mj - mi;
-        if (gap < a.zone) continue;  // refscan.cpp:15-18
+  GridFlat F{};
+  float mk[NK];
+  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t mi = 0;
+  if (valid) {
+    F = grid_flat(grid_ranges(a.grid.cfirst, sP, p, a.grid.scell[p]));
+    mi = a.sidx[p];
+    if constexpr (kSmallD)
+      me = a.sx[p];
+    else
+      load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+  }
+  const uint32_t T = valid ? F.total : 0u;
+  const uint32_t Tmax = __reduce_max_sync(kFull, T);
+  const float* xi = a.X + static_cast<size_t>(mi) * a.d;
+  const unsigned lt = (1u << lane) - 1u;
+  int c = 0;  // warp-uniform fill of wbuf[w]
+  for (uint32_t t = 0; t < Tmax; ++t) {
+    bool emit = false;
+    uint64_t key = 0;
+    if (t < T) {
+      const uint32_t j = F.at(t);
+      const uint32_t mj = a.sidx[j];
+      if (a.zone <= 1 || admissible(mi, mj, a.zone)) {  // refscan.cpp:15-18
         ++visited;
-        float kj[NK];
-        load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
-        float g = kj[0] - mk[0];
-        float sl = g * g;
-#pragma unroll
-        for (int k = 1; k < NK; ++k) {
-          g = kj[k] - mk[k];
-          sl = fmaf(g, g, sl);
+        float s32;
+        bool pass = true;
+        if constexpr (kSmallD) {
+          const float4 o = a.sx[j];
+          float g = o.x - me.x;
+          s32 = g * g;
+          g = o.y - me.y;
+          s32 = fmaf(g, g, s32);
+          g = o.z - me.z;
+          s32 = fmaf(g, g, s32);
+          g = o.w - me.w;
+          s32 = fmaf(g, g, s32);
+        } else {
+          float kj[NK];
+          load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
+          pass = lb2_full<NK>(mk, kj) <= a.th.lb2;
+          s32 = pass ? thread_sqdist(xi, a.X + static_cast<size_t>(mj) * a.d, a.d) : INFINITY;
         }
-        if (sl > a.th.lb2) continue;
-        ++examined;
-        const float* xj = a.X + static_cast<size_t>(mj) * a.d;
-        float s32 = 0.f;
-        for (int t = 0; t < a.d; ++t) {
-          const float q = __ldg(xi + t) - __ldg(xj + t);
-          s32 = fmaf(q, q, s32);
+        if (pass) {
+          ++examined;
+          if (s32 <= a.th.band && (s32 <= a.lo || exact_distance(a.src, mi, mj) <= a.R)) {  // boundary inclusive
+            emit = true;
+            key = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
+            hsum += mix64(key);
+          }
         }
-        if (s32 > a.th.band) continue;
-        if (s32 > a.lo && !(exact_distance(a.src, mi, mj) <= a.R)) continue;  // boundary inclusive
-        const uint64_t key = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
-        const unsigned long long slot = atomicAdd(a.acc, 1ull);
-        if (slot < a.cap) a.out[slot] = key;
-        hsum += mix64(key);
       }
     }
+    const unsigned mask = __ballot_sync(kFull, emit);
+    if (mask) {
+      if (emit) wbuf[w][c + __popc(mask & lt)] = key;
+      c += __popc(mask);
+      if (c >= 32) {  // flush 32 with one atomic
+        __syncwarp();
+        unsigned long long g = 0;
+        if (lane == 0) g = atomicAdd(a.acc, 32ull);
+        g = __shfl_sync(kFull, g, 0);
+        if (g + lane < a.cap) a.out[g + lane] = wbuf[w][lane];
+        __syncwarp();
+        if (lane < c - 32) wbuf[w][lane] = wbuf[w][32 + lane];
+        c -= 32;
+        __syncwarp();
+      }
+    }
+  }
+  if (c > 0) {
+    __syncwarp();
+    unsigned long long g = 0;
+    if (lane == 0) g = atomicAdd(a.acc, static_cast<unsigned long long>(c));
+    g = __shfl_sync(kFull, g, 0);
+    if (lane < c && g + lane < a.cap) a.out[g + lane] = wbuf[w][lane];
   }
   for (int o = 16; o; o >>= 1) {
     hsum += __shfl_xor_sync(kFull, hsum, o);
     visited += __shfl_xor_sync(kFull, visited, o);
     examined += __shfl_xor_sync(kFull, examined, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     if (hsum) atomicAdd(a.acc + 1, static_cast<unsigned long long>(hsum));
     if (visited) atomicAdd(a.acc + 2, static_cast<unsigned long long>(visited));
     if (examined) atomicAdd(a.acc + 3, static_cast<unsigned long long>(examined));
   }
 }
 
+// ---- CSR lists without a global sort ------------------------------------------
+__global__ void k_row_counts(const uint64_t* __restrict__ pairs, uint64_t m, bool both, uint32_t* __restrict__ cnt) {
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < m;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = pairs[k];
+    atomicAdd(cnt + (v >> 32), 1u);
+    if (both) atomicAdd(cnt + (v & 0xffffffffull), 1u);
+  }
+}
+
+__global__ void k_row_scatter(const uint64_t* __restrict__ pairs, uint64_t m, bool both, uint32_t* __restrict__ cur,
+                              uint32_t* __restrict__ cols) {
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < m;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = pairs[k];
+    const uint32_t i = static_cast<uint32_t>(v >> 32), j = static_cast<uint32_t>(v);
+    cols[atomicAdd(cur + i, 1u)] = j;
+    if (both) cols[atomicAdd(cur + j, 1u)] = i;
+  }
+}
+
+// Warp bitonic sort of 32R values held as v[r] = element r*32 + lane.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[R], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int pr = r ^ jr;
+          if (pr > r) {
+            const bool up = (((r << 5) | lane) & k) == 0;
+            const uint32_t x = v[r], y = v[pr];
+            if ((x > y) == up) {
+              v[r] = y;
+              v[pr] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t o = __shfl_xor_sync(kFull, v[r], j);
+          const bool up = (((r << 5) | lane) & k) == 0;
+          const bool lower = (lane & j) == 0;
+          v[r] = (lower == up) ? min(v[r], o) : max(v[r], o);
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void sort_row(uint32_t* __restrict__ row, uint32_t len, int lane) {
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t e = r * 32 + lane;
+    v[r] = e < len ? row[e] : 0xffffffffu;
+  }
+  warp_bitonic<R>(v, lane);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t e = r * 32 + lane;
+    if (e < len) row[e] = v[r];
+  }
+}
+
+// One warp per row; rows longer than 1024 are flagged for the global fallback.
+__global__ void k_sort_rows(const uint32_t* __restrict__ off, uint64_t n, uint32_t* __restrict__ cols,
+                            unsigned* __restrict__ too_long) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; r < n; r += nw) {
+    const uint32_t b = off[r], len = off[r + 1] - b;
+    uint32_t* row = cols + b;
+    if (len <= 1) continue;
+    if (len <= 32) sort_row<1>(row, len, lane);
+    else if (len <= 64) sort_row<2>(row, len, lane);
+    else if (len <= 128) sort_row<4>(row, len, lane);
+    else if (len <= 256) sort_row<8>(row, len, lane);
+    else if (len <= 512) sort_row<16>(row, len, lane);
+    else if (len <= 1024) sort_row<32>(row, len, lane);
+    else if (lane == 0) atomicOr(too_long, 1u);
+  }
+}
+
+__global__ void k_widen_offsets(const uint32_t* __restrict__ in, uint64_t count, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+// pairs[k] = (i<<32)|j for every row i and column j of the (i<j) CSR, in order
+__global__ void k_csr_to_pairs(const uint32_t* __restrict__ off, uint64_t n, const uint32_t* __restrict__ cols,
+                               uint64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; r < n; r += nw)
+    for (uint32_t e = off[r] + lane; e < off[r + 1]; e += 32) out[e] = (r << 32) | cols[e];
+}
+
+__global__ void k_cols_to_u64(const uint32_t* __restrict__ in, uint64_t count, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+// ---- fallback: global sort of the directed pairs (rows longer than 1024) ----
 __global__ void k_directed(const uint64_t* __restrict__ pairs, uint64_t m, int b, uint64_t* __restrict__ out) {
   const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (k >= m) return;
@@ -266,7 +356,7 @@ int bits_for(uint64_t n) {
   return b;
 }
 
-unsigned blocks(uint64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
+unsigned grid_cap(uint64_t work) { return static_cast<unsigned>(std::min<uint64_t>(blocks(work, 256), 148ull * 16)); }
 
 // Sorts `count` u64 keys of `width` bits in buf (scratch allocated here); the
 // sorted keys end in buf.
@@ -278,8 +368,39 @@ void sort_u64(DevBuf<uint64_t>& buf, uint64_t count, int width, cudaStream_t s) 
   uint32_t* vv[2] = {nullptr, nullptr};
   const int passes = (width + 7) / 8;
   const int which = radix_sort<uint64_t>(kk, vv, count, 0, passes * 8, hist.p, s);
-  g_launches += 3 * passes;
+  g_launches += 1 + passes;
   if (which == 1) std::swap(buf, tmp);
+}
+
+// Rows of the (i<j) pairs (both = false) or of both directions: offsets (n+1,
+// u32) and ascending columns.  Returns false when a row exceeds 1024 entries
+// (the caller falls back to the global sort).
+bool csr_rows(const DevBuf<uint64_t>& pairs, uint64_t m, uint64_t n, bool both, DevBuf<uint32_t>& off,
+              DevBuf<uint32_t>& cols, cudaStream_t s) {
+  const uint64_t entries = both ? 2 * m : m;
+  if (entries >= 0xffffffffull) throw std::runtime_error("pairscan_b200: neighbour list exceeds 2^32 entries");
+  DevBuf<uint32_t> cnt(n + 1, s), tmp(scan_temp_words(n + 1), s), flag(1, s);
+  off.alloc(n + 1, s);
+  cols.alloc(std::max<uint64_t>(entries, 1), s);
+  PSG_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * 4, s));
+  PSG_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+  if (m) {
+    k_row_counts<<<grid_cap(m), 256, 0, s>>>(pairs.p, m, both, cnt.p);
+    PSG_LAUNCHED();
+  }
+  exclusive_scan_u32(cnt.p, off.p, n + 1, tmp.p, s);
+  PSG_CUDA(cudaMemcpyAsync(cnt.p, off.p, (n + 1) * 4, cudaMemcpyDeviceToDevice, s));  // cursors
+  if (m) {
+    k_row_scatter<<<grid_cap(m), 256, 0, s>>>(pairs.p, m, both, cnt.p, cols.p);
+    PSG_LAUNCHED();
+  }
+  k_sort_rows<<<grid_cap(n * 32), 256, 0, s>>>(off.p, n, cols.p, flag.p);
+  PSG_LAUNCHED();
+  g_launches += 6;
+  unsigned h = 0;
+  PSG_CUDA(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
 }
 
 }  // namespace
@@ -292,27 +413,36 @@ void finish_neighbors(DevBuf<uint64_t>& pairs, uint64_t m, uint64_t n, bool want
   out->offsets = nullptr;
   out->neighbors = nullptr;
   if (!want_lists) return;
-  const int b = bits_for(n);
-  DevBuf<uint64_t> dir(std::max<uint64_t>(2 * m, 1), s);
-  if (m) {
-    k_directed<<<blocks(m, 256), 256, 0, s>>>(pairs.p, m, b, dir.p);
-    PSG_LAUNCHED();
-    ++g_launches;
-    sort_u64(dir, 2 * m, 2 * b, s);
-  }
-  DevBuf<uint64_t> off(n + 1, s);
-  k_offsets<<<blocks(n + 1, 256), 256, 0, s>>>(dir.p, 2 * m, n, b, off.p);
-  PSG_LAUNCHED();
-  if (m) {
-    k_low_bits<<<blocks(2 * m, 256), 256, 0, s>>>(dir.p, 2 * m, b);
-    PSG_LAUNCHED();
-  }
-  g_launches += 2;
   out->offsets = static_cast<uint64_t*>(std::malloc((n + 1) * sizeof(uint64_t)));
   out->neighbors = static_cast<uint64_t*>(std::malloc(std::max<uint64_t>(2 * m, 1) * sizeof(uint64_t)));
   if (!out->offsets || !out->neighbors) throw std::bad_alloc();
-  PSG_CUDA(cudaMemcpyAsync(out->offsets, off.p, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-  if (m) PSG_CUDA(cudaMemcpyAsync(out->neighbors, dir.p, 2 * m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  DevBuf<uint32_t> off32, cols;
+  if (csr_rows(pairs, m, n, true, off32, cols, s)) {
+    DevBuf<uint64_t> off(n + 1, s), nb(std::max<uint64_t>(2 * m, 1), s);
+    k_widen_offsets<<<grid_cap(n + 1), 256, 0, s>>>(off32.p, n + 1, off.p);
+    PSG_LAUNCHED();
+    if (m) {
+      k_cols_to_u64<<<grid_cap(2 * m), 256, 0, s>>>(cols.p, 2 * m, nb.p);
+      PSG_LAUNCHED();
+    }
+    g_launches += 2;
+    PSG_CUDA(cudaMemcpyAsync(out->offsets, off.p, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    if (m) PSG_CUDA(cudaMemcpyAsync(out->neighbors, nb.p, 2 * m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  } else {  // a row longer than 1024: sort the directed pairs globally
+    const int b = bits_for(n);
+    DevBuf<uint64_t> dir(std::max<uint64_t>(2 * m, 1), s);
+    k_directed<<<blocks(m, 256), 256, 0, s>>>(pairs.p, m, b, dir.p);
+    PSG_LAUNCHED();
+    sort_u64(dir, 2 * m, 2 * b, s);
+    DevBuf<uint64_t> off(n + 1, s);
+    k_offsets<<<blocks(n + 1, 256), 256, 0, s>>>(dir.p, 2 * m, n, b, off.p);
+    PSG_LAUNCHED();
+    k_low_bits<<<blocks(2 * m, 256), 256, 0, s>>>(dir.p, 2 * m, b);
+    PSG_LAUNCHED();
+    g_launches += 3;
+    PSG_CUDA(cudaMemcpyAsync(out->offsets, off.p, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(out->neighbors, dir.p, 2 * m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  }
   PSG_CUDA(cudaStreamSynchronize(s));
   g_prof.d2h_bytes += (n + 1 + 2 * m) * sizeof(uint64_t);
 }
@@ -345,83 +475,53 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   const double inner = Rw * (1.0 - 4.0 * bud.gamma64) - 2.0 * bud.Rn;
   const float lo = inner > 0 ? static_cast<float>(((inner * inner) * (1.0 - bud.e) - bud.a) * (1.0 - 1e-6)) : -1.0f;
 
-  // grid over the first g keys
-  Grid gr;
-  gr.g = std::min(3, dir.q);
+  // grid over the first g keys, cell width >= the key window of R
+  const int g = std::min(3, dir.q);
+  GridIndex gi;
+  gi.ensure(static_cast<uint32_t>(n), nk, s);
   {
     DevBuf<unsigned> mm(6, s);
     const unsigned init[6] = {~0u, ~0u, ~0u, 0u, 0u, 0u};
     PSG_CUDA(cudaMemcpyAsync(mm.p, init, 24, cudaMemcpyHostToDevice, s));
     const unsigned gb = std::min<unsigned>(blocks(n, 256), c.sm_count * 8);
     if (nk == 4)
-      k_key_range<4><<<gb, 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), gr.g, mm.p, mm.p + 3);
+      k_key_range<4><<<gb, 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), g, mm.p, mm.p + 3);
     else
-      k_key_range<8><<<gb, 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), gr.g, mm.p, mm.p + 3);
+      k_key_range<8><<<gb, 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), g, mm.p, mm.p + 3);
     PSG_LAUNCHED();
     ++g_launches;
     unsigned h[6];
     PSG_CUDA(cudaMemcpyAsync(h, mm.p, 24, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    double w = static_cast<double>(th.win) * (1.0 + 1e-6);
-    double span[3];
-    for (int t = 0; t < gr.g; ++t) {
-      gr.lo[t] = f32_unorder(h[t]);
-      span[t] = static_cast<double>(f32_unorder(h[3 + t])) - gr.lo[t];
+    double lo3[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
+    for (int t = 0; t < g; ++t) {
+      lo3[t] = f32_unorder(h[t]);
+      span[t] = std::max(static_cast<double>(f32_unorder(h[3 + t])) - lo3[t], 1e-30);
     }
-    for (;;) {
-      double cells = 1.0;
-      for (int t = 0; t < gr.g; ++t) cells *= std::floor(span[t] / w) + 1.0;
-      if (cells <= static_cast<double>(1u << 26)) break;
-      w *= 1.25;
-    }
-    gr.inv_w = 1.0 / w;
-    gr.cells = 1;
-    for (int t = 0; t < gr.g; ++t) {
-      gr.dims[t] = static_cast<uint32_t>(std::floor(span[t] / w)) + 1;
-      gr.cells *= gr.dims[t];
-    }
+    GridParams gp;
+    grid_params_for(gp, std::max(g, 1), static_cast<double>(th.win) * (1.0 + 1e-6), lo3, span);
+    PSG_CUDA(cudaMemcpyAsync(gi.gp.p, &gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
   }
-  DevBuf<uint32_t> kb0(n, s), kb1(n, s), vb0(n, s), vb1(n, s);
-  DevBuf<uint32_t> hist(radix_hist_words(n), s);
-  if (nk == 4)
-    k_cell_ids<4><<<blocks(n, 256), 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), gr, kb0.p, vb0.p);
-  else
-    k_cell_ids<8><<<blocks(n, 256), 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), gr, kb0.p, vb0.p);
-  PSG_LAUNCHED();
-  ++g_launches;
-  uint32_t* kk[2] = {kb0.p, kb1.p};
-  uint32_t* vv[2] = {vb0.p, vb1.p};
-  const int cbits = bits_for(gr.cells);
-  const int passes = (cbits + 7) / 8;
-  const int which = radix_sort<uint32_t>(kk, vv, n, 0, passes * 8, hist.p, s);
-  g_launches += 3 * passes;
-  tm.mark("sort");
-  DevBuf<float> skeys(n * nk, s);
-  DevBuf<uint32_t> sidx(n, s), cstart(gr.cells, s), cend(gr.cells, s);
-  if (nk == 4)
-    k_gather_cells<4><<<blocks(n, 256), 256, 0, s>>>(keys.p, vv[which], static_cast<uint32_t>(n), skeys.p, sidx.p);
-  else
-    k_gather_cells<8><<<blocks(n, 256), 256, 0, s>>>(keys.p, vv[which], static_cast<uint32_t>(n), skeys.p, sidx.p);
-  PSG_LAUNCHED();
-  PSG_CUDA(cudaMemsetAsync(cstart.p, 0, gr.cells * 4, s));
-  PSG_CUDA(cudaMemsetAsync(cend.p, 0, gr.cells * 4, s));
-  k_cell_ranges<<<blocks(n, 256), 256, 0, s>>>(kk[which], static_cast<uint32_t>(n), cstart.p, cend.p);
-  PSG_LAUNCHED();
-  g_launches += 2;
-  keys.release();
+  build_grid(keys.p, static_cast<uint32_t>(n), nk, gi, 24, s);
+  const bool small_d = ps->d <= 4;
+  DevBuf<float4> sx;
+  if (small_d) {
+    sx.alloc(n, s);
+    k_gather_rows4<<<blocks(n, 256), 256, 0, s>>>(ps->X, gi.sidx.p, static_cast<uint32_t>(n), ps->d, sx.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
   tm.mark("grid");
 
   FrnnArgs a{};
   a.X = ps->X;
-  a.skeys = skeys.p;
-  a.sidx = sidx.p;
-  a.scell = kk[which];
-  a.cstart = cstart.p;
-  a.cend = cend.p;
+  a.skeys = gi.skeys.p;
+  a.sx = sx.p;
+  a.sidx = gi.sidx.p;
+  a.grid = gi.dev;
   a.n = static_cast<uint32_t>(n);
   a.d = ps->d;
   a.zone = zone;
-  a.gr = gr;
   a.th = th;
   a.lo = lo;
   a.R = radius;
@@ -434,10 +534,17 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
     a.out = run.pairs.p;
     a.cap = cap;
     a.acc = acc.p;
-    if (nk == 4)
-      k_frnn_scan<4><<<blocks(n, 256), 256, 0, s>>>(a);
-    else
-      k_frnn_scan<8><<<blocks(n, 256), 256, 0, s>>>(a);
+    if (small_d) {
+      if (nk == 4)
+        k_frnn_scan<4, true><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+      else
+        k_frnn_scan<8, true><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+    } else {
+      if (nk == 4)
+        k_frnn_scan<4, false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+      else
+        k_frnn_scan<8, false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+    }
     PSG_LAUNCHED();
     ++g_launches;
     unsigned long long h[4];
@@ -482,16 +589,23 @@ void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
   *count = run.count;
   *hash = run.hash;
   if (!pairs || capacity == 0 || run.count == 0) return;
-  const int b = bits_for(ps->n);
-  DevBuf<uint64_t> packed(run.count, s);
-  k_pack<<<blocks(run.count, 256), 256, 0, s>>>(run.pairs.p, run.count, b, packed.p);
-  PSG_LAUNCHED();
-  sort_u64(packed, run.count, 2 * b, s);
-  k_unpack<<<blocks(run.count, 256), 256, 0, s>>>(packed.p, run.count, b);
-  PSG_LAUNCHED();
-  g_launches += 2;
   const uint64_t m = std::min(capacity, run.count);
-  PSG_CUDA(cudaMemcpyAsync(pairs, packed.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  DevBuf<uint32_t> off, cols;
+  DevBuf<uint64_t> sorted(run.count, s);
+  if (csr_rows(run.pairs, run.count, ps->n, false, off, cols, s)) {  // rows of i<j, ascending
+    k_csr_to_pairs<<<grid_cap(ps->n * 32), 256, 0, s>>>(off.p, ps->n, cols.p, sorted.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+  } else {
+    const int b = bits_for(ps->n);
+    k_pack<<<blocks(run.count, 256), 256, 0, s>>>(run.pairs.p, run.count, b, sorted.p);
+    PSG_LAUNCHED();
+    sort_u64(sorted, run.count, 2 * b, s);
+    k_unpack<<<blocks(run.count, 256), 256, 0, s>>>(sorted.p, run.count, b);
+    PSG_LAUNCHED();
+    g_launches += 2;
+  }
+  PSG_CUDA(cudaMemcpyAsync(pairs, sorted.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaStreamSynchronize(s));
   g_prof.d2h_bytes += m * sizeof(uint64_t);
 }

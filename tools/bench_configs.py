@@ -55,8 +55,11 @@ def main(which):
         (pairs, cnt, h), t, p = timed(lambda: psg.frnn_pairs(cube, R_C4, want_pairs=False))
         res.append({"config": "C4 FRNN n=2^22 d=3 R=cbrt(3*32/(4 pi n))", "solve_s": t, "pairs": cnt, "hash": h,
                     "device_ms": p["total_ms"], "candidates": p["window_pairs"], "stages": p["stage_list"]})
-        (pairs, cnt2, h2), t2, p2 = timed(lambda: psg.frnn_pairs(cube, R_C4, want_pairs=True), reps=1)
-        res.append({"config": "C4 FRNN sorted pair list", "solve_s": t2, "pairs": cnt2, "device_ms": p2["total_ms"]})
+        pinned = psg.PinnedBuffer(20 * len(cube))
+        (pairs, cnt2, h2), t2, p2 = timed(lambda: psg.frnn_pairs(cube, R_C4, want_pairs=True, out=pinned.array), reps=2)
+        ok = bool(np.all(pairs[1:] > pairs[:-1])) and cnt2 == cnt
+        res.append({"config": "C4 FRNN sorted pair list -> pinned host", "solve_s": t2, "pairs": cnt2,
+                    "device_ms": p2["total_ms"], "sorted_unique": ok, "stages": p2["stage_list"]})
     if "c5" in which:
         n = int(os.environ.get("C5_N", 1 << 24))
         pts = psg.gen.mixture(5, n, 64, 1024, 0.05)
