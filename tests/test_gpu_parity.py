@@ -283,3 +283,26 @@ def test_raw_windows_motif_matches_reference_engine(psg, orc):
     got = psg.motif(walk, 24, znorm=False)
     assert (got.index_i, got.index_j) == (100, 208)  # SURVEY §8(c) known answer
     assert got.distance == 5.282423415841313
+
+
+# --- CSR list building: every row-size class of the warp bitonic sort (1..1024)
+# and the global-sort fallback for rows longer than 1024 -------------------------
+@pytest.mark.parametrize("radius", [0.12, 0.5, 0.8])
+def test_fixed_radius_lists_all_row_sizes(psg, orc, radius):
+    g = gauss_points(orc, 77, 4000, 2)
+    got = psg.fixed_radius_neighbors(psg.PointSet.from_flat(g, 2), radius, 8, 10.0, 3)
+    cnt, h, pairs = orc.brute_force_neighbors(g, radius, 0, lists=True)
+    assert (got.pair_count, got.pair_hash) == (cnt, h)
+    want = [[] for _ in range(4000)]
+    for key in pairs.tolist():
+        i, j = key >> 32, key & 0xFFFFFFFF
+        want[i].append(j)
+        want[j].append(i)
+    lens = [len(w) for w in want]
+    if radius == 0.8:
+        assert max(lens) > 1024  # exercises the fallback
+    assert [list(map(int, l)) for l in got.neighbors] == [sorted(w) for w in want]
+    plist, pc, ph = psg.frnn_pairs(g.astype(np.float32), radius)
+    cnt32, h32, pairs32 = orc.brute_force_neighbors(g.astype(np.float32).astype(np.float64), radius, 0, lists=True)
+    assert (pc, ph) == (cnt32, h32)
+    assert np.array_equal(plist, np.sort(np.asarray(pairs32, dtype=np.uint64)))
