@@ -62,21 +62,55 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, double 
   atomicMax(a, static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
-// Validation of float rows: finiteness (series.cpp:20-24) and max |x|.
-__global__ void k_check_f32(const float* __restrict__ x, uint64_t count, unsigned* __restrict__ bad,
-                            unsigned* __restrict__ maxabs_bits) {
+// One pass over float rows: finiteness (series.cpp:20-24), max |x| and the
+// max row sum of squares (FP32, any order).  A warp per row (float4 lanes when
+// d % 4 == 0) for d >= 32, a thread per row below.
+__global__ void __launch_bounds__(256) k_check_rows_f32(const float* __restrict__ x, uint64_t n, int d,
+                                                        unsigned* __restrict__ flags /* bad, maxabs, norm2 */) {
   unsigned m = 0, nonfinite = 0;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const float v = x[i];
-    if (!isfinite(v)) nonfinite = 1;
+  float worst = 0.f;
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  auto take = [&](float v, float& acc) {
+    nonfinite |= !isfinite(v);
     m = max(m, __float_as_uint(fabsf(v)));
+    acc = fmaf(v, v, acc);
+  };
+  if (d >= 32) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r = tid >> 5; r < n; r += nth >> 5) {
+      const float* row = x + r * d;
+      float acc = 0.f;
+      if ((d & 3) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        for (int t = lane; t < (d >> 2); t += 32) {
+          const float4 v = __ldcs(r4 + t);
+          take(v.x, acc);
+          take(v.y, acc);
+          take(v.z, acc);
+          take(v.w, acc);
+        }
+      } else {
+        for (int t = lane; t < d; t += 32) take(__ldcs(row + t), acc);
+      }
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      worst = fmaxf(worst, acc);
+    }
+  } else {
+    for (uint64_t r = tid; r < n; r += nth) {
+      const float* row = x + r * d;
+      float acc = 0.f;
+      for (int t = 0; t < d; ++t) take(row[t], acc);
+      worst = fmaxf(worst, acc);
+    }
   }
   m = __reduce_max_sync(0xffffffffu, m);
   nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+  const unsigned wb = __reduce_max_sync(0xffffffffu, __float_as_uint(worst));
   if ((threadIdx.x & 31) == 0) {
-    if (nonfinite) atomicOr(bad, 1u);
-    atomicMax(maxabs_bits, m);
+    if (nonfinite) atomicOr(flags, 1u);
+    atomicMax(flags + 1, m);
+    atomicMax(flags + 2, wb);
   }
 }
 
@@ -272,15 +306,16 @@ psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev
   ps->kind = kRowsF32;
   ps->device = c.device;
   upload(ps->src32, p, n * d, dev_src, s, &ps->h2d_bytes);
-  DevBuf<unsigned> flags(2, s);
-  PSG_CUDA(cudaMemsetAsync(flags.p, 0, 8, s));
+  DevBuf<unsigned> flags(3, s);
+  PSG_CUDA(cudaMemsetAsync(flags.p, 0, 12, s));
   if (n * d) {
-    k_check_f32<<<grid_for(n * d, 256 * 8, c.sm_count), 256, 0, s>>>(ps->src32.p, n * d, flags.p, flags.p + 1);
+    k_check_rows_f32<<<grid_for(d >= 32 ? n * 32 : n, 256, c.sm_count), 256, 0, s>>>(ps->src32.p, n, ps->d,
+                                                                                      flags.p);
     PSG_LAUNCHED();
     ++g_launches;
   }
-  unsigned h[2];
-  PSG_CUDA(cudaMemcpyAsync(h, flags.p, 8, cudaMemcpyDeviceToHost, s));
+  unsigned h[3];
+  PSG_CUDA(cudaMemcpyAsync(h, flags.p, 12, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaStreamSynchronize(s));
   if (h[0]) throw invalid_argument("point coordinate must be finite");
   float mx;
@@ -299,7 +334,10 @@ psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev
     ps->X = ps->work.p;
   }
   ps->maxabs = static_cast<double>(mx) * ps->scale;
-  ps->norm2max = row_norm2max(ps->X, n, ps->d, s, c.sm_count);
+  if (ps->scale == 1.0)
+    std::memcpy(&ps->norm2max, &h[2], 4);  // X is the input: its norms came with the check
+  else
+    ps->norm2max = row_norm2max(ps->X, n, ps->d, s, c.sm_count);
   return ps.release();
 }
 
