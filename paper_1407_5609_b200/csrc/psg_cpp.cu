@@ -647,6 +647,7 @@ __global__ void k_scan_reset(DevState* st) {
 struct SetupArgs {
   int d, nk, g, gbox;  // gbox: keys sampled for boxes (>= g)
   double unorm, sigma, Rn, occupancy, box_sd;
+  double min_w;        // cell width learned by an earlier regrid on this point set (0: none)
   uint32_t n, m;
 };
 constexpr int kSetupPer = 16;  // sample elements per thread
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
       st->box_lo[t] = lo[t];
       st->box_span[t] = span[t];
     }
-    const double w = grid_occupancy_width(sa.n, sa.g, span, sa.occupancy);
+    const double w = fmax(grid_occupancy_width(sa.n, sa.g, span, sa.occupancy), sa.min_w);
     GridParams P;
     grid_params_for(P, sa.g, w, lo, span);
     *gp = P;
@@ -906,6 +907,8 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   auto plan = std::make_unique<CppPlan>();
   plan->ps = ps;
   plan->zone = zone;
+  plan->q_arg = q;
+  plan->seed_arg = seed;
   plan->dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
   const int nk = plan->dir.nk;
   plan->work = get_work(ps, nk, s);
@@ -925,7 +928,8 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
     static const double occupancy = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : kGridOccupancy;
     const int gbox = std::min(plan->dir.q, kMaxGridKeys);
     static const double box_sd = std::getenv("PSG_BOXSD") ? std::atof(std::getenv("PSG_BOXSD")) : kGridBoxSd;
-    SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy, box_sd,
+    const double min_w = W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone ? W.learned_w : 0.0;
+    SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy, box_sd, min_w,
                  static_cast<uint32_t>(n), 0};
     if (plan->grid) {
       // K2 (grid): cells over the first g keys at the occupancy width, sorted;
@@ -1236,6 +1240,19 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
                        static_cast<double>(nb), next);
         if (!(next < need / 1.25)) break;  // converged: keep these cells
         bound = nb;
+      }
+      if (nparts == 1) {
+        // Remember the width for later solves of the same (q, seed, zone) on
+        // this point set: their first grid is built at it, so the captured
+        // graph solve needs no regrid (a tuning hint; every stage still runs).
+        W.learned_w = plan.gp.w;
+        W.learned_q = plan.q_arg;
+        W.learned_seed = plan.seed_arg;
+        W.learned_zone = plan.zone;
+        if (W.gexec) {
+          cudaGraphExecDestroy(W.gexec);
+          W.gexec = nullptr;
+        }
       }
       continue;
     }

@@ -64,6 +64,9 @@ struct CppWork {
   cudaGraphExec_t gexec = nullptr;
   uint64_t gq = 0, gseed = 0, gzone = 0;
   uint64_t glaunches = 0;
+  // cell width a regrid converged to, for the same (q, seed, zone)
+  double learned_w = 0.0;
+  uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;
   cudaEvent_t gev[6] = {};  // project / bootstrap / scan spans recorded inside the graph
   ~CppWork();
 };
@@ -71,6 +74,7 @@ struct CppWork {
 struct CppPlan {
   psg_pointset* ps = nullptr;
   uint64_t zone = 0;
+  uint64_t q_arg = 0, seed_arg = 0;  // the call's q and seed (learned-width key)
   Directions dir;
   Budget bud;              // host copy (valid after the first readback)
   GridParams gp;           // host copy of the grid parameters
