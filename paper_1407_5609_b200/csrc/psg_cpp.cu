@@ -1189,7 +1189,8 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       PSG_CUDA(cudaMemcpyAsync(W.host_st, W.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
       plan.dense = est > kDenseFactor * n;
-      const int gd = std::min(plan.dir.q, kMaxGridKeys);
+      static const int dense_keys = std::getenv("PSG_DENSE_KEYS") ? std::atoi(std::getenv("PSG_DENSE_KEYS")) : kMaxGridKeys;
+      const int gd = std::min(plan.dir.q, dense_keys);
       if (plan.dense && plan.g < gd) {
         // Dense: rebuild the cells on more keys at the same width (still >=
         // the bound's key window): in 3 projected keys clusters overlap, in 6

@@ -14,11 +14,13 @@
 //      thread — the all-pairs kernel's arithmetic and order) from rows
 //      gathered into grid order, recording the band into the candidate list.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "psg_dense.cuh"
 #include "psg_points.cuh"
 #include "psg_sort.cuh"
+#include "psg_tc.cuh"
 
 namespace psg {
 namespace {
@@ -163,7 +165,7 @@ template <int NK>
 __global__ void k_cell_pairs(const uint32_t* __restrict__ cfirst, const GridParams* __restrict__ gpp, uint64_t cells,
                              const float* __restrict__ cbox, const Thresholds* __restrict__ th,
                              uint32_t* __restrict__ pa, uint32_t* __restrict__ pb, uint32_t* __restrict__ pt,
-                             uint32_t cap, unsigned long long* __restrict__ count) {
+                             uint32_t cap, unsigned long long* __restrict__ count, bool strips) {
   const GridParams P = *gpp;
   const float lb2 = th->lb2 * (1.0f + 0x1.0p-20f);  // box gaps are a lower bound of every pair's key gaps
   for (uint64_t A = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; A < cells;
@@ -193,7 +195,7 @@ __global__ void k_cell_pairs(const uint32_t* __restrict__ cfirst, const GridPara
         pa[slot] = static_cast<uint32_t>(A);
         pb[slot] = B;
         const uint32_t ta = (na + kT - 1) / kT, tb = (nb + kT - 1) / kT;
-        pt[slot] = s == 0 ? ta * (ta + 1) / 2 : ta * tb;
+        pt[slot] = strips ? ta : (s == 0 ? ta * (ta + 1) / 2 : ta * tb);
       }
     }
   }
@@ -317,6 +319,354 @@ __global__ void __launch_bounds__(256) k_dense_tiles(ScanArgs a, const float* __
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-core Gram tiles (d in {32, 64}): the 128x128 pair tiles of a kept
+// cell pair as D = A'.B'^T on tcgen05 (kind::tf32, both operands K-major in
+// 128 B-swizzled shared memory, the 128x128 FP32 accumulator in TMEM), where
+// A', B' are the rows shifted by the strip's first row (so |a'|, |b'| are at
+// the scale of the cell, not of the data).  The filter value
+//   s~ = |a'|^2 + |b'|^2 - 2 g~     (norms FP32, g~ from the tensor core)
+// is within gram_slack * (|a'|^2 + |b'|^2) of the pair's squared distance
+// (3xTF32 on the exact hi/lo split, FP32 accumulation, the shift's rounding:
+// gram_slack): a pair is evaluated as the canonical FP32 distance — and
+// then treated exactly like the CUDA-core tiles — only when s~ is within that
+// slack of the band.  Survivors are rare, so the tensor core does the O(n^2/c)
+// work and the exact path stays bit-identical.
+//
+// Warp roles: 0-3 loaders (one row per thread: shift, norm, swizzled store;
+// A once per strip, then the strip's B tiles), 4 MMA issuer (one thread), 5
+// TMEM allocation, 8-11 epilogue (tcgen05.ld 32x32b: thread = A row).  A strip
+// = one A tile of a kept cell pair against every B tile of the pair (self
+// pairs: tiles tj >= ti); strips are taken from a global cursor.
+constexpr int kGT = 128;
+constexpr int kGAB = 1;   // A buffers (hi + lo)
+constexpr int kGBB = 2;   // B buffers (hi + lo)
+constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM, 8-15 epilogue
+constexpr int kGEpi = 8;        // epilogue warps: two per TMEM lane quarter, 64 columns each
+constexpr uint32_t kGTmemCols = 256;  // 2 accumulators x 128 columns
+
+// Slack of the filter value per unit of (|a'|^2 + |b'|^2):
+// the 3xTF32 product (hi.hi + hi.lo + lo.hi) misses lo.lo and the TF32
+// truncation of the lo parts (<= 3 * 2^-20 |a'||b'|); the FP32 accumulation of
+// the 3d products is charged 4 ulps each (3d * 2^-22); s~ = na + nb - 2g~ doubles
+// the Gram error, sqrt(na nb) <= (na + nb)/2, and the norms, the shift and the
+// final FP32 operations add (d + 8) 2^-24; everything is doubled once more.
+template <int D>
+constexpr float gram_slack() {
+  return static_cast<float>(2.0 * ((3.0 * 0x1.0p-20 + 3.0 * D * 0x1.0p-22) * 1.01 + (D + 8) * 0x1.0p-24));
+}
+
+struct GramMeta {
+  uint32_t a0, alen, b0, blen, abuf, npar, self, last, done;
+};
+
+template <int D>
+struct GramSmem {
+  float A[kGAB][2][kGT * D];  // [hi|lo] x D/32 chunks of 128 rows x 128 B (SW128 K-major)
+  float B[kGBB][2][kGT * D];
+  float na[2][kGT];  // A-row norms per strip parity (the epilogue reads them after the A tile is reused)
+  float nb[kGBB][kGT];
+  float cnb[kGBB][kGT];  // (1 - 2 slack) nb, +inf past the tile's length: the epilogue's fast test
+  float wmaxnb[kGBB][4];
+  float mu[D];  // the current strip's shift (its first row)
+  GramMeta meta[kGBB];
+  uint64_t afull[kGAB], afree[kGAB], bfull[kGBB], bfree[kGBB], tfull[2], tempty[2];
+  uint32_t tmem, strip;
+};
+
+// Row r of a tile: load d floats (grid order), subtract mu, FP32 norm, store
+// the exact TF32 split (hi = 13 low mantissa bits cleared, lo = x - hi)
+// swizzled into the hi and lo tiles.  Zero rows past the tile's length.
+template <int D>
+__device__ __forceinline__ float gram_load_row(const float* __restrict__ Xs, uint32_t row, bool valid,
+                                               const float* __restrict__ mu, float* __restrict__ hi_tile,
+                                               float* __restrict__ lo_tile, int r) {
+  float nrm = 0.f;
+  const float4* src = reinterpret_cast<const float4*>(Xs + static_cast<size_t>(row) * D);
+#pragma unroll
+  for (int q = 0; q < D / 4; ++q) {
+    float4 v = valid ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+      v.x -= mu[4 * q];
+      v.y -= mu[4 * q + 1];
+      v.z -= mu[4 * q + 2];
+      v.w -= mu[4 * q + 3];
+    }
+    nrm = fmaf(v.x, v.x, nrm);
+    nrm = fmaf(v.y, v.y, nrm);
+    nrm = fmaf(v.z, v.z, nrm);
+    nrm = fmaf(v.w, v.w, nrm);
+    const float4 h = make_float4(__uint_as_float(__float_as_uint(v.x) & ~0x1fffu),
+                                 __uint_as_float(__float_as_uint(v.y) & ~0x1fffu),
+                                 __uint_as_float(__float_as_uint(v.z) & ~0x1fffu),
+                                 __uint_as_float(__float_as_uint(v.w) & ~0x1fffu));
+    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);  // exact
+    const int c = q >> 3, u = q & 7;  // 32-float chunk, 16 B unit inside the 128 B row
+    const int off = c * (kGT * 32) + r * 32 + ((u ^ (r & 7)) << 2);
+    *reinterpret_cast<float4*>(hi_tile + off) = h;
+    *reinterpret_cast<float4*>(lo_tile + off) = l;
+  }
+  return nrm;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_dense_gram(ScanArgs a, const float* __restrict__ Xs, const uint32_t* __restrict__ cfirst,
+                 const uint32_t* __restrict__ pa, const uint32_t* __restrict__ pb, const uint32_t* __restrict__ prefix,
+                 uint32_t npairs, uint32_t part, uint32_t nparts, unsigned long long* __restrict__ cursor) {
+  using namespace tc;
+  constexpr int NC = D / 32;
+  extern __shared__ uint8_t graw[];
+  GramSmem<D>& sm = *reinterpret_cast<GramSmem<D>*>((reinterpret_cast<uintptr_t>(graw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kGAB; ++i) {
+      mbar_init(&sm.afull[i], 4);
+      mbar_init(&sm.afree[i], 1);  // tcgen05.commit after the strip's last MMAs
+    }
+    for (int i = 0; i < kGBB; ++i) {
+      mbar_init(&sm.bfull[i], 4);
+      mbar_init(&sm.bfree[i], kGEpi);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], kGEpi);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(&sm.tmem, kGTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+  const uint32_t total = prefix[npairs];
+
+  if (warp < 4) {  // ---- loaders: thread = tile row
+    const int r = tid;
+    uint32_t scount = 0, bcount = 0;
+    for (;;) {
+      if (r == 0) sm.strip = static_cast<uint32_t>(atomicAdd(cursor, 1ull) * nparts + part);
+      named_bar(1, 128);
+      const uint32_t sid = sm.strip;
+      named_bar(1, 128);
+      if (sid >= total) {  // sentinel tile: tells the MMA and the epilogue to stop
+        const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+        mbar_wait(&sm.bfree[bb], bph ^ 1);
+        if (r == 0) sm.meta[bb].done = 1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.bfull[bb]);
+        break;
+      }
+      uint32_t lo = 0, hi = npairs;  // pair k: prefix[k] <= sid < prefix[k+1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (prefix[mid] <= sid)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      const uint32_t A = pa[lo], B = pb[lo];
+      const uint32_t la = cfirst[A], nA = cfirst[A + 1] - la;
+      const uint32_t lb = cfirst[B], nB = cfirst[B + 1] - lb;
+      const uint32_t ti = sid - prefix[lo];
+      const bool self = A == B;
+      const uint32_t a0 = la + ti * kGT, alen = min(static_cast<uint32_t>(kGT), nA - ti * kGT);
+      const uint32_t tb = (nB + kGT - 1) / kGT, tj0 = self ? ti : 0;
+      // the strip's shift: its first row (shared; the previous strip's rows are
+      // all loaded once every loader has passed the barrier below)
+      if (r < D) sm.mu[r] = Xs[static_cast<size_t>(a0) * D + r];
+      named_bar(1, 128);
+      const float* mu = sm.mu;
+      const uint32_t ab = scount % kGAB, aph = (scount / kGAB) & 1;
+      ++scount;
+      mbar_wait(&sm.afree[ab], aph ^ 1);
+      const uint32_t npar = (scount - 1) & 1;
+      sm.na[npar][r] = gram_load_row<D>(Xs, a0 + r, static_cast<uint32_t>(r) < alen, mu, sm.A[ab][0], sm.A[ab][1], r);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.afull[ab]);
+      for (uint32_t tj = tj0; tj < tb; ++tj) {
+        const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+        ++bcount;
+        mbar_wait(&sm.bfree[bb], bph ^ 1);
+        const uint32_t b0 = lb + tj * kGT, blen = min(static_cast<uint32_t>(kGT), nB - tj * kGT);
+        const float nbr = gram_load_row<D>(Xs, b0 + r, static_cast<uint32_t>(r) < blen, mu, sm.B[bb][0], sm.B[bb][1], r);
+        sm.nb[bb][r] = nbr;
+        sm.cnb[bb][r] = static_cast<uint32_t>(r) < blen ? (1.f - 2.f * gram_slack<D>()) * nbr : INFINITY;
+        const float wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nbr)));  // nbr >= 0
+        if (lane == 0) sm.wmaxnb[bb][warp] = wm;
+        if (r == 0) sm.meta[bb] = GramMeta{a0, alen, b0, blen, ab, npar, self && tj == ti, tj + 1 == tb, 0u};
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.bfull[bb]);
+      }
+    }
+  } else if (warp == 4) {  // ---- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(kGT, kGT);
+      uint32_t bcount = 0, tcount = 0, scount = 0;
+      bool need_a = true;
+      for (;;) {
+        const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+        mbar_wait(&sm.bfull[bb], bph);
+        const uint32_t acc = tcount & 1, tph = (tcount >> 1) & 1;
+        mbar_wait(&sm.tempty[acc], tph ^ 1);
+        const GramMeta m = sm.meta[bb];  // published before the barrier arrive
+        if (m.done) {
+          mbar_arrive(&sm.tfull[acc]);
+          break;
+        }
+        if (need_a) {  // first tile of a strip: its A buffer is filled
+          const uint32_t aph = (scount / kGAB) & 1;
+          mbar_wait(&sm.afull[m.abuf], aph);
+          ++scount;
+          need_a = false;
+        }
+        tc_fence_after();
+        const uint32_t dcol = tmem + acc * kGT;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {  // 3xTF32: hi.hi + hi.lo + lo.hi
+          const uint64_t ah = sw128_desc(smem_u32(sm.A[m.abuf][0] + c * (kGT * 32)));
+          const uint64_t al = sw128_desc(smem_u32(sm.A[m.abuf][1] + c * (kGT * 32)));
+          const uint64_t bh = sw128_desc(smem_u32(sm.B[bb][0] + c * (kGT * 32)));
+          const uint64_t bl = sw128_desc(smem_u32(sm.B[bb][1] + c * (kGT * 32)));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            umma_tf32_ss(dcol, ah + 2 * k, bh + 2 * k, idesc, (c | k) != 0);
+            umma_tf32_ss(dcol, ah + 2 * k, bl + 2 * k, idesc, 1);
+            umma_tf32_ss(dcol, al + 2 * k, bh + 2 * k, idesc, 1);
+          }
+        }
+        umma_commit(&sm.tfull[acc]);
+        if (m.last) {  // the strip's A tile is free once these MMAs have read it
+          umma_commit(&sm.afree[m.abuf]);
+          need_a = true;
+        }
+        ++bcount;
+        ++tcount;
+      }
+    }
+  } else if (warp >= 8) {
+    // ---- epilogue: warp w owns TMEM lanes (A rows) 32 (w%4) .. +31 and the
+    // 64 columns starting at 64 ((w-8)/4).  Fast path per pair: one FMA, one
+    // compare folded into a predicate, one min; a chunk with a hit (or a self
+    // tile, or an exclusion zone) is re-run with every check.
+    const uint32_t e = warp & 3, half = (warp - 8) >> 2, r = 32 * e + lane;
+    constexpr float g2 = 2.f * gram_slack<D>();
+    uint32_t bcount = 0, tcount = 0;
+    unsigned long long visited = 0, evals = 0;
+    for (;;) {
+      const uint32_t bb = bcount % kGBB, acc = tcount & 1, tph = (tcount >> 1) & 1;
+      mbar_wait(&sm.tfull[acc], tph);
+      tc_fence_after();
+      const GramMeta m = sm.meta[bb];
+      if (m.done) break;
+      float band = 0.f;
+      if (lane == 0) band = budget_thresholds_s32(*a.bud, best_now(a.best)).band;
+      band = __shfl_sync(kFull, band, 0);
+      const bool vr = r < m.alen;
+      const uint32_t i = m.a0 + r;
+      const float na = sm.na[m.npar][r];
+      const float maxnb = fmaxf(fmaxf(sm.wmaxnb[bb][0], sm.wmaxnb[bb][1]), fmaxf(sm.wmaxnb[bb][2], sm.wmaxnb[bb][3]));
+      const float R = band - (1.f - g2) * na;  // fast test: -2g + (1-g2) nb <= R
+      const bool general = m.self || a.zone > 1;
+      const uint32_t oi = (vr && a.zone > 1) ? a.sidx[i] : 0u;
+      float vmin = INFINITY, ubs = INFINITY;
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t c0 = half * 64 + q * 32;
+        uint32_t v[32];
+        tmem_ld32(tmem + ((32u * e) << 16) + acc * kGT + c0, v);
+        if (!vr || c0 >= m.blen) continue;
+        bool hit = false;
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          const float4 cn = *reinterpret_cast<const float4*>(&sm.cnb[bb][c0 + jj]);
+          const float x0 = fmaf(-2.f, __uint_as_float(v[jj]), cn.x);
+          const float x1 = fmaf(-2.f, __uint_as_float(v[jj + 1]), cn.y);
+          const float x2 = fmaf(-2.f, __uint_as_float(v[jj + 2]), cn.z);
+          const float x3 = fmaf(-2.f, __uint_as_float(v[jj + 3]), cn.w);
+          hit |= (x0 <= R) | (x1 <= R) | (x2 <= R) | (x3 <= R);
+          if (!general) vmin = fminf(vmin, fminf(fminf(x0, x1), fminf(x2, x3)));  // every column is a valid pair
+        }
+        if (!general) visited += min(32u, m.blen - c0);
+        if (!(hit || general)) continue;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {  // slow path: every check, the exact slack test
+          const uint32_t jl = c0 + jj;
+          if (jl >= m.blen) continue;
+          const uint32_t j = m.b0 + jl;
+          if (m.self && j <= i) continue;
+          if (a.zone > 1 && !admissible(oi, a.sidx[j], a.zone)) continue;
+          if (general) ++visited;
+          const float nbj = sm.nb[bb][jl];
+          const float st = fmaf(-2.f, __uint_as_float(v[jj]), na + nbj);
+          const float slack = gram_slack<D>() * (na + nbj) + 1e-30f;
+          if (general) ubs = fminf(ubs, st + slack);
+          if (st <= band + slack) {
+            ++evals;
+            const float s32 = thread_sqdist(Xs + static_cast<size_t>(i) * D, Xs + static_cast<size_t>(j) * D, D);
+            if (s32 <= band) record(a, i, j, s32, band);
+          }
+        }
+      }
+      // An upper bound of some valid pair's real squared distance: with
+      // slack = gs (na + nb) and vmin = -2g + (1 - 2gs) nb at the minimising
+      // pair, s~ + slack = vmin + 3gs nb + (1 + gs) na <= vmin + 3gs maxnb +
+      // (1 + gs) na (general tiles: the slow path's own s~ + slack).  Rounded up
+      // past the FP32 distance error it is a valid bound (never below the
+      // canonical minimum), and the band tightens from the tensor-core values
+      // alone.
+      constexpr float gs = gram_slack<D>();
+      float ub = vr && vmin < INFINITY ? vmin + 3.f * gs * maxnb + (1.f + gs) * na : INFINITY;
+      ub = fminf(ub, ubs);
+      ub = __fmul_ru(fmaxf(ub, 0.f), 1.0f + 0x1.0p-16f);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(kFull, ub, o));
+      if (lane == 0 && ub < INFINITY) atomicMin(a.best, __float_as_uint(ub));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.tempty[acc]);
+        mbar_arrive(&sm.bfree[bb]);
+      }
+      ++bcount;
+      ++tcount;
+    }
+    for (int o = 16; o; o >>= 1) {
+      visited += __shfl_xor_sync(kFull, visited, o);
+      evals += __shfl_xor_sync(kFull, evals, o);
+    }
+    if (lane == 0) {
+      if (visited) atomicAdd(a.visited, visited);
+      if (evals) atomicAdd(a.evals, evals);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_free(tmem, kGTmemCols);
+  }
+}
+
+template <int D>
+void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, uint32_t npairs, uint32_t part,
+                 uint32_t nparts, cudaStream_t s) {
+  constexpr size_t kSmem = sizeof(GramSmem<D>) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    PSG_CUDA(cudaFuncSetAttribute(k_dense_gram<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmem)));
+    configured = true;
+  }
+  k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
+                                                           npairs, part, nparts, w.ctr.p + 1);
+  PSG_LAUNCHED();
+}
+
+bool gram_shape(int d) { return d == 32 || d == 64; }
 }  // namespace
 
 uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s) {
@@ -334,6 +684,9 @@ uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s)
 uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, const float* X, uint32_t n, int d,
                     int nk, const Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s) {
   const int sms = ctx().sm_count;
+  // tensor-core Gram tiles for d in {32, 64}; CUDA-core canonical tiles otherwise
+  static const bool no_gram = std::getenv("PSG_NO_GRAM") != nullptr;
+  const bool gram = gram_shape(d) && !no_gram;
   if (w.Xs.n != static_cast<size_t>(n) * d) w.Xs.alloc(static_cast<size_t>(n) * d, s);
   if (w.cbox.n < cells * 2 * nk) w.cbox.alloc(cells * 2 * nk, s);
   if (w.ctr.n < 3) w.ctr.alloc(3, s);
@@ -361,10 +714,10 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     PSG_CUDA(cudaMemsetAsync(w.ctr.p, 0, 24, s));
     if (nk == 4)
       k_cell_pairs<4><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
-          gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p);
+          gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
     else
       k_cell_pairs<8><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
-          gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p);
+          gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
     PSG_LAUNCHED();
     ++g_launches;
     PSG_CUDA(cudaMemcpyAsync(&npairs, w.ctr.p, 8, cudaMemcpyDeviceToHost, s));
@@ -377,9 +730,15 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   PSG_CUDA(cudaMemsetAsync(w.ptiles.p + npairs, 0, 4, s));
   exclusive_scan_u32(w.ptiles.p, w.pprefix.p, npairs + 1, w.stmp.p, s);
   g_launches += 3;
-  k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
-                                        static_cast<uint32_t>(npairs), part, nparts, w.ctr.p + 1);
-  PSG_LAUNCHED();
+  if (gram && d == 32)
+    launch_gram<32>(a, w, gi, static_cast<uint32_t>(npairs), part, nparts, s);
+  else if (gram)
+    launch_gram<64>(a, w, gi, static_cast<uint32_t>(npairs), part, nparts, s);
+  else {
+    k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
+                                          static_cast<uint32_t>(npairs), part, nparts, w.ctr.p + 1);
+    PSG_LAUNCHED();
+  }
   ++g_launches;
   return npairs;
 }

@@ -45,9 +45,12 @@
 #include <stdexcept>
 
 #include "psg_cpp.cuh"
+#include "psg_tc.cuh"
 
 namespace psg {
 namespace {
+
+using namespace tc;
 
 constexpr int kTcM = 128;         // rows per tile (UMMA M)
 constexpr int kTcN = 16;          // UMMA N: directions padded to 16
@@ -60,92 +63,12 @@ constexpr int kTcThreads = 512;
 constexpr uint32_t kTmemCols = 512;  // [0, 64) 2 x (hi, lo) accumulators, [64, 64 + 64 kTcSlots) A slots
 constexpr uint32_t kSlotBase = 64;
 
-// tcgen05 instruction descriptor: D F32, A/B TF32, both K-major, N = 16, M = 128.
-constexpr uint32_t kIdesc = (1u << 4)             // c_format F32
-                            | (2u << 7)           // a_format TF32
-                            | (2u << 10)          // b_format TF32
-                            | ((kTcN >> 3) << 17) // n_dim
-                            | ((kTcM >> 4) << 24);// m_dim
+constexpr uint32_t kIdesc = idesc_tf32(kTcM, kTcN);  // D F32, A/B TF32, K-major, M = 128, N = 16
 
 template <int D>
 struct UTc {
   float u[8][D];  // rows >= nk are zero
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t"
-      "}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-// Shared-memory matrix descriptor: K-major, 128 B swizzle, 8-row groups 1024 B
-// apart (SBO), version 1 (sm_100).  The start address advances by 32 B per
-// K = 8 step inside a swizzle row.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
-}
-
-__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
-      "}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(addr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
-      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
-      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 template <int NK, int D>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -268,8 +191,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           // MMAs are independent, so the tensor pipe overlaps them)
 #pragma unroll
           for (int k = 0; k < kTcKChunk / 8; ++k) {
-            umma_tf32_ts(dcol, a + 8 * k, bd + 2 * k, (c | k) != 0);
-            umma_tf32_ts(dcol + kTcN, a + 32 + 8 * k, bd + 2 * k, (c | k) != 0);
+            umma_tf32_ts(dcol, a + 8 * k, bd + 2 * k, kIdesc, (c | k) != 0);
+            umma_tf32_ts(dcol + kTcN, a + 32 + 8 * k, bd + 2 * k, kIdesc, (c | k) != 0);
           }
           umma_commit(tslot + slot);  // slot reusable once these MMAs have read it
           if (++slot == kTcSlots) {
