@@ -872,6 +872,7 @@ ScanArgs make_args(CppPlan& plan) {
   a.ovf_cap = W.ovf_cap;
   a.evals = &st->evals;
   a.visited = &st->visited;
+  a.no_ub = std::getenv("PSG_NO_UB") != nullptr;
   return a;
 }
 

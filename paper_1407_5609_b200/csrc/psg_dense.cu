@@ -339,12 +339,16 @@ __global__ void __launch_bounds__(256) k_dense_tiles(ScanArgs a, const float* __
 // TMEM allocation, 8-11 epilogue (tcgen05.ld 32x32b: thread = A row).  A strip
 // = one A tile of a kept cell pair against every B tile of the pair (self
 // pairs: tiles tj >= ti); strips are taken from a global cursor.
-constexpr int kGT = 128;
-constexpr int kGAB = 1;   // A buffers (hi + lo)
-constexpr int kGBB = 2;   // B buffers (hi + lo)
+constexpr int kGT = 128;  // A tile rows (UMMA M)
+#ifndef PSG_GRAM_N
+#define PSG_GRAM_N 128
+#endif
+constexpr int kGN = PSG_GRAM_N;           // B tile rows (UMMA N)
+constexpr int kGAB = 1;                   // A buffers (hi + lo)
+constexpr int kGBB = kGN == 64 ? 4 : 2;   // B buffers (hi + lo)
 constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM, 8-15 epilogue
 constexpr int kGEpi = 8;        // epilogue warps: two per TMEM lane quarter, 64 columns each
-constexpr uint32_t kGTmemCols = 256;  // 2 accumulators x 128 columns
+constexpr uint32_t kGTmemCols = 2 * kGN;  // 2 accumulators x kGN columns
 
 // Slack of the filter value per unit of (|a'|^2 + |b'|^2):
 // the 3xTF32 product (hi.hi + hi.lo + lo.hi) misses lo.lo and the TF32
@@ -364,10 +368,10 @@ struct GramMeta {
 template <int D>
 struct GramSmem {
   float A[kGAB][2][kGT * D];  // [hi|lo] x D/32 chunks of 128 rows x 128 B (SW128 K-major)
-  float B[kGBB][2][kGT * D];
-  float na[2][kGT];  // A-row norms per strip parity (the epilogue reads them after the A tile is reused)
-  float nb[kGBB][kGT];
-  float cnb[kGBB][kGT];  // (1 - 2 slack) nb, +inf past the tile's length: the epilogue's fast test
+  float B[kGBB][2][kGN * D];
+  float na[kGBB][kGT];  // the strip's A-row norms, copied with every B tile (released with it by the epilogue)
+  float nb[kGBB][kGN];
+  float cnb[kGBB][kGN];  // (1 - 2 slack) nb, +inf past the tile's length: the epilogue's fast test
   float wmaxnb[kGBB][4];
   float mu[D];  // the current strip's shift (its first row)
   GramMeta meta[kGBB];
@@ -378,14 +382,15 @@ struct GramSmem {
 // Row r of a tile: load d floats (grid order), subtract mu, FP32 norm, store
 // the exact TF32 split (hi = 13 low mantissa bits cleared, lo = x - hi)
 // swizzled into the hi and lo tiles.  Zero rows past the tile's length.
-template <int D>
+template <int D, int ROWS, int CB, int CE>
 __device__ __forceinline__ float gram_load_row(const float* __restrict__ Xs, uint32_t row, bool valid,
                                                const float* __restrict__ mu, float* __restrict__ hi_tile,
                                                float* __restrict__ lo_tile, int r) {
+  // 32-float chunks [CB, CE) of row r; returns their FP32 sum of squares
   float nrm = 0.f;
   const float4* src = reinterpret_cast<const float4*>(Xs + static_cast<size_t>(row) * D);
 #pragma unroll
-  for (int q = 0; q < D / 4; ++q) {
+  for (int q = CB * 8; q < CE * 8; ++q) {
     float4 v = valid ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (valid) {
       v.x -= mu[4 * q];
@@ -403,7 +408,7 @@ __device__ __forceinline__ float gram_load_row(const float* __restrict__ Xs, uin
                                  __uint_as_float(__float_as_uint(v.w) & ~0x1fffu));
     const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);  // exact
     const int c = q >> 3, u = q & 7;  // 32-float chunk, 16 B unit inside the 128 B row
-    const int off = c * (kGT * 32) + r * 32 + ((u ^ (r & 7)) << 2);
+    const int off = c * (ROWS * 32) + r * 32 + ((u ^ (r & 7)) << 2);
     *reinterpret_cast<float4*>(hi_tile + off) = h;
     *reinterpret_cast<float4*>(lo_tile + off) = l;
   }
@@ -440,17 +445,16 @@ __global__ void __launch_bounds__(kGThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
-  const uint32_t total = prefix[npairs];
-
-  if (warp < 4) {  // ---- loaders: thread = tile row
+  
+  if (warp < 4) {  // ---- loaders: thread = tile row; a cursor hands out kept cell pairs
     const int r = tid;
     uint32_t scount = 0, bcount = 0;
     for (;;) {
       if (r == 0) sm.strip = static_cast<uint32_t>(atomicAdd(cursor, 1ull) * nparts + part);
       named_bar(1, 128);
-      const uint32_t sid = sm.strip;
+      const uint32_t k = sm.strip;
       named_bar(1, 128);
-      if (sid >= total) {  // sentinel tile: tells the MMA and the epilogue to stop
+      if (k >= npairs) {  // sentinel tile: tells the MMA and the epilogue to stop
         const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
         mbar_wait(&sm.bfree[bb], bph ^ 1);
         if (r == 0) sm.meta[bb].done = 1;
@@ -458,53 +462,70 @@ __global__ void __launch_bounds__(kGThreads, 1)
         if (lane == 0) mbar_arrive(&sm.bfull[bb]);
         break;
       }
-      uint32_t lo = 0, hi = npairs;  // pair k: prefix[k] <= sid < prefix[k+1]
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (prefix[mid] <= sid)
-          lo = mid;
-        else
-          hi = mid;
-      }
-      const uint32_t A = pa[lo], B = pb[lo];
+      const uint32_t A = pa[k], B = pb[k];
       const uint32_t la = cfirst[A], nA = cfirst[A + 1] - la;
       const uint32_t lb = cfirst[B], nB = cfirst[B + 1] - lb;
-      const uint32_t ti = sid - prefix[lo];
       const bool self = A == B;
-      const uint32_t a0 = la + ti * kGT, alen = min(static_cast<uint32_t>(kGT), nA - ti * kGT);
-      const uint32_t tb = (nB + kGT - 1) / kGT, tj0 = self ? ti : 0;
-      // the strip's shift: its first row (shared; the previous strip's rows are
-      // all loaded once every loader has passed the barrier below)
-      if (r < D) sm.mu[r] = Xs[static_cast<size_t>(a0) * D + r];
-      named_bar(1, 128);
-      const float* mu = sm.mu;
-      const uint32_t ab = scount % kGAB, aph = (scount / kGAB) & 1;
-      ++scount;
-      mbar_wait(&sm.afree[ab], aph ^ 1);
-      const uint32_t npar = (scount - 1) & 1;
-      sm.na[npar][r] = gram_load_row<D>(Xs, a0 + r, static_cast<uint32_t>(r) < alen, mu, sm.A[ab][0], sm.A[ab][1], r);
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.afull[ab]);
-      for (uint32_t tj = tj0; tj < tb; ++tj) {
-        const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
-        ++bcount;
-        mbar_wait(&sm.bfree[bb], bph ^ 1);
-        const uint32_t b0 = lb + tj * kGT, blen = min(static_cast<uint32_t>(kGT), nB - tj * kGT);
-        const float nbr = gram_load_row<D>(Xs, b0 + r, static_cast<uint32_t>(r) < blen, mu, sm.B[bb][0], sm.B[bb][1], r);
-        sm.nb[bb][r] = nbr;
-        sm.cnb[bb][r] = static_cast<uint32_t>(r) < blen ? (1.f - 2.f * gram_slack<D>()) * nbr : INFINITY;
-        const float wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nbr)));  // nbr >= 0
-        if (lane == 0) sm.wmaxnb[bb][warp] = wm;
-        if (r == 0) sm.meta[bb] = GramMeta{a0, alen, b0, blen, ab, npar, self && tj == ti, tj + 1 == tb, 0u};
+      const uint32_t ta = (nA + kGT - 1) / kGT, tb = (nB + kGN - 1) / kGN;
+      for (uint32_t ti = 0; ti < ta; ++ti) {  // strips of this pair
+        const uint32_t a0 = la + ti * kGT, alen = min(static_cast<uint32_t>(kGT), nA - ti * kGT);
+        const uint32_t tj0 = self ? ti * (kGT / kGN) : 0;
+        // the strip's shift: its first row (shared; every loader has finished
+        // the previous strip's tiles once it passes this barrier)
+        named_bar(1, 128);
+        if (r < D) sm.mu[r] = Xs[static_cast<size_t>(a0) * D + r];
+        named_bar(1, 128);
+        const float* mu = sm.mu;
+        const uint32_t ab = scount % kGAB, aph = (scount / kGAB) & 1;
+        ++scount;
+        mbar_wait(&sm.afree[ab], aph ^ 1);
+        const uint32_t npar = (scount - 1) & 1;
+        const float na_r =
+            gram_load_row<D, kGT, 0, D / 32>(Xs, a0 + r, static_cast<uint32_t>(r) < alen, mu, sm.A[ab][0], sm.A[ab][1], r);
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.bfull[bb]);
+        if (lane == 0) mbar_arrive(&sm.afull[ab]);
+        for (uint32_t tj = tj0; tj < tb; ++tj) {
+          const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+          ++bcount;
+          mbar_wait(&sm.bfree[bb], bph ^ 1);
+          const uint32_t b0 = lb + tj * kGN, blen = min(static_cast<uint32_t>(kGN), nB - tj * kGN);
+          // kGN = 128: one thread per B row; kGN = 64: two threads per row, each
+          // taking half of the row's 32-float chunks
+          constexpr int TPR = kGT / kGN;  // threads per B row
+          const int br = r / TPR, hf = r % TPR;
+          constexpr int HC = (D / 32) / TPR > 0 ? (D / 32) / TPR : 1;  // chunks per thread
+          float part = 0.f;
+          if (TPR == 1 || D == 32) {
+            if (hf == 0)
+              part = gram_load_row<D, kGN, 0, D / 32>(Xs, b0 + br, static_cast<uint32_t>(br) < blen, mu, sm.B[bb][0],
+                                                      sm.B[bb][1], br);
+          } else if (hf == 0) {
+            part = gram_load_row<D, kGN, 0, HC>(Xs, b0 + br, static_cast<uint32_t>(br) < blen, mu, sm.B[bb][0],
+                                                sm.B[bb][1], br);
+          } else {
+            part = gram_load_row<D, kGN, HC, 2 * HC>(Xs, b0 + br, static_cast<uint32_t>(br) < blen, mu, sm.B[bb][0],
+                                                     sm.B[bb][1], br);
+          }
+          const float nbr = TPR == 1 ? part : part + __shfl_xor_sync(kFull, part, 1);
+          sm.na[bb][r] = na_r;
+          if (hf == 0) {
+            sm.nb[bb][br] = nbr;
+            sm.cnb[bb][br] = static_cast<uint32_t>(br) < blen ? (1.f - 2.f * gram_slack<D>()) * nbr : INFINITY;
+          }
+          const float wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nbr)));  // nbr >= 0
+          if (lane == 0) sm.wmaxnb[bb][warp] = wm;
+          if (r == 0)
+            sm.meta[bb] = GramMeta{a0, alen, b0, blen, ab, npar, self && b0 < a0 + alen, tj + 1 == tb, 0u};
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.bfull[bb]);
+        }
       }
     }
   } else if (warp == 4) {  // ---- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(kGT, kGT);
+      constexpr uint32_t idesc = idesc_tf32(kGT, kGN);
       uint32_t bcount = 0, tcount = 0, scount = 0;
       bool need_a = true;
       for (;;) {
@@ -524,13 +545,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
           need_a = false;
         }
         tc_fence_after();
-        const uint32_t dcol = tmem + acc * kGT;
+        const uint32_t dcol = tmem + acc * kGN;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {  // 3xTF32: hi.hi + hi.lo + lo.hi
           const uint64_t ah = sw128_desc(smem_u32(sm.A[m.abuf][0] + c * (kGT * 32)));
           const uint64_t al = sw128_desc(smem_u32(sm.A[m.abuf][1] + c * (kGT * 32)));
-          const uint64_t bh = sw128_desc(smem_u32(sm.B[bb][0] + c * (kGT * 32)));
-          const uint64_t bl = sw128_desc(smem_u32(sm.B[bb][1] + c * (kGT * 32)));
+          const uint64_t bh = sw128_desc(smem_u32(sm.B[bb][0] + c * (kGN * 32)));
+          const uint64_t bl = sw128_desc(smem_u32(sm.B[bb][1] + c * (kGN * 32)));
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             umma_tf32_ss(dcol, ah + 2 * k, bh + 2 * k, idesc, (c | k) != 0);
@@ -549,7 +570,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     }
   } else if (warp >= 8) {
     // ---- epilogue: warp w owns TMEM lanes (A rows) 32 (w%4) .. +31 and the
-    // 64 columns starting at 64 ((w-8)/4).  Fast path per pair: one FMA, one
+    // 32 columns starting at 32 ((w-8)/4).  Fast path per pair: one FMA, one
     // compare folded into a predicate, one min; a chunk with a hit (or a self
     // tile, or an exclusion zone) is re-run with every check.
     const uint32_t e = warp & 3, half = (warp - 8) >> 2, r = 32 * e + lane;
@@ -567,17 +588,17 @@ __global__ void __launch_bounds__(kGThreads, 1)
       band = __shfl_sync(kFull, band, 0);
       const bool vr = r < m.alen;
       const uint32_t i = m.a0 + r;
-      const float na = sm.na[m.npar][r];
+      const float na = sm.na[bb][r];
       const float maxnb = fmaxf(fmaxf(sm.wmaxnb[bb][0], sm.wmaxnb[bb][1]), fmaxf(sm.wmaxnb[bb][2], sm.wmaxnb[bb][3]));
       const float R = band - (1.f - g2) * na;  // fast test: -2g + (1-g2) nb <= R
       const bool general = m.self || a.zone > 1;
       const uint32_t oi = (vr && a.zone > 1) ? a.sidx[i] : 0u;
       float vmin = INFINITY, ubs = INFINITY;
 #pragma unroll 1
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t c0 = half * 64 + q * 32;
+      for (int q = 0; q < kGN / 64; ++q) {
+        const uint32_t c0 = half * (kGN / 2) + q * 32;
         uint32_t v[32];
-        tmem_ld32(tmem + ((32u * e) << 16) + acc * kGT + c0, v);
+        tmem_ld32(tmem + ((32u * e) << 16) + acc * kGN + c0, v);
         if (!vr || c0 >= m.blen) continue;
         bool hit = false;
 #pragma unroll
@@ -624,7 +645,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       ub = __fmul_ru(fmaxf(ub, 0.f), 1.0f + 0x1.0p-16f);
 #pragma unroll
       for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(kFull, ub, o));
-      if (lane == 0 && ub < INFINITY) atomicMin(a.best, __float_as_uint(ub));
+      if (lane == 0 && ub < INFINITY && !a.no_ub) atomicMin(a.best, __float_as_uint(ub));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

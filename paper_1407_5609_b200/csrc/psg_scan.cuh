@@ -103,6 +103,7 @@ struct ScanArgs {
   uint32_t ovf_cap;
   unsigned long long* evals;
   unsigned long long* visited;  // grid engine: admissible stencil pairs
+  int no_ub;                    // debugging: dense Gram tiles do not feed their upper bounds to `best`
 };
 
 __device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {

@@ -55,9 +55,17 @@ def test_c4_full(psg, orc):
     assert np.all((pairs >> np.uint64(32)) < (pairs & np.uint64(0xFFFFFFFF)))
 
 
-def test_c5_recipe_n2_17(psg):
-    pts = psg.gen.mixture(5, 1 << 17, 64, 1024, 0.05)
+@pytest.mark.parametrize("logn", [17, 19])
+def test_c5_recipe_dense_engine(psg, logn):
+    """Clustered data: the dense cell-pair engine (tensor-core Gram tiles for
+    d = 64) against the device all-pairs engine.  n = 2^19 has many short
+    strips, which once exposed a buffer-reuse race between the loaders and the
+    epilogue of the Gram kernel."""
+    pts = psg.gen.mixture(5, 1 << logn, 64, 1024, 0.05)
     ps = psg.PointSet.from_flat(pts, 64)
     got = psg.closest_pair(ps, 10, 10.0, 1, 0)
+    for _ in range(2):  # repeated solves agree (graph replay, learned width)
+        again = psg.closest_pair(ps, 10, 10.0, 1, 0)
+        assert (again.index_i, again.index_j, again.distance) == (got.index_i, got.index_j, got.distance)
     bf = psg.brute_force_closest_pair(ps, 0)
     assert (got.index_i, got.index_j, got.distance) == (bf.index_i, bf.index_j, bf.distance)
