@@ -107,30 +107,41 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
   const uint32_t p = blockIdx.x * kFrnnThreads + tid;
   const bool valid = p < a.n;
   uint64_t visited = 0, examined = 0, hsum = 0;
-  GridFlat F{};
+  GridRanges R{};
   float mk[NK];
   float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t mi = 0;
   if (valid) {
-    F = grid_flat(grid_ranges(a.grid.cfirst, sP, p, a.grid.scell[p]));
+    R = grid_ranges(a.grid.cfirst, sP, p, a.grid.scell[p]);
     mi = a.sidx[p];
     if constexpr (kSmallD)
       me = a.sx[p];
     else
       load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
   }
-  const uint32_t T = valid ? F.total : 0u;
-  const uint32_t Tmax = __reduce_max_sync(kFull, T);
+  // walk the (at most five) ranges with a running position; the range
+  // switch is the only place the five bounds are selected
+  uint32_t j = R.b0, e = R.e0;
+  int ri = 0;
+  auto skip_empty = [&]() {
+    while (j >= e && ri < 4) {
+      ++ri;
+      j = R.b(ri);
+      e = R.e(ri);
+    }
+  };
+  skip_empty();
+  bool active = valid && j < e;
   const float* xi = a.X + static_cast<size_t>(mi) * a.d;
   const unsigned lt = (1u << lane) - 1u;
+  const bool zoned = a.zone > 1;
   int c = 0;  // warp-uniform fill of wbuf[w]
-  for (uint32_t t = 0; t < Tmax; ++t) {
+  while (__any_sync(kFull, active)) {
     bool emit = false;
     uint64_t key = 0;
-    if (t < T) {
-      const uint32_t j = F.at(t);
-      const uint32_t mj = a.sidx[j];
-      if (a.zone <= 1 || admissible(mi, mj, a.zone)) {  // refscan.cpp:15-18
+    if (active) {
+      uint32_t mj = zoned ? a.sidx[j] : 0u;
+      if (!zoned || admissible(mi, mj, a.zone)) {  // refscan.cpp:15-18
         ++visited;
         float s32;
         bool pass = true;
@@ -145,6 +156,7 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
           g = o.w - me.w;
           s32 = fmaf(g, g, s32);
         } else {
+          if (!zoned) mj = a.sidx[j];
           float kj[NK];
           load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
           pass = lb2_full<NK>(mk, kj) <= a.th.lb2;
@@ -152,13 +164,19 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
         }
         if (pass) {
           ++examined;
-          if (s32 <= a.th.band && (s32 <= a.lo || exact_distance(a.src, mi, mj) <= a.R)) {  // boundary inclusive
-            emit = true;
-            key = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
-            hsum += mix64(key);
+          if (s32 <= a.th.band) {
+            if (kSmallD && !zoned) mj = a.sidx[j];  // the original index only inside the band
+            if (s32 <= a.lo || exact_distance(a.src, mi, mj) <= a.R) {  // boundary inclusive
+              emit = true;
+              key = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
+              hsum += mix64(key);
+            }
           }
         }
       }
+      ++j;
+      if (j >= e) skip_empty();
+      active = j < e;
     }
     const unsigned mask = __ballot_sync(kFull, emit);
     if (mask) {

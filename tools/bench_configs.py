@@ -52,9 +52,15 @@ def main(which):
                     "device_ms": p["total_ms"], "window_pairs": p["window_pairs"]})
     if "c4" in which:
         cube = psg.gen.uniform(4, 1 << 22, 3)
-        (pairs, cnt, h), t, p = timed(lambda: psg.frnn_pairs(cube, R_C4, want_pairs=False))
-        res.append({"config": "C4 FRNN n=2^22 d=3 R=cbrt(3*32/(4 pi n))", "solve_s": t, "pairs": cnt, "hash": h,
-                    "device_ms": p["total_ms"], "candidates": p["window_pairs"], "stages": p["stage_list"]})
+        pc = psg.PointSet.from_flat(cube, 3)
+        nr, t, p = timed(lambda: psg.fixed_radius_neighbors(pc, R_C4, 10, 10.0, 1, 0, want_lists=False))
+        cnt, h = nr.pair_count, nr.pair_hash
+        res.append({"config": "C4 FRNN n=2^22 d=3 R=cbrt(3*32/(4 pi n)) (resident, count+hash)", "solve_s": t,
+                    "pairs": cnt, "hash": h, "device_ms": p["total_ms"], "candidates": p["window_pairs"],
+                    "stages": p["stage_list"]})
+        (pairs, cnt1, h1), t1, p1 = timed(lambda: psg.frnn_pairs(cube, R_C4, want_pairs=False))
+        res.append({"config": "C4 FRNN one-shot from host (H2D of pageable points included)", "solve_s": t1,
+                    "pairs": cnt1, "hash": h1})
         pinned = psg.PinnedBuffer(20 * len(cube))
         (pairs, cnt2, h2), t2, p2 = timed(lambda: psg.frnn_pairs(cube, R_C4, want_pairs=True, out=pinned.array), reps=2)
         ok = bool(np.all(pairs[1:] > pairs[:-1])) and cnt2 == cnt
