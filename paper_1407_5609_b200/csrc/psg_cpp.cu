@@ -55,6 +55,10 @@ constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
 constexpr double kGridOccupancy = 0.15;   // mean points per cell over the key box
 constexpr double kGridBoxSd = 2.5;        // key box: mean +- kGridBoxSd sd (clipped to the sample range)
 constexpr int kGridBootCap = 256;         // candidates per point in the grid bootstrap
+int boot_own_row() {  // the first bootstrap looks at the own cell row only (one cfirst lookup)
+  static const int v = std::getenv("PSG_BOOT_FULL") ? 0 : 1;
+  return v;
+}
 constexpr uint64_t kDenseFactor = 512;    // mean stencil candidates per point above which cells go dense
 
 // ---------------------------------------------------------------------------
@@ -371,7 +375,7 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
 // bound (at most `cap` candidates looked at); each warp evaluates its best.
 template <int NK>
 __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi,
-                                                             int cap) {
+                                                             int cap, int own_row) {
   __shared__ GridParams sP;  // one copy per block, not per thread (registers)
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) sP = *G.gp;
@@ -383,7 +387,8 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
     float mk[NK];
     load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
     const uint32_t mo = a.sidx[p];
-    const GridFlat F = grid_flat(grid_ranges(G.cfirst, sP, p, G.scell[p]));
+    const GridFlat F = grid_flat(own_row ? grid_own_row(G.cfirst, sP, p, G.scell[p])
+                                         : grid_ranges(G.cfirst, sP, p, G.scell[p]));
     const uint32_t L = min(F.total, static_cast<uint32_t>(cap));
     // more candidates than the cap: a uniform stride over all of them (a
     // cell lists its points in index order, which can correlate with
@@ -1010,10 +1015,10 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
     if (hi > lo) {
       if (plan.dir.nk == 4)
         k_grid_bootstrap<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, lo, hi,
-                                                                             kGridBootCap);
+                                                                             kGridBootCap, boot_own_row());
       else
         k_grid_bootstrap<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, lo, hi,
-                                                                             kGridBootCap);
+                                                                             kGridBootCap, boot_own_row());
       PSG_LAUNCHED();
       ++g_launches;
     }
@@ -1228,10 +1233,10 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         ScanArgs a = make_args(plan);
         if (plan.dir.nk == 4)
           k_grid_bootstrap<4><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, W.gi.dev, 0, static_cast<uint32_t>(n),
-                                                                           kGridBootCap);
+                                                                           kGridBootCap, 0);
         else
           k_grid_bootstrap<8><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, W.gi.dev, 0, static_cast<uint32_t>(n),
-                                                                           kGridBootCap);
+                                                                           kGridBootCap, 0);
         PSG_LAUNCHED();
         g_launches += 1;
         const float nb = read_best(&W.st.p->best, s);

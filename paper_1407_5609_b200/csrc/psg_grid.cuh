@@ -175,6 +175,20 @@ __device__ __forceinline__ GridRanges grid_ranges(const uint32_t* __restrict__ c
   return R;
 }
 
+// Only the own row's forward range [p+1, end of cell (.., c_last+1)): one
+// cfirst lookup (the bootstrap's cheap variant).
+__device__ __forceinline__ GridRanges grid_own_row(const uint32_t* __restrict__ cfirst, const GridParams& P,
+                                                   uint32_t p, uint32_t cell) {
+  GridRanges R{};
+  const uint32_t D = P.g == 1 ? P.dims[0] : (P.g == 2 ? P.dims[1] : P.dims[2]);
+  const uint32_t prefix = P.fD.div(cell);
+  const uint32_t c_last = cell - prefix * D;
+  const uint32_t hi_last = c_last + 1 < D ? c_last + 1 : D - 1;
+  R.b0 = p + 1;
+  R.e0 = cfirst[cell - c_last + hi_last + 1];
+  return R;
+}
+
 __device__ __forceinline__ GridFlat grid_flat(const GridRanges& R) {
   GridFlat F;
   F.b0 = R.b0;
