@@ -463,11 +463,11 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
     constexpr int B = 2;  // candidates in flight per step (registers vs latency)
     for (uint32_t t0 = 0; t0 < F.total; t0 += B) {
       uint32_t jj[B], oo[B];
-      float kk[B][NK];
+      float4 k0[B];  // keys 0-3 first: most candidates fail on them (16 B instead of 32 B)
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         jj[u] = t0 + u < F.total ? F.at(t0 + u) : p;
-        load_keys<NK>(a.skeys + static_cast<size_t>(jj[u]) * NK, kk[u]);
+        k0[u] = *reinterpret_cast<const float4*>(a.skeys + static_cast<size_t>(jj[u]) * NK);
         oo[u] = zoned ? a.sidx[jj[u]] : 0u;
       }
 #pragma unroll
@@ -476,8 +476,29 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
         if (zoned && !admissible(mo, oo[u], a.zone)) continue;
         ++visited;
         const uint32_t j = jj[u];
-        const float sl = lb2_full<NK>(mk, kk[u]);
+        // the lb2_full accumulation order, split after key 3: the partial sum
+        // only grows, so rejecting on it rejects exactly what the full sum would
+        float g = k0[u].x - mk[0];
+        float sl = g * g;
+        g = k0[u].y - mk[1];
+        sl = fmaf(g, g, sl);
+        g = k0[u].z - mk[2];
+        sl = fmaf(g, g, sl);
+        g = k0[u].w - mk[3];
+        sl = fmaf(g, g, sl);
         if (sl > lb2) continue;
+        if constexpr (NK == 8) {
+          const float4 k1 = *reinterpret_cast<const float4*>(a.skeys + static_cast<size_t>(j) * NK + 4);
+          g = k1.x - mk[4];
+          sl = fmaf(g, g, sl);
+          g = k1.y - mk[5];
+          sl = fmaf(g, g, sl);
+          g = k1.z - mk[6];
+          sl = fmaf(g, g, sl);
+          g = k1.w - mk[7];
+          sl = fmaf(g, g, sl);
+          if (sl > lb2) continue;
+        }
         const int slot = atomicAdd(&qn, 1);
         if (slot < kQueue) {
           qp[slot] = p;
