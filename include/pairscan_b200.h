@@ -39,6 +39,7 @@ extern "C" {
 #define PSG_ERR_CUDA 2    /* CUDA runtime / device failure */
 #define PSG_ERR_NOMEM 3
 #define PSG_ERR_INTERNAL 4
+#define PSG_ERR_IO 5      /* reference std::runtime_error from io.cpp (file open / parse) */
 
 /* refscan.hpp:27-36 ScanStats */
 typedef struct psg_scan_stats {
@@ -178,6 +179,25 @@ int psg_cpp_plan_bootstrap(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, f
 int psg_cpp_plan_scan(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float bound_s32,
                       psg_pair_result* out);
 void psg_cpp_plan_free(psg_cpp_plan* plan);
+
+/* ---- data formats --------------------------------------------
+ * Text series: io.cpp:44-60 load_series — one decimal real per line, strtod
+ * values, the reference's messages ("path:line: ..."; PSG_ERR_IO) and the
+ * finiteness check (series.cpp:13-17; PSG_ERR_INVALID); parsed in parallel.
+ * Needs no GPU.  *values is library-allocated: release with psg_free. */
+int psg_load_series_text(const char* path, double** values, uint64_t* length);
+/* io.cpp:62-70 save_series: "%.17g\n" per value, so load(save(x)) == x. */
+int psg_save_series_text(const char* path, const double* values, uint64_t length);
+void psg_free(void* p);
+/* Binary ".psgb": 32-byte header {"PSGB", u32 version=1, u32 dtype (1 = f64,
+ * 2 = f32), u32 0, u64 rows, u64 cols} + rows*cols little-endian values,
+ * row-major (a series is one column). */
+int psg_save_binary(const char* path, const void* data, int dtype, uint64_t rows, uint64_t cols);
+/* A device point set straight from a .psgb file: the rows stream through two
+ * pinned staging buffers into HBM (no pageable copy of the whole file). */
+int psg_pointset_from_file(const char* path, psg_pointset** out);
+/* windows_of over a one-column .psgb series (optionally z-normalised). */
+int psg_pointset_windows_from_file(const char* path, uint64_t len, int znorm, psg_pointset** out);
 
 /* ---- inspection (tests): the projection keys of a point set ---------------
  * keys[i*nk + k] = <U_k, X_i> as the solve computes them (tensor cores for

@@ -265,6 +265,10 @@ class Reference:
         L.ref_derive_seed.restype = _u64
         L.ref_derive_seed.argtypes = [_u64, _u64]
         L.ref_gen_random_walk.argtypes = [_u64, _u64, _f64, _p]
+        if hasattr(L, "ref_load_series"):
+            L.ref_load_series.argtypes = [C.c_char_p, _p, _p]
+            L.ref_save_series.argtypes = [_p, _u64, C.c_char_p]
+            L.ref_free.argtypes = [_p]
         L.ref_euclidean.restype = _f64
         L.ref_euclidean.argtypes = [_p, _p, _u64]
         L.ref_euclidean_early_abandon.argtypes = [_p, _p, _u64, _f64, _p]
@@ -328,6 +332,20 @@ class Reference:
         y = np.ascontiguousarray(y, dtype=np.float64)
         out = _f64()
         return out.value if self.lib.ref_euclidean_early_abandon(_ptr(x), _ptr(y), x.size, thr, C.byref(out)) else None
+
+    def load_series(self, path: str):
+        """io.cpp load_series: (values or None, rc, message)."""
+        out, n = C.c_void_p(), _u64()
+        rc = self.lib.ref_load_series(path.encode(), C.byref(out), C.byref(n))
+        if rc != 0:
+            return None, rc, self.lib.ref_last_error().decode()
+        vals = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_double)), shape=(n.value,)).copy()
+        self.lib.ref_free(out)
+        return vals, 0, ""
+
+    def save_series(self, values, path: str) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        assert self.lib.ref_save_series(v.ctypes.data, v.size, path.encode()) == 0
 
     def reference_bound(self, r, x, y):
         r, x, y = (np.ascontiguousarray(v, dtype=np.float64) for v in (r, x, y))

@@ -11,12 +11,14 @@
 // std::invalid_argument (message retrievable with ref_last_error()).
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "pairscan/datagen.hpp"
+#include "pairscan/io.hpp"
 #include "pairscan/metrics.hpp"
 #include "pairscan/refscan.hpp"
 #include "pairscan/rng.hpp"
@@ -185,5 +187,26 @@ int ref_build_reference_set(const double* pts, uint64_t n, uint64_t d, uint64_t 
     for (uint64_t i = 0; i < n; ++i) order[i] = rs.order[i];
   });
 }
+
+// io.cpp:44-60 / 62-70: the series text format.  Returns 0, -1 (invalid_argument)
+// or -2 (runtime_error); *out is malloc'd.
+int ref_load_series(const char* path, double** out, uint64_t* n) {
+  return guarded([&] {
+    const TimeSeries ts = load_series(path);
+    *n = ts.values.size();
+    *out = static_cast<double*>(std::malloc(ts.values.size() * sizeof(double)));
+    std::memcpy(*out, ts.values.data(), ts.values.size() * sizeof(double));
+  });
+}
+
+int ref_save_series(const double* v, uint64_t n, const char* path) {
+  return guarded([&] {
+    TimeSeries ts;
+    ts.values.assign(v, v + n);
+    save_series(ts, path);
+  });
+}
+
+void ref_free(void* p) { std::free(p); }
 
 }  // extern "C"

@@ -43,10 +43,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpairscan_b200.so")
 
 PSG_OK, PSG_ERR_INVALID, PSG_ERR_CUDA, PSG_ERR_NOMEM, PSG_ERR_INTERNAL = 0, 1, 2, 3, 4
+PSG_ERR_IO = 5
 
 
 class InvalidArgument(ValueError):
     """The reference's std::invalid_argument (same messages)."""
+
+
+class SeriesFileError(RuntimeError):
+    """io.cpp's std::runtime_error (file open / parse errors), PSG_ERR_IO."""
 
 
 class DeviceError(RuntimeError):
@@ -123,6 +128,12 @@ _SIGS = {
     "psg_host_alloc": (_int, [C.c_size_t, _p]),
     "psg_host_free": (None, [_p]),
     "psg_debug_projection": (_int, [_p, _u64, _u64, _p, _p, _p, _p, _p]),
+    "psg_load_series_text": (_int, [C.c_char_p, _p, _p]),
+    "psg_save_series_text": (_int, [C.c_char_p, _p, _u64]),
+    "psg_free": (None, [_p]),
+    "psg_save_binary": (_int, [C.c_char_p, _p, _int, _u64, _u64]),
+    "psg_pointset_from_file": (_int, [C.c_char_p, _p]),
+    "psg_pointset_windows_from_file": (_int, [C.c_char_p, _u64, _int, _p]),
 }
 
 _lib = None
@@ -152,6 +163,8 @@ def _check(rc: int) -> None:
         raise InvalidArgument(msg)
     if rc == PSG_ERR_NOMEM:
         raise MemoryError(msg)
+    if rc == PSG_ERR_IO:
+        raise SeriesFileError(msg)
     raise DeviceError(msg)
 
 
@@ -532,3 +545,48 @@ def debug_projection(points: "PointSet", q: int = 10, seed: int = 1):
     _check(lib().psg_debug_projection(points._device(), q, seed, C.byref(nk), keys.ctypes.data, dirs.ctypes.data,
                                       C.byref(E), C.byref(scale)))
     return keys, dirs, E.value, scale.value
+
+
+# ---- data formats ------------------------------------------------------
+def load_series_text(path: str) -> np.ndarray:
+    """io.cpp:44-60 load_series (one decimal real per line, strtod values, the
+    reference's messages), parsed in parallel; needs no GPU."""
+    out, n = C.c_void_p(), _u64()
+    _check(lib().psg_load_series_text(os.fsencode(path), C.byref(out), C.byref(n)))
+    vals = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_double)), shape=(n.value,)).copy()
+    lib().psg_free(out)
+    return vals
+
+
+def save_series_text(values, path: str) -> None:
+    """io.cpp:62-70 save_series: '%.17g' per line."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    _check(lib().psg_save_series_text(os.fsencode(path), _ptr(v), v.size))
+
+
+def save_binary(array, path: str) -> None:
+    """.psgb: 32-byte header + row-major f32/f64 values (a 1-D array is one column)."""
+    a = np.ascontiguousarray(array)
+    if a.dtype not in (np.float32, np.float64):
+        a = a.astype(np.float64)
+    rows, cols = (a.shape[0], 1) if a.ndim == 1 else a.shape
+    _check(lib().psg_save_binary(os.fsencode(path), _ptr(a), 2 if a.dtype == np.float32 else 1, rows, cols))
+
+
+class FilePointSet(PointSet):
+    """A device point set read straight from a .psgb file (psg_pointset_from_file
+    / psg_pointset_windows_from_file): no host copy of the rows is kept."""
+
+    def __init__(self, path: str, window: int = 0, znorm: bool = False):
+        super().__init__()
+        h = _p()
+        if window:
+            _check(lib().psg_pointset_windows_from_file(os.fsencode(path), window, int(znorm), C.byref(h)))
+        else:
+            _check(lib().psg_pointset_from_file(os.fsencode(path), C.byref(h)))
+        self._handle = h
+        self._n = int(lib().psg_pointset_size(h))
+        self._d = int(lib().psg_pointset_dim(h))
+
+    def point(self, i: int):
+        raise InvalidArgument("FilePointSet keeps its rows on the device only")

@@ -10,6 +10,7 @@
 #include "host_rng.hpp"
 #include "psg_cpp.cuh"
 #include "psg_engines.cuh"
+#include "psg_io.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -28,6 +29,9 @@ int guarded(F&& f) {
   } catch (const psg::invalid_argument& e) {
     g_err = e.what();
     return PSG_ERR_INVALID;
+  } catch (const psg::io_error& e) {
+    g_err = e.what();
+    return PSG_ERR_IO;
   } catch (const psg::cuda_error& e) {
     g_err = e.what();
     return PSG_ERR_CUDA;
@@ -38,6 +42,63 @@ int guarded(F&& f) {
     g_err = e.what();
     return PSG_ERR_INTERNAL;
   }
+}
+
+// Host-only entries (file formats): no device context is touched.
+template <class F>
+int guarded_host(F&& f) {
+  try {
+    f();
+    return PSG_OK;
+  } catch (const psg::invalid_argument& e) {
+    g_err = e.what();
+    return PSG_ERR_INVALID;
+  } catch (const psg::io_error& e) {
+    g_err = e.what();
+    return PSG_ERR_IO;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of memory";
+    return PSG_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PSG_ERR_INTERNAL;
+  }
+}
+
+// Stream a .psgb payload into device memory through two pinned staging
+// buffers (read of chunk k+1 overlaps the upload of chunk k).
+psg::DevBuf<char> upload_file(psg::BinaryFile& bf, cudaStream_t s) {
+  constexpr size_t kChunk = size_t(32) << 20;
+  psg::DevBuf<char> dev(std::max<uint64_t>(bf.bytes, 1), s);
+  char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2; ++k) {
+    PSG_CUDA(cudaMallocHost(&stage[k], kChunk));
+    PSG_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+  }
+  try {
+    for (uint64_t off = 0, k = 0; off < bf.bytes; off += kChunk, k ^= 1) {
+      const size_t len = static_cast<size_t>(std::min<uint64_t>(kChunk, bf.bytes - off));
+      PSG_CUDA(cudaEventSynchronize(done[k]));  // the previous upload from this buffer has finished
+      if (bf.read(stage[k], len) != len) throw psg::io_error("short read from a .psgb file");
+      PSG_CUDA(cudaMemcpyAsync(dev.p + off, stage[k], len, cudaMemcpyHostToDevice, s));
+      PSG_CUDA(cudaEventRecord(done[k], s));
+    }
+    PSG_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    for (int k = 0; k < 2; ++k) {
+      cudaFreeHost(stage[k]);
+      cudaEventDestroy(done[k]);
+    }
+    throw;
+  }
+  for (int k = 0; k < 2; ++k) {
+    cudaFreeHost(stage[k]);
+    cudaEventDestroy(done[k]);
+  }
+  psg::g_prof.h2d_bytes += bf.bytes;
+  return dev;
 }
 
 void require_dim(uint64_t dim) {
@@ -306,5 +367,60 @@ int psg_debug_projection(psg_pointset* ps, uint64_t q, uint64_t seed, int* nk, f
     if (dirs) std::copy(dir.U.begin(), dir.U.end(), dirs);
     if (key_error) *key_error = b.E;
     if (scale) *scale = ps->scale;
+  });
+}
+
+// ---- data formats --------------------------------------------------
+int psg_load_series_text(const char* path, double** values, uint64_t* length) {
+  return guarded_host([&] {
+    if (!path || !values || !length) throw psg::invalid_argument("null argument");
+    const std::vector<double> v = psg::load_series_text(path);
+    double* out = static_cast<double*>(std::malloc(v.size() * sizeof(double)));
+    if (!out) throw std::bad_alloc();
+    std::copy(v.begin(), v.end(), out);
+    *values = out;
+    *length = v.size();
+  });
+}
+
+int psg_save_series_text(const char* path, const double* values, uint64_t length) {
+  return guarded_host([&] {
+    if (!path || (!values && length)) throw psg::invalid_argument("null argument");
+    psg::save_series_text(path, values, length);
+  });
+}
+
+void psg_free(void* p) { std::free(p); }
+
+int psg_save_binary(const char* path, const void* data, int dtype, uint64_t rows, uint64_t cols) {
+  return guarded_host([&] {
+    if (!path || (!data && rows * cols)) throw psg::invalid_argument("null argument");
+    psg::save_binary(path, data, dtype, rows, cols);
+  });
+}
+
+int psg_pointset_from_file(const char* path, psg_pointset** out) {
+  return guarded([&] {
+    if (!path || !out) throw psg::invalid_argument("null argument");
+    psg::BinaryFile bf = psg::open_binary(path);
+    require_dim(bf.cols);
+    cudaStream_t s = psg::ctx().stream;
+    psg::DevBuf<char> dev = upload_file(bf, s);
+    *out = bf.dtype == 2 ? rows32(reinterpret_cast<const float*>(dev.p), bf.rows, bf.cols, true).release()
+                         : rows64(reinterpret_cast<const double*>(dev.p), bf.rows, bf.cols, true).release();
+  });
+}
+
+int psg_pointset_windows_from_file(const char* path, uint64_t len, int znorm, psg_pointset** out) {
+  return guarded([&] {
+    if (!path || !out) throw psg::invalid_argument("null argument");
+    psg::BinaryFile bf = psg::open_binary(path);
+    if (bf.cols != 1) throw psg::invalid_argument("a series file has one column");
+    cudaStream_t s = psg::ctx().stream;
+    psg::DevBuf<char> dev = upload_file(bf, s);
+    *out = bf.dtype == 2 ? psg::pointset_windows(nullptr, reinterpret_cast<const float*>(dev.p), bf.rows, len,
+                                                 znorm != 0, true)
+                         : psg::pointset_windows(reinterpret_cast<const double*>(dev.p), nullptr, bf.rows, len,
+                                                 znorm != 0, true);
   });
 }

@@ -17,9 +17,12 @@ namespace psg {
 // Mirrors the reference's std::invalid_argument contract (refscan.cpp:33-35,
 // 70, 129, 136, 162-163, 214; series.cpp:9, 20-24); surfaced through the C ABI
 // as PSG_ERR_INVALID with the identical message.
+#ifndef PSG_INVALID_ARGUMENT_DEFINED
+#define PSG_INVALID_ARGUMENT_DEFINED
 struct invalid_argument : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
+#endif
 struct cuda_error : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
