@@ -66,37 +66,28 @@ int guarded_host(F&& f) {
 }
 
 // Stream a .psgb payload into device memory through two pinned staging
-// buffers (read of chunk k+1 overlaps the upload of chunk k).
+// buffers (kept for the process): the parallel read of chunk k+1 overlaps the
+// upload of chunk k.
 psg::DevBuf<char> upload_file(psg::BinaryFile& bf, cudaStream_t s) {
-  constexpr size_t kChunk = size_t(32) << 20;
+  constexpr size_t kChunk = size_t(64) << 20;
+  static char* stage[2] = {nullptr, nullptr};
+  static cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2; ++k) {
+    if (!stage[k]) PSG_CUDA(cudaMallocHost(&stage[k], kChunk));
+    if (!done[k]) PSG_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+  }
   psg::DevBuf<char> dev(std::max<uint64_t>(bf.bytes, 1), s);
-  char* stage[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
-  for (int k = 0; k < 2; ++k) {
-    PSG_CUDA(cudaMallocHost(&stage[k], kChunk));
-    PSG_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
-  }
-  try {
-    for (uint64_t off = 0, k = 0; off < bf.bytes; off += kChunk, k ^= 1) {
-      const size_t len = static_cast<size_t>(std::min<uint64_t>(kChunk, bf.bytes - off));
-      PSG_CUDA(cudaEventSynchronize(done[k]));  // the previous upload from this buffer has finished
-      if (bf.read(stage[k], len) != len) throw psg::io_error("short read from a .psgb file");
-      PSG_CUDA(cudaMemcpyAsync(dev.p + off, stage[k], len, cudaMemcpyHostToDevice, s));
-      PSG_CUDA(cudaEventRecord(done[k], s));
+  for (uint64_t off = 0, k = 0; off < bf.bytes; off += kChunk, k ^= 1) {
+    const size_t len = static_cast<size_t>(std::min<uint64_t>(kChunk, bf.bytes - off));
+    PSG_CUDA(cudaEventSynchronize(done[k]));  // the previous upload from this buffer has finished
+    if (bf.pread_payload(stage[k], off, len, 8) != len) {
+      cudaStreamSynchronize(s);
+      throw psg::io_error("short read from a .psgb file");
     }
-    PSG_CUDA(cudaStreamSynchronize(s));
-  } catch (...) {
-    cudaStreamSynchronize(s);
-    for (int k = 0; k < 2; ++k) {
-      cudaFreeHost(stage[k]);
-      cudaEventDestroy(done[k]);
-    }
-    throw;
+    PSG_CUDA(cudaMemcpyAsync(dev.p + off, stage[k], len, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaEventRecord(done[k], s));
   }
-  for (int k = 0; k < 2; ++k) {
-    cudaFreeHost(stage[k]);
-    cudaEventDestroy(done[k]);
-  }
+  PSG_CUDA(cudaStreamSynchronize(s));
   psg::g_prof.h2d_bytes += bf.bytes;
   return dev;
 }

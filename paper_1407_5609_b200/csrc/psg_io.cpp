@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <stdexcept>
 #include <string>
 #include <functional>
@@ -191,6 +192,29 @@ BinaryFile open_binary(const std::string& path) {
 }
 
 size_t BinaryFile::read(void* dst, size_t bytes) { return std::fread(dst, 1, bytes, f); }
+
+size_t BinaryFile::pread_payload(void* dst, uint64_t off, size_t len, int threads) const {
+  const int fd = fileno(f);
+  std::vector<size_t> got(static_cast<size_t>(std::max(threads, 1)), 0);
+  auto work = [&](int k) {
+    const size_t b = len * k / got.size(), e = len * (k + 1) / got.size();
+    size_t done = 0;
+    while (b + done < e) {
+      const ssize_t r = ::pread(fd, static_cast<char*>(dst) + b + done, e - b - done,
+                                static_cast<off_t>(sizeof(Header) + off + b + done));
+      if (r <= 0) break;
+      done += static_cast<size_t>(r);
+    }
+    got[static_cast<size_t>(k)] = done;
+  };
+  std::vector<std::thread> th;
+  for (int k = 1; k < static_cast<int>(got.size()); ++k) th.emplace_back(work, k);
+  work(0);
+  for (std::thread& t : th) t.join();
+  size_t total = 0;
+  for (const size_t g : got) total += g;
+  return total;
+}
 
 BinaryFile::~BinaryFile() {
   if (f) std::fclose(f);

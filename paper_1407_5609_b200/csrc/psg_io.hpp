@@ -32,6 +32,8 @@ struct BinaryFile {
   int dtype = 0;  // 1 = f64, 2 = f32
   uint64_t rows = 0, cols = 0, bytes = 0;
   size_t read(void* dst, size_t bytes);
+  // payload bytes [off, off+len) into dst, read by `threads` parallel preads
+  size_t pread_payload(void* dst, uint64_t off, size_t len, int threads) const;
   BinaryFile() = default;
   BinaryFile(BinaryFile&& o) noexcept : f(o.f), dtype(o.dtype), rows(o.rows), cols(o.cols), bytes(o.bytes) {
     o.f = nullptr;
