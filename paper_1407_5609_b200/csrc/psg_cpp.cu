@@ -1216,6 +1216,14 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       PSG_CUDA(cudaMemcpyAsync(W.host_st, W.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
       plan.dense = est > kDenseFactor * n;
+      if (nparts == 1 && plan.dense) {  // later solves of this (q, seed, zone) skip the graph attempt
+        if (W.learned_q != plan.q_arg || W.learned_seed != plan.seed_arg || W.learned_zone != plan.zone)
+          W.learned_w = 0.0;  // hints of another (q, seed, zone)
+        W.learned_dense = true;
+        W.learned_q = plan.q_arg;
+        W.learned_seed = plan.seed_arg;
+        W.learned_zone = plan.zone;
+      }
       static const int dense_keys = std::getenv("PSG_DENSE_KEYS") ? std::atoi(std::getenv("PSG_DENSE_KEYS")) : kMaxGridKeys;
       const int gd = std::min(plan.dir.q, dense_keys);
       if (plan.dense && plan.g < gd) {
@@ -1273,6 +1281,8 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         // Remember the width for later solves of the same (q, seed, zone) on
         // this point set: their first grid is built at it, so the captured
         // graph solve needs no regrid (a tuning hint; every stage still runs).
+        if (W.learned_q != plan.q_arg || W.learned_seed != plan.seed_arg || W.learned_zone != plan.zone)
+          W.learned_dense = false;  // hints of another (q, seed, zone)
         W.learned_w = plan.gp.w;
         W.learned_q = plan.q_arg;
         W.learned_seed = plan.seed_arg;
@@ -1339,6 +1349,7 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   if (!(d < 32 || d == 32 || d == 64 || d == 128 || d == 256)) return false;  // projection needs a host buffer
   std::shared_ptr<CppWork> work = get_work(ps, dir.nk, s);
   CppWork& W = *work;
+  if (W.learned_dense && W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone) return false;
   if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone) {
     if (W.gexec) {
       cudaGraphExecDestroy(W.gexec);

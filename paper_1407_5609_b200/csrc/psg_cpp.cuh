@@ -67,6 +67,7 @@ struct CppWork {
   // cell width a regrid converged to, for the same (q, seed, zone)
   double learned_w = 0.0;
   uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;
+  bool learned_dense = false;  // the solve went to the dense engine (not graph-capturable: host decisions)
   cudaEvent_t gev[6] = {};  // project / bootstrap / scan spans recorded inside the graph
   ~CppWork();
 };

@@ -340,12 +340,10 @@ __global__ void __launch_bounds__(256) k_dense_tiles(ScanArgs a, const float* __
 // = one A tile of a kept cell pair against every B tile of the pair (self
 // pairs: tiles tj >= ti); strips are taken from a global cursor.
 constexpr int kGT = 128;  // A tile rows (UMMA M)
-#ifndef PSG_GRAM_N
-#define PSG_GRAM_N 128
-#endif
-constexpr int kGN = PSG_GRAM_N;           // B tile rows (UMMA N)
-constexpr int kGAB = 1;                   // A buffers (hi + lo)
-constexpr int kGBB = kGN == 64 ? 4 : 2;   // B buffers (hi + lo)
+constexpr int kGN = 128;       // B tile rows (UMMA N)
+constexpr int kGAB = 1;        // A buffers (hi + lo)
+constexpr int kGBB = 2;        // B buffers (hi + lo)
+constexpr int kMaxPartners = 366;  // the own cell + the (3^6 - 1)/2 forward stencil cells
 constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM, 8-15 epilogue
 constexpr int kGEpi = 8;        // epilogue warps: two per TMEM lane quarter, 64 columns each
 constexpr uint32_t kGTmemCols = 2 * kGN;  // 2 accumulators x kGN columns
@@ -373,7 +371,10 @@ struct GramSmem {
   float nb[kGBB][kGN];
   float cnb[kGBB][kGN];  // (1 - 2 slack) nb, +inf past the tile's length: the epilogue's fast test
   float wmaxnb[kGBB][4];
-  float mu[D];  // the current strip's shift (its first row)
+  uint32_t jpos[kGBB][kGN];  // grid position of each B row; bit 31: the row is in A's own cell
+  float mu[D];               // the current strip's shift (its first row)
+  uint32_t ostart[kMaxPartners + 1], obase[kMaxPartners];  // the group's other partners: stream prefix, first position
+  uint32_t grp[7];           // group: A, la, nA, has_own, npartners, others_total; the strip's A tile
   GramMeta meta[kGBB];
   uint64_t afull[kGAB], afree[kGAB], bfull[kGBB], bfree[kGBB], tfull[2], tempty[2];
   uint32_t tmem, strip;
@@ -418,8 +419,10 @@ __device__ __forceinline__ float gram_load_row(const float* __restrict__ Xs, uin
 template <int D>
 __global__ void __launch_bounds__(kGThreads, 1)
     k_dense_gram(ScanArgs a, const float* __restrict__ Xs, const uint32_t* __restrict__ cfirst,
-                 const uint32_t* __restrict__ pa, const uint32_t* __restrict__ pb, const uint32_t* __restrict__ prefix,
-                 uint32_t npairs, uint32_t part, uint32_t nparts, unsigned long long* __restrict__ cursor) {
+                 const uint32_t* __restrict__ pa, const uint32_t* __restrict__ pb, const uint32_t* __restrict__ gstart,
+                 const uint32_t* __restrict__ gprefix, const uint32_t* __restrict__ ngroups, uint32_t npairs,
+                 uint32_t part, uint32_t nparts,
+                 unsigned long long* __restrict__ cursor) {
   using namespace tc;
   constexpr int NC = D / 32;
   extern __shared__ uint8_t graw[];
@@ -446,15 +449,51 @@ __global__ void __launch_bounds__(kGThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
   
-  if (warp < 4) {  // ---- loaders: thread = tile row; a cursor hands out kept cell pairs
+  if (warp < 4) {
+    // ---- loaders: thread = tile row.  A cursor hands out groups (a cell A
+    // with every kept partner cell; the kept pairs are sorted by A, the own
+    // cell first).  A strip is one 128-row tile of A against the
+    // concatenation of its partners' points (the own cell from the strip's
+    // first row on), cut into 128-row B tiles: small cells fill the tiles.
     const int r = tid;
     uint32_t scount = 0, bcount = 0;
     for (;;) {
-      if (r == 0) sm.strip = static_cast<uint32_t>(atomicAdd(cursor, 1ull) * nparts + part);
+      named_bar(1, 128);  // every loader is done with the previous group's table
+      if (r == 0) {
+        const uint32_t st = static_cast<uint32_t>(atomicAdd(cursor, 1ull) * nparts + part);
+        const uint32_t ng = *ngroups;
+        sm.strip = st < gprefix[ng] ? st : 0xffffffffu;
+        if (st < gprefix[ng]) {
+          uint32_t lo = 0, hi = ng;  // group g: gprefix[g] <= st < gprefix[g+1]
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (gprefix[mid] <= st)
+              lo = mid;
+            else
+              hi = mid;
+          }
+          sm.grp[6] = st - gprefix[lo];  // the strip's A tile
+          const uint32_t gs = gstart[lo], A = pa[gs];
+          const uint32_t la = cfirst[A], nA = cfirst[A + 1] - la;
+          const bool own = pb[gs] == A;
+          uint32_t np = 0, tot = 0;
+          for (uint32_t k = gs + (own ? 1u : 0u); k < npairs && pa[k] == A && np < kMaxPartners; ++k, ++np) {
+            const uint32_t B = pb[k], lb = cfirst[B], nB = cfirst[B + 1] - lb;
+            sm.ostart[np] = tot;
+            sm.obase[np] = lb;
+            tot += nB;
+          }
+          sm.ostart[np] = tot;
+          sm.grp[0] = A;
+          sm.grp[1] = la;
+          sm.grp[2] = nA;
+          sm.grp[3] = own;
+          sm.grp[4] = np;
+          sm.grp[5] = tot;
+        }
+      }
       named_bar(1, 128);
-      const uint32_t k = sm.strip;
-      named_bar(1, 128);
-      if (k >= npairs) {  // sentinel tile: tells the MMA and the epilogue to stop
+      if (sm.strip == 0xffffffffu) {  // sentinel tile: tells the MMA and the epilogue to stop
         const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
         mbar_wait(&sm.bfree[bb], bph ^ 1);
         if (r == 0) sm.meta[bb].done = 1;
@@ -462,14 +501,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
         if (lane == 0) mbar_arrive(&sm.bfull[bb]);
         break;
       }
-      const uint32_t A = pa[k], B = pb[k];
-      const uint32_t la = cfirst[A], nA = cfirst[A + 1] - la;
-      const uint32_t lb = cfirst[B], nB = cfirst[B + 1] - lb;
-      const bool self = A == B;
-      const uint32_t ta = (nA + kGT - 1) / kGT, tb = (nB + kGN - 1) / kGN;
-      for (uint32_t ti = 0; ti < ta; ++ti) {  // strips of this pair
+      const uint32_t la = sm.grp[1], nA = sm.grp[2], np = sm.grp[4], others = sm.grp[5];
+      const bool own = sm.grp[3] != 0;
+      {
+        const uint32_t ti = sm.grp[6];  // this work item's strip of the group
         const uint32_t a0 = la + ti * kGT, alen = min(static_cast<uint32_t>(kGT), nA - ti * kGT);
-        const uint32_t tj0 = self ? ti * (kGT / kGN) : 0;
+        const uint32_t own_len = own ? la + nA - a0 : 0u;  // own cell from the strip's first row on
+        const uint32_t L = own_len + others, tb = (L + kGN - 1) / kGN;
         // the strip's shift: its first row (shared; every loader has finished
         // the previous strip's tiles once it passes this barrier)
         named_bar(1, 128);
@@ -485,38 +523,37 @@ __global__ void __launch_bounds__(kGThreads, 1)
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.afull[ab]);
-        for (uint32_t tj = tj0; tj < tb; ++tj) {
+        for (uint32_t tj = 0; tj < tb; ++tj) {
           const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
           ++bcount;
           mbar_wait(&sm.bfree[bb], bph ^ 1);
-          const uint32_t b0 = lb + tj * kGN, blen = min(static_cast<uint32_t>(kGN), nB - tj * kGN);
-          // kGN = 128: one thread per B row; kGN = 64: two threads per row, each
-          // taking half of the row's 32-float chunks
-          constexpr int TPR = kGT / kGN;  // threads per B row
-          const int br = r / TPR, hf = r % TPR;
-          constexpr int HC = (D / 32) / TPR > 0 ? (D / 32) / TPR : 1;  // chunks per thread
-          float part = 0.f;
-          if (TPR == 1 || D == 32) {
-            if (hf == 0)
-              part = gram_load_row<D, kGN, 0, D / 32>(Xs, b0 + br, static_cast<uint32_t>(br) < blen, mu, sm.B[bb][0],
-                                                      sm.B[bb][1], br);
-          } else if (hf == 0) {
-            part = gram_load_row<D, kGN, 0, HC>(Xs, b0 + br, static_cast<uint32_t>(br) < blen, mu, sm.B[bb][0],
-                                                sm.B[bb][1], br);
-          } else {
-            part = gram_load_row<D, kGN, HC, 2 * HC>(Xs, b0 + br, static_cast<uint32_t>(br) < blen, mu, sm.B[bb][0],
-                                                     sm.B[bb][1], br);
+          const uint32_t q = tj * kGN + r, blen = min(static_cast<uint32_t>(kGN), L - tj * kGN);
+          const bool valid = q < L, mine = q < own_len;
+          uint32_t pos = 0;
+          if (valid) {
+            if (mine) {
+              pos = a0 + q;
+            } else {  // partner k with ostart[k] <= q' < ostart[k+1]
+              const uint32_t qq = q - own_len;
+              uint32_t lo = 0, hi = np;
+              while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sm.ostart[mid] <= qq)
+                  lo = mid;
+                else
+                  hi = mid;
+              }
+              pos = sm.obase[lo] + (qq - sm.ostart[lo]);
+            }
           }
-          const float nbr = TPR == 1 ? part : part + __shfl_xor_sync(kFull, part, 1);
+          const float nbr = gram_load_row<D, kGN, 0, D / 32>(Xs, pos, valid, mu, sm.B[bb][0], sm.B[bb][1], r);
           sm.na[bb][r] = na_r;
-          if (hf == 0) {
-            sm.nb[bb][br] = nbr;
-            sm.cnb[bb][br] = static_cast<uint32_t>(br) < blen ? (1.f - 2.f * gram_slack<D>()) * nbr : INFINITY;
-          }
+          sm.nb[bb][r] = nbr;
+          sm.cnb[bb][r] = valid ? (1.f - 2.f * gram_slack<D>()) * nbr : INFINITY;
+          sm.jpos[bb][r] = pos | (mine ? 0x80000000u : 0u);
           const float wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nbr)));  // nbr >= 0
           if (lane == 0) sm.wmaxnb[bb][warp] = wm;
-          if (r == 0)
-            sm.meta[bb] = GramMeta{a0, alen, b0, blen, ab, npar, self && b0 < a0 + alen, tj + 1 == tb, 0u};
+          if (r == 0) sm.meta[bb] = GramMeta{a0, alen, 0u, blen, ab, npar, tj * kGN < own_len, tj + 1 == tb, 0u};
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.bfull[bb]);
@@ -617,8 +654,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
         for (int jj = 0; jj < 32; ++jj) {  // slow path: every check, the exact slack test
           const uint32_t jl = c0 + jj;
           if (jl >= m.blen) continue;
-          const uint32_t j = m.b0 + jl;
-          if (m.self && j <= i) continue;
+          const uint32_t jp = sm.jpos[bb][jl], j = jp & 0x7fffffffu;
+          if ((jp >> 31) && j <= i) continue;  // own cell: pairs j > i only
           if (a.zone > 1 && !admissible(oi, a.sidx[j], a.zone)) continue;
           if (general) ++visited;
           const float nbj = sm.nb[bb][jl];
@@ -673,8 +710,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
 }
 
 template <int D>
-void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, uint32_t npairs, uint32_t part,
-                 uint32_t nparts, cudaStream_t s) {
+void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, const uint32_t* pa, const uint32_t* pb,
+                 uint32_t npairs, uint32_t part, uint32_t nparts, cudaStream_t s) {
   constexpr size_t kSmem = sizeof(GramSmem<D>) + 1024;
   static bool configured = false;
   if (!configured) {
@@ -682,9 +719,30 @@ void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, uin
                                   static_cast<int>(kSmem)));
     configured = true;
   }
-  k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
+  k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.cfirst.p, pa, pb, w.gstart.p,
+                                                           w.gprefix.p, reinterpret_cast<const uint32_t*>(w.ctr.p + 3),
                                                            npairs, part, nparts, w.ctr.p + 1);
   PSG_LAUNCHED();
+}
+
+// Strips (128-row A tiles) per group.
+__global__ void k_group_strips(const uint32_t* __restrict__ pa, const uint32_t* __restrict__ gstart, uint32_t ngroups,
+                               const uint32_t* __restrict__ cfirst, uint32_t* __restrict__ gstrips) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > ngroups) return;
+  if (g == ngroups) {
+    gstrips[g] = 0;
+    return;
+  }
+  const uint32_t A = pa[gstart[g]];
+  gstrips[g] = (cfirst[A + 1] - cfirst[A] + kGT - 1) / kGT;
+}
+
+// Group starts of the pairs sorted by A (any order: groups are handed out by a cursor).
+__global__ void k_group_starts(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ gstart,
+                               unsigned long long* __restrict__ ngroups) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += gridDim.x * blockDim.x)
+    if (k == 0 || pa[k] != pa[k - 1]) gstart[atomicAdd(reinterpret_cast<unsigned*>(ngroups), 1u)] = k;
 }
 
 bool gram_shape(int d) { return d == 32 || d == 64; }
@@ -710,7 +768,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   const bool gram = gram_shape(d) && !no_gram;
   if (w.Xs.n != static_cast<size_t>(n) * d) w.Xs.alloc(static_cast<size_t>(n) * d, s);
   if (w.cbox.n < cells * 2 * nk) w.cbox.alloc(cells * 2 * nk, s);
-  if (w.ctr.n < 3) w.ctr.alloc(3, s);
+  if (w.ctr.n < 4) w.ctr.alloc(4, s);
   k_gather_rows<<<sms * 16, 256, 0, s>>>(X, gi.sidx.p, n, d, w.Xs.p);
   PSG_LAUNCHED();
   if (nk == 4)
@@ -732,7 +790,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
       w.pprefix.alloc(w.pair_cap + 1, s);
       w.stmp.alloc(scan_temp_words(w.pair_cap + 1), s);
     }
-    PSG_CUDA(cudaMemsetAsync(w.ctr.p, 0, 24, s));
+    PSG_CUDA(cudaMemsetAsync(w.ctr.p, 0, 32, s));
     if (nk == 4)
       k_cell_pairs<4><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
           gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
@@ -751,11 +809,35 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   PSG_CUDA(cudaMemsetAsync(w.ptiles.p + npairs, 0, 4, s));
   exclusive_scan_u32(w.ptiles.p, w.pprefix.p, npairs + 1, w.stmp.p, s);
   g_launches += 3;
-  if (gram && d == 32)
-    launch_gram<32>(a, w, gi, static_cast<uint32_t>(npairs), part, nparts, s);
-  else if (gram)
-    launch_gram<64>(a, w, gi, static_cast<uint32_t>(npairs), part, nparts, s);
-  else {
+  if (gram) {
+    // kept pairs grouped by A (stable: the own cell stays first in its group)
+    if (w.hist.n < radix_hist_words(w.pair_cap)) w.hist.alloc(radix_hist_words(w.pair_cap), s);
+    if (w.gstart.n < w.pair_cap) w.gstart.alloc(w.pair_cap, s);
+    uint32_t* kk[2] = {w.pa.p, w.ptiles.p};
+    uint32_t* vv[2] = {w.pb.p, w.pprefix.p};
+    int bits = 1;
+    while ((1ull << bits) < cells) ++bits;
+    const int which = radix_sort<uint32_t>(kk, vv, npairs, 0, ((bits + 7) / 8) * 8, w.hist.p, s);
+    PSG_CUDA(cudaMemsetAsync(w.ctr.p + 3, 0, 8, s));
+    k_group_starts<<<std::min<unsigned>(blocks(npairs, 256), 4096), 256, 0, s>>>(kk[which], static_cast<uint32_t>(npairs),
+                                                                                 w.gstart.p, w.ctr.p + 3);
+    PSG_LAUNCHED();
+    unsigned long long ng64 = 0;
+    PSG_CUDA(cudaMemcpyAsync(&ng64, w.ctr.p + 3, 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    const uint32_t ng = static_cast<uint32_t>(ng64);
+    if (w.gprefix.n < ng + 1) w.gprefix.alloc(ng + 1, s);
+    if (w.gstrips.n < ng + 1) w.gstrips.alloc(ng + 1, s);
+    if (w.gtmp.n < scan_temp_words(ng + 1)) w.gtmp.alloc(scan_temp_words(ng + 1), s);
+    k_group_strips<<<blocks(ng + 1, 256), 256, 0, s>>>(kk[which], w.gstart.p, ng, gi.cfirst.p, w.gstrips.p);
+    PSG_LAUNCHED();
+    exclusive_scan_u32(w.gstrips.p, w.gprefix.p, ng + 1, w.gtmp.p, s);
+    g_launches += 6 + (bits + 7) / 8;
+    if (d == 32)
+      launch_gram<32>(a, w, gi, kk[which], vv[which], static_cast<uint32_t>(npairs), part, nparts, s);
+    else
+      launch_gram<64>(a, w, gi, kk[which], vv[which], static_cast<uint32_t>(npairs), part, nparts, s);
+  } else {
     k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
                                           static_cast<uint32_t>(npairs), part, nparts, w.ctr.p + 1);
     PSG_LAUNCHED();

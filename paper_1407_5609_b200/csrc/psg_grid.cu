@@ -86,7 +86,22 @@ __global__ void __launch_bounds__(256) k_cfirst(const uint32_t* __restrict__ sce
       uint32_t res = 0;
       bool done = c > cend;  // lanes past the range have nothing to write
       uint32_t base = pos;
-      while (!__all_sync(kGridFull, done)) {
+      for (int win = 0; !__all_sync(kGridFull, done); ++win) {
+        if (win == 4) {  // dense cells: stop walking, each open lane binary-searches [base, n)
+          if (!done) {
+            uint32_t lo2 = base, hi2 = n;
+            while (lo2 < hi2) {
+              const uint32_t mid = (lo2 + hi2) >> 1;
+              if (scell[mid] < c)
+                lo2 = mid + 1;
+              else
+                hi2 = mid;
+            }
+            res = lo2;
+            done = true;
+          }
+          break;
+        }
         const uint32_t v = base + lane < n ? scell[base + lane] : 0xffffffffu;
         // r = #(window values < c); the window is ascending across lanes
         // (every shuffle is executed by all lanes: no shuffle under a branch)
