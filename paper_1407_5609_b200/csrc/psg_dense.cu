@@ -14,7 +14,9 @@
 //      thread — the all-pairs kernel's arithmetic and order) from rows
 //      gathered into grid order, recording the band into the candidate list.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <cmath>
 
 #include "psg_dense.cuh"
@@ -341,12 +343,13 @@ __global__ void __launch_bounds__(256) k_dense_tiles(ScanArgs a, const float* __
 // pairs: tiles tj >= ti); strips are taken from a global cursor.
 constexpr int kGT = 128;  // A tile rows (UMMA M)
 constexpr int kGN = 128;       // B tile rows (UMMA N)
-constexpr int kGAB = 1;        // A buffers (hi + lo)
-constexpr int kGBB = 2;        // B buffers (hi + lo)
+constexpr int kGAB = 1;        // A buffers (hi + lo, in TMEM)
+constexpr int kGBB = 3;        // B buffers (hi + lo, in shared memory)
 constexpr int kMaxPartners = 366;  // the own cell + the (3^6 - 1)/2 forward stencil cells
 constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM, 8-15 epilogue
 constexpr int kGEpi = 8;        // epilogue warps: two per TMEM lane quarter, 64 columns each
-constexpr uint32_t kGTmemCols = 2 * kGN;  // 2 accumulators x kGN columns
+constexpr uint32_t kGTmemCols = 512;   // [0, 256) 2 accumulators; [256, 256 + 2D) the A tile, hi | lo
+constexpr uint32_t kGAcol = 2 * kGN;
 
 // Slack of the filter value per unit of (|a'|^2 + |b'|^2):
 // the 3xTF32 product (hi.hi + hi.lo + lo.hi) misses lo.lo and the TF32
@@ -365,8 +368,7 @@ struct GramMeta {
 
 template <int D>
 struct GramSmem {
-  float A[kGAB][2][kGT * D];  // [hi|lo] x D/32 chunks of 128 rows x 128 B (SW128 K-major)
-  float B[kGBB][2][kGN * D];
+  float B[kGBB][2][kGN * D];  // [hi|lo] x D/32 chunks of 128 rows x 128 B (SW128 K-major); A lives in TMEM
   float na[kGBB][kGT];  // the strip's A-row norms, copied with every B tile (released with it by the epilogue)
   float nb[kGBB][kGN];
   float cnb[kGBB][kGN];  // (1 - 2 slack) nb, +inf past the tile's length: the epilogue's fast test
@@ -517,10 +519,43 @@ __global__ void __launch_bounds__(kGThreads, 1)
         const uint32_t ab = scount % kGAB, aph = (scount / kGAB) & 1;
         ++scount;
         mbar_wait(&sm.afree[ab], aph ^ 1);
+        tc_fence_after();  // the previous strip's MMAs have read the A tile
         const uint32_t npar = (scount - 1) & 1;
-        const float na_r =
-            gram_load_row<D, kGT, 0, D / 32>(Xs, a0 + r, static_cast<uint32_t>(r) < alen, mu, sm.A[ab][0], sm.A[ab][1], r);
-        fence_proxy_async();
+        // the A tile goes to TMEM (the MMAs take A from there): row r = TMEM
+        // lane r, hi in columns kGAcol + [0, D), lo in kGAcol + D + [0, D)
+        float na_r = 0.f;
+        {
+          const bool va = static_cast<uint32_t>(r) < alen;
+          const float4* src = reinterpret_cast<const float4*>(Xs + static_cast<size_t>(a0 + (va ? r : 0)) * D);
+          const uint32_t lane_base = tmem + ((32u * warp) << 16) + kGAcol;
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 v = va ? __ldg(src + c * 8 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+              const int t = c * 32 + q * 4;
+              if (va) {
+                v.x -= mu[t];
+                v.y -= mu[t + 1];
+                v.z -= mu[t + 2];
+                v.w -= mu[t + 3];
+              }
+              const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int w2 = 0; w2 < 4; ++w2) {
+                na_r = fmaf(x[w2], x[w2], na_r);
+                const uint32_t h = __float_as_uint(x[w2]) & ~0x1fffu;
+                hi[q * 4 + w2] = h;
+                lo[q * 4 + w2] = __float_as_uint(x[w2] - __uint_as_float(h));  // exact
+              }
+            }
+            tmem_st32(lane_base + c * 32, hi);
+            tmem_st32(lane_base + D + c * 32, lo);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.afull[ab]);
         for (uint32_t tj = 0; tj < tb; ++tj) {
@@ -563,6 +598,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   } else if (warp == 4) {  // ---- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(kGT, kGN);
+      unsigned long long ntiles = 0;
       uint32_t bcount = 0, tcount = 0, scount = 0;
       bool need_a = true;
       for (;;) {
@@ -573,6 +609,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         const GramMeta m = sm.meta[bb];  // published before the barrier arrive
         if (m.done) {
           mbar_arrive(&sm.tfull[acc]);
+          atomicAdd(cursor + 1, ntiles);  // ctr[2]: tiles issued (profiling)
           break;
         }
         if (need_a) {  // first tile of a strip: its A buffer is filled
@@ -584,19 +621,19 @@ __global__ void __launch_bounds__(kGThreads, 1)
         tc_fence_after();
         const uint32_t dcol = tmem + acc * kGN;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {  // 3xTF32: hi.hi + hi.lo + lo.hi
-          const uint64_t ah = sw128_desc(smem_u32(sm.A[m.abuf][0] + c * (kGT * 32)));
-          const uint64_t al = sw128_desc(smem_u32(sm.A[m.abuf][1] + c * (kGT * 32)));
+        for (int c = 0; c < NC; ++c) {  // 3xTF32: hi.hi + hi.lo + lo.hi; A from TMEM, B from smem
+          const uint32_t ah = tmem + kGAcol + c * 32, al = tmem + kGAcol + D + c * 32;
           const uint64_t bh = sw128_desc(smem_u32(sm.B[bb][0] + c * (kGN * 32)));
           const uint64_t bl = sw128_desc(smem_u32(sm.B[bb][1] + c * (kGN * 32)));
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            umma_tf32_ss(dcol, ah + 2 * k, bh + 2 * k, idesc, (c | k) != 0);
-            umma_tf32_ss(dcol, ah + 2 * k, bl + 2 * k, idesc, 1);
-            umma_tf32_ss(dcol, al + 2 * k, bh + 2 * k, idesc, 1);
+            umma_tf32_ts(dcol, ah + 8 * k, bh + 2 * k, idesc, (c | k) != 0);
+            umma_tf32_ts(dcol, ah + 8 * k, bl + 2 * k, idesc, 1);
+            umma_tf32_ts(dcol, al + 8 * k, bh + 2 * k, idesc, 1);
           }
         }
         umma_commit(&sm.tfull[acc]);
+        ++ntiles;
         if (m.last) {  // the strip's A tile is free once these MMAs have read it
           umma_commit(&sm.afree[m.abuf]);
           need_a = true;
@@ -614,15 +651,27 @@ __global__ void __launch_bounds__(kGThreads, 1)
     constexpr float g2 = 2.f * gram_slack<D>();
     uint32_t bcount = 0, tcount = 0;
     unsigned long long visited = 0, evals = 0;
+    unsigned band_bits = 0xffffffffu;
+    float band_c = 0.f;
     for (;;) {
       const uint32_t bb = bcount % kGBB, acc = tcount & 1, tph = (tcount >> 1) & 1;
       mbar_wait(&sm.tfull[acc], tph);
       tc_fence_after();
       const GramMeta m = sm.meta[bb];
       if (m.done) break;
-      float band = 0.f;
-      if (lane == 0) band = budget_thresholds_s32(*a.bud, best_now(a.best)).band;
-      band = __shfl_sync(kFull, band, 0);
+      // the band from the current bound, recomputed (FP64) only when the bound moved
+      {
+        unsigned cur = 0;
+        if (lane == 0) cur = *reinterpret_cast<const volatile unsigned*>(a.best);
+        cur = __shfl_sync(kFull, cur, 0);
+        if (cur != band_bits) {
+          float b = 0.f;
+          if (lane == 0) b = budget_thresholds_s32(*a.bud, __uint_as_float(cur)).band;
+          band_c = __shfl_sync(kFull, b, 0);
+          band_bits = cur;
+        }
+      }
+      const float band = band_c;
       const bool vr = r < m.alen;
       const uint32_t i = m.a0 + r;
       const float na = sm.na[bb][r];
@@ -715,8 +764,15 @@ void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, con
   constexpr size_t kSmem = sizeof(GramSmem<D>) + 1024;
   static bool configured = false;
   if (!configured) {
-    PSG_CUDA(cudaFuncSetAttribute(k_dense_gram<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmem)));
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_dense_gram<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, k_dense_gram<D>);
+      throw cuda_error("k_dense_gram: dynamic smem " + std::to_string(kSmem) + " refused (" + cudaGetErrorString(e) +
+                       "); static " + std::to_string(fa.sharedSizeBytes) + ", regs " + std::to_string(fa.numRegs) +
+                       ", max threads " + std::to_string(fa.maxThreadsPerBlock));
+    }
     configured = true;
   }
   k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.cfirst.p, pa, pb, w.gstart.p,
@@ -837,6 +893,13 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
       launch_gram<32>(a, w, gi, kk[which], vv[which], static_cast<uint32_t>(npairs), part, nparts, s);
     else
       launch_gram<64>(a, w, gi, kk[which], vv[which], static_cast<uint32_t>(npairs), part, nparts, s);
+    if (std::getenv("PSG_TRACE")) {
+      unsigned long long t = 0;
+      PSG_CUDA(cudaMemcpyAsync(&t, w.ctr.p + 2, 8, cudaMemcpyDeviceToHost, s));
+      PSG_CUDA(cudaStreamSynchronize(s));
+      std::fprintf(stderr, "[psg] gram: %llu kept cell pairs, %u groups, %llu tiles\n",
+                   static_cast<unsigned long long>(npairs), ng, t);
+    }
   } else {
     k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
                                           static_cast<uint32_t>(npairs), part, nparts, w.ctr.p + 1);
