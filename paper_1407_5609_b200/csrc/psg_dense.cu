@@ -794,11 +794,31 @@ __global__ void k_group_strips(const uint32_t* __restrict__ pa, const uint32_t* 
   gstrips[g] = (cfirst[A + 1] - cfirst[A] + kGT - 1) / kGT;
 }
 
-// Group starts of the pairs sorted by A (any order: groups are handed out by a cursor).
-__global__ void k_group_starts(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ gstart,
-                               unsigned long long* __restrict__ ngroups) {
+// Group flags of the pairs sorted by A: flags[k] = 1 at the first pair of a group
+// (flags[npairs] = 0); after an exclusive scan, the group index of its first pair.
+__global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ flags) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= npairs; k += gridDim.x * blockDim.x)
+    flags[k] = k < npairs && (k == 0 || pa[k] != pa[k - 1]);
+}
+
+__global__ void k_group_scatter(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ gidx, uint32_t npairs,
+                                uint32_t* __restrict__ gstart) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += gridDim.x * blockDim.x)
-    if (k == 0 || pa[k] != pa[k - 1]) gstart[atomicAdd(reinterpret_cast<unsigned*>(ngroups), 1u)] = k;
+    if (flags[k]) gstart[gidx[k]] = k;
+}
+
+// CUDA-core tiles per sorted pair (self pairs: the upper triangle of tiles).
+__global__ void k_pair_tiles(const uint32_t* __restrict__ pa, const uint32_t* __restrict__ pb, uint32_t npairs,
+                             const uint32_t* __restrict__ cfirst, uint32_t* __restrict__ pt) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= npairs; k += gridDim.x * blockDim.x) {
+    if (k == npairs) {
+      pt[k] = 0;
+      continue;
+    }
+    const uint32_t A = pa[k], B = pb[k];
+    const uint32_t ta = (cfirst[A + 1] - cfirst[A] + kT - 1) / kT, tb = (cfirst[B + 1] - cfirst[B] + kT - 1) / kT;
+    pt[k] = A == B ? ta * (ta + 1) / 2 : ta * tb;
+  }
 }
 
 bool gram_shape(int d) { return d == 32 || d == 64; }
@@ -840,8 +860,8 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   unsigned long long npairs = 0;
   for (;;) {
     if (w.pa.n < w.pair_cap) {
-      w.pa.alloc(w.pair_cap, s);
-      w.pb.alloc(w.pair_cap, s);
+      w.pa.alloc(w.pair_cap + 1, s);
+      w.pb.alloc(w.pair_cap + 1, s);
       w.ptiles.alloc(w.pair_cap + 1, s);
       w.pprefix.alloc(w.pair_cap + 1, s);
       w.stmp.alloc(scan_temp_words(w.pair_cap + 1), s);
@@ -861,38 +881,46 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     w.pair_cap = static_cast<uint32_t>(npairs);
   }
   if (npairs == 0) return 0;
-  // tile prefix over the kept pairs (ptiles[npairs] = 0 so prefix[npairs] = total)
-  PSG_CUDA(cudaMemsetAsync(w.ptiles.p + npairs, 0, 4, s));
-  exclusive_scan_u32(w.ptiles.p, w.pprefix.p, npairs + 1, w.stmp.p, s);
-  g_launches += 3;
+  const uint32_t np32 = static_cast<uint32_t>(npairs);
+  // Deterministic work order: every rank of a sharded solve enumerates the
+  // same pairs / strips, so the round-robin split covers each exactly once.
+  // Stable sort by A; within an A the appending thread's stencil order (the
+  // own cell first).  Sorted pairs land in (spa, spb); the other two arrays
+  // are scratch.
+  if (w.hist.n < radix_hist_words(w.pair_cap)) w.hist.alloc(radix_hist_words(w.pair_cap), s);
+  uint32_t* kk[2] = {w.pa.p, w.ptiles.p};
+  uint32_t* vv[2] = {w.pb.p, w.pprefix.p};
+  int bits = 1;
+  while ((1ull << bits) < cells) ++bits;
+  const int which = radix_sort<uint32_t>(kk, vv, npairs, 0, ((bits + 7) / 8) * 8, w.hist.p, s);
+  const uint32_t* spa = kk[which];
+  const uint32_t* spb = vv[which];
+  uint32_t* scr0 = kk[which ^ 1];  // npairs + 1 entries each
+  uint32_t* scr1 = vv[which ^ 1];
+  g_launches += 1 + (bits + 7) / 8;
   if (gram) {
-    // kept pairs grouped by A (stable: the own cell stays first in its group)
-    if (w.hist.n < radix_hist_words(w.pair_cap)) w.hist.alloc(radix_hist_words(w.pair_cap), s);
-    if (w.gstart.n < w.pair_cap) w.gstart.alloc(w.pair_cap, s);
-    uint32_t* kk[2] = {w.pa.p, w.ptiles.p};
-    uint32_t* vv[2] = {w.pb.p, w.pprefix.p};
-    int bits = 1;
-    while ((1ull << bits) < cells) ++bits;
-    const int which = radix_sort<uint32_t>(kk, vv, npairs, 0, ((bits + 7) / 8) * 8, w.hist.p, s);
-    PSG_CUDA(cudaMemsetAsync(w.ctr.p + 3, 0, 8, s));
-    k_group_starts<<<std::min<unsigned>(blocks(npairs, 256), 4096), 256, 0, s>>>(kk[which], static_cast<uint32_t>(npairs),
-                                                                                 w.gstart.p, w.ctr.p + 3);
+    // groups (a cell A and its kept partners), in pair order
+    k_group_flags<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, np32, scr0);
     PSG_LAUNCHED();
-    unsigned long long ng64 = 0;
-    PSG_CUDA(cudaMemcpyAsync(&ng64, w.ctr.p + 3, 8, cudaMemcpyDeviceToHost, s));
+    exclusive_scan_u32(scr0, scr1, npairs + 1, w.stmp.p, s);
+    uint32_t ng = 0;
+    PSG_CUDA(cudaMemcpyAsync(&ng, scr1 + npairs, 4, cudaMemcpyDeviceToHost, s));
+    if (w.gstart.n < w.pair_cap + 1) w.gstart.alloc(w.pair_cap + 1, s);
+    k_group_scatter<<<std::min<unsigned>(blocks(npairs, 256), 4096), 256, 0, s>>>(scr0, scr1, np32, w.gstart.p);
+    PSG_LAUNCHED();
     PSG_CUDA(cudaStreamSynchronize(s));
-    const uint32_t ng = static_cast<uint32_t>(ng64);
+    PSG_CUDA(cudaMemcpyAsync(w.ctr.p + 3, &ng, 4, cudaMemcpyHostToDevice, s));
     if (w.gprefix.n < ng + 1) w.gprefix.alloc(ng + 1, s);
     if (w.gstrips.n < ng + 1) w.gstrips.alloc(ng + 1, s);
     if (w.gtmp.n < scan_temp_words(ng + 1)) w.gtmp.alloc(scan_temp_words(ng + 1), s);
-    k_group_strips<<<blocks(ng + 1, 256), 256, 0, s>>>(kk[which], w.gstart.p, ng, gi.cfirst.p, w.gstrips.p);
+    k_group_strips<<<blocks(ng + 1, 256), 256, 0, s>>>(spa, w.gstart.p, ng, gi.cfirst.p, w.gstrips.p);
     PSG_LAUNCHED();
     exclusive_scan_u32(w.gstrips.p, w.gprefix.p, ng + 1, w.gtmp.p, s);
-    g_launches += 6 + (bits + 7) / 8;
+    g_launches += 9;
     if (d == 32)
-      launch_gram<32>(a, w, gi, kk[which], vv[which], static_cast<uint32_t>(npairs), part, nparts, s);
+      launch_gram<32>(a, w, gi, spa, spb, np32, part, nparts, s);
     else
-      launch_gram<64>(a, w, gi, kk[which], vv[which], static_cast<uint32_t>(npairs), part, nparts, s);
+      launch_gram<64>(a, w, gi, spa, spb, np32, part, nparts, s);
     if (std::getenv("PSG_TRACE")) {
       unsigned long long t = 0;
       PSG_CUDA(cudaMemcpyAsync(&t, w.ctr.p + 2, 8, cudaMemcpyDeviceToHost, s));
@@ -901,8 +929,12 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
                    static_cast<unsigned long long>(npairs), ng, t);
     }
   } else {
-    k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, w.pa.p, w.pb.p, w.pprefix.p,
-                                          static_cast<uint32_t>(npairs), part, nparts, w.ctr.p + 1);
+    // tiles per sorted pair -> prefix (scr0[npairs] = 0 so prefix[npairs] = total)
+    k_pair_tiles<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, spb, np32, gi.cfirst.p, scr0);
+    PSG_LAUNCHED();
+    exclusive_scan_u32(scr0, scr1, npairs + 1, w.stmp.p, s);
+    g_launches += 4;
+    k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, spa, spb, scr1, np32, part, nparts, w.ctr.p + 1);
     PSG_LAUNCHED();
   }
   ++g_launches;

@@ -1,0 +1,50 @@
+"""GPU: the key-range sharded solve (psg_cpp_plan_*, paper_1407_5609_b200/
+sharded.py) with W parts run on one device, one point set per emulated rank
+(every rank of a real run owns its copy), combined exactly as the NCCL path
+combines them: the bound is the MIN over parts' bootstraps, the answer the
+lexicographic minimum of the parts' results.  Must equal the single solve and
+the brute force, for the grid engine, the window-z-norm motif and the dense
+cell-pair engine (clustered data, tensor-core Gram tiles, strips round-robin
+over parts)."""
+import numpy as np
+import pytest
+
+from paper_1407_5609_b200 import sharded
+
+pytestmark = pytest.mark.gpu
+
+
+def run_parts(psg, make_points, world, q=10, f=10.0, seed=1, zone=0):
+    sets = [make_points() for _ in range(world)]
+    plans = [sharded.DevicePlan(ps._device(), q, f, seed, zone) for ps in sets]
+    bound = min(plans[r].bootstrap(r, world) for r in range(world))
+    parts = [plans[r].scan(r, world, bound) for r in range(world)]
+    n = sets[0].size()
+    return sharded.combine(parts, sharded.admissible_pairs(n, zone))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gauss_planted(psg, world):
+    pts, planted = psg.gen.gauss_planted(2, 60_000, 128)
+    got = run_parts(psg, lambda: psg.PointSet.from_flat(pts, 128), world)
+    one = psg.closest_pair(psg.PointSet.from_flat(pts, 128), 10, 10.0, 1, 0)
+    assert (got.index_i, got.index_j, got.distance) == (one.index_i, one.index_j, one.distance)
+    assert (got.index_i, got.index_j) == tuple(sorted(planted))
+    assert got.stats.admissible_pairs() == 60_000 * 59_999 // 2
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_dense_engine(psg, world):
+    pts = psg.gen.mixture(5, 1 << 17, 64, 1024, 0.05)
+    got = run_parts(psg, lambda: psg.PointSet.from_flat(pts, 64), world)
+    ps = psg.PointSet.from_flat(pts, 64)
+    bf = psg.brute_force_closest_pair(ps, 0)
+    assert (got.index_i, got.index_j, got.distance) == (bf.index_i, bf.index_j, bf.distance)
+
+
+def test_sharded_motif_windows(psg):
+    s, (a, b) = psg.gen.walk_motif(3, 50_000, 64)
+    series = s.astype(np.float64)
+    got = run_parts(psg, lambda: psg.PointSet.windows_of(series, 64, znorm=True), 2, zone=64)
+    one = psg.closest_pair(psg.PointSet.windows_of(series, 64, znorm=True), 10, 10.0, 1, 64)
+    assert (got.index_i, got.index_j, got.distance) == (one.index_i, one.index_j, one.distance)
