@@ -42,6 +42,16 @@ def test_sharded_dense_engine(psg, world):
     assert (got.index_i, got.index_j, got.distance) == (bf.index_i, bf.index_j, bf.distance)
 
 
+@pytest.mark.parametrize("d,clusters", [(16, 16), (128, 64)])
+def test_sharded_dense_cuda_core_tiles(psg, d, clusters):
+    # d outside {32, 64}: the dense engine's CUDA-core tiles, tiles round-robin over parts
+    pts = psg.gen.mixture(6, 1 << 17, d, clusters, 0.05)
+    got = run_parts(psg, lambda: psg.PointSet.from_flat(pts, d), 3)
+    assert "dense grid" in psg.last_profile()["stages"]  # the last part went through the dense engine
+    bf = psg.brute_force_closest_pair(psg.PointSet.from_flat(pts, d), 0)
+    assert (got.index_i, got.index_j, got.distance) == (bf.index_i, bf.index_j, bf.distance)
+
+
 def test_sharded_motif_windows(psg):
     s, (a, b) = psg.gen.walk_motif(3, 50_000, 64)
     series = s.astype(np.float64)
