@@ -164,6 +164,9 @@ int psg_closest_pair_ps(psg_pointset* ps, uint64_t q, double f, uint64_t seed, u
 int psg_brute_force_closest_pair_ps(psg_pointset* ps, uint64_t exclusion_zone, psg_pair_result* out);
 int psg_fixed_radius_neighbors_ps(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed,
                                   uint64_t exclusion_zone, int want_lists, psg_neighbor_result* out);
+/* brute_force_neighbors (refscan.cpp:211-227) over a device point set. */
+int psg_brute_force_neighbors_ps(psg_pointset* ps, double radius, uint64_t exclusion_zone, int want_lists,
+                                 psg_neighbor_result* out);
 
 /* ---- key-range sharding across ranks (one process per GPU) --------------
  * plan_create projects + sorts (identical on every rank); bootstrap returns a

@@ -269,6 +269,10 @@ class Reference:
             L.ref_load_series.argtypes = [C.c_char_p, _p, _p]
             L.ref_save_series.argtypes = [_p, _u64, C.c_char_p]
             L.ref_free.argtypes = [_p]
+        if hasattr(L, "ref_report_render"):
+            L.ref_report_render.argtypes = [C.c_char_p] * 3 + [_u64, _u64, _f64, _u64, _u64, _f64, _u64, _p, _p]
+            L.ref_derive_seed3.restype = _u64
+            L.ref_derive_seed3.argtypes = [_u64, _u64, _u64]
         L.ref_euclidean.restype = _f64
         L.ref_euclidean.argtypes = [_p, _p, _u64]
         L.ref_euclidean_early_abandon.argtypes = [_p, _p, _u64, _f64, _p]
@@ -342,6 +346,21 @@ class Reference:
         vals = np.ctypeslib.as_array(C.cast(out, C.POINTER(C.c_double)), shape=(n.value,)).copy()
         self.lib.ref_free(out)
         return vals, 0, ""
+
+    def report(self, algorithm, params, dataset, i1, i2, dom, examined, iterations, wall, seed):
+        """io.cpp report_to_json / reports_to_csv of one Report: (json, csv)."""
+        j, c = C.c_void_p(), C.c_void_p()
+        rc = self.lib.ref_report_render(algorithm.encode(), params.encode(), dataset.encode(), i1, i2, dom, examined,
+                                        iterations, wall, seed, C.byref(j), C.byref(c))
+        if rc != 0:
+            self._err()
+        out = (C.string_at(j).decode(), C.string_at(c).decode())
+        self.lib.ref_free(j)
+        self.lib.ref_free(c)
+        return out
+
+    def derive_seed3(self, base, s1, s2):
+        return self.lib.ref_derive_seed3(base, s1, s2)
 
     def save_series(self, values, path: str) -> None:
         v = np.ascontiguousarray(values, dtype=np.float64)

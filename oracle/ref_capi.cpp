@@ -209,4 +209,29 @@ int ref_save_series(const double* v, uint64_t n, const char* path) {
 
 void ref_free(void* p) { std::free(p); }
 
+// io.cpp:177-225: one Report rendered as JSON (report_to_json) and CSV
+// (reports_to_csv); both strings malloc'd.
+int ref_report_render(const char* algorithm, const char* params, const char* dataset, uint64_t i1, uint64_t i2,
+                      double dom, uint64_t examined, uint64_t iterations, double wall, uint64_t seed, char** json,
+                      char** csv) {
+  return guarded([&] {
+    Report r;
+    r.algorithm = algorithm;
+    r.params = params;
+    r.dataset = dataset;
+    r.pair_index_1 = i1;
+    r.pair_index_2 = i2;
+    r.distance_or_matches = dom;
+    r.pairs_examined = examined;
+    r.iterations = iterations;
+    r.wall_seconds = wall;
+    r.seed = seed;
+    const std::string j = report_to_json(r), c = reports_to_csv({r});
+    *json = strdup(j.c_str());
+    *csv = strdup(c.c_str());
+  });
+}
+
+uint64_t ref_derive_seed3(uint64_t base, uint64_t s1, uint64_t s2) { return derive_seed(base, s1, s2); }
+
 }  // extern "C"

@@ -303,6 +303,13 @@ int psg_closest_pair_ps(psg_pointset* ps, uint64_t q, double f, uint64_t seed, u
 int psg_brute_force_closest_pair_ps(psg_pointset* ps, uint64_t exclusion_zone, psg_pair_result* out) {
   return guarded([&] { *out = psg::brute_solve(ps, exclusion_zone); });
 }
+int psg_brute_force_neighbors_ps(psg_pointset* ps, double radius, uint64_t exclusion_zone, int want_lists,
+                                 psg_neighbor_result* out) {
+  return guarded([&] {
+    if (ps->n == 0) throw psg::invalid_argument("empty input");  // refscan.cpp:214
+    psg::brute_neighbors(ps, radius, exclusion_zone, want_lists != 0, out);
+  });
+}
 int psg_fixed_radius_neighbors_ps(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed,
                                   uint64_t exclusion_zone, int want_lists, psg_neighbor_result* out) {
   return guarded([&] { psg::frnn_solve(ps, radius, q, f, seed, exclusion_zone, want_lists != 0, out); });
