@@ -595,52 +595,50 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
       }
     }
-  } else if (warp == 4) {  // ---- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(kGT, kGN);
-      unsigned long long ntiles = 0;
-      uint32_t bcount = 0, tcount = 0, scount = 0;
-      bool need_a = true;
-      for (;;) {
-        const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
-        mbar_wait(&sm.bfull[bb], bph);
-        const uint32_t acc = tcount & 1, tph = (tcount >> 1) & 1;
-        mbar_wait(&sm.tempty[acc], tph ^ 1);
-        const GramMeta m = sm.meta[bb];  // published before the barrier arrive
-        if (m.done) {
+  } else if (warp == 4) {
+    // ---- MMA issuer: the whole warp runs the loop (uniform registers), one
+    // elected lane issues the MMAs and their commits
+    constexpr uint32_t idesc = idesc_tf32(kGT, kGN);
+    unsigned long long ntiles = 0;
+    uint32_t bcount = 0, tcount = 0, scount = 0;
+    bool need_a = true;
+    for (;;) {
+      const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+      mbar_wait(&sm.bfull[bb], bph);
+      const uint32_t acc = tcount & 1, tph = (tcount >> 1) & 1;
+      mbar_wait(&sm.tempty[acc], tph ^ 1);
+      const GramMeta m = sm.meta[bb];  // published before the barrier arrive
+      if (m.done) {
+        if (lane == 0) {
           mbar_arrive(&sm.tfull[acc]);
           atomicAdd(cursor + 1, ntiles);  // ctr[2]: tiles issued (profiling)
-          break;
         }
-        if (need_a) {  // first tile of a strip: its A buffer is filled
-          const uint32_t aph = (scount / kGAB) & 1;
-          mbar_wait(&sm.afull[m.abuf], aph);
-          ++scount;
-          need_a = false;
-        }
-        tc_fence_after();
-        const uint32_t dcol = tmem + acc * kGN;
+        break;
+      }
+      if (need_a) {  // first tile of a strip: its A buffer is filled
+        const uint32_t aph = (scount / kGAB) & 1;
+        mbar_wait(&sm.afull[m.abuf], aph);
+        ++scount;
+        need_a = false;
+      }
+      tc_fence_after();
+      const uint32_t dcol = tmem + acc * kGN;
+      if (elect_one()) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {  // 3xTF32: hi.hi + hi.lo + lo.hi; A from TMEM, B from smem
           const uint32_t ah = tmem + kGAcol + c * 32, al = tmem + kGAcol + D + c * 32;
           const uint64_t bh = sw128_desc(smem_u32(sm.B[bb][0] + c * (kGN * 32)));
           const uint64_t bl = sw128_desc(smem_u32(sm.B[bb][1] + c * (kGN * 32)));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            umma_tf32_ts(dcol, ah + 8 * k, bh + 2 * k, idesc, (c | k) != 0);
-            umma_tf32_ts(dcol, ah + 8 * k, bl + 2 * k, idesc, 1);
-            umma_tf32_ts(dcol, al + 8 * k, bh + 2 * k, idesc, 1);
-          }
+          umma_tf32_ts_3x_chunk32(dcol, ah, al, bh, bl, idesc, c != 0);
         }
         umma_commit(&sm.tfull[acc]);
-        ++ntiles;
-        if (m.last) {  // the strip's A tile is free once these MMAs have read it
-          umma_commit(&sm.afree[m.abuf]);
-          need_a = true;
-        }
-        ++bcount;
-        ++tcount;
+        if (m.last) umma_commit(&sm.afree[m.abuf]);  // the strip's A tile is free once these MMAs have read it
       }
+      __syncwarp();
+      ++ntiles;
+      if (m.last) need_a = true;
+      ++bcount;
+      ++tcount;
     }
   } else if (warp >= 8) {
     // ---- epilogue: warp w owns TMEM lanes (A rows) 32 (w%4) .. +31 and the

@@ -175,33 +175,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (lane == 0) mbar_arrive(tready + slot);
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
-      uint32_t slot = 0, sphase = 0, it = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const uint32_t acc = it & 1, aphase = (it >> 1) & 1;
-        mbar_wait(tempty + acc, aphase ^ 1);  // the epilogue has drained this accumulator
+    // MMA issuer: the whole warp runs the loop (addresses stay in uniform
+    // registers), one elected lane issues the MMAs and their commits
+    uint32_t slot = 0, sphase = 0, it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const uint32_t acc = it & 1, aphase = (it >> 1) & 1;
+      mbar_wait(tempty + acc, aphase ^ 1);  // the epilogue has drained this accumulator
+      tc_fence_after();
+      const uint32_t dcol = tmem + acc * 2 * kTcN;  // two chains of 16 columns
+      for (int c = 0; c < NC; ++c) {
+        mbar_wait(tready + slot, sphase);  // hi | lo of this chunk are in TMEM
         tc_fence_after();
-        const uint32_t dcol = tmem + acc * 2 * kTcN;  // two chains of 16 columns
-        for (int c = 0; c < NC; ++c) {
-          mbar_wait(tready + slot, sphase);  // hi | lo of this chunk are in TMEM
-          tc_fence_after();
-          const uint32_t a = tmem + kSlotBase + slot * 64;
-          const uint64_t bd = sw128_desc(smem_u32(sb + c * kBChunkBytes));
-          // hi products accumulate in chain 0, lo products in chain 1 (adjacent
-          // MMAs are independent, so the tensor pipe overlaps them)
-#pragma unroll
-          for (int k = 0; k < kTcKChunk / 8; ++k) {
-            umma_tf32_ts(dcol, a + 8 * k, bd + 2 * k, kIdesc, (c | k) != 0);
-            umma_tf32_ts(dcol + kTcN, a + 32 + 8 * k, bd + 2 * k, kIdesc, (c | k) != 0);
-          }
+        const uint32_t a = tmem + kSlotBase + slot * 64;
+        const uint64_t bd = sw128_desc(smem_u32(sb + c * kBChunkBytes));
+        // hi products accumulate in chain 0, lo products in chain 1 (adjacent
+        // MMAs are independent, so the tensor pipe overlaps them)
+        static_assert(kTcKChunk == 32 && kTcN == 16, "umma_tf32_ts_chunk32 layout");
+        if (elect_one()) {
+          umma_tf32_ts_chunk32(dcol, a, bd, kIdesc, c != 0);
           umma_commit(tslot + slot);  // slot reusable once these MMAs have read it
-          if (++slot == kTcSlots) {
-            slot = 0;
-            sphase ^= 1;
-          }
         }
-        umma_commit(tfull + acc);  // accumulator complete
+        __syncwarp();
+        if (++slot == kTcSlots) {
+          slot = 0;
+          sphase ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(tfull + acc);  // accumulator complete
+      __syncwarp();
     }
   } else if (warp >= 8) {  // epilogue: warp (8 + e) owns TMEM lanes 32e .. 32e+31
     const uint32_t e = warp - 8;

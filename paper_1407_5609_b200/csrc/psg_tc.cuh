@@ -72,6 +72,100 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, u
       : "memory");
 }
 
+// One lane of a fully active warp (the lowest), chosen by elect.sync: lets a
+// whole warp run the issue loop in uniform registers while one lane issues.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// One 32-float K chunk of the split projection as a single asm block (the
+// per-instruction operand moves are hoisted): hi products into chain d0 from
+// TMEM A columns a + 8k, lo products into chain d0 + 16 from a + 32 + 8k,
+// against B descriptors bd + 2k (k = 0..3; SW128 K-major rows of 128 B).
+// The first MMA pair accumulates only when `accumulate` != 0.
+__device__ __forceinline__ void umma_tf32_ts_chunk32(uint32_t d0, uint32_t a, uint64_t bd, uint32_t idesc,
+                                                     uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .b32 d1, a1, a2, a3, a4, a5, a6, a7;\n\t"
+      ".reg .b64 b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %4, %4;\n\t"
+      "add.u32 d1, %0, 16;\n\t"
+      "add.u32 a1, %1, 8;\n\t"
+      "add.u32 a2, %1, 16;\n\t"
+      "add.u32 a3, %1, 24;\n\t"
+      "add.u32 a4, %1, 32;\n\t"
+      "add.u32 a5, %1, 40;\n\t"
+      "add.u32 a6, %1, 48;\n\t"
+      "add.u32 a7, %1, 56;\n\t"
+      "add.u64 b1, %2, 2;\n\t"
+      "add.u64 b2, %2, 4;\n\t"
+      "add.u64 b3, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], [a4], %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], b1, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], [a5], b1, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], b2, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], [a6], b2, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], b3, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], [a7], b3, %3, q;\n\t"
+      "}" ::"r"(d0),
+      "r"(a), "l"(bd), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 3xTF32 over one 32-float K chunk into one accumulator d: for k = 0..3,
+// hi.hi + hi.lo + lo.hi with A hi / lo from TMEM columns ah + 8k / al + 8k and
+// B hi / lo descriptors bh + 2k / bl + 2k.  The first MMA accumulates only when
+// `accumulate` != 0.
+__device__ __forceinline__ void umma_tf32_ts_3x_chunk32(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh,
+                                                        uint64_t bl, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .b32 h1, h2, h3, l1, l2, l3;\n\t"
+      ".reg .b64 bh1, bh2, bh3, bl1, bl2, bl3;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 q, %6, %6;\n\t"
+      "add.u32 h1, %1, 8;\n\t"
+      "add.u32 h2, %1, 16;\n\t"
+      "add.u32 h3, %1, 24;\n\t"
+      "add.u32 l1, %2, 8;\n\t"
+      "add.u32 l2, %2, 16;\n\t"
+      "add.u32 l3, %2, 24;\n\t"
+      "add.u64 bh1, %3, 2;\n\t"
+      "add.u64 bh2, %3, 4;\n\t"
+      "add.u64 bh3, %3, 6;\n\t"
+      "add.u64 bl1, %4, 2;\n\t"
+      "add.u64 bl2, %4, 4;\n\t"
+      "add.u64 bl3, %4, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [h1], bh1, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [h1], bl1, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [l1], bh1, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [h2], bh2, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [h2], bl2, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [l2], bh2, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [h3], bh3, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [h3], bl3, %5, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [l3], bh3, %5, q;\n\t"
+      "}" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
