@@ -346,7 +346,7 @@ constexpr int kGN = 128;       // B tile rows (UMMA N)
 constexpr int kGAB = 1;        // A buffers (hi + lo, in TMEM)
 constexpr int kGBB = 3;        // B buffers (hi + lo, in shared memory)
 constexpr int kMaxPartners = 366;  // the own cell + the (3^6 - 1)/2 forward stencil cells
-constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM, 8-15 epilogue
+constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM + strip scheduler, 8-15 epilogue
 constexpr int kGEpi = 8;        // epilogue warps: two per TMEM lane quarter, 64 columns each
 constexpr uint32_t kGTmemCols = 512;   // [0, 256) 2 accumulators; [256, 256 + 2D) the A tile, hi | lo
 constexpr uint32_t kGAcol = 2 * kGN;
@@ -366,6 +366,15 @@ struct GramMeta {
   uint32_t a0, alen, b0, blen, abuf, npar, self, last, done;
 };
 
+// One strip's work description, resolved by the scheduler warp while the
+// loaders stream the previous strip: the group (cell A and its kept partner
+// cells) and which 128-row A tile of it; partners as a stream prefix.
+constexpr int kGS = 2;  // strip setups in flight
+struct StripSetup {
+  uint32_t done, A, la, nA, own, np, tot, ti;
+  uint32_t ostart[kMaxPartners + 1], obase[kMaxPartners];
+};
+
 template <int D>
 struct GramSmem {
   float B[kGBB][2][kGN * D];  // [hi|lo] x D/32 chunks of 128 rows x 128 B (SW128 K-major); A lives in TMEM
@@ -375,48 +384,11 @@ struct GramSmem {
   float wmaxnb[kGBB][4];
   uint32_t jpos[kGBB][kGN];  // grid position of each B row; bit 31: the row is in A's own cell
   float mu[D];               // the current strip's shift (its first row)
-  uint32_t ostart[kMaxPartners + 1], obase[kMaxPartners];  // the group's other partners: stream prefix, first position
-  uint32_t grp[7];           // group: A, la, nA, has_own, npartners, others_total; the strip's A tile
+  StripSetup setup[kGS];     // strips prepared ahead by the scheduler warp
   GramMeta meta[kGBB];
-  uint64_t afull[kGAB], afree[kGAB], bfull[kGBB], bfree[kGBB], tfull[2], tempty[2];
-  uint32_t tmem, strip;
+  uint64_t afull[kGAB], afree[kGAB], bfull[kGBB], bfree[kGBB], tfull[2], tempty[2], sfull[kGS], sfree[kGS];
+  uint32_t tmem;
 };
-
-// Row r of a tile: load d floats (grid order), subtract mu, FP32 norm, store
-// the exact TF32 split (hi = 13 low mantissa bits cleared, lo = x - hi)
-// swizzled into the hi and lo tiles.  Zero rows past the tile's length.
-template <int D, int ROWS, int CB, int CE>
-__device__ __forceinline__ float gram_load_row(const float* __restrict__ Xs, uint32_t row, bool valid,
-                                               const float* __restrict__ mu, float* __restrict__ hi_tile,
-                                               float* __restrict__ lo_tile, int r) {
-  // 32-float chunks [CB, CE) of row r; returns their FP32 sum of squares
-  float nrm = 0.f;
-  const float4* src = reinterpret_cast<const float4*>(Xs + static_cast<size_t>(row) * D);
-#pragma unroll
-  for (int q = CB * 8; q < CE * 8; ++q) {
-    float4 v = valid ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid) {
-      v.x -= mu[4 * q];
-      v.y -= mu[4 * q + 1];
-      v.z -= mu[4 * q + 2];
-      v.w -= mu[4 * q + 3];
-    }
-    nrm = fmaf(v.x, v.x, nrm);
-    nrm = fmaf(v.y, v.y, nrm);
-    nrm = fmaf(v.z, v.z, nrm);
-    nrm = fmaf(v.w, v.w, nrm);
-    const float4 h = make_float4(__uint_as_float(__float_as_uint(v.x) & ~0x1fffu),
-                                 __uint_as_float(__float_as_uint(v.y) & ~0x1fffu),
-                                 __uint_as_float(__float_as_uint(v.z) & ~0x1fffu),
-                                 __uint_as_float(__float_as_uint(v.w) & ~0x1fffu));
-    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);  // exact
-    const int c = q >> 3, u = q & 7;  // 32-float chunk, 16 B unit inside the 128 B row
-    const int off = c * (ROWS * 32) + r * 32 + ((u ^ (r & 7)) << 2);
-    *reinterpret_cast<float4*>(hi_tile + off) = h;
-    *reinterpret_cast<float4*>(lo_tile + off) = l;
-  }
-  return nrm;
-}
 
 template <int D>
 __global__ void __launch_bounds__(kGThreads, 1)
@@ -428,7 +400,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
   using namespace tc;
   constexpr int NC = D / 32;
   extern __shared__ uint8_t graw[];
-  GramSmem<D>& sm = *reinterpret_cast<GramSmem<D>*>((reinterpret_cast<uintptr_t>(graw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by offsetting the shared array itself (not via an integer
+  // cast), so every sm.* access stays a shared-memory (LDS/STS) access
+  GramSmem<D>& sm = *reinterpret_cast<GramSmem<D>*>(graw + ((1024u - (smem_u32(graw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < kGAB; ++i) {
@@ -442,6 +416,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1);
       mbar_init(&sm.tempty[i], kGEpi);
+    }
+    for (int i = 0; i < kGS; ++i) {
+      mbar_init(&sm.sfull[i], 1);
+      mbar_init(&sm.sfree[i], 4);  // one arrive per loader warp
     }
     fence_mbar_init();
   }
@@ -459,43 +437,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
     // first row on), cut into 128-row B tiles: small cells fill the tiles.
     const int r = tid;
     uint32_t scount = 0, bcount = 0;
-    for (;;) {
-      named_bar(1, 128);  // every loader is done with the previous group's table
-      if (r == 0) {
-        const uint32_t st = static_cast<uint32_t>(atomicAdd(cursor, 1ull) * nparts + part);
-        const uint32_t ng = *ngroups;
-        sm.strip = st < gprefix[ng] ? st : 0xffffffffu;
-        if (st < gprefix[ng]) {
-          uint32_t lo = 0, hi = ng;  // group g: gprefix[g] <= st < gprefix[g+1]
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (gprefix[mid] <= st)
-              lo = mid;
-            else
-              hi = mid;
-          }
-          sm.grp[6] = st - gprefix[lo];  // the strip's A tile
-          const uint32_t gs = gstart[lo], A = pa[gs];
-          const uint32_t la = cfirst[A], nA = cfirst[A + 1] - la;
-          const bool own = pb[gs] == A;
-          uint32_t np = 0, tot = 0;
-          for (uint32_t k = gs + (own ? 1u : 0u); k < npairs && pa[k] == A && np < kMaxPartners; ++k, ++np) {
-            const uint32_t B = pb[k], lb = cfirst[B], nB = cfirst[B + 1] - lb;
-            sm.ostart[np] = tot;
-            sm.obase[np] = lb;
-            tot += nB;
-          }
-          sm.ostart[np] = tot;
-          sm.grp[0] = A;
-          sm.grp[1] = la;
-          sm.grp[2] = nA;
-          sm.grp[3] = own;
-          sm.grp[4] = np;
-          sm.grp[5] = tot;
-        }
-      }
-      named_bar(1, 128);
-      if (sm.strip == 0xffffffffu) {  // sentinel tile: tells the MMA and the epilogue to stop
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t slot = k % kGS;
+      mbar_wait(&sm.sfull[slot], (k / kGS) & 1);
+      const StripSetup& S = sm.setup[slot];
+      if (S.done) {  // sentinel tile: tells the MMA and the epilogue to stop
         const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
         mbar_wait(&sm.bfree[bb], bph ^ 1);
         if (r == 0) sm.meta[bb].done = 1;
@@ -503,10 +449,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
         if (lane == 0) mbar_arrive(&sm.bfull[bb]);
         break;
       }
-      const uint32_t la = sm.grp[1], nA = sm.grp[2], np = sm.grp[4], others = sm.grp[5];
-      const bool own = sm.grp[3] != 0;
+      const uint32_t la = S.la, nA = S.nA, np = S.np, others = S.tot;
+      const bool own = S.own != 0;
       {
-        const uint32_t ti = sm.grp[6];  // this work item's strip of the group
+        const uint32_t ti = S.ti;  // this work item's strip of the group
         const uint32_t a0 = la + ti * kGT, alen = min(static_cast<uint32_t>(kGT), nA - ti * kGT);
         const uint32_t own_len = own ? la + nA - a0 : 0u;  // own cell from the strip's first row on
         const uint32_t L = own_len + others, tb = (L + kGN - 1) / kGN;
@@ -558,10 +504,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.afull[ab]);
+        // B rows are loaded warp-cooperatively: kLpr lanes per row (16 B
+        // each), kRpi rows per instruction, so a load touches whole 128 B
+        // lines; every load of the tile is in flight before the buffer wait
+        constexpr int kLpr = D / 4, kRpi = 32 / kLpr, kNi = 32 / kRpi;
+        const int sub = lane % kLpr, rsel = lane / kLpr;
+        const float4 mu4 = *reinterpret_cast<const float4*>(mu + 4 * sub);
         for (uint32_t tj = 0; tj < tb; ++tj) {
           const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
           ++bcount;
-          mbar_wait(&sm.bfree[bb], bph ^ 1);
           const uint32_t q = tj * kGN + r, blen = min(static_cast<uint32_t>(kGN), L - tj * kGN);
           const bool valid = q < L, mine = q < own_len;
           uint32_t pos = 0;
@@ -573,20 +524,63 @@ __global__ void __launch_bounds__(kGThreads, 1)
               uint32_t lo = 0, hi = np;
               while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) >> 1;
-                if (sm.ostart[mid] <= qq)
+                if (S.ostart[mid] <= qq)
                   lo = mid;
                 else
                   hi = mid;
               }
-              pos = sm.obase[lo] + (qq - sm.ostart[lo]);
+              pos = S.obase[lo] + (qq - S.ostart[lo]);
             }
           }
-          const float nbr = gram_load_row<D, kGN, 0, D / 32>(Xs, pos, valid, mu, sm.B[bb][0], sm.B[bb][1], r);
+          float4 v[kNi];
+          const unsigned vmask = __ballot_sync(kFull, valid);
+#pragma unroll
+          for (int i = 0; i < kNi; ++i) {
+            const int src = i * kRpi + rsel;  // the warp's row this lane loads in step i
+            const uint32_t p = __shfl_sync(kFull, pos, src);
+            v[i] = (vmask >> src) & 1u ? __ldg(reinterpret_cast<const float4*>(Xs + static_cast<size_t>(p) * D) + sub)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          mbar_wait(&sm.bfree[bb], bph ^ 1);
+          float* hi_tile = sm.B[bb][0];
+          float* lo_tile = sm.B[bb][1];
+          float wm = 0.f;
+#pragma unroll
+          for (int i = 0; i < kNi; ++i) {
+            const int src = i * kRpi + rsel;
+            const int rr = 32 * warp + src;
+            float4 x = v[i];
+            if ((vmask >> src) & 1u) {
+              x.x -= mu4.x;
+              x.y -= mu4.y;
+              x.z -= mu4.z;
+              x.w -= mu4.w;
+            }
+            float nrm = x.x * x.x;
+            nrm = fmaf(x.y, x.y, nrm);
+            nrm = fmaf(x.z, x.z, nrm);
+            nrm = fmaf(x.w, x.w, nrm);
+#pragma unroll
+            for (int o = kLpr / 2; o; o >>= 1) nrm += __shfl_xor_sync(kFull, nrm, o);
+            const float4 h = make_float4(__uint_as_float(__float_as_uint(x.x) & ~0x1fffu),
+                                         __uint_as_float(__float_as_uint(x.y) & ~0x1fffu),
+                                         __uint_as_float(__float_as_uint(x.z) & ~0x1fffu),
+                                         __uint_as_float(__float_as_uint(x.w) & ~0x1fffu));
+            const float4 l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);  // exact
+            const int c = sub >> 3, u = sub & 7;  // 32-float chunk, 16 B unit inside the 128 B row
+            const int off = c * (kGN * 32) + rr * 32 + ((u ^ (rr & 7)) << 2);
+            *reinterpret_cast<float4*>(hi_tile + off) = h;
+            *reinterpret_cast<float4*>(lo_tile + off) = l;
+            if (sub == 0) {
+              const bool ok = (vmask >> src) & 1u;
+              sm.nb[bb][rr] = nrm;
+              sm.cnb[bb][rr] = ok ? (1.f - 2.f * gram_slack<D>()) * nrm : INFINITY;
+            }
+            wm = fmaxf(wm, nrm);
+          }
           sm.na[bb][r] = na_r;
-          sm.nb[bb][r] = nbr;
-          sm.cnb[bb][r] = valid ? (1.f - 2.f * gram_slack<D>()) * nbr : INFINITY;
           sm.jpos[bb][r] = pos | (mine ? 0x80000000u : 0u);
-          const float wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nbr)));  // nbr >= 0
+          wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(wm)));  // norms >= 0
           if (lane == 0) sm.wmaxnb[bb][warp] = wm;
           if (r == 0) sm.meta[bb] = GramMeta{a0, alen, 0u, blen, ab, npar, tj * kGN < own_len, tj + 1 == tb, 0u};
           fence_proxy_async();
@@ -594,6 +588,77 @@ __global__ void __launch_bounds__(kGThreads, 1)
           if (lane == 0) mbar_arrive(&sm.bfull[bb]);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.sfree[slot]);  // this warp is done with the strip's setup
+    }
+  } else if (warp == 5) {
+    // ---- strip scheduler: takes strips from the global cursor and resolves
+    // each one's group and partner table into the setup ring while the
+    // loaders stream the previous strip (warp-parallel searches and loads)
+    const uint32_t ng = *ngroups, total = gprefix[ng];
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t slot = k % kGS;
+      mbar_wait(&sm.sfree[slot], ((k / kGS) & 1) ^ 1);
+      StripSetup& S = sm.setup[slot];
+      uint32_t st = 0;
+      if (lane == 0) st = static_cast<uint32_t>(atomicAdd(cursor, 1ull) * nparts + part);
+      st = __shfl_sync(kFull, st, 0);
+      if (st >= total) {
+        if (lane == 0) {
+          S.done = 1;
+          mbar_arrive(&sm.sfull[slot]);
+        }
+        break;
+      }
+      // group g with gprefix[g] <= st < gprefix[g+1] (gprefix strictly increasing):
+      // 32-way search, every lane probes one point of the current range
+      uint32_t lo = 0, hi = ng;  // answer in [lo, hi)
+      while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t probe = min(lo + lane * step, hi - 1);
+        const int c = __popc(__ballot_sync(kFull, gprefix[probe] <= st));  // >= 1: gprefix[lo] <= st
+        const uint32_t nlo = min(lo + (c - 1) * step, hi - 1);  // lane c-1's probe
+        if (c < 32) hi = min(lo + c * step, hi);                 // lane c's probe failed
+        lo = nlo;
+      }
+      const uint32_t g = lo, gs = gstart[g], gend = g + 1 < ng ? gstart[g + 1] : npairs;
+      const uint32_t A = pa[gs], la = cfirst[A], nA = cfirst[A + 1] - la;
+      const uint32_t own = pb[gs] == A;
+      const uint32_t np = min(gend - gs - own, static_cast<uint32_t>(kMaxPartners));
+      uint32_t run = 0;
+      for (uint32_t b0 = 0; b0 < np; b0 += 32) {
+        const uint32_t t = b0 + lane;
+        uint32_t lb = 0, nB = 0;
+        if (t < np) {
+          const uint32_t B = pb[gs + own + t];
+          lb = cfirst[B];
+          nB = cfirst[B + 1] - lb;
+        }
+        uint32_t incl = nB;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (t < np) {
+          S.ostart[t] = run + incl - nB;
+          S.obase[t] = lb;
+        }
+        run += __shfl_sync(kFull, incl, 31);
+      }
+      if (lane == 0) {
+        S.ostart[np] = run;
+        S.done = 0;
+        S.A = A;
+        S.la = la;
+        S.nA = nA;
+        S.own = own;
+        S.np = np;
+        S.tot = run;
+        S.ti = st - gprefix[g];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.sfull[slot]);
     }
   } else if (warp == 4) {
     // ---- MMA issuer: the whole warp runs the loop (uniform registers), one

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  float* __restrict__ keys, unsigned* __restrict__ norm2_bits, unsigned set_norm2_bits) {
   constexpr int NC = D / kTcKChunk;  // K chunks (stages) per tile
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared pointer
   uint8_t* sa = smem;                             // kTcStages x 16 KB (A stages)
   uint8_t* sb = smem + kTcStages * kStageBytes;   // NC x 2 KB (B = U, SW128 K-major)
   uint64_t* full = reinterpret_cast<uint64_t*>(sb + NC * kBChunkBytes);  // TMA -> split   (tx)
