@@ -716,17 +716,19 @@ __global__ void __launch_bounds__(kGThreads, 1)
     unsigned long long visited = 0, evals = 0;
     unsigned band_bits = 0xffffffffu;
     float band_c = 0.f;
+    unsigned next_best = lane == 0 ? ld_relaxed_u32(a.best) : 0u;
     for (;;) {
       const uint32_t bb = bcount % kGBB, acc = tcount & 1, tph = (tcount >> 1) & 1;
       mbar_wait(&sm.tfull[acc], tph);
       tc_fence_after();
       const GramMeta m = sm.meta[bb];
       if (m.done) break;
-      // the band from the current bound, recomputed (FP64) only when the bound moved
+      // the band from the bound read during the previous tile (a stale bound
+      // only widens the band), recomputed (FP64) only when the bound moved;
+      // the next read is issued now and lands while this tile is filtered
       {
-        unsigned cur = 0;
-        if (lane == 0) cur = *reinterpret_cast<const volatile unsigned*>(a.best);
-        cur = __shfl_sync(kFull, cur, 0);
+        const unsigned cur = __shfl_sync(kFull, next_best, 0);
+        if (lane == 0) next_best = ld_relaxed_u32(a.best);
         if (cur != band_bits) {
           float b = 0.f;
           if (lane == 0) b = budget_thresholds_s32(*a.bud, __uint_as_float(cur)).band;

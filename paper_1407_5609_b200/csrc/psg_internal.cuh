@@ -188,6 +188,16 @@ struct KernelSpan {
 
 // ---------------------------------------------------------------------------
 // Orderable integer images of floats (radix sort keys, atomic min/max).
+#ifdef __CUDACC__
+// A relaxed GPU-scope load of a word other blocks update with atomics (the
+// shared bound): not cached in L1, no system-scope ordering cost.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+#endif
+
 __host__ __device__ __forceinline__ uint32_t f32_order(float f) {
 #ifdef __CUDA_ARCH__
   uint32_t u = __float_as_uint(f);
