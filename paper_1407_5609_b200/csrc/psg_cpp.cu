@@ -965,7 +965,9 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
       sa.m = grid_sample(W.keys.p, static_cast<uint32_t>(n), nk, gbox, W.gi, s);
       k_setup<<<1, 256, 0, s>>>(W.st.p, W.gi.gp.p, W.gi.sample.p, sa);
       PSG_LAUNCHED();
-      build_grid(W.keys.p, static_cast<uint32_t>(n), nk, W.gi, 24, s);
+      // a width learned on dense data makes big cells: the radix build then
+      const bool dense_hint = min_w > 0.0 && W.learned_dense;
+      build_grid(W.keys.p, static_cast<uint32_t>(n), nk, W.gi, 24, s, /*counting=*/!dense_hint);
       g_launches += 3;
       tm.mark("grid");
     } else {
@@ -1232,7 +1234,7 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         // they separate, so cell pairs stop mixing clusters.
         grid_params_for(plan.gp, gd, plan.gp.w, W.host_st->box_lo, W.host_st->box_span);
         PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
-        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
+        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s, /*counting=*/false);  // large cells
         plan.g = gd;
         tm.mark("dense grid");
       }

@@ -148,6 +148,156 @@ __global__ void k_verify_cfirst(const uint32_t* __restrict__ scell, uint32_t n, 
 }
 #endif
 
+// ---- counting build ----------------------------------------------------------
+// Cell id and the point's arrival rank in its cell (atomic, so arbitrary
+// order; k_cell_fix makes the final order deterministic).
+template <int NK>
+__global__ void k_cell_count(const float* __restrict__ keys, uint32_t n, const GridParams* __restrict__ gpp,
+                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ cid, uint32_t* __restrict__ rnk,
+                             uint32_t* __restrict__ bctr) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    bctr[0] = 0;  // big cells
+    bctr[1] = 0;  // their cursor
+  }
+  if (i >= n) return;
+  const GridParams P = *gpp;
+  uint32_t c = 0;
+#pragma unroll
+  for (int t = 0; t < (NK < kMaxGridKeys ? NK : kMaxGridKeys); ++t) {
+    if (t >= P.g) break;
+    const uint32_t dim = P.dims[t];
+    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - P.lo[t]) * P.inv_w;
+    const uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(dim - 1) ? dim - 1 : static_cast<uint32_t>(v));
+    c = c * dim + ct;
+  }
+  cid[i] = c;
+  rnk[i] = atomicAdd(cnt + c, 1u);
+}
+
+// Arrival-order placement; the counters go back to zero for the next build
+// (every non-zero counter has at least one point here).
+__global__ void k_cell_place(const uint32_t* __restrict__ cid, const uint32_t* __restrict__ rnk, uint32_t n,
+                             const uint32_t* __restrict__ cfirst, uint32_t* __restrict__ cnt,
+                             uint32_t* __restrict__ tmp) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = cid[i];
+  tmp[cfirst[c] + rnk[i]] = i;
+  cnt[c] = 0;
+}
+
+constexpr uint32_t kFixSmall = 64;  // cells up to this size are ranked per position
+
+// Final position of the point at arrival position p: its cell's start plus
+// the number of points of the cell with a smaller original index; gathers its
+// keys there.  Cells above kFixSmall points are listed for k_cell_fix_big.
+template <int NK>
+__global__ void k_cell_fix(const float* __restrict__ keys, const uint32_t* __restrict__ tmp,
+                           const uint32_t* __restrict__ cid, uint32_t n, const uint32_t* __restrict__ cfirst,
+                           float* __restrict__ skeys, uint32_t* __restrict__ sidx, uint32_t* __restrict__ scell,
+                           uint32_t* __restrict__ big, uint32_t* __restrict__ bctr) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t i = tmp[p], c = cid[i], b = cfirst[c], e = cfirst[c + 1];
+  if (e - b > kFixSmall) {
+    if (p == b) big[atomicAdd(bctr, 1u)] = c;
+    return;
+  }
+  uint32_t r = 0;
+  for (uint32_t k = b; k < e; ++k) r += tmp[k] < i;
+  const uint32_t q = b + r;
+  sidx[q] = i;
+  scell[q] = c;
+  const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
+  float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(q) * NK);
+#pragma unroll
+  for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+}
+
+// Big cells (duplicates, tight clusters): a block per cell.  The cell's
+// indices are bitonic-sorted in shared memory in runs of kFixRun; a cell of
+// one run is written out directly, a longer one ranks every point as the sum
+// of its lower bounds in the sorted runs (indices are distinct).
+constexpr int kFixBigThreads = 512, kFixRun = 8192;
+template <int NK>
+__device__ __forceinline__ void fix_write(const float* __restrict__ keys, uint32_t q, uint32_t i, uint32_t c,
+                                          float* __restrict__ skeys, uint32_t* __restrict__ sidx,
+                                          uint32_t* __restrict__ scell) {
+  sidx[q] = i;
+  scell[q] = c;
+  const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
+  float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(q) * NK);
+#pragma unroll
+  for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+}
+
+template <int NK>
+__global__ void __launch_bounds__(kFixBigThreads) k_cell_fix_big(
+    const float* __restrict__ keys, const uint32_t* __restrict__ tmp, uint32_t* __restrict__ runs,
+    const uint32_t* __restrict__ cfirst, float* __restrict__ skeys, uint32_t* __restrict__ sidx,
+    uint32_t* __restrict__ scell, const uint32_t* __restrict__ big, uint32_t* __restrict__ bctr) {
+  __shared__ uint32_t sk[kFixRun];
+  __shared__ uint32_t s_c;
+  const uint32_t tid = threadIdx.x;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t k = atomicAdd(bctr + 1, 1u);
+      s_c = k < bctr[0] ? big[k] : 0xffffffffu;
+    }
+    __syncthreads();
+    const uint32_t c = s_c;
+    if (c == 0xffffffffu) return;
+    const uint32_t b = cfirst[c], e = cfirst[c + 1], L = e - b;
+    for (uint32_t r0 = b; r0 < e; r0 += kFixRun) {
+      const uint32_t len = min(static_cast<uint32_t>(kFixRun), e - r0);
+      uint32_t P = 1;
+      while (P < len) P <<= 1;
+      __syncthreads();
+      for (uint32_t k = tid; k < P; k += kFixBigThreads) sk[k] = k < len ? tmp[r0 + k] : 0xffffffffu;
+      __syncthreads();
+      for (uint32_t k2 = 2; k2 <= P; k2 <<= 1)
+        for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+          for (uint32_t t = tid; t < P / 2; t += kFixBigThreads) {
+            const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), l = i + j;
+            const uint32_t x = sk[i], y = sk[l];
+            if ((x > y) == ((i & k2) == 0)) {
+              sk[i] = y;
+              sk[l] = x;
+            }
+          }
+          __syncthreads();
+        }
+      if (L <= kFixRun) {
+        for (uint32_t k = tid; k < len; k += kFixBigThreads) fix_write<NK>(keys, b + k, sk[k], c, skeys, sidx, scell);
+      } else {
+        for (uint32_t k = tid; k < len; k += kFixBigThreads) runs[r0 + k] = sk[k];
+      }
+    }
+    if (L > kFixRun) {
+      __threadfence_block();
+      __syncthreads();
+      for (uint32_t p = b + tid; p < e; p += kFixBigThreads) {
+        const uint32_t i = tmp[p];
+        uint32_t rank = 0;
+        for (uint32_t r0 = b; r0 < e; r0 += kFixRun) {  // lower bound of i in each sorted run
+          uint32_t lo = 0, hi = min(static_cast<uint32_t>(kFixRun), e - r0);
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (runs[r0 + mid] < i)
+              lo = mid + 1;
+            else
+              hi = mid;
+          }
+          rank += lo;
+        }
+        fix_write<NK>(keys, b + rank, i, c, skeys, sidx, scell);
+      }
+    }
+  }
+}
+
 template <int NK>
 __global__ void k_gather_sorted(const float* __restrict__ keys, const uint32_t* __restrict__ perm, uint32_t n,
                                 float* __restrict__ skeys, uint32_t* __restrict__ sidx) {
@@ -175,6 +325,13 @@ void GridIndex::ensure(uint32_t n_, int nk_, cudaStream_t s) {
   idx1.alloc(n, s);
   hist.alloc(radix_hist_words(n), s);
   cfirst.alloc(kMaxCells + 1, s);
+  if (!cnt.p) {
+    cnt.alloc(kMaxCells + 1, s);
+    PSG_CUDA(cudaMemsetAsync(cnt.p, 0, (kMaxCells + 1) * sizeof(uint32_t), s));  // invariant: all zero
+    ctmp.alloc(scan_temp_words(kMaxCells + 1), s);
+    bctr.alloc(2, s);
+  }
+  big.alloc(n / kFixSmall + 1, s);
   sample.alloc(kMaxKeys * kGridSample, s);
   gp.alloc(1, s);
 }
@@ -210,7 +367,45 @@ void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double 
   }
 }
 
-void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s) {
+void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s, bool counting) {
+  if (counting) {
+    const unsigned nb = blocks(n, 256);
+    if (nk == 4)
+      k_cell_count<4><<<nb, 256, 0, s>>>(keys, n, gi.gp.p, gi.cnt.p, gi.cid0.p, gi.idx0.p, gi.bctr.p);
+    else
+      k_cell_count<8><<<nb, 256, 0, s>>>(keys, n, gi.gp.p, gi.cnt.p, gi.cid0.p, gi.idx0.p, gi.bctr.p);
+    PSG_LAUNCHED();
+    // cfirst = exclusive scan of the counts over cells 0..cells (count read on device)
+    exclusive_scan_u32_dev(gi.cnt.p, gi.cfirst.p, kMaxCells + 1, &gi.gp.p->cells, gi.ctmp.p, s);
+    k_cell_place<<<nb, 256, 0, s>>>(gi.cid0.p, gi.idx0.p, n, gi.cfirst.p, gi.cnt.p, gi.idx1.p);
+    PSG_LAUNCHED();
+    if (nk == 4) {
+      k_cell_fix<4><<<nb, 256, 0, s>>>(keys, gi.idx1.p, gi.cid0.p, n, gi.cfirst.p, gi.skeys.p, gi.sidx.p, gi.cid1.p,
+                                       gi.big.p, gi.bctr.p);
+      PSG_LAUNCHED();
+      k_cell_fix_big<4><<<148, kFixBigThreads, 0, s>>>(keys, gi.idx1.p, gi.idx0.p, gi.cfirst.p, gi.skeys.p,
+                                                       gi.sidx.p, gi.cid1.p, gi.big.p, gi.bctr.p);
+    } else {
+      k_cell_fix<8><<<nb, 256, 0, s>>>(keys, gi.idx1.p, gi.cid0.p, n, gi.cfirst.p, gi.skeys.p, gi.sidx.p, gi.cid1.p,
+                                       gi.big.p, gi.bctr.p);
+      PSG_LAUNCHED();
+      k_cell_fix_big<8><<<148, kFixBigThreads, 0, s>>>(keys, gi.idx1.p, gi.idx0.p, gi.cfirst.p, gi.skeys.p,
+                                                       gi.sidx.p, gi.cid1.p, gi.big.p, gi.bctr.p);
+    }
+    PSG_LAUNCHED();
+#ifdef PSG_DEBUG_SYNC
+    k_verify_cfirst<<<1024, 256, 0, s>>>(gi.cid1.p, n, gi.gp.p, gi.cfirst.p);
+    PSG_LAUNCHED();
+#endif
+    g_launches += 8;
+    gi.dev.skeys = gi.skeys.p;
+    gi.dev.sidx = gi.sidx.p;
+    gi.dev.scell = gi.cid1.p;
+    gi.dev.cfirst = gi.cfirst.p;
+    gi.dev.gp = gi.gp.p;
+    gi.dev.n = n;
+    return;
+  }
   if (nk == 4)
     k_cell_ids<4><<<blocks(n, 256), 256, 0, s>>>(keys, n, gi.gp.p, gi.cid0.p, gi.idx0.p);
   else

@@ -86,15 +86,25 @@ struct GridIndex {
   uint32_t n = 0;
   DevBuf<float> skeys;
   DevBuf<uint32_t> sidx, cid0, cid1, idx0, idx1, hist, cfirst;
+  // counting build: per-cell counters (kept all-zero between builds), the
+  // scan's temp, the list of cells too big for the per-position fix-up, and
+  // two device counters (big-cell count, cursor)
+  DevBuf<uint32_t> cnt, ctmp, big, bctr;
   DevBuf<float> sample;
   DevBuf<GridParams> gp;
   GridDev dev;
   void ensure(uint32_t n_, int nk_, cudaStream_t s);
 };
 
-// Enqueue the build (no host synchronisation): cell ids from *G.gp, stable
-// radix sort by cell (sort_bits), cfirst by search of the sorted ids, gather.
-void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s);
+// Enqueue the build (no host synchronisation): cell ids from *G.gp, points
+// ordered by (cell, original index), cfirst, keys gathered into that order.
+// counting = true (sparse grids, a few points per cell): per-cell atomic
+// counts, one scan (which IS cfirst), atomic placement, then a deterministic
+// fix-up that ranks each point inside its cell by original index.
+// counting = false (the dense engine's large cells): stable LSD radix sort on
+// sort_bits, cfirst by search of the sorted ids.  Both give the same order.
+void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s,
+                bool counting = true);
 // Strided sample of the first g keys into gi.sample (g x m floats); returns m.
 uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s);
 // Host-side box from a host copy of the sample (mean +- 3 sd, clipped).
