@@ -185,6 +185,47 @@ __device__ __forceinline__ GridRanges grid_ranges(const uint32_t* __restrict__ c
   return R;
 }
 
+// grid_ranges restricted by the point's position inside its cell: a
+// neighbour cell across a face the point is farther than `win` from holds no
+// point within `win` in that key, so no pair passing the key test (every
+// key gap <= sqrt(lb2) <= win).  Own row: the next cell only near the upper
+// face of the last key; other rows only near the faces they lie across, and
+// their last-key span only as wide as the point's nearness allows.
+__device__ __forceinline__ GridRanges grid_ranges_pruned(const uint32_t* __restrict__ cfirst, const GridParams& P,
+                                                         uint32_t p, uint32_t cell, const float* key, double win) {
+  GridRanges R{};
+  const uint32_t D = P.g == 1 ? P.dims[0] : (P.g == 2 ? P.dims[1] : P.dims[2]);
+  const uint32_t prefix = P.fD.div(cell);
+  const uint32_t c_last = cell - prefix * D;
+  const int tl = P.g - 1;  // the last grid key (0, 1 or 2)
+  const double lo_l = (tl == 0 ? P.lo[0] : tl == 1 ? P.lo[1] : P.lo[2]) + c_last * P.w;
+  const double x_l = tl == 0 ? key[0] : tl == 1 ? key[1] : key[2];
+  const bool lo_near = c_last > 0 && x_l - lo_l <= win;
+  const bool hi_near = c_last + 1 < D && lo_l + P.w - x_l <= win;
+  const uint32_t lo_last = lo_near ? c_last - 1 : c_last;
+  const uint32_t hi_last = hi_near ? c_last + 1 : c_last;
+  R.b0 = p + 1;
+  R.e0 = cfirst[cell - c_last + hi_last + 1];
+  if (P.g == 2) {
+    const double lo0 = P.lo[0] + prefix * P.w;
+    if (prefix + 1 < P.dims[0] && lo0 + P.w - key[0] <= win)
+      grid_row(cfirst, P, static_cast<int>(prefix) + 1, 0, D, lo_last, hi_last, R.b1, R.e1);
+  } else if (P.g == 3) {
+    const uint32_t q1 = P.f1.div(prefix);
+    const int c0 = static_cast<int>(q1), c1 = static_cast<int>(prefix - q1 * P.dims[1]);
+    const double lo0 = P.lo[0] + c0 * P.w, lo1 = P.lo[1] + c1 * P.w;
+    const bool hi0 = lo0 + P.w - key[0] <= win;
+    const bool lo1n = key[1] - lo1 <= win, hi1 = lo1 + P.w - key[1] <= win;
+    if (hi1) grid_row(cfirst, P, c0, c1 + 1, D, lo_last, hi_last, R.b1, R.e1);
+    if (hi0) {
+      if (lo1n) grid_row(cfirst, P, c0 + 1, c1 - 1, D, lo_last, hi_last, R.b2, R.e2);
+      grid_row(cfirst, P, c0 + 1, c1, D, lo_last, hi_last, R.b3, R.e3);
+      if (hi1) grid_row(cfirst, P, c0 + 1, c1 + 1, D, lo_last, hi_last, R.b4, R.e4);
+    }
+  }
+  return R;
+}
+
 // Only the own row's forward range [p+1, end of cell (.., c_last+1)): one
 // cfirst lookup (the bootstrap's cheap variant).
 __device__ __forceinline__ GridRanges grid_own_row(const uint32_t* __restrict__ cfirst, const GridParams& P,
