@@ -679,8 +679,7 @@ struct SetupArgs {
   double min_w;        // cell width learned by an earlier regrid on this point set (0: none)
   uint32_t n, m;
 };
-constexpr int kSetupPer = 16;  // sample elements per thread
-static_assert(kSetupPer * 256 >= kGridSample, "k_setup covers the whole sample");
+static_assert(kMaxGridKeys <= 8, "k_setup: one warp per boxed key");
 
 // The error budget from the projection's max norm (same formula as the host
 // make_budget), then — grid engine — the key box from the sample moments
@@ -707,55 +706,52 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
   }
   if (sa.g == 0) return;
   // boxes of every key a grid may use (the sparse grid takes the first g,
-  // the dense engine up to kMaxGridKeys)
-  double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
-  for (int t = 0; t < sa.gbox; ++t) {
-    // every load of this key in flight before any arithmetic (m <= kGridSample
-    // = 16 x 256): one memory round trip per key, not one per element
-    const float* v = sample + static_cast<size_t>(t) * sa.m;
-    float x[kSetupPer];
+  // the dense engine up to kMaxGridKeys): warp t reduces key t, every load of
+  // its sample in flight at once, four independent FP64 accumulators per lane
+  __shared__ double s_lo[kMaxGridKeys], s_span[kMaxGridKeys];
+  if (warp < sa.gbox) {
+    const float* v = sample + static_cast<size_t>(warp) * sa.m;
+    constexpr int kPer = kGridSample / 32;  // 128 sample values per lane
+    float x[kPer];  // all 128 loads issued before any use: one memory round trip
 #pragma unroll
-    for (int r = 0; r < kSetupPer; ++r) {
-      const uint32_t i = tid + r * 256u;
-      x[r] = i < sa.m ? v[i] : v[0];
+    for (int r = 0; r < kPer; ++r) {
+      const uint32_t i = lane + 32u * r;
+      x[r] = i < sa.m ? v[i] : 0.f;
     }
-    double s1 = 0, s2 = 0, mn = 1e300, mx = -1e300;
+    double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+    float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
-    for (int r = 0; r < kSetupPer; ++r) {
-      if (tid + r * 256u >= sa.m) break;
-      const double y = x[r];
-      s1 += y;
-      s2 += y * y;
-      mn = fmin(mn, y);
-      mx = fmax(mx, y);
-    }
-    for (int o = 16; o; o >>= 1) {
-      s1 += __shfl_xor_sync(kFull, s1, o);
-      s2 += __shfl_xor_sync(kFull, s2, o);
-      mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
-      mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
-    }
-    __syncthreads();
-    if (lane == 0) {
-      red[0][warp] = s1;
-      red[1][warp] = s2;
-      red[2][warp] = mn;
-      red[3][warp] = mx;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int w = 1; w < 8; ++w) {
-        s1 += red[0][w];
-        s2 += red[1][w];
-        mn = fmin(mn, red[2][w]);
-        mx = fmax(mx, red[3][w]);
+    for (int r = 0; r < kPer; ++r) {
+      if (lane + 32u * r < sa.m) {
+        const float y = x[r];
+        s1[r & 3] += y;
+        s2[r & 3] = fma(static_cast<double>(y), static_cast<double>(y), s2[r & 3]);
+        mn = fminf(mn, y);
+        mx = fmaxf(mx, y);
       }
-      const double mean = s1 / sa.m, sd = sqrt(fmax(s2 / sa.m - mean * mean, 0.0));
-      const double a = fmax(mn, mean - sa.box_sd * sd), b = fmin(mx, mean + sa.box_sd * sd);
-      lo[t] = a;
-      span[t] = fmax(b - a, 1e-30);
+    }
+    double a1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), a2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+    for (int o = 16; o; o >>= 1) {
+      a1 += __shfl_xor_sync(kFull, a1, o);
+      a2 += __shfl_xor_sync(kFull, a2, o);
+      mn = fminf(mn, __shfl_xor_sync(kFull, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    }
+    if (lane == 0) {
+      const double mean = a1 / sa.m, sd = sqrt(fmax(a2 / sa.m - mean * mean, 0.0));
+      const double lo_t = fmax(static_cast<double>(mn), mean - sa.box_sd * sd);
+      const double hi_t = fmin(static_cast<double>(mx), mean + sa.box_sd * sd);
+      s_lo[warp] = lo_t;
+      s_span[warp] = fmax(hi_t - lo_t, 1e-30);
     }
   }
+  __syncthreads();
+  double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
+  if (tid == 0)
+    for (int t = 0; t < sa.gbox; ++t) {
+      lo[t] = s_lo[t];
+      span[t] = s_span[t];
+    }
   if (tid == 0) {
     for (int t = 0; t < kMaxGridKeys; ++t) {
       st->box_lo[t] = lo[t];

@@ -29,7 +29,13 @@ struct FastDiv {
       int l = 0;
       while ((1u << l) < divisor) ++l;  // ceil(log2)
       const int p = 31 + l;
-      f.m = static_cast<uint32_t>(((1ull << p) + divisor - 1) / divisor);
+      // m = ceil(2^p / d) (< 2^32): from the FP64 quotient (53 bits) with an
+      // exact 64-bit fix-up, not a 64-bit integer division (slow on device)
+      const uint64_t two_p = 1ull << p;
+      uint64_t m = static_cast<uint64_t>(static_cast<double>(two_p) / static_cast<double>(divisor));
+      while (m * divisor < two_p) ++m;
+      while (m > 0 && (m - 1) * divisor >= two_p) --m;
+      f.m = static_cast<uint32_t>(m);
       f.s = static_cast<uint32_t>(p - 32);
     }
     return f;
@@ -113,7 +119,8 @@ void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double 
 __host__ __device__ inline double grid_occupancy_width(uint32_t n, int g, const double span[3], double occupancy) {
   double vol = 1.0;
   for (int t = 0; t < g; ++t) vol *= span[t];
-  return pow(vol * occupancy / (n > 0 ? static_cast<double>(n) : 1.0), 1.0 / g);
+  const double x = vol * occupancy / (n > 0 ? static_cast<double>(n) : 1.0);
+  return g == 1 ? x : g == 2 ? sqrt(x) : g == 3 ? cbrt(x) : pow(x, 1.0 / g);  // no pow for g <= 3
 }
 
 struct GridRanges {  // five ranges held in registers; empty ranges have b == e
