@@ -537,9 +537,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll
           for (int i = 0; i < kNi; ++i) {
             const int src = i * kRpi + rsel;  // the warp's row this lane loads in step i
+            // unconditional (pos = 0 for invalid rows, zeroed at the split): a
+            // predicated select here would serialise the loads on their results
             const uint32_t p = __shfl_sync(kFull, pos, src);
-            v[i] = (vmask >> src) & 1u ? __ldg(reinterpret_cast<const float4*>(Xs + static_cast<size_t>(p) * D) + sub)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[i] = __ldg(reinterpret_cast<const float4*>(Xs + static_cast<size_t>(p) * D) + sub);
           }
           mbar_wait(&sm.bfree[bb], bph ^ 1);
           float* hi_tile = sm.B[bb][0];
@@ -555,6 +556,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
               x.y -= mu4.y;
               x.z -= mu4.z;
               x.w -= mu4.w;
+            } else {
+              x = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             float nrm = x.x * x.x;
             nrm = fmaf(x.y, x.y, nrm);
@@ -724,12 +727,16 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const GramMeta m = sm.meta[bb];
       if (m.done) break;
       // the band from the bound read during the previous tile (a stale bound
-      // only widens the band), recomputed (FP64) only when the bound moved;
-      // the next read is issued now and lands while this tile is filtered
+      // only widens the band), recomputed (FP64) only when the bound moved enough;
+      // the next read is issued now and lands while tiles are filtered
       {
         const unsigned cur = __shfl_sync(kFull, next_best, 0);
-        if (lane == 0) next_best = ld_relaxed_u32(a.best);
-        if (cur != band_bits) {
+        // (re-read every 16th tile: the read itself waits behind every SM's atomicMin traffic)
+        if (lane == 0 && (tcount & 15) == 0) next_best = ld_relaxed_u32(a.best);
+        // hysteresis: a band up to ~3 % wider than the current bound's is
+        // still a superset, so the FP64 recomputation runs a few hundred
+        // times per solve instead of on every small move of the bound
+        if (band_bits == 0xffffffffu || __uint_as_float(cur) < 0.97f * __uint_as_float(band_bits)) {
           float b = 0.f;
           if (lane == 0) b = budget_thresholds_s32(*a.bud, __uint_as_float(cur)).band;
           band_c = __shfl_sync(kFull, b, 0);

@@ -72,6 +72,18 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, u
       : "memory");
 }
 
+// 16-byte global -> shared async copy (no registers held while in flight);
+// ok = false zero-fills the destination without reading the source.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // One lane of a fully active warp (the lowest), chosen by elect.sync: lets a
 // whole warp run the issue loop in uniform registers while one lane issues.
 __device__ __forceinline__ bool elect_one() {
