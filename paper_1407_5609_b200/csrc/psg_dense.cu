@@ -510,12 +510,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
         constexpr int kLpr = D / 4, kRpi = 32 / kLpr, kNi = 32 / kRpi;
         const int sub = lane % kLpr, rsel = lane / kLpr;
         const float4 mu4 = *reinterpret_cast<const float4*>(mu + 4 * sub);
-        for (uint32_t tj = 0; tj < tb; ++tj) {
-          const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
-          ++bcount;
-          const uint32_t q = tj * kGN + r, blen = min(static_cast<uint32_t>(kGN), L - tj * kGN);
-          const bool valid = q < L, mine = q < own_len;
-          uint32_t pos = 0;
+        // lane l resolves the grid position of tile row 32 w + l; tile tj+1's
+        // positions are resolved while tile tj's loads are in flight
+        auto resolve = [&](uint32_t tj, uint32_t& pos, bool& mine) -> bool {
+          const uint32_t q = tj * kGN + r;
+          const bool valid = q < L;
+          mine = q < own_len;
+          pos = 0;
           if (valid) {
             if (mine) {
               pos = a0 + q;
@@ -532,6 +533,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
               pos = S.obase[lo] + (qq - S.ostart[lo]);
             }
           }
+          return valid;
+        };
+        uint32_t pos = 0;
+        bool mine = false;
+        bool valid = tb > 0 ? resolve(0, pos, mine) : false;
+        for (uint32_t tj = 0; tj < tb; ++tj) {
+          const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+          ++bcount;
+          const uint32_t blen = min(static_cast<uint32_t>(kGN), L - tj * kGN);
           float4 v[kNi];
           const unsigned vmask = __ballot_sync(kFull, valid);
 #pragma unroll
@@ -542,6 +552,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
             const uint32_t p = __shfl_sync(kFull, pos, src);
             v[i] = __ldg(reinterpret_cast<const float4*>(Xs + static_cast<size_t>(p) * D) + sub);
           }
+          const uint32_t jpos_c = pos | (mine ? 0x80000000u : 0u);
+          if (tj + 1 < tb) valid = resolve(tj + 1, pos, mine);
           mbar_wait(&sm.bfree[bb], bph ^ 1);
           float* hi_tile = sm.B[bb][0];
           float* lo_tile = sm.B[bb][1];
@@ -582,7 +594,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             wm = fmaxf(wm, nrm);
           }
           sm.na[bb][r] = na_r;
-          sm.jpos[bb][r] = pos | (mine ? 0x80000000u : 0u);
+          sm.jpos[bb][r] = jpos_c;
           wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(wm)));  // norms >= 0
           if (lane == 0) sm.wmaxnb[bb][warp] = wm;
           if (r == 0) sm.meta[bb] = GramMeta{a0, alen, 0u, blen, ab, npar, tj * kGN < own_len, tj + 1 == tb, 0u};
