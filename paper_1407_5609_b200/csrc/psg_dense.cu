@@ -764,11 +764,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const bool general = m.self || a.zone > 1;
       const uint32_t oi = (vr && a.zone > 1) ? a.sidx[i] : 0u;
       float vmin = INFINITY, ubs = INFINITY;
-#pragma unroll 1
+      static_assert(kGN / 64 == 2, "two 32-column loads per epilogue warp");
+      uint32_t vv[2][32];  // both loads in flight before one wait
+      tmem_ld32_nowait(tmem + ((32u * e) << 16) + acc * kGN + half * (kGN / 2), vv[0]);
+      tmem_ld32_nowait(tmem + ((32u * e) << 16) + acc * kGN + half * (kGN / 2) + 32, vv[1]);
+      tmem_wait_ld();
+#pragma unroll
       for (int q = 0; q < kGN / 64; ++q) {
         const uint32_t c0 = half * (kGN / 2) + q * 32;
-        uint32_t v[32];
-        tmem_ld32(tmem + ((32u * e) << 16) + acc * kGN + c0, v);
+        const uint32_t (&v)[32] = vv[q];
         if (!vr || c0 >= m.blen) continue;
         bool hit = false;
 #pragma unroll
