@@ -90,7 +90,9 @@ struct FrnnArgs {
   ExactSrc src;
   uint64_t* out;
   uint64_t cap;
-  unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined
+  unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined, [4] band pairs
+  uint64_t* band;           // k_frnn_scan_small: pairs inside the rounding band, decided by k_frnn_band
+  uint64_t bcap;
 };
 
 constexpr int kFrnnThreads = 256;
@@ -211,6 +213,146 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
     if (hsum) atomicAdd(a.acc + 1, static_cast<unsigned long long>(hsum));
     if (visited) atomicAdd(a.acc + 2, static_cast<unsigned long long>(visited));
     if (examined) atomicAdd(a.acc + 3, static_cast<unsigned long long>(examined));
+  }
+}
+
+// d <= 4 (the C4 shape): the same walk over the flattened ranges, kFB
+// candidates per step with every coordinate load in flight before any math
+// (the one-at-a-time walk above is load-latency bound: one dependent L1/L2
+// load per candidate per lane).  Same decisions, same emitted set.
+#ifndef PSG_FRNN_FB
+#define PSG_FRNN_FB 4
+#endif
+constexpr int kFB = PSG_FRNN_FB;
+// kEmit = false (count + hash only): no pair buffer, no per-group atomics —
+// the single global counter was the kernel's serialisation point.
+template <bool kEmit>
+__global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan_small(FrnnArgs a) {
+  __shared__ GridParams sP;
+  constexpr int kFlush = 128;  // pairs per global atomic (list mode)
+  __shared__ uint64_t wbuf[kEmit ? kFrnnThreads / 32 : 1][kEmit ? kFlush + 32 * kFB : 1];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) sP = *a.grid.gp;
+  __syncthreads();
+  const uint32_t p = blockIdx.x * kFrnnThreads + tid;
+  const bool valid = p < a.n;
+  uint64_t visited = 0, examined = 0, hsum = 0, emitted = 0;
+  GridFlat F{};
+  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t mi = 0;
+  if (valid) {
+    F = grid_flat(grid_ranges(a.grid.cfirst, sP, p, a.grid.scell[p]));
+    mi = a.sidx[p];
+    me = a.sx[p];
+  }
+  const uint32_t dummy = valid ? p : 0u;
+  const bool zoned = a.zone > 1;
+  const unsigned lt = (1u << lane) - 1u;
+  const float band = a.th.band, lo = a.lo;
+  int c = 0;  // warp-uniform fill of wbuf[w]
+  for (uint32_t t0 = 0; __any_sync(kFull, t0 < F.total); t0 += kFB) {
+    uint32_t jj[kFB];
+    float4 o[kFB];
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      jj[u] = t0 + u < F.total ? F.at(t0 + u) : dummy;
+      o[u] = a.sx[jj[u]];
+    }
+    unsigned emit = 0;
+    uint64_t key[kFB];
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      key[u] = 0;
+      if (t0 + u >= F.total) continue;
+      uint32_t mj = 0;
+      if (zoned) {
+        mj = a.sidx[jj[u]];
+        if (!admissible(mi, mj, a.zone)) continue;  // refscan.cpp:15-18
+      }
+      ++visited;
+      ++examined;
+      float g = o[u].x - me.x;
+      float s32 = g * g;
+      g = o[u].y - me.y;
+      s32 = fmaf(g, g, s32);
+      g = o[u].z - me.z;
+      s32 = fmaf(g, g, s32);
+      g = o[u].w - me.w;
+      s32 = fmaf(g, g, s32);
+      if (s32 <= band) {
+        if (!zoned) mj = a.sidx[jj[u]];  // the original index only inside the band
+        const uint64_t k = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
+        if (s32 <= lo) {  // inside R for certain
+          emit |= 1u << u;
+          key[u] = k;
+          hsum += mix64(k);
+        } else {  // the FP64 decision (rare) is deferred to k_frnn_band: keeps this loop's registers low
+          const unsigned long long slot = atomicAdd(a.acc + 4, 1ull);
+          if (slot < a.bcap) a.band[slot] = k;
+        }
+      }
+    }
+    if constexpr (!kEmit) {
+      emitted += __popc(emit);
+      continue;
+    }
+    // append this step's pairs (at most 32 kFB per warp) behind the c pending
+    int base = c;
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      const unsigned mask = __ballot_sync(kFull, (emit >> u) & 1u);
+      if ((emit >> u) & 1u) wbuf[w][base + __popc(mask & lt)] = key[u];
+      base += __popc(mask);
+    }
+    c = base;
+    if (c >= kFlush) {  // flush whole groups of 32 with one atomic
+      __syncwarp();
+      const int full = c & ~31;
+      unsigned long long gpos = 0;
+      if (lane == 0) gpos = atomicAdd(a.acc, static_cast<unsigned long long>(full));
+      gpos = __shfl_sync(kFull, gpos, 0);
+      for (int k = lane; k < full; k += 32)
+        if (gpos + k < a.cap) a.out[gpos + k] = wbuf[w][k];
+      __syncwarp();
+      if (lane < c - full) wbuf[w][lane] = wbuf[w][full + lane];
+      c -= full;
+      __syncwarp();
+    }
+  }
+  if (kEmit && c > 0) {
+    __syncwarp();
+    unsigned long long gpos = 0;
+    if (lane == 0) gpos = atomicAdd(a.acc, static_cast<unsigned long long>(c));
+    gpos = __shfl_sync(kFull, gpos, 0);
+    for (int k = lane; k < c; k += 32)
+      if (gpos + k < a.cap) a.out[gpos + k] = wbuf[w][k];
+  }
+  for (int o = 16; o; o >>= 1) {
+    hsum += __shfl_xor_sync(kFull, hsum, o);
+    visited += __shfl_xor_sync(kFull, visited, o);
+    examined += __shfl_xor_sync(kFull, examined, o);
+    if constexpr (!kEmit) emitted += __shfl_xor_sync(kFull, emitted, o);
+  }
+  if (lane == 0) {
+    if (!kEmit && emitted) atomicAdd(a.acc, static_cast<unsigned long long>(emitted));
+    if (hsum) atomicAdd(a.acc + 1, static_cast<unsigned long long>(hsum));
+    if (visited) atomicAdd(a.acc + 2, static_cast<unsigned long long>(visited));
+    if (examined) atomicAdd(a.acc + 3, static_cast<unsigned long long>(examined));
+  }
+}
+
+// The rounding-band pairs of k_frnn_scan_small: the reference's FP64
+// distance (metrics.cpp:16-24, symmetric in i, j), boundary inclusive (<= R)
+__global__ void k_frnn_band(FrnnArgs a) {
+  const unsigned long long m = min(static_cast<unsigned long long>(a.acc[4]), static_cast<unsigned long long>(a.bcap));
+  for (unsigned long long t = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; t < m;
+       t += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const uint64_t k = a.band[t];
+    if (exact_distance(a.src, k >> 32, k & 0xffffffffull) <= a.R) {
+      const unsigned long long g = atomicAdd(a.acc, 1ull);
+      if (g < a.cap) a.out[g] = k;  // cap = 0 when only the count is wanted
+      atomicAdd(a.acc + 1, static_cast<unsigned long long>(mix64(k)));
+    }
   }
 }
 
@@ -472,7 +614,9 @@ struct FrnnRun {
   uint64_t count = 0, hash = 0, visited = 0, examined = 0;
 };
 
-FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone) {
+// emit = false: count + hash only (no pair list is materialised)
+FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                 bool emit = true) {
   const uint64_t n = ps->n;
   if (!(radius > 0.0) || !std::isfinite(radius)) throw invalid_argument("radius must be positive");
   check_reference_args(n, std::min(q, n), f);  // refscan.cpp:165 clamps q to n
@@ -544,19 +688,29 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   a.lo = lo;
   a.R = radius;
   a.src = ps->exact();
-  DevBuf<unsigned long long> acc(4, s);
-  uint64_t cap = std::max<uint64_t>(1u << 20, 24 * n);
+  DevBuf<unsigned long long> acc(5, s);
+  // count-only runs of the small-d scan never write pairs
+  const bool no_list = small_d && !emit;
+  uint64_t cap = no_list ? 0 : std::max<uint64_t>(1u << 20, 24 * n);
+  uint64_t bcap = 1u << 16;
+  DevBuf<uint64_t> band;
   for (;;) {
-    run.pairs.alloc(cap, s);
-    PSG_CUDA(cudaMemsetAsync(acc.p, 0, 32, s));
+    run.pairs.alloc(std::max<uint64_t>(cap, 1), s);
+    PSG_CUDA(cudaMemsetAsync(acc.p, 0, 40, s));
     a.out = run.pairs.p;
     a.cap = cap;
     a.acc = acc.p;
     if (small_d) {
-      if (nk == 4)
-        k_frnn_scan<4, true><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+      if (band.n < bcap) band.alloc(bcap, s);
+      a.band = band.p;
+      a.bcap = bcap;
+      if (no_list)
+        k_frnn_scan_small<false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
       else
-        k_frnn_scan<8, true><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+        k_frnn_scan_small<true><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+      PSG_LAUNCHED();
+      ++g_launches;
+      k_frnn_band<<<c.sm_count * 2, 256, 0, s>>>(a);
     } else {
       if (nk == 4)
         k_frnn_scan<4, false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
@@ -565,10 +719,14 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
     }
     PSG_LAUNCHED();
     ++g_launches;
-    unsigned long long h[4];
-    PSG_CUDA(cudaMemcpyAsync(h, acc.p, 32, cudaMemcpyDeviceToHost, s));
+    unsigned long long h[5];
+    PSG_CUDA(cudaMemcpyAsync(h, acc.p, 40, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    if (h[0] <= cap) {
+    if (small_d && h[4] > bcap) {  // more rounding-band pairs than room: again with room for all
+      bcap = h[4];
+      continue;
+    }
+    if (no_list || h[0] <= cap) {
       run.count = h[0];
       run.hash = h[1];
       run.visited = h[2];
@@ -589,7 +747,7 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
 
 void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                 bool want_lists, psg_neighbor_result* out) {
-  FrnnRun run = frnn_run(ps, radius, q, f, seed, zone);
+  FrnnRun run = frnn_run(ps, radius, q, f, seed, zone, want_lists);
   cudaStream_t s = ctx().stream;
   finish_neighbors(run.pairs, run.count, ps->n, want_lists, out, s);
   out->pair_hash = run.hash;
@@ -602,7 +760,7 @@ void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
 
 void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                 uint64_t* pairs, uint64_t capacity, uint64_t* count, uint64_t* hash) {
-  FrnnRun run = frnn_run(ps, radius, q, f, seed, zone);
+  FrnnRun run = frnn_run(ps, radius, q, f, seed, zone, pairs && capacity);
   cudaStream_t s = ctx().stream;
   *count = run.count;
   *hash = run.hash;
