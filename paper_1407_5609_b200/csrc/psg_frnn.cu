@@ -6,15 +6,19 @@
 //                 implied by R (+ rounding slack): every pair within R sits in
 //                 the same or an adjacent cell; stable radix sort by cell, so a
 //                 point's forward half-stencil is <= 5 contiguous position ranges
-//   K4 scan       one thread per sorted position, warps iterate in lockstep over
-//                 their lanes' flattened ranges; d <= 4: coordinates gathered
-//                 into cell order (one float4 per point) and the FP32 distance
-//                 is the only filter; d > 4: all nk keys prune (lower bound) first.
+//   K4 scan       d <= 4 (k_frnn_cells): one warp per non-empty cell, lanes =
+//                 32 stencil candidates at a time against the cell's points in
+//                 shared memory; coordinates gathered into cell order (one
+//                 float4 per point), the FP32 distance is the only filter.
+//                 d > 4 (k_frnn_scan): one thread per sorted position, warps
+//                 iterate in lockstep over their lanes' ranges; all nk keys
+//                 prune (lower bound) before the distance.
 //                 The FP32 distance decides outside the rounding band, the
 //                 reference's FP64 arithmetic inside it (boundary inclusive,
-//                 <= R).  Pairs (min(i,j)<<32)|max(i,j) are appended through a
-//                 per-warp shared-memory buffer (one global atomic per 32
-//                 pairs) and hashed in-kernel (order-independent sum)
+//                 <= R; d <= 4: the rare band pairs go to k_frnn_band).  Pairs
+//                 (min(i,j)<<32)|max(i,j) are appended through a per-warp
+//                 shared-memory buffer (one global atomic per 32-128 pairs)
+//                 and hashed in-kernel (order-independent sum)
 //   lists         CSR without a global sort: per-row counts (atomics), scan,
 //                 scatter, then each row sorted by one warp (bitonic in
 //                 registers); the (i<j) pair list is the same with one direction
@@ -90,8 +94,8 @@ struct FrnnArgs {
   ExactSrc src;
   uint64_t* out;
   uint64_t cap;
-  unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined, [4] band pairs
-  uint64_t* band;           // k_frnn_scan_small: pairs inside the rounding band, decided by k_frnn_band
+  unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined, [4] band pairs, [5] cell cursor
+  uint64_t* band;           // k_frnn_cells: pairs inside the rounding band, decided by k_frnn_band
   uint64_t bcap;
 };
 
@@ -216,132 +220,179 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
   }
 }
 
-// d <= 4 (the C4 shape): the same walk over the flattened ranges, kFB
-// candidates per step with every coordinate load in flight before any math
-// (the one-at-a-time walk above is load-latency bound: one dependent L1/L2
-// load per candidate per lane).  Same decisions, same emitted set.
-#ifndef PSG_FRNN_FB
-#define PSG_FRNN_FB 4
-#endif
-constexpr int kFB = PSG_FRNN_FB;
-// kEmit = false (count + hash only): no pair buffer, no per-group atomics —
-// the single global counter was the kernel's serialisation point.
-template <bool kEmit>
-__global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan_small(FrnnArgs a) {
+// d <= 4, cell-cooperative: one warp per non-empty cell.  Every point of a
+// cell has the same stencil (the own row starts at the cell's first point;
+// a pair needs sorted position j > i, which every later row satisfies), so
+// the warp loads 32 stencil candidates at a time — lane = candidate, one
+// coalesced float4 each — and runs them against the cell's points, which sit
+// in shared memory and are read as broadcasts.  Compared with a thread per
+// point this removes the per-candidate range decode and the lanes idling on
+// their neighbours' longer stencils; the pair set, the FP32/FP64 decisions and
+// the counters are the same.  A warp takes 32 consecutive cells at once and
+// its lanes resolve those cells' ranges in parallel (one cfirst latency).
+// kD4: the fourth coordinate is used (d = 4); for d <= 3 it is zero in both
+// points and fmaf(0, 0, s) == s, so it is skipped without changing s32.
+// Warps claim 32-cell chunks from a counter (acc[5]): cells differ widely in
+// work (empty border cells vs full interior cells).
+template <bool kEmit, bool kD4, bool kZoned>
+__global__ void __launch_bounds__(kFrnnThreads, 4) k_frnn_cells(FrnnArgs a) {
   __shared__ GridParams sP;
-  constexpr int kFlush = 128;  // pairs per global atomic (list mode)
-  __shared__ uint64_t wbuf[kEmit ? kFrnnThreads / 32 : 1][kEmit ? kFlush + 32 * kFB : 1];
+  // accepted pairs are compacted into a per-warp buffer and hashed (and, in
+  // list mode, written with one global atomic) kFlush at a time, lane-parallel:
+  // hashing inside the divergent accept branch cost more than the distances
+  constexpr int kW = kFrnnThreads / 32, kFlush = kEmit ? 128 : 64;
+  __shared__ float4 cp[kW][32];
+  __shared__ uint32_t ci[kW][32];
+  __shared__ uint64_t wbuf[kW][kFlush + 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) sP = *a.grid.gp;
   __syncthreads();
-  const uint32_t p = blockIdx.x * kFrnnThreads + tid;
-  const bool valid = p < a.n;
-  uint64_t visited = 0, examined = 0, hsum = 0, emitted = 0;
-  GridFlat F{};
-  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint32_t mi = 0;
-  if (valid) {
-    F = grid_flat(grid_ranges(a.grid.cfirst, sP, p, a.grid.scell[p]));
-    mi = a.sidx[p];
-    me = a.sx[p];
-  }
-  const uint32_t dummy = valid ? p : 0u;
-  const bool zoned = a.zone > 1;
+  const uint64_t cells = sP.cells;
+  const uint32_t* __restrict__ cfirst = a.grid.cfirst;
   const unsigned lt = (1u << lane) - 1u;
   const float band = a.th.band, lo = a.lo;
+  uint64_t visited = 0, hsum = 0, emitted = 0;  // emitted: warp-uniform (list mode: acc[0] counts)
   int c = 0;  // warp-uniform fill of wbuf[w]
-  for (uint32_t t0 = 0; __any_sync(kFull, t0 < F.total); t0 += kFB) {
-    uint32_t jj[kFB];
-    float4 o[kFB];
-#pragma unroll
-    for (int u = 0; u < kFB; ++u) {
-      jj[u] = t0 + u < F.total ? F.at(t0 + u) : dummy;
-      o[u] = a.sx[jj[u]];
-    }
-    unsigned emit = 0;
-    uint64_t key[kFB];
-#pragma unroll
-    for (int u = 0; u < kFB; ++u) {
-      key[u] = 0;
-      if (t0 + u >= F.total) continue;
-      uint32_t mj = 0;
-      if (zoned) {
-        mj = a.sidx[jj[u]];
-        if (!admissible(mi, mj, a.zone)) continue;  // refscan.cpp:15-18
-      }
-      ++visited;
-      ++examined;
-      float g = o[u].x - me.x;
-      float s32 = g * g;
-      g = o[u].y - me.y;
-      s32 = fmaf(g, g, s32);
-      g = o[u].z - me.z;
-      s32 = fmaf(g, g, s32);
-      g = o[u].w - me.w;
-      s32 = fmaf(g, g, s32);
-      if (s32 <= band) {
-        if (!zoned) mj = a.sidx[jj[u]];  // the original index only inside the band
-        const uint64_t k = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
-        if (s32 <= lo) {  // inside R for certain
-          emit |= 1u << u;
-          key[u] = k;
-          hsum += mix64(k);
-        } else {  // the FP64 decision (rare) is deferred to k_frnn_band: keeps this loop's registers low
-          const unsigned long long slot = atomicAdd(a.acc + 4, 1ull);
-          if (slot < a.bcap) a.band[slot] = k;
-        }
-      }
-    }
-    if constexpr (!kEmit) {
-      emitted += __popc(emit);
-      continue;
-    }
-    // append this step's pairs (at most 32 kFB per warp) behind the c pending
-    int base = c;
-#pragma unroll
-    for (int u = 0; u < kFB; ++u) {
-      const unsigned mask = __ballot_sync(kFull, (emit >> u) & 1u);
-      if ((emit >> u) & 1u) wbuf[w][base + __popc(mask & lt)] = key[u];
-      base += __popc(mask);
-    }
-    c = base;
-    if (c >= kFlush) {  // flush whole groups of 32 with one atomic
-      __syncwarp();
-      const int full = c & ~31;
-      unsigned long long gpos = 0;
-      if (lane == 0) gpos = atomicAdd(a.acc, static_cast<unsigned long long>(full));
-      gpos = __shfl_sync(kFull, gpos, 0);
-      for (int k = lane; k < full; k += 32)
-        if (gpos + k < a.cap) a.out[gpos + k] = wbuf[w][k];
-      __syncwarp();
-      if (lane < c - full) wbuf[w][lane] = wbuf[w][full + lane];
-      c -= full;
-      __syncwarp();
-    }
-  }
-  if (kEmit && c > 0) {
+  // hash (and write) the first `cnt` buffered pairs; warp-converged
+  auto flush = [&](int cnt) {
     __syncwarp();
     unsigned long long gpos = 0;
-    if (lane == 0) gpos = atomicAdd(a.acc, static_cast<unsigned long long>(c));
-    gpos = __shfl_sync(kFull, gpos, 0);
-    for (int k = lane; k < c; k += 32)
-      if (gpos + k < a.cap) a.out[gpos + k] = wbuf[w][k];
+    if (kEmit && lane == 0) gpos = atomicAdd(a.acc, static_cast<unsigned long long>(cnt));
+    if constexpr (kEmit) gpos = __shfl_sync(kFull, gpos, 0);
+    for (int t = lane; t < cnt; t += 32) {
+      const uint64_t k = wbuf[w][t];
+      hsum += mix64(k);
+      if (kEmit && gpos + t < a.cap) a.out[gpos + t] = k;
+    }
+    emitted += cnt;
+    __syncwarp();
+  };
+  for (;;) {
+    unsigned long long claim = 0;
+    if (lane == 0) claim = atomicAdd(a.acc + 5, 1ull);
+    const uint64_t c0 = __shfl_sync(kFull, claim, 0) * 32ull;
+    if (c0 >= cells) break;
+    const uint64_t mycell = c0 + lane;
+    uint32_t s = 0, e = 0;
+    if (mycell < cells) {
+      s = cfirst[mycell];
+      e = cfirst[mycell + 1];
+    }
+    GridRanges mine{};
+    if (e > s) mine = grid_ranges(cfirst, sP, s, static_cast<uint32_t>(mycell));
+    unsigned todo = __ballot_sync(kFull, e > s);
+    while (todo) {
+      const int k = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t cs = __shfl_sync(kFull, s, k), ce = __shfl_sync(kFull, e, k);
+      GridRanges R;
+      R.e0 = __shfl_sync(kFull, mine.e0, k);
+      R.b1 = __shfl_sync(kFull, mine.b1, k);
+      R.e1 = __shfl_sync(kFull, mine.e1, k);
+      R.b2 = __shfl_sync(kFull, mine.b2, k);
+      R.e2 = __shfl_sync(kFull, mine.e2, k);
+      R.b3 = __shfl_sync(kFull, mine.b3, k);
+      R.e3 = __shfl_sync(kFull, mine.e3, k);
+      R.b4 = __shfl_sync(kFull, mine.b4, k);
+      R.e4 = __shfl_sync(kFull, mine.e4, k);
+      for (uint32_t g0 = cs; g0 < ce; g0 += 32) {  // the cell's points, 32 at a time
+        const int m = static_cast<int>(min(32u, ce - g0));
+        R.b0 = g0 + 1;  // no candidate at or before the group's first point pairs with it
+        const GridFlat F = grid_flat(R);
+        // the group's points and the first candidate chunk are loaded together;
+        // each chunk's loads are issued before the previous chunk's math
+        float4 gx = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t gi = 0;
+        if (lane < m) {
+          gx = a.sx[g0 + lane];
+          gi = a.sidx[g0 + lane];
+        }
+        bool in = static_cast<uint32_t>(lane) < F.total;
+        uint32_t j = in ? F.at(lane) : g0;
+        float4 o = a.sx[j];
+        uint32_t mj = a.sidx[j];
+        __syncwarp();
+        if (lane < m) {
+          cp[w][lane] = gx;
+          ci[w][lane] = gi;
+        }
+        __syncwarp();
+        uint32_t vis = 0;
+        for (uint32_t t0 = 0; t0 < F.total; t0 += 32) {
+          const bool in2 = t0 + 32 + lane < F.total;
+          const uint32_t j2 = in2 ? F.at(t0 + 32 + lane) : g0;
+          float4 o2 = o;
+          uint32_t mj2 = mj;
+          if (t0 + 32 < F.total) {
+            o2 = a.sx[j2];
+            mj2 = a.sidx[j2];
+          }
+          for (int q = 0; q < m; ++q) {
+            const float4 x = cp[w][q];
+            const uint32_t pi = g0 + q;
+            bool ok = in && j > pi;
+            if constexpr (kZoned) ok = ok && admissible(ci[w][q], mj, a.zone);  // refscan.cpp:15-18
+            float g = o.x - x.x;
+            float s32 = g * g;
+            g = o.y - x.y;
+            s32 = fmaf(g, g, s32);
+            g = o.z - x.z;
+            s32 = fmaf(g, g, s32);
+            if constexpr (kD4) {
+              g = o.w - x.w;
+              s32 = fmaf(g, g, s32);
+            }
+            vis += ok;
+            const bool emit = ok && s32 <= lo;  // inside R for certain
+            if (ok && s32 <= band && !emit) {  // the reference's FP64 decision, deferred to k_frnn_band (rare)
+              const uint32_t mi = ci[w][q];
+              const uint64_t key =
+                  mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
+              const unsigned long long slot = atomicAdd(a.acc + 4, 1ull);
+              if (slot < a.bcap) a.band[slot] = key;
+            }
+            const unsigned mask = __ballot_sync(kFull, emit);
+            if (mask) {
+              if (emit) {
+                const uint32_t mi = ci[w][q];
+                wbuf[w][c + __popc(mask & lt)] =
+                    mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
+              }
+              c += __popc(mask);
+              if (c >= kFlush) {
+                flush(kFlush);
+                if (lane < c - kFlush) wbuf[w][lane] = wbuf[w][kFlush + lane];
+                c -= kFlush;
+                __syncwarp();
+              }
+            }
+          }
+          in = in2;
+          j = j2;
+          o = o2;
+          mj = mj2;
+        }
+        visited += vis;
+        __syncwarp();  // cp/ci are rewritten by the next group
+      }
+    }
   }
+  if (c > 0) flush(c);
   for (int o = 16; o; o >>= 1) {
     hsum += __shfl_xor_sync(kFull, hsum, o);
     visited += __shfl_xor_sync(kFull, visited, o);
-    examined += __shfl_xor_sync(kFull, examined, o);
-    if constexpr (!kEmit) emitted += __shfl_xor_sync(kFull, emitted, o);
   }
   if (lane == 0) {
     if (!kEmit && emitted) atomicAdd(a.acc, static_cast<unsigned long long>(emitted));
     if (hsum) atomicAdd(a.acc + 1, static_cast<unsigned long long>(hsum));
-    if (visited) atomicAdd(a.acc + 2, static_cast<unsigned long long>(visited));
-    if (examined) atomicAdd(a.acc + 3, static_cast<unsigned long long>(examined));
+    if (visited) {
+      atomicAdd(a.acc + 2, static_cast<unsigned long long>(visited));
+      atomicAdd(a.acc + 3, static_cast<unsigned long long>(visited));
+    }
   }
 }
 
-// The rounding-band pairs of k_frnn_scan_small: the reference's FP64
+// The rounding-band pairs of k_frnn_cells: the reference's FP64
 // distance (metrics.cpp:16-24, symmetric in i, j), boundary inclusive (<= R)
 __global__ void k_frnn_band(FrnnArgs a) {
   const unsigned long long m = min(static_cast<unsigned long long>(a.acc[4]), static_cast<unsigned long long>(a.bcap));
@@ -641,6 +692,7 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   const int g = std::min(3, dir.q);
   GridIndex gi;
   gi.ensure(static_cast<uint32_t>(n), nk, s);
+  uint64_t ncells = 1;
   {
     DevBuf<unsigned> mm(6, s);
     const unsigned init[6] = {~0u, ~0u, ~0u, 0u, 0u, 0u};
@@ -662,6 +714,7 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
     }
     GridParams gp;
     grid_params_for(gp, std::max(g, 1), static_cast<double>(th.win) * (1.0 + 1e-6), lo3, span);
+    ncells = gp.cells;
     PSG_CUDA(cudaMemcpyAsync(gi.gp.p, &gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
   }
   build_grid(keys.p, static_cast<uint32_t>(n), nk, gi, 24, s);
@@ -688,7 +741,7 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   a.lo = lo;
   a.R = radius;
   a.src = ps->exact();
-  DevBuf<unsigned long long> acc(5, s);
+  DevBuf<unsigned long long> acc(6, s);
   // count-only runs of the small-d scan never write pairs
   const bool no_list = small_d && !emit;
   uint64_t cap = no_list ? 0 : std::max<uint64_t>(1u << 20, 24 * n);
@@ -696,7 +749,7 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   DevBuf<uint64_t> band;
   for (;;) {
     run.pairs.alloc(std::max<uint64_t>(cap, 1), s);
-    PSG_CUDA(cudaMemsetAsync(acc.p, 0, 40, s));
+    PSG_CUDA(cudaMemsetAsync(acc.p, 0, 48, s));
     a.out = run.pairs.p;
     a.cap = cap;
     a.acc = acc.p;
@@ -704,10 +757,19 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
       if (band.n < bcap) band.alloc(bcap, s);
       a.band = band.p;
       a.bcap = bcap;
-      if (no_list)
-        k_frnn_scan_small<false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
-      else
-        k_frnn_scan_small<true><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+      const unsigned cb = static_cast<unsigned>(
+          std::min<uint64_t>((ncells + 32 * (kFrnnThreads / 32) - 1) / (32 * (kFrnnThreads / 32)), c.sm_count * 4ull));
+      const int v = (no_list ? 0 : 4) + (ps->d == 4 ? 2 : 0) + (zone > 1 ? 1 : 0);
+      switch (v) {
+        case 0: k_frnn_cells<false, false, false><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        case 1: k_frnn_cells<false, false, true><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        case 2: k_frnn_cells<false, true, false><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        case 3: k_frnn_cells<false, true, true><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        case 4: k_frnn_cells<true, false, false><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        case 5: k_frnn_cells<true, false, true><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        case 6: k_frnn_cells<true, true, false><<<cb, kFrnnThreads, 0, s>>>(a); break;
+        default: k_frnn_cells<true, true, true><<<cb, kFrnnThreads, 0, s>>>(a); break;
+      }
       PSG_LAUNCHED();
       ++g_launches;
       k_frnn_band<<<c.sm_count * 2, 256, 0, s>>>(a);
