@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
     }
   }
   __syncthreads();
-  double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
+  double lo[kMaxGridKeys] = {}, span[kMaxGridKeys] = {};
   if (tid == 0)
     for (int t = 0; t < sa.gbox; ++t) {
       lo[t] = s_lo[t];
@@ -1229,11 +1229,14 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       const int gd = std::min(plan.dir.q, dense_keys);
       if (plan.dense && plan.g < gd) {
         // Dense: rebuild the cells on more keys at the same width (still >=
-        // the bound's key window): in 3 projected keys clusters overlap, in 6
-        // they separate, so cell pairs stop mixing clusters.
-        grid_params_for(plan.gp, gd, plan.gp.w, W.host_st->box_lo, W.host_st->box_span);
+        // the bound's key window): in 3 projected keys clusters overlap; every
+        // further key divides the clusters a cell pair mixes by ~2.5 (C5:
+        // 4 -> 5 -> 6 keys = 5.0e12 -> 1.9e12 -> 7.7e11 tile pairs).  Up to 8
+        // keys and 2^27 cells (the table is a 512 MiB radix-sorted grid).
+        grid_params_for(plan.gp, gd, plan.gp.w, W.host_st->box_lo, W.host_st->box_span, kMaxDenseCells);
         PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
-        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s, /*counting=*/false);  // large cells
+        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s, /*counting=*/false,
+                   plan.gp.cells);  // large cells
         plan.g = gd;
         tm.mark("dense grid");
       }
@@ -1255,9 +1258,11 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         const double need =
             static_cast<double>(budget_thresholds_s32(plan.bud, bound).win) * (1.0 + 2e-5);
         if (!(need < 1e300)) throw std::runtime_error("closest_pair: no finite bound before the scan");
-        grid_params_for(plan.gp, plan.g, need, h.box_lo, h.box_span);
+        const bool dense_grid = plan.g > 3;  // the dense engine's grid (more keys, radix-sorted, up to 2^27 cells)
+        grid_params_for(plan.gp, plan.g, need, h.box_lo, h.box_span, dense_grid ? kMaxDenseCells : kMaxCells);
         PSG_CUDA(cudaMemcpyAsync(W.gi.gp.p, &plan.gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
-        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s);
+        build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s, !dense_grid,
+                   dense_grid ? plan.gp.cells : 0);
         tm.mark("regrid");
         if (nparts != 1) break;  // every rank must derive the same grid from the shared bound
         ScanArgs a = make_args(plan);

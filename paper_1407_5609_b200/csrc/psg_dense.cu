@@ -337,18 +337,18 @@ __global__ void __launch_bounds__(256) k_dense_tiles(ScanArgs a, const float* __
 // work and the exact path stays bit-identical.
 //
 // Warp roles: 0-3 loaders (one row per thread: shift, norm, swizzled store;
-// A once per strip, then the strip's B tiles), 4 MMA issuer (one thread), 5
+// A once per strip into one of two TMEM buffers, then the strip's B tiles), 4 MMA issuer (one thread), 5
 // TMEM allocation, 8-11 epilogue (tcgen05.ld 32x32b: thread = A row).  A strip
 // = one A tile of a kept cell pair against every B tile of the pair (self
 // pairs: tiles tj >= ti); strips are taken from a global cursor.
 constexpr int kGT = 128;  // A tile rows (UMMA M)
 constexpr int kGN = 128;       // B tile rows (UMMA N)
-constexpr int kGAB = 1;        // A buffers (hi + lo, in TMEM)
+constexpr int kGAB = 2;        // A buffers (hi + lo, in TMEM): the next strip's A is written while the last one's MMAs run
 constexpr int kGBB = 3;        // B buffers (hi + lo, in shared memory)
-constexpr int kMaxPartners = 366;  // the own cell + the (3^6 - 1)/2 forward stencil cells
+constexpr int kMaxPartners = 366;  // pairs per group (k_group_flags splits longer runs of one A)
 constexpr int kGThreads = 512;  // warps 0-3 loaders, 4 MMA, 5 TMEM + strip scheduler, 8-15 epilogue
 constexpr int kGEpi = 8;        // epilogue warps: two per TMEM lane quarter, 64 columns each
-constexpr uint32_t kGTmemCols = 512;   // [0, 256) 2 accumulators; [256, 256 + 2D) the A tile, hi | lo
+constexpr uint32_t kGTmemCols = 512;   // [0, 256) 2 accumulators; [256 + 2D b, 256 + 2D (b+1)) A buffer b, hi | lo
 constexpr uint32_t kGAcol = 2 * kGN;
 
 // Slack of the filter value per unit of (|a'|^2 + |b'|^2):
@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                  unsigned long long* __restrict__ cursor) {
   using namespace tc;
   constexpr int NC = D / 32;
+  static_assert(kGAcol + kGAB * 2 * D <= kGTmemCols, "accumulators + A buffers exceed the TMEM allocation");
   extern __shared__ uint8_t graw[];
   // 1024-aligned by offsetting the shared array itself (not via an integer
   // cast), so every sm.* access stays a shared-memory (LDS/STS) access
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         {
           const bool va = static_cast<uint32_t>(r) < alen;
           const float4* src = reinterpret_cast<const float4*>(Xs + static_cast<size_t>(a0 + (va ? r : 0)) * D);
-          const uint32_t lane_base = tmem + ((32u * warp) << 16) + kGAcol;
+          const uint32_t lane_base = tmem + ((32u * warp) << 16) + kGAcol + ab * 2u * D;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t hi[32], lo[32];
@@ -706,7 +707,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {  // 3xTF32: hi.hi + hi.lo + lo.hi; A from TMEM, B from smem
-          const uint32_t ah = tmem + kGAcol + c * 32, al = tmem + kGAcol + D + c * 32;
+          const uint32_t ah = tmem + kGAcol + m.abuf * 2u * D + c * 32, al = ah + D;
           const uint64_t bh = sw128_desc(smem_u32(sm.B[bb][0] + c * (kGN * 32)));
           const uint64_t bl = sw128_desc(smem_u32(sm.B[bb][1] + c * (kGN * 32)));
           umma_tf32_ts_3x_chunk32(dcol, ah, al, bh, bl, idesc, c != 0);
@@ -863,7 +864,7 @@ void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, con
     }
     configured = true;
   }
-  k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.cfirst.p, pa, pb, w.gstart.p,
+  k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.dev.cfirst, pa, pb, w.gstart.p,
                                                            w.gprefix.p, reinterpret_cast<const uint32_t*>(w.ctr.p + 3),
                                                            npairs, part, nparts, w.ctr.p + 1);
   PSG_LAUNCHED();
@@ -884,9 +885,29 @@ __global__ void k_group_strips(const uint32_t* __restrict__ pa, const uint32_t* 
 
 // Group flags of the pairs sorted by A: flags[k] = 1 at the first pair of a group
 // (flags[npairs] = 0); after an exclusive scan, the group index of its first pair.
+// A group is an A cell with at most kMaxPartners of its kept pairs (the own
+// pair first): an A with more (up to 3^8/2 stencil cells) spans several groups.
 __global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ flags) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= npairs; k += gridDim.x * blockDim.x)
-    flags[k] = k < npairs && (k == 0 || pa[k] != pa[k - 1]);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= npairs; k += gridDim.x * blockDim.x) {
+    uint32_t f = 0;
+    if (k < npairs) {
+      if (k == 0 || pa[k] != pa[k - 1]) {
+        f = 1;
+      } else {  // rank inside A's run: first index with pa == pa[k] (binary search, pa sorted)
+        const uint32_t A = pa[k];
+        uint32_t lo = 0, hi = k;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (pa[mid] < A)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        f = (k - lo) % kMaxPartners == 0;
+      }
+    }
+    flags[k] = f;
+  }
 }
 
 __global__ void k_group_scatter(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ gidx, uint32_t npairs,
@@ -915,7 +936,7 @@ bool gram_shape(int d) { return d == 32 || d == 64; }
 uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s) {
   DevBuf<unsigned long long> est(1, s);
   PSG_CUDA(cudaMemsetAsync(est.p, 0, 8, s));
-  k_estimate<<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(gi.cfirst.p, gi.gp.p, cells, est.p);
+  k_estimate<<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, cells, est.p);
   PSG_LAUNCHED();
   ++g_launches;
   unsigned long long h = 0;
@@ -936,10 +957,10 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   k_gather_rows<<<sms * 16, 256, 0, s>>>(X, gi.sidx.p, n, d, w.Xs.p);
   PSG_LAUNCHED();
   if (nk == 4)
-    k_cell_boxes<4><<<static_cast<unsigned>(std::min<uint64_t>(cells, 65535)), 256, 0, s>>>(gi.skeys.p, gi.cfirst.p,
+    k_cell_boxes<4><<<static_cast<unsigned>(std::min<uint64_t>(cells, 65535)), 256, 0, s>>>(gi.skeys.p, gi.dev.cfirst,
                                                                                             cells, w.cbox.p);
   else
-    k_cell_boxes<8><<<static_cast<unsigned>(std::min<uint64_t>(cells, 65535)), 256, 0, s>>>(gi.skeys.p, gi.cfirst.p,
+    k_cell_boxes<8><<<static_cast<unsigned>(std::min<uint64_t>(cells, 65535)), 256, 0, s>>>(gi.skeys.p, gi.dev.cfirst,
                                                                                             cells, w.cbox.p);
   PSG_LAUNCHED();
   g_launches += 2;
@@ -957,10 +978,10 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     PSG_CUDA(cudaMemsetAsync(w.ctr.p, 0, 32, s));
     if (nk == 4)
       k_cell_pairs<4><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
-          gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
+          gi.dev.cfirst, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
     else
       k_cell_pairs<8><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
-          gi.cfirst.p, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
+          gi.dev.cfirst, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
     PSG_LAUNCHED();
     ++g_launches;
     PSG_CUDA(cudaMemcpyAsync(&npairs, w.ctr.p, 8, cudaMemcpyDeviceToHost, s));
@@ -1001,7 +1022,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     if (w.gprefix.n < ng + 1) w.gprefix.alloc(ng + 1, s);
     if (w.gstrips.n < ng + 1) w.gstrips.alloc(ng + 1, s);
     if (w.gtmp.n < scan_temp_words(ng + 1)) w.gtmp.alloc(scan_temp_words(ng + 1), s);
-    k_group_strips<<<blocks(ng + 1, 256), 256, 0, s>>>(spa, w.gstart.p, ng, gi.cfirst.p, w.gstrips.p);
+    k_group_strips<<<blocks(ng + 1, 256), 256, 0, s>>>(spa, w.gstart.p, ng, gi.dev.cfirst, w.gstrips.p);
     PSG_LAUNCHED();
     exclusive_scan_u32(w.gstrips.p, w.gprefix.p, ng + 1, w.gtmp.p, s);
     g_launches += 9;
@@ -1018,11 +1039,11 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     }
   } else {
     // tiles per sorted pair -> prefix (scr0[npairs] = 0 so prefix[npairs] = total)
-    k_pair_tiles<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, spb, np32, gi.cfirst.p, scr0);
+    k_pair_tiles<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, spb, np32, gi.dev.cfirst, scr0);
     PSG_LAUNCHED();
     exclusive_scan_u32(scr0, scr1, npairs + 1, w.stmp.p, s);
     g_launches += 4;
-    k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.cfirst.p, spa, spb, scr1, np32, part, nparts, w.ctr.p + 1);
+    k_dense_tiles<<<sms * 2, 256, 0, s>>>(a, w.Xs.p, gi.dev.cfirst, spa, spb, scr1, np32, part, nparts, w.ctr.p + 1);
     PSG_LAUNCHED();
   }
   ++g_launches;

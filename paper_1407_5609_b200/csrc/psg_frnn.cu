@@ -707,7 +707,7 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
     unsigned h[6];
     PSG_CUDA(cudaMemcpyAsync(h, mm.p, 24, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    double lo3[kMaxGridKeys] = {0, 0, 0, 0, 0, 0}, span[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
+    double lo3[kMaxGridKeys] = {}, span[kMaxGridKeys] = {};
     for (int t = 0; t < g; ++t) {
       lo3[t] = f32_unorder(h[t]);
       span[t] = std::max(static_cast<double>(f32_unorder(h[3 + t])) - lo3[t], 1e-30);

@@ -367,7 +367,8 @@ void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double 
   }
 }
 
-void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s, bool counting) {
+void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s, bool counting,
+                uint64_t dense_cells) {
   if (counting) {
     const unsigned nb = blocks(n, 256);
     if (nk == 4)
@@ -413,13 +414,19 @@ void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_b
   PSG_LAUNCHED();
   uint32_t* kk[2] = {gi.cid0.p, gi.cid1.p};
   uint32_t* vv[2] = {gi.idx0.p, gi.idx1.p};
+  uint32_t* cfirst = gi.cfirst.p;
+  if (dense_cells > kMaxCells) {
+    if (gi.dcfirst.n < dense_cells + 1) gi.dcfirst.alloc(dense_cells + 1, s);
+    cfirst = gi.dcfirst.p;
+    while ((1ull << sort_bits) < dense_cells) ++sort_bits;
+  }
   const int passes = (sort_bits + 7) / 8;
   const int which = radix_sort<uint32_t>(kk, vv, n, 0, passes * 8, gi.hist.p, s);
   // every warp resident at once: the binary searches overlap
-  k_cfirst<<<2 * 148 * 8, 256, 0, s>>>(kk[which], n, gi.gp.p, gi.cfirst.p);
+  k_cfirst<<<2 * 148 * 8, 256, 0, s>>>(kk[which], n, gi.gp.p, cfirst);
   PSG_LAUNCHED();
 #ifdef PSG_DEBUG_SYNC
-  k_verify_cfirst<<<1024, 256, 0, s>>>(kk[which], n, gi.gp.p, gi.cfirst.p);
+  k_verify_cfirst<<<1024, 256, 0, s>>>(kk[which], n, gi.gp.p, cfirst);
   PSG_LAUNCHED();
 #endif
   if (nk == 4)
@@ -431,7 +438,7 @@ void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_b
   gi.dev.skeys = gi.skeys.p;
   gi.dev.sidx = gi.sidx.p;
   gi.dev.scell = kk[which];
-  gi.dev.cfirst = gi.cfirst.p;
+  gi.dev.cfirst = cfirst;
   gi.dev.gp = gi.gp.p;
   gi.dev.n = n;
 }

@@ -17,6 +17,8 @@
 namespace psg {
 
 constexpr uint64_t kMaxCells = 1ull << 24;
+// the dense engine's radix-sorted grids over up to 8 keys (cfirst: 512 MiB)
+constexpr uint64_t kMaxDenseCells = 1ull << 27;
 constexpr uint32_t kGridSample = 4096;  // keys sampled (hashed positions) for the key box
 
 // q = x / d for x < 2^31 by multiply-high (CUTLASS-style FastDivmod).
@@ -43,26 +45,26 @@ struct FastDiv {
   __device__ __forceinline__ uint32_t div(uint32_t x) const { return d == 1 ? x : (__umulhi(x, m) >> s); }
 };
 
-constexpr int kMaxGridKeys = 6;  // sparse engine uses g <= 3; the dense engine up to 6
+constexpr int kMaxGridKeys = 8;  // sparse engine uses g <= 3; the dense engine up to 8
 
 struct GridParams {
   int g = 1;
-  uint32_t dims[kMaxGridKeys] = {1, 1, 1, 1, 1, 1};
-  double lo[kMaxGridKeys] = {0, 0, 0, 0, 0, 0};
+  uint32_t dims[kMaxGridKeys] = {1, 1, 1, 1, 1, 1, 1, 1};
+  double lo[kMaxGridKeys] = {};
   double w = 1.0, inv_w = 1.0;
   uint64_t cells = 1;
   FastDiv fD, f1;  // division by the last dim and by dims[1] (g <= 3)
 };
 
 // Fill dims/cells/divisors for width >= w over the box (widened until the dense
-// cell table fits kMaxCells).  Host and device.  lo/span have >= g entries.
+// cell table fits max_cells).  Host and device.  lo/span have >= g entries.
 __host__ __device__ inline void grid_params_for(GridParams& gp, int g, double w, const double* lo,
-                                                const double* span) {
+                                                const double* span, uint64_t max_cells = kMaxCells) {
   gp.g = g;
   for (;;) {
     double cells = 1.0;
     for (int t = 0; t < g; ++t) cells *= floor(span[t] / w) + 1.0;
-    if (cells <= static_cast<double>(kMaxCells)) break;
+    if (cells <= static_cast<double>(max_cells)) break;
     w *= 1.25;
   }
   gp.w = w;
@@ -92,6 +94,7 @@ struct GridIndex {
   uint32_t n = 0;
   DevBuf<float> skeys;
   DevBuf<uint32_t> sidx, cid0, cid1, idx0, idx1, hist, cfirst;
+  DevBuf<uint32_t> dcfirst;  // cfirst of a dense grid with more than kMaxCells cells
   // counting build: per-cell counters (kept all-zero between builds), the
   // scan's temp, the list of cells too big for the per-position fix-up, and
   // two device counters (big-cell count, cursor)
@@ -109,8 +112,10 @@ struct GridIndex {
 // fix-up that ranks each point inside its cell by original index.
 // counting = false (the dense engine's large cells): stable LSD radix sort on
 // sort_bits, cfirst by search of the sorted ids.  Both give the same order.
+// dense_cells (counting = false): the grid's cell count when the host knows
+// it; above kMaxCells the table goes to gi.dcfirst and the sort covers its bits.
 void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s,
-                bool counting = true);
+                bool counting = true, uint64_t dense_cells = 0);
 // Strided sample of the first g keys into gi.sample (g x m floats); returns m.
 uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s);
 // Host-side box from a host copy of the sample (mean +- 3 sd, clipped).

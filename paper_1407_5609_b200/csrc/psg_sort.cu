@@ -261,70 +261,89 @@ __device__ __forceinline__ size_t scan_count(size_t count, const uint64_t* dcell
   return dcells ? static_cast<size_t>(*dcells) + 1 : count;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint32_t* __restrict__ in, size_t count,
-                                                             const uint64_t* __restrict__ dcells,
-                                                             uint32_t* __restrict__ sums) {
-  __shared__ uint32_t ws[33];
-  count = scan_count(count, dcells);
-  if (static_cast<size_t>(blockIdx.x) * kScanTile >= count) return;
-  const size_t base = static_cast<size_t>(blockIdx.x) * kScanTile + static_cast<size_t>(threadIdx.x) * kScanItems;
-  uint32_t v = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) v += base + i < count ? in[base + i] : 0u;
-  uint32_t total;
-  block_exclusive(v, ws, total);
-  if (threadIdx.x == 0) sums[blockIdx.x] = total;
-}
+// Single pass (decoupled look-back): each block claims the next tile from a
+// ticket, scans its 4096 values (one 16-byte load per thread), publishes its
+// aggregate, then one warp looks back over its predecessors' status words
+// (flag in the top bits, value in the low 32; zeroed before the launch) until
+// it reaches an inclusive prefix.  Reads the input once and writes the output
+// once (the three-kernel tile/top/apply scan read it twice).
+constexpr uint64_t kScanAgg = 1ull << 62, kScanInc = 2ull << 62;
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_top(uint32_t* __restrict__ sums, size_t count,
-                                                           const uint64_t* __restrict__ dcells) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const uint32_t* __restrict__ in, size_t count,
+                                                                const uint64_t* __restrict__ dcells,
+                                                                unsigned long long* __restrict__ status,
+                                                                uint32_t* __restrict__ ticket,
+                                                                uint32_t* __restrict__ out) {
   __shared__ uint32_t ws[33];
+  __shared__ uint32_t tile_s, prefix_s;
   count = scan_count(count, dcells);
-  const int nb = static_cast<int>((count + kScanTile - 1) / kScanTile);
-  constexpr int kPer = 8;  // up to 8192 tiles
-  uint32_t v[kPer], s = 0;
+  if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = tile_s;
+  if (static_cast<size_t>(tile) * kScanTile >= count) return;
+  const size_t base = static_cast<size_t>(tile) * kScanTile + static_cast<size_t>(threadIdx.x) * kScanItems;
+  uint32_t v[kScanItems];
+  if (base + kScanItems <= count) {
+    const uint4 q = *reinterpret_cast<const uint4*>(in + base);
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+  } else {
 #pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int k = threadIdx.x * kPer + i;
-    v[i] = k < nb ? sums[k] : 0u;
-    s += v[i];
+    for (int i = 0; i < kScanItems; ++i) v[i] = base + i < count ? in[base + i] : 0u;
   }
+  const uint32_t sum = v[0] + v[1] + v[2] + v[3];
   uint32_t total;
-  uint32_t run = block_exclusive(s, ws, total);
+  const uint32_t excl = block_exclusive(sum, ws, total);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) atomicExch(status, kScanInc | total);
+    } else {
+      if (lane == 0) atomicExch(status + tile, kScanAgg | total);
+      const volatile unsigned long long* st = status;
+      int64_t t0 = static_cast<int64_t>(tile) - 1;
+      for (;;) {
+        const int64_t idx = t0 - lane;
+        unsigned long long w = idx >= 0 ? st[idx] : (kScanInc | 0ull);
+        while (__any_sync(0xffffffffu, (w >> 62) == 0))  // a predecessor has not published yet
+          if ((w >> 62) == 0) w = st[idx];
+        const unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive prefix, or the whole window
+        uint32_t part = lane <= stop ? static_cast<uint32_t>(w) : 0u;
 #pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int k = threadIdx.x * kPer + i;
-    if (k < nb) sums[k] = run;
-    run += v[i];
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        prefix += part;
+        if (inc) break;
+        t0 -= 32;
+      }
+      if (lane == 0) atomicExch(status + tile, kScanInc | static_cast<uint32_t>(prefix + total));
+    }
+    if (lane == 0) prefix_s = prefix;
   }
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __restrict__ in, size_t count,
-                                                             const uint64_t* __restrict__ dcells,
-                                                             const uint32_t* __restrict__ sums,
-                                                             uint32_t* __restrict__ out) {
-  __shared__ uint32_t ws[33];
-  count = scan_count(count, dcells);
-  if (static_cast<size_t>(blockIdx.x) * kScanTile >= count) return;
-  const size_t base = static_cast<size_t>(blockIdx.x) * kScanTile + static_cast<size_t>(threadIdx.x) * kScanItems;
-  uint32_t v[kScanItems], s = 0;
+  __syncthreads();
+  uint32_t run = excl + prefix_s;
+  uint32_t o[kScanItems];
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    v[i] = base + i < count ? in[base + i] : 0u;
-    s += v[i];
-  }
-  uint32_t total;
-  uint32_t run = block_exclusive(s, ws, total) + sums[blockIdx.x];
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    if (base + i < count) out[base + i] = run;
+    o[i] = run;
     run += v[i];
+  }
+  if (base + kScanItems <= count) {
+    *reinterpret_cast<uint4*>(out + base) = make_uint4(o[0], o[1], o[2], o[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+      if (base + i < count) out[base + i] = o[i];
   }
 }
 
 }  // namespace
 
-size_t scan_temp_words(size_t count) { return (count + kScanTile - 1) / kScanTile + 1; }
+// temp layout: [tiles + 1 u64 status words][ticket]
+size_t scan_temp_words(size_t count) { return 2 * ((count + kScanTile - 1) / kScanTile + 1) + 2; }
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_t* temp, cudaStream_t s) {
   exclusive_scan_u32_dev(in, out, count, nullptr, temp, s);
@@ -333,13 +352,14 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_
 void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count, const uint64_t* dcells,
                             uint32_t* temp, cudaStream_t s) {
   if (max_count == 0) return;
-  const int nb = static_cast<int>((max_count + kScanTile - 1) / kScanTile);
-  if (nb > 8 * kScanThreads) throw std::runtime_error("exclusive_scan_u32: input too large");
-  k_scan_tiles<<<nb, kScanThreads, 0, s>>>(in, max_count, dcells, temp);
-  PSG_LAUNCHED();
-  k_scan_top<<<1, kScanThreads, 0, s>>>(temp, max_count, dcells);
-  PSG_LAUNCHED();
-  k_scan_apply<<<nb, kScanThreads, 0, s>>>(in, max_count, dcells, temp, out);
+  const size_t nb = (max_count + kScanTile - 1) / kScanTile;
+  if (reinterpret_cast<uintptr_t>(in) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+    throw std::runtime_error("exclusive_scan_u32: buffers must be 16-byte aligned");
+  const size_t words = scan_temp_words(max_count);
+  PSG_CUDA(cudaMemsetAsync(temp, 0, words * sizeof(uint32_t), s));
+  auto* status = reinterpret_cast<unsigned long long*>(temp);
+  k_scan_lookback<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, max_count, dcells, status,
+                                                                     temp + 2 * (nb + 1), out);
   PSG_LAUNCHED();
 }
 

@@ -17,8 +17,8 @@ namespace psg {
 size_t radix_hist_words(size_t n);
 
 // out[i] = in[0] + ... + in[i-1] (u32), count <= 2^25; `temp` needs
-// scan_temp_words(count) words.  Three kernels: tile sums, scan of the tile
-// sums (one block), tile scans with the carried-in offset.
+// scan_temp_words(count) words.  One single-pass kernel (decoupled
+// look-back) after a memset of the temp; in/out 16-byte aligned.
 size_t scan_temp_words(size_t count);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_t* temp, cudaStream_t s);
 // Same with the length read on device: count = *dcells + 1 (<= max_count).
