@@ -167,6 +167,39 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------------
+C4_N, C4_R = 1 << 22, float.fromhex("0x1.902ce9269f6dp-7")
+C4_EXPECT = (66173431, 8231864707796938076)  # oracle cell-grid FRNN (tests/test_gpu_fullsize.py)
+
+
+def candidate_kernel_c4(hbm_gbs, peak_kind, reps=3):
+    """North-star check of the candidate-distance kernel where it is the hot
+    spot: C4 (FRNN, n=2^22, d=3, ~32 neighbours), count + hash on a resident
+    point set.  SURVEY §8(d) streaming model: one candidate = one d-dim FP32
+    distance streaming 4d bytes, so the roofline is HBM / 4d candidates/s
+    (546 G/s at d=3).  Kernel time = the scan stage's CUDA events (the cell
+    scan + the rounding-band kernel) on the library stream."""
+    import paper_1407_5609_b200 as psg
+
+    pc = psg.PointSet.from_flat(psg.gen.uniform(4, C4_N, 3), 3)
+    psg.fixed_radius_neighbors(pc, C4_R, Q, F, SEED, 0, want_lists=False)  # warm-up
+    ms, cands, ok = [], 0, True
+    for _ in range(reps):
+        r = psg.fixed_radius_neighbors(pc, C4_R, Q, F, SEED, 0, want_lists=False)
+        p = psg.last_profile()
+        ms.append(dict(p["stage_list"])["scan"])
+        cands = p["window_pairs"]
+        ok = ok and (r.pair_count, r.pair_hash) == C4_EXPECT
+    t = min(ms)
+    rate = cands / (t / 1e3)
+    roof = hbm_gbs * 1e9 / (4 * 3)
+    return {"kernel": "k_frnn_cells (+ k_frnn_band)", "config": "C4 FRNN n=2^22 d=3 R=cbrt(3*32/(4 pi n)), count+hash",
+            "candidates_per_launch": cands, "kernel_ms": t, "candidates_per_s": rate,
+            "roofline_candidates_per_s": roof, "frac": rate / roof, "achieved_gbs": rate * 12 / 1e9,
+            "peak": hbm_gbs, "peak_source": peak_kind,
+            "model": "SURVEY 8(d): 4d B per candidate (streaming); candidates are re-read from L1/L2, so true DRAM traffic is far lower",
+            "pairs": r.pair_count, "correct": ok}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -335,6 +368,9 @@ def run_ours(args, rank, world, local_rank):
         "correct": ok, "answer": {"planted": planted, "got": [results[-1].index_i, results[-1].index_j],
                                   "distance": results[-1].distance},
     }
+    if world == 1 and rank == 0 and not args.no_candidate_kernel:
+        line["candidate_kernel"] = candidate_kernel_c4(hbm, peak_kind)
+        line["correct"] = line["correct"] and line["candidate_kernel"]["correct"]
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, wall, kind, _ = cpu_reference_rate(CPU_SAMPLE_N, threads)
@@ -352,6 +388,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--no-candidate-kernel", action="store_true", help="skip the C4 candidate-kernel roofline line")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
