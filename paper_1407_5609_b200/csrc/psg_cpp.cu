@@ -1215,8 +1215,15 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       // dense cells (clustered data): cell-pair tiles beat per-point lists
       PSG_CUDA(cudaMemcpyAsync(&plan.gp, W.gi.gp.p, sizeof(GridParams), cudaMemcpyDeviceToHost, s));
       PSG_CUDA(cudaMemcpyAsync(W.host_st, W.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-      const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
-      plan.dense = est > kDenseFactor * n;
+      // a grid over more than 3 keys is already the dense engine's (a regrid
+      // of it): no estimate (it would walk the 3^g stencil of every cell)
+      if (plan.g > 3) {
+        PSG_CUDA(cudaStreamSynchronize(s));
+        plan.dense = true;
+      } else {
+        const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
+        plan.dense = est > kDenseFactor * n;
+      }
       if (nparts == 1 && plan.dense) {  // later solves of this (q, seed, zone) skip the graph attempt
         if (W.learned_q != plan.q_arg || W.learned_seed != plan.seed_arg || W.learned_zone != plan.zone)
           W.learned_w = 0.0;  // hints of another (q, seed, zone)

@@ -4,10 +4,12 @@
 // sits at the scale of a cluster, so a key window of the bound spans whole
 // clusters), per-point candidate lists degenerate: every point would walk
 // ~10^4-10^5 candidates.  Here the unit of work is a pair of cells instead:
-//   1. per-cell boxes over all nk keys (block per cell)
+//   1. the non-empty cells (a list), per-cell boxes over all nk keys (warp
+//      per non-empty cell)
 //   2. keep a forward-stencil cell pair (A, B) only if the box gap lower
 //      bound is within the threshold — pairs of points of different clusters
-//      are dropped a whole cell pair at a time
+//      are dropped a whole cell pair at a time (warp per A, lanes over the
+//      3^g/2 stencil offsets)
 //   3. kept cell pairs are cut into 128x128 tiles; a persistent kernel takes
 //      tiles from an atomic cursor and evaluates every pair as a canonical
 //      FP32 distance (16-wide coordinate slabs in shared memory, 8x8 pairs per
@@ -113,91 +115,132 @@ __global__ void k_gather_rows(const float* __restrict__ X, const uint32_t* __res
   }
 }
 
+// The non-empty cells (run starts of the cell-sorted ids), in arbitrary order:
+// every consumer below is per cell, and a cell's pairs keep their stencil order.
+__global__ void k_cell_list(const uint32_t* __restrict__ scell, uint32_t n, uint32_t* __restrict__ list,
+                            unsigned long long* __restrict__ count) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool start = p < n && (p == 0 || scell[p] != scell[p - 1]);
+  const unsigned m = __ballot_sync(kFull, start);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(count, static_cast<unsigned long long>(__popc(m)));
+  base = __shfl_sync(kFull, base, __ffs(m) - 1);
+  if (start) list[base + __popc(m & ((1u << lane) - 1u))] = scell[p];
+}
+
+// Per-cell key boxes, one warp per non-empty cell.
 template <int NK>
-__global__ void __launch_bounds__(256) k_cell_boxes(const float* __restrict__ skeys, const uint32_t* __restrict__ cfirst,
-                                                    uint64_t cells, float* __restrict__ cbox) {
-  __shared__ float red[2][NK][8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (uint64_t c = blockIdx.x; c < cells; c += gridDim.x) {
-    const uint32_t lo = cfirst[c], hi = cfirst[c + 1];
-    if (lo == hi) continue;  // uniform per block
+__global__ void __launch_bounds__(256) k_cell_boxes_list(const float* __restrict__ skeys,
+                                                         const uint32_t* __restrict__ cfirst,
+                                                         const uint32_t* __restrict__ list, uint32_t ncells,
+                                                         float* __restrict__ cbox) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < ncells; k += nw) {
+    const uint32_t c = list[k], lo = cfirst[c], hi = cfirst[c + 1];
     float mn[NK], mx[NK];
 #pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      mn[k] = INFINITY;
-      mx[k] = -INFINITY;
+    for (int t = 0; t < NK; ++t) {
+      mn[t] = INFINITY;
+      mx[t] = -INFINITY;
     }
-    for (uint32_t p = lo + tid; p < hi; p += blockDim.x) {
+    for (uint32_t p = lo + lane; p < hi; p += 32) {
       float kv[NK];
       load_keys<NK>(skeys + static_cast<size_t>(p) * NK, kv);
 #pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        mn[k] = fminf(mn[k], kv[k]);
-        mx[k] = fmaxf(mx[k], kv[k]);
+      for (int t = 0; t < NK; ++t) {
+        mn[t] = fminf(mn[t], kv[t]);
+        mx[t] = fmaxf(mx[t], kv[t]);
       }
     }
 #pragma unroll
-    for (int k = 0; k < NK; ++k)
+    for (int t = 0; t < NK; ++t)
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
-        mn[k] = fminf(mn[k], __shfl_xor_sync(kFull, mn[k], o));
-        mx[k] = fmaxf(mx[k], __shfl_xor_sync(kFull, mx[k], o));
+        mn[t] = fminf(mn[t], __shfl_xor_sync(kFull, mn[t], o));
+        mx[t] = fmaxf(mx[t], __shfl_xor_sync(kFull, mx[t], o));
       }
-    __syncthreads();
-    if (lane == 0)
+    if (lane < NK) {
+      float a = mn[0], b = mx[0];
 #pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        red[0][k][warp] = mn[k];
-        red[1][k][warp] = mx[k];
-      }
-    __syncthreads();
-    if (tid < NK) {
-      float a = INFINITY, b = -INFINITY;
-      for (int w = 0; w < 8; ++w) {
-        a = fminf(a, red[0][tid][w]);
-        b = fmaxf(b, red[1][tid][w]);
-      }
-      cbox[c * 2 * NK + tid] = a;
-      cbox[c * 2 * NK + NK + tid] = b;
+      for (int t = 1; t < NK; ++t)
+        if (lane == t) {
+          a = mn[t];
+          b = mx[t];
+        }
+      cbox[static_cast<size_t>(c) * 2 * NK + lane] = a;
+      cbox[static_cast<size_t>(c) * 2 * NK + NK + lane] = b;
     }
   }
 }
 
+// Kept cell pairs, one warp per non-empty A cell: lanes take 32 stencil
+// offsets at a time (s = 0 is the own cell) and a warp appends its kept pairs
+// with one atomic per 32 offsets, in lane order — so each A's pairs are in
+// stencil order, as the per-thread version emitted them (the stable sort by A
+// then gives the same deterministic work list).
 template <int NK>
-__global__ void k_cell_pairs(const uint32_t* __restrict__ cfirst, const GridParams* __restrict__ gpp, uint64_t cells,
-                             const float* __restrict__ cbox, const Thresholds* __restrict__ th,
-                             uint32_t* __restrict__ pa, uint32_t* __restrict__ pb, uint32_t* __restrict__ pt,
-                             uint32_t cap, unsigned long long* __restrict__ count, bool strips) {
-  const GridParams P = *gpp;
+__global__ void __launch_bounds__(256) k_cell_pairs_list(const uint32_t* __restrict__ cfirst,
+                                                         const GridParams* __restrict__ gpp,
+                                                         const uint32_t* __restrict__ list, uint32_t ncells,
+                                                         const float* __restrict__ cbox,
+                                                         const Thresholds* __restrict__ th, uint32_t* __restrict__ pa,
+                                                         uint32_t* __restrict__ pb, uint32_t* __restrict__ pt,
+                                                         uint32_t cap, unsigned long long* __restrict__ count,
+                                                         bool strips) {
+  __shared__ GridParams sP;
+  if (threadIdx.x == 0) sP = *gpp;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   const float lb2 = th->lb2 * (1.0f + 0x1.0p-20f);  // box gaps are a lower bound of every pair's key gaps
-  for (uint64_t A = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; A < cells;
-       A += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  const int fc = forward_count(sP.g);
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < ncells; k += nw) {
+    const uint32_t A = list[k];
     const uint32_t na = cfirst[A + 1] - cfirst[A];
-    if (na == 0) continue;
     int cc[kMaxGridKeys];
-    cell_decode(P, static_cast<uint32_t>(A), cc);
-    const float* ba = cbox + A * 2 * NK;
-    for (int s = 0; s <= forward_count(P.g); ++s) {
-      uint32_t B = static_cast<uint32_t>(A);
-      if (s > 0 && !cell_forward(P, cc, s, &B)) continue;
-      const uint32_t nb = cfirst[B + 1] - cfirst[B];
-      if (nb == 0 || (s == 0 && na < 2)) continue;
-      if (s > 0) {
-        const float* bb = cbox + static_cast<size_t>(B) * 2 * NK;
-        float acc = 0.f;
+    cell_decode(sP, A, cc);
+    const float* ba = cbox + static_cast<size_t>(A) * 2 * NK;
+    float alo[NK], ahi[NK];
 #pragma unroll
-        for (int k = 0; k < NK; ++k) {
-          const float gap = fmaxf(0.f, fmaxf(bb[k] - ba[NK + k], ba[k] - bb[NK + k]));
-          acc = fmaf(gap, gap, acc);
+    for (int t = 0; t < NK; ++t) {
+      alo[t] = ba[t];
+      ahi[t] = ba[NK + t];
+    }
+    const uint32_t ta = (na + kT - 1) / kT;
+    for (int s0 = 0; s0 <= fc; s0 += 32) {
+      const int s = s0 + lane;
+      bool keep = false;
+      uint32_t B = A, nb = 0;
+      if (s <= fc && (s == 0 || cell_forward(sP, cc, s, &B))) {
+        nb = cfirst[B + 1] - cfirst[B];
+        keep = nb != 0 && !(s == 0 && na < 2);
+        if (keep && s > 0) {
+          const float* bb = cbox + static_cast<size_t>(B) * 2 * NK;
+          float acc = 0.f;
+#pragma unroll
+          for (int t = 0; t < NK; ++t) {
+            const float gap = fmaxf(0.f, fmaxf(bb[t] - ahi[t], alo[t] - bb[NK + t]));
+            acc = fmaf(gap, gap, acc);
+          }
+          keep = acc <= lb2;
         }
-        if (acc > lb2) continue;
       }
-      const unsigned long long slot = atomicAdd(count, 1ull);
-      if (slot < cap) {
-        pa[slot] = static_cast<uint32_t>(A);
-        pb[slot] = B;
-        const uint32_t ta = (na + kT - 1) / kT, tb = (nb + kT - 1) / kT;
-        pt[slot] = strips ? ta : (s == 0 ? ta * (ta + 1) / 2 : ta * tb);
+      const unsigned m = __ballot_sync(kFull, keep);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(count, static_cast<unsigned long long>(__popc(m)));
+      base = __shfl_sync(kFull, base, 0);
+      if (keep) {
+        const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+        if (slot < cap) {
+          pa[slot] = A;
+          pb[slot] = B;
+          const uint32_t tb = (nb + kT - 1) / kT;
+          pt[slot] = strips ? ta : (s == 0 ? ta * (ta + 1) / 2 : ta * tb);
+        }
       }
     }
   }
@@ -536,32 +579,26 @@ __global__ void __launch_bounds__(kGThreads, 1)
           }
           return valid;
         };
-        uint32_t pos = 0;
-        bool mine = false;
-        bool valid = tb > 0 ? resolve(0, pos, mine) : false;
-        for (uint32_t tj = 0; tj < tb; ++tj) {
-          const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
-          ++bcount;
-          const uint32_t blen = min(static_cast<uint32_t>(kGN), L - tj * kGN);
-          float4 v[kNi];
-          const unsigned vmask = __ballot_sync(kFull, valid);
+        // The loads run half a tile ahead of the split: the next half's rows
+        // are in flight while this half is shifted, split and stored (same
+        // registers as one whole tile in flight).
+        constexpr int kNh = kNi / 2;
+        auto load_half = [&](float4 (&v)[kNh], uint32_t ps, int h) {
 #pragma unroll
-          for (int i = 0; i < kNi; ++i) {
-            const int src = i * kRpi + rsel;  // the warp's row this lane loads in step i
+          for (int i = 0; i < kNh; ++i) {
+            const int src = (h * kNh + i) * kRpi + rsel;  // the warp's row this lane loads in step i
             // unconditional (pos = 0 for invalid rows, zeroed at the split): a
             // predicated select here would serialise the loads on their results
-            const uint32_t p = __shfl_sync(kFull, pos, src);
+            const uint32_t p = __shfl_sync(kFull, ps, src);
             v[i] = __ldg(reinterpret_cast<const float4*>(Xs + static_cast<size_t>(p) * D) + sub);
           }
-          const uint32_t jpos_c = pos | (mine ? 0x80000000u : 0u);
-          if (tj + 1 < tb) valid = resolve(tj + 1, pos, mine);
-          mbar_wait(&sm.bfree[bb], bph ^ 1);
+        };
+        auto split_half = [&](const float4 (&v)[kNh], int h, unsigned vmask, uint32_t bb, float& wm) {
           float* hi_tile = sm.B[bb][0];
           float* lo_tile = sm.B[bb][1];
-          float wm = 0.f;
 #pragma unroll
-          for (int i = 0; i < kNi; ++i) {
-            const int src = i * kRpi + rsel;
+          for (int i = 0; i < kNh; ++i) {
+            const int src = (h * kNh + i) * kRpi + rsel;
             const int rr = 32 * warp + src;
             float4 x = v[i];
             if ((vmask >> src) & 1u) {
@@ -578,14 +615,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
             nrm = fmaf(x.w, x.w, nrm);
 #pragma unroll
             for (int o = kLpr / 2; o; o >>= 1) nrm += __shfl_xor_sync(kFull, nrm, o);
-            const float4 h = make_float4(__uint_as_float(__float_as_uint(x.x) & ~0x1fffu),
-                                         __uint_as_float(__float_as_uint(x.y) & ~0x1fffu),
-                                         __uint_as_float(__float_as_uint(x.z) & ~0x1fffu),
-                                         __uint_as_float(__float_as_uint(x.w) & ~0x1fffu));
-            const float4 l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);  // exact
+            const float4 hh = make_float4(__uint_as_float(__float_as_uint(x.x) & ~0x1fffu),
+                                          __uint_as_float(__float_as_uint(x.y) & ~0x1fffu),
+                                          __uint_as_float(__float_as_uint(x.z) & ~0x1fffu),
+                                          __uint_as_float(__float_as_uint(x.w) & ~0x1fffu));
+            const float4 l = make_float4(x.x - hh.x, x.y - hh.y, x.z - hh.z, x.w - hh.w);  // exact
             const int c = sub >> 3, u = sub & 7;  // 32-float chunk, 16 B unit inside the 128 B row
             const int off = c * (kGN * 32) + rr * 32 + ((u ^ (rr & 7)) << 2);
-            *reinterpret_cast<float4*>(hi_tile + off) = h;
+            *reinterpret_cast<float4*>(hi_tile + off) = hh;
             *reinterpret_cast<float4*>(lo_tile + off) = l;
             if (sub == 0) {
               const bool ok = (vmask >> src) & 1u;
@@ -594,6 +631,25 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
             wm = fmaxf(wm, nrm);
           }
+        };
+        uint32_t pos = 0;
+        bool mine = false;
+        bool valid = tb > 0 ? resolve(0, pos, mine) : false;
+        float4 vc[kNh], vn[kNh];
+        if (tb > 0) load_half(vc, pos, 0);
+        for (uint32_t tj = 0; tj < tb; ++tj) {
+          const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
+          ++bcount;
+          const uint32_t blen = min(static_cast<uint32_t>(kGN), L - tj * kGN);
+          const unsigned vmask = __ballot_sync(kFull, valid);
+          const uint32_t jpos_c = pos | (mine ? 0x80000000u : 0u);
+          load_half(vn, pos, 1);  // this tile's second half
+          if (tj + 1 < tb) valid = resolve(tj + 1, pos, mine);  // the next tile's rows
+          mbar_wait(&sm.bfree[bb], bph ^ 1);
+          float wm = 0.f;
+          split_half(vc, 0, vmask, bb, wm);
+          if (tj + 1 < tb) load_half(vc, pos, 0);  // the next tile's first half
+          split_half(vn, 1, vmask, bb, wm);
           sm.na[bb][r] = na_r;
           sm.jpos[bb][r] = jpos_c;
           wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(wm)));  // norms >= 0
@@ -953,17 +1009,26 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   const bool gram = gram_shape(d) && !no_gram;
   if (w.Xs.n != static_cast<size_t>(n) * d) w.Xs.alloc(static_cast<size_t>(n) * d, s);
   if (w.cbox.n < cells * 2 * nk) w.cbox.alloc(cells * 2 * nk, s);
-  if (w.ctr.n < 4) w.ctr.alloc(4, s);
+  if (w.ctr.n < 5) w.ctr.alloc(5, s);
+  if (w.clist.n < n) w.clist.alloc(n, s);
   k_gather_rows<<<sms * 16, 256, 0, s>>>(X, gi.sidx.p, n, d, w.Xs.p);
   PSG_LAUNCHED();
-  if (nk == 4)
-    k_cell_boxes<4><<<static_cast<unsigned>(std::min<uint64_t>(cells, 65535)), 256, 0, s>>>(gi.skeys.p, gi.dev.cfirst,
-                                                                                            cells, w.cbox.p);
-  else
-    k_cell_boxes<8><<<static_cast<unsigned>(std::min<uint64_t>(cells, 65535)), 256, 0, s>>>(gi.skeys.p, gi.dev.cfirst,
-                                                                                            cells, w.cbox.p);
+  // the non-empty cells: boxes and pairs are per non-empty cell (a dense grid
+  // over 8 keys has up to 2^27 cells, almost all empty)
+  PSG_CUDA(cudaMemsetAsync(w.ctr.p + 4, 0, 8, s));
+  k_cell_list<<<blocks(n, 256), 256, 0, s>>>(gi.dev.scell, n, w.clist.p, w.ctr.p + 4);
   PSG_LAUNCHED();
-  g_launches += 2;
+  unsigned long long ne64 = 0;
+  PSG_CUDA(cudaMemcpyAsync(&ne64, w.ctr.p + 4, 8, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  const uint32_t ne = static_cast<uint32_t>(ne64);
+  const unsigned lb = std::max(1u, std::min<unsigned>(blocks(static_cast<uint64_t>(ne) * 32, 256), sms * 16));
+  if (nk == 4)
+    k_cell_boxes_list<4><<<lb, 256, 0, s>>>(gi.skeys.p, gi.dev.cfirst, w.clist.p, ne, w.cbox.p);
+  else
+    k_cell_boxes_list<8><<<lb, 256, 0, s>>>(gi.skeys.p, gi.dev.cfirst, w.clist.p, ne, w.cbox.p);
+  PSG_LAUNCHED();
+  g_launches += 3;
   if (w.pair_cap == 0) w.pair_cap = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(cells * 14, 1024),
                                                                              1u << 26));
   unsigned long long npairs = 0;
@@ -977,11 +1042,11 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     }
     PSG_CUDA(cudaMemsetAsync(w.ctr.p, 0, 32, s));
     if (nk == 4)
-      k_cell_pairs<4><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
-          gi.dev.cfirst, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
+      k_cell_pairs_list<4><<<lb, 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, w.clist.p, ne, w.cbox.p, th, w.pa.p, w.pb.p,
+                                             w.ptiles.p, w.pair_cap, w.ctr.p, gram);
     else
-      k_cell_pairs<8><<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(
-          gi.dev.cfirst, gi.gp.p, cells, w.cbox.p, th, w.pa.p, w.pb.p, w.ptiles.p, w.pair_cap, w.ctr.p, gram);
+      k_cell_pairs_list<8><<<lb, 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, w.clist.p, ne, w.cbox.p, th, w.pa.p, w.pb.p,
+                                             w.ptiles.p, w.pair_cap, w.ctr.p, gram);
     PSG_LAUNCHED();
     ++g_launches;
     PSG_CUDA(cudaMemcpyAsync(&npairs, w.ctr.p, 8, cudaMemcpyDeviceToHost, s));

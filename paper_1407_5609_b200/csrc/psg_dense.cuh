@@ -12,7 +12,8 @@ namespace psg {
 // Buffers reused across solves on one point set.
 struct DenseWork {
   DevBuf<float> Xs;                // n x d rows in grid-sorted order
-  DevBuf<float> cbox;              // cells x 2nk: per-cell key boxes (lo, hi)
+  DevBuf<float> cbox;              // cells x 2nk: per-cell key boxes (lo, hi); only non-empty cells are written
+  DevBuf<uint32_t> clist;          // the non-empty cells (any order)
   DevBuf<uint32_t> pa, pb, ptiles, pprefix, stmp;  // surviving cell pairs, tiles per pair, prefix
   DevBuf<uint32_t> hist, gstart, gstrips, gprefix, gtmp;  // Gram path: pairs sorted by A, groups, strip prefix
   DevBuf<unsigned long long> ctr;  // [0] pair count, [1] tile / group cursor, [2] estimate, [3] groups
