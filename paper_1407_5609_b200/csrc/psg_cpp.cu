@@ -52,7 +52,7 @@ constexpr int kThreads = 256;
 constexpr int kChunk = 256;
 constexpr int kQueue = 1024;
 constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
-constexpr double kGridOccupancy = 0.15;   // mean points per cell over the key box
+constexpr double kGridOccupancy = 0.25;   // mean points per cell over the key box (sweep: tools/occ_sweep.sh)
 constexpr double kGridBoxSd = 2.5;        // key box: mean +- kGridBoxSd sd (clipped to the sample range)
 constexpr int kGridBootCap = 256;         // candidates per point in the grid bootstrap
 int boot_own_row() {  // the first bootstrap looks at the own cell row only (one cfirst lookup)

@@ -1,3 +1,2 @@
 python -m pytest tests -m gpu -x -q -k "dense or sharded or gram or c5 or mixture or fullsize" > gpurun_out/dense_tests.log 2>&1; echo rc=$? >> gpurun_out/dense_tests.log
 python tools/one_c5.py 16777216 3 > gpurun_out/c5_sweep.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python tools/one_c5.py 16777216 2 > gpurun_out/ncu_c5.log 2>&1

@@ -1,3 +1,5 @@
-for occ in 0.08 0.15 0.25 0.4 0.7; do
-  echo "occ=$occ $(PSG_OCC=$occ python bench.py --steps 20 --no-candidate-kernel --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.readline()); print(d["ms_per_step"], d["kernel_ms_per_step"], d["correct"])')" >> gpurun_out/occ_sweep.log
+# grid occupancy (mean points per cell) vs C1/C2/C3 device solve times
+for occ in 0.15 0.25 0.35; do
+  echo "occ=$occ" >> gpurun_out/occ_sweep.log
+  PSG_OCC=$occ python tools/bench_configs.py c1 c2 c3 2>/dev/null | cut -c1-160 >> gpurun_out/occ_sweep.log
 done
