@@ -101,9 +101,9 @@ struct FrnnArgs {
 
 constexpr int kFrnnThreads = 256;
 
-// One thread per sorted position; the warp walks its lanes' flattened ranges
-// in lockstep (lane predicate t < total), so emission is warp-converged.
-template <int NK, bool kSmallD>
+// d > 4: one thread per sorted position; the warp walks its lanes' ranges in
+// lockstep (lane predicate t < total), so emission is warp-converged.
+template <int NK>
 __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
   __shared__ GridParams sP;
   __shared__ uint64_t wbuf[kFrnnThreads / 32][64];
@@ -115,15 +115,11 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
   uint64_t visited = 0, examined = 0, hsum = 0;
   GridRanges R{};
   float mk[NK];
-  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t mi = 0;
   if (valid) {
     R = grid_ranges(a.grid.cfirst, sP, p, a.grid.scell[p]);
     mi = a.sidx[p];
-    if constexpr (kSmallD)
-      me = a.sx[p];
-    else
-      load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
+    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
   }
   // walk the (at most five) ranges with a running position; the range
   // switch is the only place the five bounds are selected
@@ -149,29 +145,14 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
       uint32_t mj = zoned ? a.sidx[j] : 0u;
       if (!zoned || admissible(mi, mj, a.zone)) {  // refscan.cpp:15-18
         ++visited;
-        float s32;
-        bool pass = true;
-        if constexpr (kSmallD) {
-          const float4 o = a.sx[j];
-          float g = o.x - me.x;
-          s32 = g * g;
-          g = o.y - me.y;
-          s32 = fmaf(g, g, s32);
-          g = o.z - me.z;
-          s32 = fmaf(g, g, s32);
-          g = o.w - me.w;
-          s32 = fmaf(g, g, s32);
-        } else {
-          if (!zoned) mj = a.sidx[j];
-          float kj[NK];
-          load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
-          pass = lb2_full<NK>(mk, kj) <= a.th.lb2;
-          s32 = pass ? thread_sqdist(xi, a.X + static_cast<size_t>(mj) * a.d, a.d) : INFINITY;
-        }
+        if (!zoned) mj = a.sidx[j];
+        float kj[NK];
+        load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
+        const bool pass = lb2_full<NK>(mk, kj) <= a.th.lb2;
+        const float s32 = pass ? thread_sqdist(xi, a.X + static_cast<size_t>(mj) * a.d, a.d) : INFINITY;
         if (pass) {
           ++examined;
           if (s32 <= a.th.band) {
-            if (kSmallD && !zoned) mj = a.sidx[j];  // the original index only inside the band
             if (s32 <= a.lo || exact_distance(a.src, mi, mj) <= a.R) {  // boundary inclusive
               emit = true;
               key = mi < mj ? (static_cast<uint64_t>(mi) << 32) | mj : (static_cast<uint64_t>(mj) << 32) | mi;
@@ -775,9 +756,9 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
       k_frnn_band<<<c.sm_count * 2, 256, 0, s>>>(a);
     } else {
       if (nk == 4)
-        k_frnn_scan<4, false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+        k_frnn_scan<4><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
       else
-        k_frnn_scan<8, false><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+        k_frnn_scan<8><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
     }
     PSG_LAUNCHED();
     ++g_launches;
