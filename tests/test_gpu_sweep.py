@@ -86,3 +86,21 @@ def test_fixed_radius_large_matches_device_brute_force(psg, d, fam):
     want = psg.brute_force_neighbors(ps, radius, 0)
     cnt = sum(len(l) for l in want) // 2
     assert got.pair_count == cnt
+
+
+# The d <= 4 cell scan's variants (list / count, d = 4, exclusion zone): the
+# count, hash and sorted pair list against the device brute force (a13), and
+# the count + hash run against the list run.
+@pytest.mark.parametrize("d,zone", [(1, 0), (2, 7), (3, 0), (3, 5), (4, 0), (4, 9)])
+def test_fixed_radius_cell_scan_variants(psg, d, zone):
+    rng = np.random.default_rng(100 + 10 * d + zone)
+    n = 30_000
+    pts = rng.random((n, d)).astype(np.float32)
+    ps = psg.PointSet.from_flat(pts, d)
+    radius = float((24.0 / n) ** (1.0 / d)) * 0.6  # tens of neighbours per point
+    want = psg.brute_force_neighbors(ps, radius, zone)
+    lists = psg.fixed_radius_neighbors(ps, radius, 10, 10.0, 3, zone)
+    assert [list(map(int, l)) for l in lists.neighbors] == [list(map(int, l)) for l in want]
+    counted = psg.fixed_radius_neighbors(ps, radius, 10, 10.0, 3, zone, want_lists=False)
+    assert (counted.pair_count, counted.pair_hash) == (lists.pair_count, lists.pair_hash)
+    assert counted.pair_count == sum(len(l) for l in want) // 2 > 0
