@@ -85,6 +85,13 @@ typedef struct psg_profile {
   double bootstrap_kernel_ms;/* device time of the delta-bootstrap kernel(s) */
   double total_ms;           /* device span of the whole call on the library stream */
   uint64_t scan_launches;    /* launches of the candidate kernel */
+  /* dense cell-pair engine (clustered data) of the last solve; 0 when unused */
+  uint64_t dense_cells;        /* cells of the dense grid (up to 2^27) */
+  uint64_t dense_cell_pairs;   /* kept (A, B) cell pairs */
+  uint64_t dense_groups;       /* Gram groups (an A cell and <= 366 partners) */
+  uint64_t dense_split_groups; /* groups that continue an A cell with more than 366 kept partners */
+  uint64_t dense_tiles;        /* 128 x 128 Gram tiles issued */
+  uint64_t inline_fp64;        /* band pairs past the candidate list, evaluated inline in FP64 */
 } psg_profile;
 
 const char* psg_last_error(void);
@@ -209,6 +216,17 @@ int psg_pointset_windows_from_file(const char* path, uint64_t len, int znorm, ps
  * (X = fl(scale * points)).  nk = 4 or 8 for q clamped to [1, 8]. */
 int psg_debug_projection(psg_pointset* ps, uint64_t q, uint64_t seed, int* nk, float* keys, float* dirs,
                          double* key_error, double* scale);
+
+/* ---- inspection (tests): exhaustive search under a known upper bound --------
+ * brute_force_closest_pair (refscan.cpp:134-157) in ONE all-pairs pass: every
+ * admissible pair whose FP32 distance lies inside the rounding band of
+ * `upper` (an FP64 distance some admissible pair is known to reach, e.g. the
+ * distance of a returned pair recomputed by the caller) is re-evaluated in the
+ * reference's FP64 order.  The band holds every pair at FP64 distance
+ * <= upper, so the result is the exact minimum whenever upper >= it; it
+ * reports index_i = UINT64_MAX if no pair is that close.  Half the work of the
+ * two-pass brute force at sizes where that takes minutes (C5: 1.4e14 pairs). */
+int psg_debug_brute_bounded_ps(psg_pointset* ps, uint64_t exclusion_zone, double upper, psg_pair_result* out);
 
 /* ---- host helpers: the reference's seeded synthetic data (datagen.cpp) --- */
 int psg_gen_random_walk(uint64_t n, uint64_t seed, double stddev, double* out);

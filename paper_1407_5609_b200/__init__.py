@@ -80,7 +80,9 @@ class _Profile(C.Structure):
                 ("launches", _u64), ("window_pairs", _u64), ("lb_survivors", _u64),
                 ("candidates", _u64), ("bootstrap_width", _u64), ("h2d_bytes", _u64),
                 ("d2h_bytes", _u64), ("scan_kernel_ms", _f64), ("project_kernel_ms", _f64),
-                ("bootstrap_kernel_ms", _f64), ("total_ms", _f64), ("scan_launches", _u64)]
+                ("bootstrap_kernel_ms", _f64), ("total_ms", _f64), ("scan_launches", _u64),
+                ("dense_cells", _u64), ("dense_cell_pairs", _u64), ("dense_groups", _u64),
+                ("dense_split_groups", _u64), ("dense_tiles", _u64), ("inline_fp64", _u64)]
 
 
 _SIGS = {
@@ -128,6 +130,7 @@ _SIGS = {
     "psg_host_alloc": (_int, [C.c_size_t, _p]),
     "psg_host_free": (None, [_p]),
     "psg_debug_projection": (_int, [_p, _u64, _u64, _p, _p, _p, _p, _p]),
+    "psg_debug_brute_bounded_ps": (_int, [_p, _u64, _f64, _p]),
     "psg_load_series_text": (_int, [C.c_char_p, _p, _p]),
     "psg_save_series_text": (_int, [C.c_char_p, _p, _u64]),
     "psg_free": (None, [_p]),
@@ -185,6 +188,8 @@ def last_profile() -> dict:
         "h2d_bytes": p.h2d_bytes, "d2h_bytes": p.d2h_bytes,
         "scan_kernel_ms": p.scan_kernel_ms, "project_kernel_ms": p.project_kernel_ms,
         "bootstrap_kernel_ms": p.bootstrap_kernel_ms, "total_ms": p.total_ms, "scan_launches": p.scan_launches,
+        "dense_cells": p.dense_cells, "dense_cell_pairs": p.dense_cell_pairs, "dense_groups": p.dense_groups,
+        "dense_split_groups": p.dense_split_groups, "dense_tiles": p.dense_tiles, "inline_fp64": p.inline_fp64,
     }
 
 
@@ -371,6 +376,14 @@ def brute_force_closest_pair(points: PointSet, exclusion_zone: int) -> PairResul
     """refscan.hpp:58 / refscan.cpp:134-157 (on device)."""
     out = _Pair()
     _check(lib().psg_brute_force_closest_pair_ps(points._device(), exclusion_zone, C.byref(out)))
+    return _pair(out)
+
+
+def brute_force_bounded(points: PointSet, exclusion_zone: int, upper: float) -> PairResult:
+    """Test inspection: the exhaustive minimum over pairs at FP64 distance <=
+    `upper` in one all-pairs pass (psg_debug_brute_bounded_ps)."""
+    out = _Pair()
+    _check(lib().psg_debug_brute_bounded_ps(points._device(), exclusion_zone, float(upper), C.byref(out)))
     return _pair(out)
 
 

@@ -32,7 +32,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
-#include <fstream>
+#include <iomanip>
 #include <functional>
 #include <iostream>
 #include <map>
@@ -103,97 +103,105 @@ struct Report {
   uint64_t seed = 0;
 };
 
+// The report schema as one table: the JSON object, the CSV header and row,
+// and verify's field comparison all walk it in this (the reference's
+// io.cpp:140-155) order.
+struct Field {
+  const char* name;
+  nlohmann::json (*get)(const Report&);
+  bool replayed;  // compared by verify (params and wall time are not)
+};
+const Field kFields[] = {
+    {"algorithm", [](const Report& r) { return nlohmann::json(r.algorithm); }, true},
+    {"params", [](const Report& r) { return nlohmann::json(r.params); }, false},
+    {"dataset", [](const Report& r) { return nlohmann::json(r.dataset); }, true},
+    {"pair_index_1", [](const Report& r) { return nlohmann::json(r.pair_index_1); }, true},
+    {"pair_index_2", [](const Report& r) { return nlohmann::json(r.pair_index_2); }, true},
+    {"distance_or_matches", [](const Report& r) { return nlohmann::json(r.distance_or_matches); }, true},
+    {"pairs_examined", [](const Report& r) { return nlohmann::json(r.pairs_examined); }, true},
+    {"iterations", [](const Report& r) { return nlohmann::json(r.iterations); }, true},
+    {"wall_seconds", [](const Report& r) { return nlohmann::json(r.wall_seconds); }, false},
+    {"seed", [](const Report& r) { return nlohmann::json(r.seed); }, true},
+};
+
 nlohmann::json to_json(const Report& r) {
-  nlohmann::json j;
-  j["algorithm"] = r.algorithm;
-  j["params"] = r.params;
-  j["dataset"] = r.dataset;
-  j["pair_index_1"] = r.pair_index_1;
-  j["pair_index_2"] = r.pair_index_2;
-  j["distance_or_matches"] = r.distance_or_matches;
-  j["pairs_examined"] = r.pairs_examined;
-  j["iterations"] = r.iterations;
-  j["wall_seconds"] = r.wall_seconds;
-  j["seed"] = r.seed;
+  nlohmann::json j = nlohmann::json::object();
+  for (const Field& f : kFields) j[f.name] = f.get(r);
   return j;
 }
 
+// RFC 4180 cell from the JSON scalar text, so a value has the same bytes in
+// both formats; std::quoted with '"' as its own escape doubles inner quotes.
 std::string csv_cell(const nlohmann::json& v) {
-  std::string s = v.is_string() ? v.get<std::string>() : v.dump();
-  if (s.find_first_of(",\"\n") == std::string::npos) return s;
-  std::string q = "\"";
-  for (const char c : s) {
-    if (c == '"') q += '"';
-    q += c;
-  }
-  return q + '"';
+  const std::string text = v.is_string() ? v.get<std::string>() : v.dump();
+  if (text.find_first_of(",\"\n") == std::string::npos) return text;
+  std::ostringstream q;
+  q << std::quoted(text, '"', '"');
+  return q.str();
 }
 
 std::string reports_to_csv(const std::vector<Report>& reports) {
-  static const char* kCols[] = {"algorithm",      "params",     "dataset",      "pair_index_1", "pair_index_2",
-                                "distance_or_matches", "pairs_examined", "iterations", "wall_seconds", "seed"};
-  std::string out;
-  for (size_t i = 0; i < std::size(kCols); ++i) out += (i ? "," : "") + std::string(kCols[i]);
-  out += '\n';
+  std::ostringstream csv;
+  const char* sep = "";
+  for (const Field& f : kFields) csv << std::exchange(sep, ",") << f.name;
+  csv << '\n';
   for (const Report& r : reports) {
-    const nlohmann::json j = to_json(r);
-    for (size_t i = 0; i < std::size(kCols); ++i) out += (i ? "," : "") + csv_cell(j.at(kCols[i]));
-    out += '\n';
+    sep = "";
+    for (const Field& f : kFields) csv << std::exchange(sep, ",") << csv_cell(f.get(r));
+    csv << '\n';
   }
-  return out;
+  return csv.str();
 }
 
-void write_text_file(const std::string& path, const std::string& content) {  // io.cpp:227-232
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw std::runtime_error("cannot open " + path + " for writing");
-  out << content;
-  if (!out) throw std::runtime_error("write failed for " + path);
+// Whole-file text I/O (stdio); failures are the reference's messages.
+void write_text_file(const std::string& path, const std::string& content) {
+  std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path.c_str(), "wb"), &std::fclose);
+  if (!f) throw std::runtime_error("cannot open " + path + " for writing");
+  if (std::fwrite(content.data(), 1, content.size(), f.get()) != content.size() || std::fflush(f.get()) != 0)
+    throw std::runtime_error("write failed for " + path);
 }
 
 std::string read_text_file(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw std::runtime_error("cannot open " + path + " for reading");
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return ss.str();
+  std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path.c_str(), "rb"), &std::fclose);
+  if (!f) throw std::runtime_error("cannot open " + path + " for reading");
+  std::string text;
+  char buf[1 << 16];
+  for (size_t got; (got = std::fread(buf, 1, sizeof buf, f.get())) > 0;) text.append(buf, got);
+  return text;
 }
 
-std::string strip_extension(const std::string& p) {  // main.cpp:166-174
-  const auto slash = p.find_last_of('/');
-  const auto dot = p.find_last_of('.');
-  if (dot == std::string::npos) return p;
-  if (slash != std::string::npos && dot < slash) return p;
-  return p.substr(0, dot);
+// "--out dir/name.ext" -> "dir/name": the last '.' of the file-name part.
+std::string strip_extension(const std::string& p) {
+  const size_t name = p.find_last_of('/') + 1;  // npos + 1 == 0
+  const size_t dot = p.find_last_of('.');
+  return dot != std::string::npos && dot >= name ? p.substr(0, dot) : p;
 }
 
 // ---------------------------------------------------------------------------
-// params lines (main.cpp:48-78) and their replay tokenizer
+// params lines: the report's replayable command line, kept as tokens and
+// rendered once; a token that is empty or holds a blank or a quote is
+// double-quoted (split_params below takes it apart again).
 
-std::string quoted_token(const std::string& s) {
-  if (!s.empty() && s.find_first_of(" \t\"'") == std::string::npos) return s;
-  return "\"" + s + "\"";
-}
-
-class ParamsBuilder {
- public:
-  explicit ParamsBuilder(std::string cmd) : s_(std::move(cmd)) {}
-  ParamsBuilder& arg(const std::string& v) {
-    s_ += ' ';
-    s_ += quoted_token(v);
-    return *this;
+struct ParamLine {
+  std::vector<std::string> toks;
+  explicit ParamLine(std::string cmd) { toks.push_back(std::move(cmd)); }
+  void value(std::string v) { toks.push_back(std::move(v)); }
+  void flag(const char* name) { toks.emplace_back(name); }
+  void option(const char* name, std::string v) {
+    flag(name);
+    value(std::move(v));
   }
-  ParamsBuilder& flag(const char* f) {
-    s_ += ' ';
-    s_ += f;
-    return *this;
+  void option(const char* name, uint64_t v) { option(name, std::to_string(v)); }
+  void option(const char* name, double v) { option(name, fmt_num(v)); }
+  std::string render() const {
+    std::string line;
+    for (const std::string& t : toks) {
+      if (!line.empty()) line += ' ';
+      const bool bare = !t.empty() && t.find_first_of(" \t\"'") == std::string::npos;
+      line += bare ? t : '"' + t + '"';
+    }
+    return line;
   }
-  ParamsBuilder& opt(const char* f, const std::string& v) { return flag(f).arg(v); }
-  ParamsBuilder& opt(const char* f, uint64_t v) { return opt(f, std::to_string(v)); }
-  ParamsBuilder& opt(const char* f, double v) { return opt(f, fmt_num(v)); }
-  const std::string& str() const { return s_; }
-
- private:
-  std::string s_;
 };
 
 // Whitespace split honouring "..." and '...' quoting (what CLI11's split_up
@@ -341,8 +349,8 @@ CommonOpts common_of(const Parsed& p) {
   return c;
 }
 
-void finish_params(ParamsBuilder& pb, const CommonOpts& c) {
-  pb.opt("--version-tag", c.version_tag);
+void finish_params(ParamLine& pb, const CommonOpts& c) {
+  pb.option("--version-tag", c.version_tag);
   if (c.deterministic) pb.flag("--deterministic");
 }
 
@@ -520,33 +528,33 @@ std::pair<std::vector<double>, std::string> series_input(const SeriesOpts& o) { 
   return {load_series(o.series), o.series};
 }
 
-void series_params(ParamsBuilder& pb, const SeriesOpts& o, uint64_t zone, double f_eff) {  // main.cpp:319-331
+void series_params(ParamLine& pb, const SeriesOpts& o, uint64_t zone, double f_eff) {  // main.cpp:319-331
   if (!o.series.empty()) {
-    pb.arg(o.series);
+    pb.value(o.series);
   } else {
-    pb.opt("--gen-walk", o.gen_n);
-    pb.opt("--walk-stddev", o.stddev);
+    pb.option("--gen-walk", o.gen_n);
+    pb.option("--walk-stddev", o.stddev);
   }
-  pb.opt("--len", o.len);
-  pb.opt("--refs", o.refs);
-  pb.opt("--factor", f_eff);
-  pb.opt("--seed", o.seed);
-  pb.opt("--exclusion", zone);
-  pb.opt("--engine", o.engine);
+  pb.option("--len", o.len);
+  pb.option("--refs", o.refs);
+  pb.option("--factor", f_eff);
+  pb.option("--seed", o.seed);
+  pb.option("--exclusion", zone);
+  pb.option("--engine", o.engine);
 }
 
 int pair_report(const std::string& cmd, psg_pointset* ps, const std::string& dataset, uint64_t q, double factor,
                 uint64_t seed, uint64_t zone, const std::string& engine, const std::string& verify_engine,
-                const CommonOpts& common, const std::function<void(ParamsBuilder&, double)>& input_params,
+                const CommonOpts& common, const std::function<void(ParamLine&, double)>& input_params,
                 std::vector<Report>* capture) {
   const PairRun res = run_pair(ps, engine, q, factor, seed, zone);
   const double f_eff = engine == "mk" ? 1.0 : factor;
-  ParamsBuilder pb(cmd);
+  ParamLine pb(cmd);
   input_params(pb, f_eff);
   finish_params(pb, common);
   Report r;
   r.algorithm = engine;
-  r.params = pb.str();
+  r.params = pb.render();
   r.dataset = dataset;
   r.pair_index_1 = res.r.index_i + 1;
   r.pair_index_2 = res.r.index_j + 1;
@@ -574,7 +582,7 @@ int pair_report(const std::string& cmd, psg_pointset* ps, const std::string& dat
 int frnn_report(const std::string& cmd, psg_pointset* ps, const std::string& dataset, double radius, uint64_t q,
                 double factor, uint64_t seed, uint64_t zone, const std::string& engine,
                 const std::string& verify_engine, const std::string& pairs_out, const CommonOpts& common,
-                const std::function<void(ParamsBuilder&, double)>& input_params, std::vector<Report>* capture) {
+                const std::function<void(ParamLine&, double)>& input_params, std::vector<Report>* capture) {
   const FrnnRun res = run_frnn(ps, engine, radius, q, factor, seed, zone);
   const Lists& L = res.lists;
   const uint64_t pair_count = L.neighbors.size() / 2;
@@ -587,13 +595,13 @@ int frnn_report(const std::string& cmd, psg_pointset* ps, const std::string& dat
         break;
       }
   const double f_eff = engine == "mk" ? 1.0 : factor;
-  ParamsBuilder pb(cmd);
+  ParamLine pb(cmd);
   input_params(pb, f_eff);
-  pb.opt("--radius", radius);
+  pb.option("--radius", radius);
   finish_params(pb, common);
   Report r;
   r.algorithm = engine;
-  r.params = pb.str();
+  r.params = pb.render();
   r.dataset = dataset;
   r.pair_index_1 = first_a;
   r.pair_index_2 = first_b;
@@ -632,7 +640,7 @@ int cmd_motif(const std::vector<std::string>& args, std::vector<Report>* capture
   const uint64_t zone = o.exclusion < 0 ? o.len : static_cast<uint64_t>(o.exclusion);
   return pair_report(
       "motif", ps.get(), dataset, o.refs, o.factor, o.seed, zone, o.engine, o.verify_engine, o.common,
-      [&](ParamsBuilder& pb, double f_eff) { series_params(pb, o, zone, f_eff); }, capture);
+      [&](ParamLine& pb, double f_eff) { series_params(pb, o, zone, f_eff); }, capture);
 }
 
 int cmd_frnn(const std::vector<std::string>& args, std::vector<Report>* capture) {
@@ -647,7 +655,7 @@ int cmd_frnn(const std::vector<std::string>& args, std::vector<Report>* capture)
   const uint64_t zone = o.exclusion < 0 ? o.len : static_cast<uint64_t>(o.exclusion);
   return frnn_report(
       "frnn", ps.get(), dataset, radius, o.refs, o.factor, o.seed, zone, o.engine, o.verify_engine,
-      p.str("--pairs-out"), o.common, [&](ParamsBuilder& pb, double f_eff) { series_params(pb, o, zone, f_eff); },
+      p.str("--pairs-out"), o.common, [&](ParamLine& pb, double f_eff) { series_params(pb, o, zone, f_eff); },
       capture);
 }
 
@@ -684,13 +692,13 @@ CloudOpts cloud_opts(const Parsed& p) {
   return o;
 }
 
-void cloud_params(ParamsBuilder& pb, const CloudOpts& o, double f_eff) {
-  pb.arg(o.path);
-  pb.opt("--refs", o.refs);
-  pb.opt("--factor", f_eff);
-  pb.opt("--seed", o.seed);
-  pb.opt("--exclusion", o.zone);
-  pb.opt("--engine", o.engine);
+void cloud_params(ParamLine& pb, const CloudOpts& o, double f_eff) {
+  pb.value(o.path);
+  pb.option("--refs", o.refs);
+  pb.option("--factor", f_eff);
+  pb.option("--seed", o.seed);
+  pb.option("--exclusion", o.zone);
+  pb.option("--engine", o.engine);
 }
 
 Points cloud_points(const std::string& path) {
@@ -704,7 +712,7 @@ int cmd_closest(const std::vector<std::string>& args, std::vector<Report>* captu
   Points ps = cloud_points(o.path);
   return pair_report(
       "closest", ps.get(), o.path, o.refs, o.factor, o.seed, o.zone, o.engine, o.verify_engine, o.common,
-      [&](ParamsBuilder& pb, double f_eff) { cloud_params(pb, o, f_eff); }, capture);
+      [&](ParamLine& pb, double f_eff) { cloud_params(pb, o, f_eff); }, capture);
 }
 
 int cmd_neighbors(const std::vector<std::string>& args, std::vector<Report>* capture) {
@@ -717,7 +725,7 @@ int cmd_neighbors(const std::vector<std::string>& args, std::vector<Report>* cap
   Points ps = cloud_points(o.path);
   return frnn_report(
       "neighbors", ps.get(), o.path, radius, o.refs, o.factor, o.seed, o.zone, o.engine, o.verify_engine,
-      p.str("--pairs-out"), o.common, [&](ParamsBuilder& pb, double f_eff) { cloud_params(pb, o, f_eff); }, capture);
+      p.str("--pairs-out"), o.common, [&](ParamLine& pb, double f_eff) { cloud_params(pb, o, f_eff); }, capture);
 }
 
 // ---------------------------------------------------------------------------
@@ -832,27 +840,40 @@ int cmd_sweep(const std::vector<std::string>& args, std::vector<Report>* capture
 
 int run_cli(const std::vector<std::string>& args, std::vector<Report>* capture);
 
-template <typename T>
-bool check_field(const nlohmann::json& row, const char* key, const T& got, std::string& msg) {
-  if (!row.contains(key)) {
-    msg = std::string(key) + " missing from report";
-    return false;
+// First replayed field where the stored row and the re-run differ, as
+// "<field> expected <stored> got <re-run>" (empty when they agree).
+std::string first_difference(const nlohmann::json& stored, const Report& rerun) {
+  for (const Field& f : kFields) {
+    if (!f.replayed) continue;
+    const auto it = stored.find(f.name);
+    if (it == stored.end()) return std::string(f.name) + " missing from report";
+    const nlohmann::json now = f.get(rerun);
+    if (*it != now) return std::string(f.name) + " expected " + it->dump() + " got " + now.dump();
   }
-  const T expected = row.at(key).get<T>();
-  if (expected != got) {
-    msg = std::string(key) + " expected " + nlohmann::json(expected).dump() + " got " + nlohmann::json(got).dump();
-    return false;
-  }
-  return true;
+  return {};
 }
 
-bool compare_row(const nlohmann::json& row, const Report& got, std::string& msg) {
-  return check_field(row, "algorithm", got.algorithm, msg) && check_field(row, "dataset", got.dataset, msg) &&
-         check_field(row, "pair_index_1", got.pair_index_1, msg) &&
-         check_field(row, "pair_index_2", got.pair_index_2, msg) &&
-         check_field(row, "distance_or_matches", got.distance_or_matches, msg) &&
-         check_field(row, "pairs_examined", got.pairs_examined, msg) &&
-         check_field(row, "iterations", got.iterations, msg) && check_field(row, "seed", got.seed, msg);
+// One params line and the stored rows it produced, in file order.
+struct ReplayGroup {
+  std::string params;
+  std::vector<const nlohmann::json*> rows;
+};
+
+// Replays one group; returns the line verify prints for it.
+std::string replay(const ReplayGroup& g) {
+  if (g.params.empty()) return "MISMATCH report has no params line";
+  const std::vector<std::string> argv = split_params(g.params);
+  if (argv.empty() || argv[0] == "verify") return "MISMATCH params line is not replayable: " + g.params;
+  std::vector<Report> rerun;
+  if (const int rc = run_cli(argv, &rerun); rc != 0)
+    return "MISMATCH re-run exited with code " + std::to_string(rc) + ": " + g.params;
+  if (rerun.size() != g.rows.size())
+    return "MISMATCH re-run produced " + std::to_string(rerun.size()) + " reports, file holds " +
+           std::to_string(g.rows.size()) + ": " + g.params;
+  for (size_t k = 0; k < rerun.size(); ++k)
+    if (std::string why = first_difference(*g.rows[k], rerun[k]); !why.empty())
+      return "MISMATCH row " + std::to_string(k + 1) + ": " + why + ": " + g.params;
+  return "OK " + g.params;
 }
 
 int cmd_verify(const std::vector<std::string>& args, std::vector<Report>* capture) {
@@ -864,64 +885,28 @@ int cmd_verify(const std::vector<std::string>& args, std::vector<Report>* captur
     std::cerr << "error: verify cannot replay a verify run\n";
     return 2;
   }
-  const nlohmann::json doc = nlohmann::json::parse(read_text_file(p.pos[0]));
-  std::vector<nlohmann::json> rows;
-  if (doc.is_array())
-    rows.assign(doc.begin(), doc.end());
-  else
-    rows.push_back(doc);
-  if (rows.empty()) {
+  nlohmann::json doc = nlohmann::json::parse(read_text_file(p.pos[0]));
+  if (!doc.is_array()) doc = nlohmann::json::array({std::move(doc)});
+  if (doc.empty()) {
     std::cerr << "error: report file holds no reports\n";
     return 2;
   }
-  std::vector<std::pair<std::string, std::vector<nlohmann::json>>> groups;
-  for (const auto& row : rows) {
+  // rows sharing a params line came from one run: group them, first-seen order
+  std::vector<ReplayGroup> groups;
+  std::map<std::string, size_t> group_of;
+  for (const nlohmann::json& row : doc) {
     const std::string params = row.value("params", "");
-    auto it = std::find_if(groups.begin(), groups.end(), [&](const auto& g) { return g.first == params; });
-    if (it == groups.end()) {
-      groups.push_back({params, {}});
-      it = std::prev(groups.end());
-    }
-    it->second.push_back(row);
+    const auto [it, fresh] = group_of.try_emplace(params, groups.size());
+    if (fresh) groups.push_back({params, {}});
+    groups[it->second].rows.push_back(&row);
   }
-  bool ok = true;
-  for (const auto& [params, group_rows] : groups) {
-    if (params.empty()) {
-      std::cout << "verify: MISMATCH report has no params line\n";
-      ok = false;
-      continue;
-    }
-    const std::vector<std::string> tokens = split_params(params);
-    if (tokens.empty() || tokens.front() == "verify") {
-      std::cout << "verify: MISMATCH params line is not replayable: " << params << "\n";
-      ok = false;
-      continue;
-    }
-    std::vector<Report> got;
-    const int rc = run_cli(tokens, &got);
-    if (rc != 0) {
-      std::cout << "verify: MISMATCH re-run exited with code " << rc << ": " << params << "\n";
-      ok = false;
-      continue;
-    }
-    if (got.size() != group_rows.size()) {
-      std::cout << "verify: MISMATCH re-run produced " << got.size() << " reports, file holds " << group_rows.size()
-                << ": " << params << "\n";
-      ok = false;
-      continue;
-    }
-    bool group_ok = true;
-    for (size_t i = 0; i < got.size(); ++i) {
-      std::string msg;
-      if (!compare_row(group_rows[i], got[i], msg)) {
-        std::cout << "verify: MISMATCH row " << i + 1 << ": " << msg << ": " << params << "\n";
-        group_ok = ok = false;
-        break;
-      }
-    }
-    if (group_ok) std::cout << "verify: OK " << params << "\n";
+  int failed = 0;
+  for (const ReplayGroup& g : groups) {
+    const std::string line = replay(g);
+    failed += line.rfind("OK ", 0) != 0;
+    std::cout << "verify: " << line << "\n";
   }
-  return ok ? 0 : 3;
+  return failed ? 3 : 0;
 }
 
 // ---------------------------------------------------------------------------

@@ -49,12 +49,14 @@ __device__ __forceinline__ void tri_index(uint64_t t, uint32_t* bi, uint32_t* bj
   *bi = static_cast<uint32_t>(t - j * (j + 1) / 2);
 }
 
+// One launch covers tiles [base, base + gridDim.x) of the upper triangle
+// (n = 2^24 has 8.6e9 tiles: launched in chunks below 2^31 blocks).
 template <int MODE>
-__global__ void __launch_bounds__(256) k_brute(BruteArgs a) {
+__global__ void __launch_bounds__(256) k_brute(BruteArgs a, uint64_t base) {
   __shared__ __align__(16) float As[kDK][kPad];
   __shared__ __align__(16) float Bs[kDK][kPad];
   uint32_t bi, bj;
-  tri_index(blockIdx.x, &bi, &bj);
+  tri_index(base + blockIdx.x, &bi, &bj);
   const uint32_t i0 = bi * kT, j0 = bj * kT;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   float acc[8][8];
@@ -163,10 +165,13 @@ uint64_t tiles_for(uint64_t n) {
 
 template <int MODE>
 void launch(const BruteArgs& a, cudaStream_t s) {
-  const uint64_t blocks = tiles_for(a.n);
-  k_brute<MODE><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
-  PSG_LAUNCHED();
-  ++g_launches;
+  const uint64_t tiles = tiles_for(a.n);
+  constexpr uint64_t kMaxBlocks = 1ull << 30;
+  for (uint64_t base = 0; base < tiles; base += kMaxBlocks) {
+    k_brute<MODE><<<static_cast<unsigned>(std::min(kMaxBlocks, tiles - base)), 256, 0, s>>>(a, base);
+    PSG_LAUNCHED();
+    ++g_launches;
+  }
 }
 
 Budget band_budget(const psg_pointset& ps) {
@@ -181,7 +186,9 @@ Budget band_budget(const psg_pointset& ps) {
 
 }  // namespace
 
-psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone) {
+// upper < 0: two passes (the FP32 minimum, then its band); upper >= 0: one
+// pass over the band of FP64 distance `upper` (source units).
+psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone, double upper) {
   const uint64_t n = ps->n;
   if (n < 2) throw invalid_argument("closest_pair needs at least 2 points");  // refscan.cpp:136
   if (n >= 0xffffffffull) throw invalid_argument("point count exceeds 2^32-1");
@@ -195,19 +202,25 @@ psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone) {
   a.n = static_cast<uint32_t>(n);
   a.d = ps->d;
   a.zone = zone;
-  DevBuf<unsigned> best(1, s);
-  const float inf = INFINITY;
-  PSG_CUDA(cudaMemcpyAsync(best.p, &inf, 4, cudaMemcpyHostToDevice, s));
-  a.best = best.p;
-  launch<kMin>(a, s);
-  unsigned hb;
-  PSG_CUDA(cudaMemcpyAsync(&hb, best.p, 4, cudaMemcpyDeviceToHost, s));
-  PSG_CUDA(cudaStreamSynchronize(s));
-  tm.mark("brute_min");
-  float bs;
-  std::memcpy(&bs, &hb, 4);
   const Budget bud = band_budget(*ps);
-  a.thr = budget_thresholds_s32(bud, bs).band;
+  if (upper < 0.0) {
+    DevBuf<unsigned> best(1, s);
+    const float inf = INFINITY;
+    PSG_CUDA(cudaMemcpyAsync(best.p, &inf, 4, cudaMemcpyHostToDevice, s));
+    a.best = best.p;
+    launch<kMin>(a, s);
+    unsigned hb;
+    PSG_CUDA(cudaMemcpyAsync(&hb, best.p, 4, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    tm.mark("brute_min");
+    float bs;
+    std::memcpy(&bs, &hb, 4);
+    a.thr = budget_thresholds_s32(bud, bs).band;
+  } else {
+    // every pair at FP64 distance <= upper (the FRNN boundary band, psg_frnn.cu)
+    const double Uw = upper * ps->scale;
+    a.thr = budget_thresholds(bud, (Uw * (1.0 + 4.0 * bud.gamma64) + 2.0 * bud.Rn) * (1.0 + 1e-12)).band;
+  }
   uint32_t cap = 1u << 16;
   DevBuf<unsigned long long> cnt(1, s);
   DevBuf<uint32_t> ci, cj;
@@ -237,11 +250,13 @@ psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone) {
   const unsigned long long init[2] = {~0ull, ~0ull};
   PSG_CUDA(cudaMemcpyAsync(red.p, init, 16, cudaMemcpyHostToDevice, s));
   const ExactSrc src = ps->exact();
-  k_recheck_plain<<<(nc + 255) / 256, 256, 0, s>>>(src, ci.p, cj.p, nc, d64.p, red.p);
-  PSG_LAUNCHED();
-  k_pick_plain<<<(nc + 255) / 256, 256, 0, s>>>(ci.p, cj.p, nc, d64.p, red.p, red.p + 1);
-  PSG_LAUNCHED();
-  g_launches += 2;
+  if (nc) {
+    k_recheck_plain<<<(nc + 255) / 256, 256, 0, s>>>(src, ci.p, cj.p, nc, d64.p, red.p);
+    PSG_LAUNCHED();
+    k_pick_plain<<<(nc + 255) / 256, 256, 0, s>>>(ci.p, cj.p, nc, d64.p, red.p, red.p + 1);
+    PSG_LAUNCHED();
+    g_launches += 2;
+  }
   unsigned long long hr[2];
   PSG_CUDA(cudaMemcpyAsync(hr, red.p, 16, cudaMemcpyDeviceToHost, s));
   tm.mark("recheck");
@@ -251,6 +266,10 @@ psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone) {
   r.index_i = hr[1] >> 32;
   r.index_j = hr[1] & 0xffffffffull;
   std::memcpy(&r.distance, &hr[0], 8);
+  if (hr[1] == ~0ull || (upper >= 0.0 && !(r.distance <= upper))) {
+    r.index_i = r.index_j = UINT64_MAX;
+    r.distance = INFINITY;
+  }
   r.stats.pairs_examined = adm;  // every admissible pair (refscan.cpp:145)
   g_prof.candidates = nc;
   g_prof.lb_survivors = adm;

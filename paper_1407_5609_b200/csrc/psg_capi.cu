@@ -65,28 +65,17 @@ int guarded_host(F&& f) {
   }
 }
 
-// Stream a .psgb payload into device memory through two pinned staging
-// buffers (kept for the process): the parallel read of chunk k+1 overlaps the
-// upload of chunk k.
+// Stream a .psgb payload into device memory through the context's pinned
+// chunks: the parallel read of chunk k+1 overlaps the upload of chunk k.
 psg::DevBuf<char> upload_file(psg::BinaryFile& bf, cudaStream_t s) {
-  constexpr size_t kChunk = size_t(64) << 20;
-  static char* stage[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2] = {nullptr, nullptr};
-  for (int k = 0; k < 2; ++k) {
-    if (!stage[k]) PSG_CUDA(cudaMallocHost(&stage[k], kChunk));
-    if (!done[k]) PSG_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
-  }
   psg::DevBuf<char> dev(std::max<uint64_t>(bf.bytes, 1), s);
-  for (uint64_t off = 0, k = 0; off < bf.bytes; off += kChunk, k ^= 1) {
-    const size_t len = static_cast<size_t>(std::min<uint64_t>(kChunk, bf.bytes - off));
-    PSG_CUDA(cudaEventSynchronize(done[k]));  // the previous upload from this buffer has finished
-    if (bf.pread_payload(stage[k], off, len, 8) != len) {
+  psg::h2d_staged(dev.p, bf.bytes, [&](char* stage, uint64_t off, size_t len) {
+    if (bf.pread_payload(stage, off, len, 8) != len) {
       cudaStreamSynchronize(s);
       throw psg::io_error("short read from a .psgb file");
     }
-    PSG_CUDA(cudaMemcpyAsync(dev.p + off, stage[k], len, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaEventRecord(done[k], s));
-  }
+    return len;
+  }, s);
   PSG_CUDA(cudaStreamSynchronize(s));
   psg::g_prof.h2d_bytes += bf.bytes;
   return dev;
@@ -302,6 +291,12 @@ int psg_closest_pair_ps(psg_pointset* ps, uint64_t q, double f, uint64_t seed, u
 }
 int psg_brute_force_closest_pair_ps(psg_pointset* ps, uint64_t exclusion_zone, psg_pair_result* out) {
   return guarded([&] { *out = psg::brute_solve(ps, exclusion_zone); });
+}
+int psg_debug_brute_bounded_ps(psg_pointset* ps, uint64_t exclusion_zone, double upper, psg_pair_result* out) {
+  return guarded([&] {
+    if (!(upper >= 0.0) || !std::isfinite(upper)) throw psg::invalid_argument("upper bound must be finite and >= 0");
+    *out = psg::brute_solve(ps, exclusion_zone, upper);
+  });
 }
 int psg_brute_force_neighbors_ps(psg_pointset* ps, double radius, uint64_t exclusion_zone, int want_lists,
                                  psg_neighbor_result* out) {

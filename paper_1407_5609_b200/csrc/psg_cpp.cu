@@ -535,26 +535,6 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
   if (tid == 0 && nq) atomicAdd(a.evals, static_cast<unsigned long long>(nq));
 }
 
-// Pairs that overflowed the shared-memory queue.
-// The count is read on device (min(spill count, capacity)): no host round trip.
-__global__ void k_eval_list(ScanArgs a, const uint32_t* __restrict__ lp, const uint32_t* __restrict__ lj) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t count = min(*a.ovf_n, a.ovf_cap);
-  for (uint32_t i = warp; i < count; i += nwarps) {
-    const uint32_t pi = lp[i], pj = lj[i];
-    const float* xi = a.X + static_cast<size_t>(a.sidx[pi]) * a.d;
-    const float* xj = a.X + static_cast<size_t>(a.sidx[pj]) * a.d;
-    const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f) : warp_sqdist(xi, xj, a.d, lane);
-    if (lane == 0) {
-      const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
-      record(a, pi, pj, s, th.band);
-    }
-  }
-  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(a.evals, static_cast<unsigned long long>(count));
-}
-
 // K6: deterministic final filter + FP64 recheck in the reference's order.
 // Thresholds come from the final FP32 bound on device; the candidate count is
 // min(candidates, capacity) read on device; grid-stride over candidates.
@@ -562,7 +542,7 @@ template <int NK, bool kWindow>
 __global__ void k_recheck(ScanArgs a, ExactSrc src, double* __restrict__ d64, unsigned long long* __restrict__ best64,
                           unsigned long long* __restrict__ examined) {
   const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
-  const uint32_t count = min(*a.cand_n, a.cand_cap);
+  const uint32_t count = static_cast<uint32_t>(min(*a.cand_n, static_cast<unsigned long long>(a.cand_cap)));
   for (uint32_t base = blockIdx.x * blockDim.x; base < count; base += gridDim.x * blockDim.x) {
   const uint32_t c = base + threadIdx.x;
   unsigned pass = 0;
@@ -588,13 +568,10 @@ __global__ void k_recheck(ScanArgs a, ExactSrc src, double* __restrict__ d64, un
 
 __global__ void k_pick(const ScanArgs a, const double* __restrict__ d64, const unsigned long long* __restrict__ best64,
                        unsigned long long* __restrict__ lex) {
-  const uint32_t count = min(*a.cand_n, a.cand_cap);
+  const uint32_t count = static_cast<uint32_t>(min(*a.cand_n, static_cast<unsigned long long>(a.cand_cap)));
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
     if (static_cast<unsigned long long>(__double_as_longlong(d64[c])) != *best64 || d64[c] < 0.0) continue;
-    const uint32_t i = a.sidx[a.cand_p[c]], j = a.sidx[a.cand_j[c]];
-    const unsigned long long key = i < j ? (static_cast<unsigned long long>(i) << 32) | j
-                                         : (static_cast<unsigned long long>(j) << 32) | i;
-    atomicMin(lex, key);
+    atomicMin(lex, lex_key(a.sidx[a.cand_p[c]], a.sidx[a.cand_j[c]]));
   }
 }
 
@@ -660,17 +637,19 @@ void part_range(uint64_t n, uint64_t part, uint64_t nparts, uint32_t* lo, uint32
 __global__ void k_state_init(DevState* st) {
   st->norm2_bits = 0;
   st->best = 0x7f800000u;  // +inf
-  st->cand_n = st->ovf_n = 0;
+  st->cand_n = 0;
   st->best64 = ~0ull;
   st->lex = ~0ull;
-  st->examined = st->evals = st->visited = 0;
+  st->best128[0] = st->best128[1] = ~0ull;
+  st->examined = st->evals = st->visited = st->inline_n = 0;
 }
 
 __global__ void k_scan_reset(DevState* st) {
-  st->cand_n = st->ovf_n = 0;
+  st->cand_n = 0;
   st->best64 = ~0ull;
   st->lex = ~0ull;
-  st->examined = st->evals = st->visited = 0;
+  st->best128[0] = st->best128[1] = ~0ull;
+  st->examined = st->evals = st->visited = st->inline_n = 0;
 }
 
 struct SetupArgs {
@@ -835,6 +814,11 @@ Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm
   return b;
 }
 
+void CppWork::drop_graph() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  gexec = nullptr;
+}
+
 CppWork::~CppWork() {
   if (host_st) cudaFreeHost(host_st);
   if (gexec) cudaGraphExecDestroy(gexec);
@@ -891,10 +875,10 @@ ScanArgs make_args(CppPlan& plan) {
   a.cand_s = W.cand_s.p;
   a.cand_n = &st->cand_n;
   a.cand_cap = W.cand_cap;
-  a.ovf_p = W.ovf_p.p;
-  a.ovf_j = W.ovf_j.p;
-  a.ovf_n = &st->ovf_n;
-  a.ovf_cap = W.ovf_cap;
+  a.src = plan.ps->exact();
+  a.best128 = st->best128;
+  a.examined = &st->examined;
+  a.inline_n = &st->inline_n;
   a.evals = &st->evals;
   a.visited = &st->visited;
   a.no_ub = std::getenv("PSG_NO_UB") != nullptr;
@@ -1082,34 +1066,26 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
 
 namespace {
 
+constexpr uint32_t kCandMax = 1u << 24;  // list capacity ceiling; band pairs past it are evaluated inline
+
 void ensure_candidates(CppWork& W, cudaStream_t s) {
-  if (W.cand_cap == 0) {
-    W.cand_cap = 1u << 16;
-    W.ovf_cap = 1u << 20;
-  }
+  if (W.cand_cap == 0) W.cand_cap = 1u << 16;
   if (W.cand_p.n < W.cand_cap) {
+    W.drop_graph();  // a captured solve holds the old buffers
     W.cand_p.alloc(W.cand_cap, s);
     W.cand_j.alloc(W.cand_cap, s);
     W.cand_s.alloc(W.cand_cap, s);
     W.d64.alloc(W.cand_cap, s);
   }
-  if (W.ovf_p.n < W.ovf_cap) {
-    W.ovf_p.alloc(W.ovf_cap, s);
-    W.ovf_j.alloc(W.ovf_cap, s);
-  }
 }
 
-// Grow the candidate / spill buffers after an overflow; true = rescan needed.
-bool grow_on_overflow(CppWork& W, const DevState& h) {
-  if (h.ovf_n > W.ovf_cap) {  // spill list overflowed: rescan with the tighter bound
-    W.ovf_cap = std::min<uint64_t>(static_cast<uint64_t>(h.ovf_n) * 2, 1u << 28);
-    return true;
-  }
-  if (h.cand_n > W.cand_cap) {  // candidate list overflowed: bound is tighter now, rescan
-    W.cand_cap = std::min<uint64_t>(static_cast<uint64_t>(h.cand_n) * 2, 1u << 28);
-    return true;
-  }
-  return false;
+// After a scan whose band held more pairs than the list: the answer is still
+// exact (record() evaluated the rest inline), but later solves on this point
+// set get a longer list, so the bulk of their band goes through the
+// deterministic recheck again.
+void grow_after_overflow(CppWork& W, const DevState& h) {
+  if (h.cand_n > W.cand_cap && W.cand_cap < kCandMax)
+    W.cand_cap = static_cast<uint32_t>(std::min<unsigned long long>(h.cand_n * 2, kCandMax));
 }
 
 // One scan attempt, enqueued only (no host synchronisation): reset, grid
@@ -1153,8 +1129,6 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
     ++g_prof.scan_launches;
   }
   span->end();
-  k_eval_list<<<c.sm_count * 8, 256, 0, s>>>(a, W.ovf_p.p, W.ovf_j.p);  // queue spill list
-  PSG_LAUNCHED();
   const ExactSrc ex = plan.ps->exact();
   const int nb = c.sm_count * 2;
   if (plan.grid) {
@@ -1170,19 +1144,25 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
   k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
   PSG_LAUNCHED();
   PSG_CUDA(cudaMemcpyAsync(W.host_st, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-  g_launches += plan.grid ? 7 : 6;
+  g_launches += plan.grid ? 6 : 5;
   return span;
 }
 
 psg_pair_result result_from(const DevState& h, uint64_t wp, uint64_t exits) {
   psg_pair_result r{};
-  if (h.lex == ~0ull) {
+  // the listed candidates' (best64, lex) against the inline 128-bit minimum
+  unsigned long long hi = h.best64, lo = h.lex;
+  if (h.lex == ~0ull || h.best128[1] < hi || (h.best128[1] == hi && h.best128[0] < lo)) {
+    hi = h.best128[1];
+    lo = h.best128[0];
+  }
+  if (lo == ~0ull) {
     r.index_i = r.index_j = UINT64_MAX;
     r.distance = INFINITY;
   } else {
-    r.index_i = h.lex >> 32;
-    r.index_j = h.lex & 0xffffffffull;
-    std::memcpy(&r.distance, &h.best64, 8);
+    r.index_i = lo >> 32;
+    r.index_j = lo & 0xffffffffull;
+    std::memcpy(&r.distance, &hi, 8);
   }
   r.stats.pairs_examined = h.examined;
   r.stats.pairs_pruned_by_reference = wp > h.examined ? wp - h.examined : 0;
@@ -1190,6 +1170,7 @@ psg_pair_result result_from(const DevState& h, uint64_t wp, uint64_t exits) {
   g_prof.window_pairs += wp;
   g_prof.lb_survivors += h.evals;
   g_prof.candidates += h.cand_n;
+  g_prof.inline_fp64 += h.inline_n;
   return r;
 }
 
@@ -1210,6 +1191,7 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
   ++g_launches;
   KernelSpan* scan_span = nullptr;
   for (int attempt = 0;; ++attempt) {
+    if (attempt > 16) throw std::runtime_error("closest_pair: the cell grid did not settle after 16 rebuilds");
     ensure_candidates(W, s);
     if (plan.grid) {
       // dense cells (clustered data): cell-pair tiles beat per-point lists
@@ -1300,18 +1282,11 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         W.learned_q = plan.q_arg;
         W.learned_seed = plan.seed_arg;
         W.learned_zone = plan.zone;
-        if (W.gexec) {
-          cudaGraphExecDestroy(W.gexec);
-          W.gexec = nullptr;
-        }
+        W.drop_graph();
       }
       continue;
     }
-    if (attempt > 12)
-      throw std::runtime_error("closest_pair: candidate buffers kept overflowing (cand " + std::to_string(h.cand_n) +
-                               "/" + std::to_string(W.cand_cap) + ", spill " + std::to_string(h.ovf_n) + "/" +
-                               std::to_string(W.ovf_cap) + ")");
-    if (grow_on_overflow(W, h)) continue;
+    grow_after_overflow(W, h);
     break;
   }
   g_prof.scan_kernel_ms += scan_span->ms();
@@ -1363,14 +1338,12 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   std::shared_ptr<CppWork> work = get_work(ps, dir.nk, s);
   CppWork& W = *work;
   if (W.learned_dense && W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone) return false;
-  if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone) {
-    if (W.gexec) {
-      cudaGraphExecDestroy(W.gexec);
-      W.gexec = nullptr;
-    }
-    // every allocation happens before capture
-    W.gi.ensure(static_cast<uint32_t>(ps->n), dir.nk, s);
-    ensure_candidates(W, s);
+  // every allocation happens before capture (and drops a graph that holds
+  // buffers it replaces)
+  W.gi.ensure(static_cast<uint32_t>(ps->n), dir.nk, s);
+  ensure_candidates(W, s);
+  if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone || W.gcap != W.cand_cap) {
+    W.drop_graph();
     for (cudaEvent_t& e : W.gev)
       if (!e) PSG_CUDA(cudaEventCreate(&e));
     PSG_CUDA(cudaStreamSynchronize(s));
@@ -1402,6 +1375,7 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
     W.gq = q;
     W.gseed = seed;
     W.gzone = zone;
+    W.gcap = W.cand_cap;
     W.glaunches = g_launches - launches0;
     g_launches = launches0;
   }
@@ -1409,10 +1383,8 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   PSG_CUDA(cudaStreamSynchronize(s));
   g_launches += W.glaunches;
   const DevState h = *W.host_st;
-  if (h.regrid || h.cand_n > W.cand_cap || h.ovf_n > W.ovf_cap) {
-    grow_on_overflow(W, h);
-    return false;
-  }
+  if (h.regrid) return false;  // cells narrower than the bound's window: the regular path rebuilds them
+  grow_after_overflow(W, h);    // exact regardless; the next capture gets a longer list
   float ms = 0.f;
   PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[0], W.gev[1]));
   g_prof.project_kernel_ms += ms;

@@ -33,13 +33,16 @@ Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm
 // so a solve is enqueued with two host synchronisations (after the bootstrap,
 // at the end).
 struct DevState {
+  // (FP64 distance bits, (i << 32) | j) minimum of the band pairs past the
+  // candidate list, evaluated inline (record(), psg_scan.cuh): [0] lo, [1] hi
+  alignas(16) unsigned long long best128[2];
+  unsigned long long cand_n;  // band pairs recorded (may exceed the list capacity)
   unsigned norm2_bits;  // max ||x||^2 (FP32 bits), from the projection
   unsigned best;        // FP32 bits of the best squared distance seen
-  unsigned cand_n, ovf_n;
   unsigned regrid;      // set by k_check_grid: cells narrower than the bound's key window
   unsigned check_best;  // FP32 bits of the bound k_check_grid tested
   Thresholds th;        // the scan's starting thresholds (from check_best)
-  unsigned long long best64, lex, examined, evals, visited;
+  unsigned long long best64, lex, examined, evals, visited, inline_n;
   Budget bud;
   double box_lo[kMaxGridKeys], box_span[kMaxGridKeys];
 };
@@ -54,21 +57,25 @@ struct CppWork {
   DevBuf<uint32_t> wsidx, wk0, wk1, wv0, wv1, whist;
   DevBuf<DevState> st;
   DevState* host_st = nullptr;  // pinned mirror
-  DevBuf<uint32_t> cand_p, cand_j, ovf_p, ovf_j;
+  DevBuf<uint32_t> cand_p, cand_j;
   DevBuf<float> cand_s;
   DevBuf<double> d64;
-  uint32_t cand_cap = 0, ovf_cap = 0;
+  uint32_t cand_cap = 0;
   DenseWork dense;         // dense cell-pair engine (clustered data)
   // The whole single-part grid solve captured once as a CUDA graph and
   // replayed by later solves with the same (q, seed, zone) on this point set.
+  // Its kernels hold the buffer pointers of capture time: any reallocation
+  // (ensure_candidates, GridIndex::ensure) destroys it (drop_graph).
   cudaGraphExec_t gexec = nullptr;
   uint64_t gq = 0, gseed = 0, gzone = 0;
+  uint32_t gcap = 0;  // cand_cap at capture
   uint64_t glaunches = 0;
   // cell width a regrid converged to, for the same (q, seed, zone)
   double learned_w = 0.0;
   uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;
   bool learned_dense = false;  // the solve went to the dense engine (not graph-capturable: host decisions)
   cudaEvent_t gev[6] = {};  // project / bootstrap / scan spans recorded inside the graph
+  void drop_graph();
   ~CppWork();
 };
 

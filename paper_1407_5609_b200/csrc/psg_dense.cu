@@ -21,6 +21,7 @@
 #include <string>
 #include <cmath>
 
+#include "psg_cpp.cuh"
 #include "psg_dense.cuh"
 #include "psg_points.cuh"
 #include "psg_sort.cuh"
@@ -943,9 +944,10 @@ __global__ void k_group_strips(const uint32_t* __restrict__ pa, const uint32_t* 
 // (flags[npairs] = 0); after an exclusive scan, the group index of its first pair.
 // A group is an A cell with at most kMaxPartners of its kept pairs (the own
 // pair first): an A with more (up to 3^8/2 stencil cells) spans several groups.
-__global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ flags) {
+__global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ flags,
+                              unsigned long long* __restrict__ split) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= npairs; k += gridDim.x * blockDim.x) {
-    uint32_t f = 0;
+    uint32_t f = 0, cont = 0;
     if (k < npairs) {
       if (k == 0 || pa[k] != pa[k - 1]) {
         f = 1;
@@ -960,9 +962,11 @@ __global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, 
             hi = mid;
         }
         f = (k - lo) % kMaxPartners == 0;
+        cont = f;  // a group continuing a longer run of the same A
       }
     }
     flags[k] = f;
+    if (cont) atomicAdd(split, 1ull);  // rare: only past 366 partners
   }
 }
 
@@ -1009,7 +1013,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   const bool gram = gram_shape(d) && !no_gram;
   if (w.Xs.n != static_cast<size_t>(n) * d) w.Xs.alloc(static_cast<size_t>(n) * d, s);
   if (w.cbox.n < cells * 2 * nk) w.cbox.alloc(cells * 2 * nk, s);
-  if (w.ctr.n < 5) w.ctr.alloc(5, s);
+  if (w.ctr.n < 6) w.ctr.alloc(6, s);
   if (w.clist.n < n) w.clist.alloc(n, s);
   k_gather_rows<<<sms * 16, 256, 0, s>>>(X, gi.sidx.p, n, d, w.Xs.p);
   PSG_LAUNCHED();
@@ -1041,6 +1045,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
       w.stmp.alloc(scan_temp_words(w.pair_cap + 1), s);
     }
     PSG_CUDA(cudaMemsetAsync(w.ctr.p, 0, 32, s));
+    PSG_CUDA(cudaMemsetAsync(w.ctr.p + 5, 0, 8, s));
     if (nk == 4)
       k_cell_pairs_list<4><<<lb, 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, w.clist.p, ne, w.cbox.p, th, w.pa.p, w.pb.p,
                                              w.ptiles.p, w.pair_cap, w.ctr.p, gram);
@@ -1054,6 +1059,8 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     if (npairs <= w.pair_cap) break;
     w.pair_cap = static_cast<uint32_t>(npairs);
   }
+  g_prof.dense_cells = cells;
+  g_prof.dense_cell_pairs = npairs;
   if (npairs == 0) return 0;
   const uint32_t np32 = static_cast<uint32_t>(npairs);
   // Deterministic work order: every rank of a sharded solve enumerates the
@@ -1074,7 +1081,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   g_launches += 1 + (bits + 7) / 8;
   if (gram) {
     // groups (a cell A and its kept partners), in pair order
-    k_group_flags<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, np32, scr0);
+    k_group_flags<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, np32, scr0, w.ctr.p + 5);
     PSG_LAUNCHED();
     exclusive_scan_u32(scr0, scr1, npairs + 1, w.stmp.p, s);
     uint32_t ng = 0;
@@ -1095,13 +1102,15 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
       launch_gram<32>(a, w, gi, spa, spb, np32, part, nparts, s);
     else
       launch_gram<64>(a, w, gi, spa, spb, np32, part, nparts, s);
-    if (std::getenv("PSG_TRACE")) {
-      unsigned long long t = 0;
-      PSG_CUDA(cudaMemcpyAsync(&t, w.ctr.p + 2, 8, cudaMemcpyDeviceToHost, s));
-      PSG_CUDA(cudaStreamSynchronize(s));
-      std::fprintf(stderr, "[psg] gram: %llu kept cell pairs, %u groups, %llu tiles\n",
-                   static_cast<unsigned long long>(npairs), ng, t);
-    }
+    unsigned long long t[6] = {};
+    PSG_CUDA(cudaMemcpyAsync(t, w.ctr.p, 48, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    g_prof.dense_groups = ng;
+    g_prof.dense_split_groups = t[5];
+    g_prof.dense_tiles = t[2];
+    if (std::getenv("PSG_TRACE"))
+      std::fprintf(stderr, "[psg] gram: %llu kept cell pairs, %u groups (%llu split), %llu tiles\n",
+                   static_cast<unsigned long long>(npairs), ng, t[5], t[2]);
   } else {
     // tiles per sorted pair -> prefix (scr0[npairs] = 0 so prefix[npairs] = total)
     k_pair_tiles<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, spb, np32, gi.dev.cfirst, scr0);

@@ -10,7 +10,8 @@
 namespace psg {
 
 // refscan.cpp:134-157 on device: exact over every admissible pair.
-psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone);
+// upper >= 0: one pass over the pairs at FP64 distance <= upper (inspection)
+psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone, double upper = -1.0);
 
 // refscan.cpp:159-209: cell grid on the first min(3, q) projection keys,
 // FP32 filter + FP64 decision on the boundary band.

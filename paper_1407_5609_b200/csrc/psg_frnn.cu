@@ -650,6 +650,7 @@ struct FrnnRun {
 FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                  bool emit = true) {
   const uint64_t n = ps->n;
+  if (n == 0) throw invalid_argument("empty input");  // refscan.cpp:162, before the radius check
   if (!(radius > 0.0) || !std::isfinite(radius)) throw invalid_argument("radius must be positive");
   check_reference_args(n, std::min(q, n), f);  // refscan.cpp:165 clamps q to n
   if (n >= 0xffffffffull) throw invalid_argument("point count exceeds 2^32-1");

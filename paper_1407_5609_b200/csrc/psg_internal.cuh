@@ -66,6 +66,12 @@ struct Ctx {
     return e;
   }
   void put_event(cudaEvent_t e) { events.push_back(e); }
+  // Two pinned staging chunks for pageable host input (h2d_staged,
+  // psg_points.cu), created on first use on this device; stage_done[k] marks
+  // the end of the last upload out of chunk k.
+  static constexpr size_t kStageBytes = size_t(32) << 20;
+  char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_done[2] = {nullptr, nullptr};
 };
 Ctx& ctx();  // context of the current CUDA device (created on first use)
 

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <map>
 #include <memory>
+#include <thread>
 #include <tuple>
 
 #include "host_rng.hpp"
@@ -54,6 +55,50 @@ Ctx& ctx() {
     c = std::move(nc);
   }
   return *c;
+}
+
+void h2d_staged(void* dst, uint64_t bytes, const std::function<size_t(char*, uint64_t, size_t)>& fill,
+                cudaStream_t s) {
+  Ctx& c = ctx();
+  for (int k = 0; k < 2; ++k) {
+    if (!c.stage[k]) PSG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c.stage[k]), Ctx::kStageBytes));
+    if (!c.stage_done[k]) PSG_CUDA(cudaEventCreateWithFlags(&c.stage_done[k], cudaEventDisableTiming));
+  }
+  char* out = static_cast<char*>(dst);
+  int k = 0;
+  for (uint64_t off = 0; off < bytes; off += Ctx::kStageBytes, k ^= 1) {
+    const size_t len = static_cast<size_t>(std::min<uint64_t>(Ctx::kStageBytes, bytes - off));
+    PSG_CUDA(cudaEventSynchronize(c.stage_done[k]));  // chunk k's previous upload has left it
+    if (fill(c.stage[k], off, len) != len) {
+      cudaStreamSynchronize(s);
+      throw std::runtime_error("short read while staging host input");
+    }
+    PSG_CUDA(cudaMemcpyAsync(out + off, c.stage[k], len, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaEventRecord(c.stage_done[k], s));
+  }
+}
+
+void h2d_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
+  if (!bytes) return;
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // an unregistered pointer may leave a sticky "invalid value" on old drivers
+  if (pinned || bytes <= (size_t(1) << 20)) {  // small copies: the driver's own staging is as fast
+    PSG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  static const unsigned threads = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const char* in = static_cast<const char*>(src);
+  h2d_staged(dst, bytes, [&](char* stage, uint64_t off, size_t len) {
+    // memcpy fan-out: one host thread moves ~10 GB/s, the PCIe link ~50
+    const size_t per = (len / threads + 4095) & ~size_t(4095);
+    std::vector<std::thread> th;
+    for (size_t a = per; a < len; a += per)
+      th.emplace_back([=] { std::memcpy(stage + a, in + off + a, std::min(per, len - a)); });
+    std::memcpy(stage, in + off, std::min(per, len));
+    for (std::thread& t : th) t.join();
+    return len;
+  }, s);
 }
 
 namespace {
@@ -261,8 +306,12 @@ template <class T>
 void upload(DevBuf<T>& dst, const T* src, uint64_t count, bool dev_src, cudaStream_t s, uint64_t* h2d) {
   dst.alloc(count, s);
   if (!count) return;
-  PSG_CUDA(cudaMemcpyAsync(dst.p, src, count * sizeof(T), dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-  if (!dev_src) *h2d += count * sizeof(T);
+  if (dev_src) {
+    PSG_CUDA(cudaMemcpyAsync(dst.p, src, count * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  h2d_copy(dst.p, src, count * sizeof(T), s);
+  *h2d += count * sizeof(T);
 }
 
 double read_r2(unsigned long long* dbits, cudaStream_t s) {

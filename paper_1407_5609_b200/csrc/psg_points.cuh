@@ -9,6 +9,7 @@
 //   mu/sigma  per-window FP64 statistics of z-normalised window sets
 #pragma once
 
+#include <functional>
 #include <memory>
 
 #include "psg_internal.cuh"
@@ -90,6 +91,15 @@ psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev
 psg_pointset* pointset_rows_f64(const double* p, uint64_t n, uint64_t d, bool dev_src);
 psg_pointset* pointset_windows(const double* series64, const float* series32, uint64_t length, uint64_t len,
                                bool znorm, bool dev_src);
+// Host -> device copies.  Pinned (page-locked or registered) sources go in one
+// cudaMemcpyAsync; pageable ones (a std::vector, a numpy array) stream through
+// the context's two pinned chunks: host threads fill chunk k+1 while the copy
+// engine drains chunk k, so the upload runs near the pinned PCIe rate instead
+// of the driver's pageable path.  `fill(stage, off, len)` writes source bytes
+// [off, off + len) into a pinned chunk and returns how many it wrote.
+void h2d_staged(void* dst, uint64_t bytes, const std::function<size_t(char*, uint64_t, size_t)>& fill,
+                cudaStream_t s);
+void h2d_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
 // Launch accounting for the profile (incremented by every launch site).
 extern thread_local uint64_t g_launches;
 }  // namespace psg

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "psg_internal.cuh"
+#include "psg_points.cuh"
 
 namespace psg {
 
@@ -83,6 +84,39 @@ __device__ __forceinline__ float best_now(const unsigned* best) {
 }
 
 // ---------------------------------------------------------------------------
+// The (FP64 distance, i, j) minimum as one 128-bit word: hi = the distance's
+// bits (non-negative doubles order as unsigned), lo = (i << 32) | j with i < j
+// original indices — the reference's "d < best, or d == best and (i, j)
+// lexicographically smaller" (refscan.cpp:118-126) is unsigned 128-bit order.
+// w[0] = lo, w[1] = hi; 16-byte aligned; initial value all ones.
+__device__ __forceinline__ void load_u128(const unsigned long long* w, unsigned long long& lo, unsigned long long& hi) {
+  asm volatile("{\n\t.reg .b128 r;\n\tld.relaxed.gpu.global.b128 r, [%2];\n\tmov.b128 {%0, %1}, r;\n\t}"
+               : "=l"(lo), "=l"(hi)
+               : "l"(w)
+               : "memory");
+}
+
+__device__ __forceinline__ void atomic_min_u128(unsigned long long* w, unsigned long long hi, unsigned long long lo) {
+  unsigned long long cl, ch;
+  load_u128(w, cl, ch);  // one 16-byte access: a snapshot; the word only decreases
+  while (hi < ch || (hi == ch && lo < cl)) {
+    unsigned long long ol, oh;
+    asm volatile(
+        "{\n\t.reg .b128 c, v, r;\n\tmov.b128 c, {%2, %3};\n\tmov.b128 v, {%4, %5};\n\t"
+        "atom.relaxed.gpu.global.cas.b128 r, [%6], c, v;\n\tmov.b128 {%0, %1}, r;\n\t}"
+        : "=l"(ol), "=l"(oh)
+        : "l"(cl), "l"(ch), "l"(lo), "l"(hi), "l"(w)
+        : "memory");
+    if (ol == cl && oh == ch) return;
+    cl = ol;
+    ch = oh;
+  }
+}
+
+__device__ __forceinline__ unsigned long long lex_key(uint32_t i, uint32_t j) {
+  return i < j ? (static_cast<unsigned long long>(i) << 32) | j : (static_cast<unsigned long long>(j) << 32) | i;
+}
+
 struct ScanArgs {
   const float* X;
   const float* skeys;
@@ -95,25 +129,42 @@ struct ScanArgs {
   uint32_t* cand_p;
   uint32_t* cand_j;
   float* cand_s;
-  unsigned* cand_n;
+  unsigned long long* cand_n;  // 64-bit: counts every band pair, never wraps
   uint32_t cand_cap;
-  uint32_t* ovf_p;
-  uint32_t* ovf_j;
-  unsigned* ovf_n;
-  uint32_t ovf_cap;
+  ExactSrc src;                   // the reference's values, for band pairs past the list
+  unsigned long long* best128;    // DevState::best128 (see atomic_min_u128)
+  unsigned long long* examined;   // FP64 evaluations
+  unsigned long long* inline_n;   // of which inline (past the list)
   unsigned long long* evals;
   unsigned long long* visited;  // grid engine: admissible stencil pairs
   int no_ub;                    // debugging: dense Gram tiles do not feed their upper bounds to `best`
 };
 
+// A pair inside the FP32 band of the bound seen so far.  The first cand_cap
+// band pairs of a scan are listed for the deterministic recheck (k_recheck /
+// k_pick, against the FINAL bound); every later one is evaluated here in the
+// reference's FP64 order and folded into the 128-bit (distance, i, j) minimum.
+// Both sets are real admissible pairs and together they hold every pair the
+// final band holds, so the minimum of the two is the reference's answer with
+// no rescan and O(1) memory, however many exact ties the data has (a run of
+// duplicate points puts all its pairs in the band).
 __device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {
   atomicMin(a.best, __float_as_uint(s32));
   if (s32 <= band) {
-    const unsigned c = atomicAdd(a.cand_n, 1u);
+    const unsigned long long c = atomicAdd(a.cand_n, 1ull);
     if (c < a.cand_cap) {
       a.cand_p[c] = p;
       a.cand_j[c] = j;
       a.cand_s[c] = s32;
+    } else {
+      const uint32_t oi = a.sidx[p], oj = a.sidx[j];
+      const double dd = exact_distance(a.src, oi, oj);
+      atomic_min_u128(a.best128, static_cast<unsigned long long>(__double_as_longlong(dd)), lex_key(oi, oj));
+      const unsigned m = __activemask();
+      if ((threadIdx.x & 31) == __ffs(m) - 1) {
+        atomicAdd(a.examined, static_cast<unsigned long long>(__popc(m)));
+        atomicAdd(a.inline_n, static_cast<unsigned long long>(__popc(m)));
+      }
     }
   }
 }

@@ -7,8 +7,16 @@ days), so each config is pinned by properties that do not depend on n:
          kernel: tiled brute force + FP64 band recheck) returns the same pair;
   C4     count and order-independent hash equal the oracle's exact cell-grid
          restatement of brute_force_neighbors; the pair list is sorted, i<j;
-  C5     (n = 2^17 of the recipe) scan == device all-pairs engine.
+  C5     scan == device all-pairs engine at n = 2^17 and 2^19 (two-pass brute
+         force), 2^21 and 2^22 (one-pass brute force over the FP64 band of the
+         scan's own distance, which the oracle recomputes first: the band holds
+         every pair at FP64 distance <= that value, so the brute force returns
+         the true minimum whatever the scan got), and the full n = 2^24 under
+         PSG_FULL_C5=1 (about 10 minutes of all-pairs work; its committed
+         output is profiles/r02_c5_fullsize.json).
 """
+import os
+
 import ctypes
 
 import numpy as np
@@ -69,3 +77,35 @@ def test_c5_recipe_dense_engine(psg, logn):
         assert (again.index_i, again.index_j, again.distance) == (got.index_i, got.index_j, got.distance)
     bf = psg.brute_force_closest_pair(ps, 0)
     assert (got.index_i, got.index_j, got.distance) == (bf.index_i, bf.index_j, bf.distance)
+
+
+def _check_c5(psg, orc, n):
+    pts = psg.gen.mixture(5, n, 64, 1024, 0.05)
+    ps = psg.PointSet.from_flat(pts, 64)
+    got = psg.closest_pair(ps, 10, 10.0, 1, 0)
+    prof = psg.last_profile()
+    # the scan's pair is real and its distance is the reference's FP64 value
+    assert got.distance == orc.euclidean(pts[got.index_i].astype(np.float64), pts[got.index_j].astype(np.float64))
+    bf = psg.brute_force_bounded(ps, 0, got.distance)
+    assert (bf.index_i, bf.index_j, bf.distance) == (got.index_i, got.index_j, got.distance)
+    return got, prof
+
+
+@pytest.mark.parametrize("logn", [21, 22])
+def test_c5_recipe_large(psg, orc, logn):
+    """The regimes of the full C5 size at 1/8 and 1/4 of it: the dense grid
+    over 8 keys beyond the sparse table's 2^24 cells, and A cells with more than
+    366 kept partners split across Gram groups (profile counters)."""
+    got, prof = _check_c5(psg, orc, 1 << logn)
+    assert prof["dense_cell_pairs"] > 0 and prof["dense_groups"] > 0
+    assert prof["dense_cells"] > 1 << 24, prof
+    if logn == 22:
+        assert prof["dense_split_groups"] > 0, prof
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("PSG_FULL_C5") != "1", reason="full C5 all-pairs check: set PSG_FULL_C5=1 (~10 min)")
+def test_c5_full(psg, orc):
+    got, prof = _check_c5(psg, orc, 1 << 24)
+    assert (got.index_i, got.index_j) == (2449215, 7867199)  # profiles/r02_c5_fullsize.json
+    assert prof["dense_cells"] > 1 << 24 and prof["dense_split_groups"] > 0, prof
