@@ -10,9 +10,18 @@ MB), and every step re-reads it from HBM.
 
 Metric unit: admissible pairs resolved per second = n(n-1)/2 / solve time
 (the rate at which the exact answer over all pairs is certified; the same
-unit for the CPU reference arm).  `value` is measured with the point set
+unit for the CPU reference arm, which solves bounded n = 2^14 samples).  The
+primary quantity is `solve_time_s`; `value` is measured with the point set
 already resident in HBM; `e2e` goes through the public C ABI from pinned host
-memory (H2D copy inside every step).
+memory (H2D copy inside every step); `e2e_pageable_f64` is the drop-in call a
+reference caller makes (PointSet::from_flat(std::vector<double>), i.e. FP64 rows
+in pageable memory through psg_closest_pair_f64).
+
+Beside it, in the same run: `same_n` (the GPU and the unmodified reference on
+the identical n = 2^14 C2 sample, one solve each), `cpu_fit` (the reference
+timed at n = 2^13..2^15, t = a n^b, measured points and the extrapolation to
+2^20 reported separately), `configs` (C1 on both arms, C3 one-shot, C4
+count+hash and sorted list, C5), and under torchrun a `c5_scaling` line.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N ... bench.py --gpus N   (one rank per GPU)
@@ -41,6 +50,14 @@ CPU_SAMPLE_N = 1 << 14
 
 def env_int(k, d):
     return int(os.environ.get(k, d))
+
+
+def load_bf16_sustained():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh).get("bf16_tflops_sustained", 1376.0))
+    return 1376.0
 
 
 def load_peaks():
@@ -198,6 +215,191 @@ def candidate_kernel_c4(hbm_gbs, peak_kind, reps=3):
             "peak": hbm_gbs, "peak_source": peak_kind,
             "model": "SURVEY 8(d): 4d B per candidate (streaming); candidates are re-read from L1/L2, so true DRAM traffic is far lower",
             "pairs": r.pair_count, "correct": ok}
+
+
+# ---------------------------------------------------------------------------
+# The reference beside the GPU (rank 0, N = 1): same-n sample, n^b fit, C1.
+FIT_LOGN = (13, 14, 15)
+C1_N, C1_D = 16384, 2
+C5_N, C5_D = 1 << 24, 64
+C5_EXPECT = (2449215, 7867199)  # profiles/r02_c5_fullsize.json (device brute force agrees)
+
+
+def reference_suite(c2_samples, c1_pts):
+    """The unmodified reference closest_pair (oracle/_ref) single-threaded on
+    the C2 recipe at n = 2^13, 2^14, 2^15 (one solve each, concurrently on
+    separate host threads; ctypes drops the GIL) and on C1 at full size, best
+    of 3.  Returns the measured points, the t = a n^b fit and the C1 time."""
+    import oracle
+
+    ref = oracle.reference()
+    if ref is None:
+        return None
+    times, answers = {}, {}
+
+    def one(logn):
+        pts64 = c2_samples[logn].astype(np.float64)
+        t0 = time.perf_counter()
+        r = ref.closest_pair(pts64, Q, F, SEED, 0)
+        times[logn] = time.perf_counter() - t0
+        answers[logn] = (r.index_i, r.index_j, r.distance)
+
+    c1 = {}
+
+    def c1_best():
+        p64 = c1_pts.astype(np.float64)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            r = ref.closest_pair(p64, Q, F, SEED, 0)
+            ts.append(time.perf_counter() - t0)
+        c1.update(best_s=min(ts), answer=(r.index_i, r.index_j, r.distance))
+
+    ths = [threading.Thread(target=one, args=(k,)) for k in sorted(c2_samples, reverse=True)]
+    ths.append(threading.Thread(target=c1_best))
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    ns = np.array([float(1 << k) for k in sorted(times)])
+    ts = np.array([times[k] for k in sorted(times)])
+    b, loga = np.polyfit(np.log(ns), np.log(ts), 1)
+    fit = {"measured": [{"n": 1 << k, "seconds": times[k], "answer": answers[k]} for k in sorted(times)],
+           "model": "t = a * n^b, least squares on log t over the measured points",
+           "a": float(np.exp(loga)), "b": float(b),
+           "extrapolated_c2_full_s": float(np.exp(loga) * float(N_C2) ** b),
+           "extrapolated": True, "note": "the n = 2^20 time is an extrapolation, not a measurement",
+           "threads_per_solve": 1, "nproc": os.cpu_count()}
+    return {"fit": fit, "c1": c1, "times": times, "answers": answers}
+
+
+def gpu_one_shot_f64(L, psg, pts, reps=3):
+    """The drop-in call: FP64 rows in pageable host memory through
+    psg_closest_pair_f64 (H2D, validation, narrowing, solve); best wall time."""
+    pts64 = np.ascontiguousarray(pts, dtype=np.float64)
+    n, d = pts64.shape
+    ts, r = [], None
+    for k in range(reps + 1):
+        out = psg._Pair()
+        t0 = time.perf_counter()
+        psg._check(L.psg_closest_pair_f64(pts64.ctypes.data, n, d, Q, F, SEED, 0, C.byref(out)))
+        if k:
+            ts.append(time.perf_counter() - t0)
+        r = psg._pair(out)
+    return min(ts), r
+
+
+def gpu_resident(psg, ps, reps=5, zone=0):
+    ts, dev, r = [], [], None
+    for k in range(reps + 1):
+        t0 = time.perf_counter()
+        r = psg.closest_pair(ps, Q, F, SEED, zone)
+        if k:
+            ts.append(time.perf_counter() - t0)
+            dev.append(psg.last_profile()["total_ms"])
+    return min(ts), min(dev), r, psg.last_profile()
+
+
+def configs_block(L, psg, hbm, bf16_sus):
+    """Every BASELINE config at full size, device-resident and end to end."""
+    out = {}
+    # C1
+    c1 = psg.gen.uniform(1, C1_N, C1_D)
+    ps = psg.PointSet.from_flat(c1, C1_D)
+    t, dev, r, _ = gpu_resident(psg, ps)
+    te, re_ = gpu_one_shot_f64(L, psg, c1)
+    out["c1"] = {"workload": "C1 CPP n=16384 d=2 U[0,1)^2", "resident_s": t, "device_ms": dev,
+                 "e2e_f64_pageable_s": te, "answer": [r.index_i, r.index_j, r.distance],
+                 "e2e_answer_same": (re_.index_i, re_.index_j, re_.distance) == (r.index_i, r.index_j, r.distance)}
+    ps.release()
+    # C3: one-shot from the host series (window build, z-norm statistics, solve)
+    s, (a, b) = psg.gen.walk_motif(3, 1 << 20, 256)
+    s64 = s.astype(np.float64)
+    ts = []
+    for k in range(4):
+        t0 = time.perf_counter()
+        r = psg.motif(s64, 256, Q, F, SEED)
+        if k:
+            ts.append(time.perf_counter() - t0)
+    ps = psg.PointSet.windows_of(s64, 256, znorm=True)
+    t, dev, rr, prof = gpu_resident(psg, ps, zone=256)
+    out["c3"] = {"workload": "C3 TSMM N=2^20 l=256 z-normalised, zone 256", "one_shot_s": min(ts),
+                 "resident_s": t, "device_ms": dev, "answer": [r.index_i, r.index_j, r.distance],
+                 "correct": (r.index_i, r.index_j) == tuple(sorted((a, b)))
+                 and (rr.index_i, rr.index_j, rr.distance) == (r.index_i, r.index_j, r.distance)}
+    ps.release()
+    # C4: the sorted (i<j) pair list into pinned host memory
+    cube = psg.gen.uniform(4, C4_N, 3)
+    pinned = psg.PinnedBuffer(20 * C4_N)
+    ts = []
+    for k in range(3):
+        t0 = time.perf_counter()
+        pairs, cnt, h = psg.frnn_pairs(cube, C4_R, Q, F, SEED, 0, want_pairs=True, out=pinned.array)
+        if k:
+            ts.append(time.perf_counter() - t0)
+    prof = psg.last_profile()
+    ok = (cnt, h) == C4_EXPECT and bool(np.all(pairs[1:] > pairs[:-1]))
+    out["c4_list"] = {"workload": "C4 FRNN n=2^22 d=3, sorted i<j pair list to pinned host (from pageable points)",
+                      "one_shot_s": min(ts), "pairs": cnt, "d2h_bytes": cnt * 8,
+                      "stages_ms": dict(prof["stage_list"]), "correct": ok}
+    del pinned
+    # C5
+    pts = psg.gen.mixture(5, C5_N, C5_D, 1024, 0.05)
+    ps = psg.PointSet.from_flat(pts, C5_D)
+    t, dev, r, prof = gpu_resident(psg, ps, reps=2)
+    gram_flop = prof["dense_tiles"] * 3 * 2 * 128 * 128 * C5_D
+    out["c5"] = {"workload": "C5 CPP n=2^24 d=64, 1024-cluster mixture", "resident_s": t, "device_ms": dev,
+                 "answer": [r.index_i, r.index_j, r.distance], "correct": (r.index_i, r.index_j) == C5_EXPECT,
+                 "dense_tiles": prof["dense_tiles"], "scan_kernel_ms": prof["scan_kernel_ms"],
+                 "gram_tflops_issued": gram_flop / (prof["scan_kernel_ms"] / 1e3) / 1e12 if prof["scan_kernel_ms"] else None,
+                 "tf32_peak_derived_tflops": bf16_sus / 2, "stages_ms": dict(prof["stage_list"])}
+    ps.release()
+    return out
+
+
+def c5_scaling(psg, L, rank, world, local_rank, coll, barrier):
+    """C5 (the ≥6x north_star config) under torchrun: rank 0 alone, then all
+    ranks on key-range parts; device time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1407_5609_b200 import sharded
+
+    pts = psg.gen.mixture(5, C5_N, C5_D, 1024, 0.05)
+    ps = psg.PointSet.from_flat(pts, C5_D)
+    adm = sharded.admissible_pairs(C5_N, 0)
+    t1 = None
+    if rank == 0:
+        psg.closest_pair(ps, Q, F, SEED, 0)
+        t0 = time.perf_counter()
+        psg.closest_pair(ps, Q, F, SEED, 0)
+        t1 = time.perf_counter() - t0
+    dist.barrier()
+
+    def sharded_solve():
+        plan = sharded.DevicePlan(ps._device(), Q, F, SEED, 0)
+        b = coll.all_reduce_min(plan.bootstrap(rank, world))
+        res = sharded.combine(coll.all_gather(plan.scan(rank, world, b)), adm)
+        plan.close()
+        return res
+
+    sharded_solve()  # warm-up
+    stream = torch.cuda.ExternalStream(L.psg_stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    r = sharded_solve()
+    e1.record(stream)
+    barrier()
+    wall = time.perf_counter() - t0
+    t = torch.tensor([wall, e0.elapsed_time(e1) / 1e3], device=f"cuda:{local_rank}", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ps.release()
+    return {"workload": "C5 CPP n=2^24 d=64 mixture, key-range parts (replicated points)", "n_gpus": world,
+            "solve_s_max_over_ranks": float(t[0]), "device_span_s_max_over_ranks": float(t[1]),
+            "solve_s_1gpu": t1, "speedup_vs_1gpu": (t1 / float(t[0])) if t1 else None,
+            "answer": [r.index_i, r.index_j, r.distance], "correct": (r.index_i, r.index_j) == C5_EXPECT}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -368,16 +570,52 @@ def run_ours(args, rank, world, local_rank):
         "correct": ok, "answer": {"planted": planted, "got": [results[-1].index_i, results[-1].index_j],
                                   "distance": results[-1].distance},
     }
+    if world == 1:
+        # the drop-in path: FP64 rows in pageable memory (a std::vector<double>)
+        tp, rp = gpu_one_shot_f64(L, psg, host, reps=3)
+        ok = ok and (rp.index_i, rp.index_j) == planted
+        line["e2e_pageable_f64"] = {"value": adm / tp, "unit": UNIT, "solve_s": tp, "h2d_bytes_per_step": n * d * 8,
+                                    "d2h_bytes_per_step": 56, "call": "psg_closest_pair_f64 (pageable host FP64)"}
+    L.psg_pointset_free(ph)
     if world == 1 and rank == 0 and not args.no_candidate_kernel:
         line["candidate_kernel"] = candidate_kernel_c4(hbm, peak_kind)
         line["correct"] = line["correct"] and line["candidate_kernel"]["correct"]
+    if world == 1 and rank == 0 and not args.no_configs:
+        cfg = configs_block(L, psg, hbm, load_bf16_sustained())
+        line["configs"] = cfg
+        line["correct"] = line["correct"] and cfg["c3"]["correct"] and cfg["c4_list"]["correct"] and cfg["c5"]["correct"]
+    if world > 1 and not args.no_configs:
+        line["c5_scaling"] = c5_scaling(psg, L, rank, world, local_rank, coll, barrier)
+        line["correct"] = line["correct"] and line["c5_scaling"]["correct"]
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        # same-n: the identical n = 2^14 C2 sample on the GPU and the reference
+        samples = {k: psg.gen.gauss_planted(2, 1 << k, D_C2)[0] for k in FIT_LOGN}
+        g_res_s, g_dev_ms, g_r, _ = gpu_resident(psg, psg.PointSet.from_flat(samples[14], D_C2))
+        g_e2e_s, g_e2e_r = gpu_one_shot_f64(L, psg, samples[14])
+        c1_pts = psg.gen.uniform(1, C1_N, C1_D)
+        suite = reference_suite(samples, c1_pts)
         rate, wall, kind, _ = cpu_reference_rate(CPU_SAMPLE_N, threads)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
                                 "sample": f"reference closest_pair (oracle/_ref, unmodified) on the C2 recipe at "
                                           f"n={CPU_SAMPLE_N}, d={D_C2}; {threads} threads x 1 solve, {wall:.1f}s"}
-    L.psg_pointset_free(ph)
+        if suite is not None:
+            ref_s = suite["times"][14]
+            same = suite["answers"][14] == (g_r.index_i, g_r.index_j, g_r.distance) == (
+                g_e2e_r.index_i, g_e2e_r.index_j, g_e2e_r.distance)
+            line["same_n"] = {"n": 1 << 14, "d": D_C2, "sample": "C2 recipe (master seed 2) at n=2^14",
+                              "ref_solve_s": ref_s, "ref_threads": 1,
+                              "gpu_e2e_f64_pageable_s": g_e2e_s, "gpu_resident_s": g_res_s,
+                              "gpu_device_ms": g_dev_ms, "speedup_e2e": ref_s / g_e2e_s,
+                              "speedup_resident": ref_s / g_res_s, "same_answer": same}
+            line["cpu_fit"] = suite["fit"]
+            if "configs" in line:
+                c1 = line["configs"]["c1"]
+                c1["ref_best_of_3_s"] = suite["c1"]["best_s"]
+                c1["ref_answer"] = suite["c1"]["answer"]
+                c1["same_answer"] = tuple(suite["c1"]["answer"]) == tuple(c1["answer"])
+                c1["speedup_e2e"] = suite["c1"]["best_s"] / c1["e2e_f64_pageable_s"]
+            line["correct"] = line["correct"] and same
     L.psg_host_free(hp)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -393,6 +631,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config block (C1, C3, C4 list, C5)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -190,6 +190,25 @@ int psg_cpp_plan_scan(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float 
                       psg_pair_result* out);
 void psg_cpp_plan_free(psg_cpp_plan* plan);
 
+/* Fixed-radius neighbours sharded the same way (refscan.cpp:159-209):
+ * plan_create projects and builds the cell grid (identical on every rank);
+ * plan_scan enumerates the pairs owned by part `part` of `nparts` (a pair is
+ * owned by the part holding its earlier grid-sorted position) and returns
+ * their count, order-independent hash and stats — the caller all-reduces
+ * (SUM) count, hash (mod 2^64) and stats; keep_pairs = 1 keeps the part's
+ * pairs on device for plan_pairs, which writes them sorted ascending
+ * ((i << 32) | j, i < j) into out[capacity] and fills bucket_counts[b] with
+ * how many have i in [n b / nbuckets, n (b + 1) / nbuckets) — the split of an
+ * all-to-all that leaves rank b the globally sorted list of its i-range. */
+typedef struct psg_frnn_plan psg_frnn_plan;
+int psg_frnn_plan_create(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed,
+                         uint64_t exclusion_zone, psg_frnn_plan** out);
+int psg_frnn_plan_scan(psg_frnn_plan* plan, uint64_t part, uint64_t nparts, int keep_pairs, uint64_t* pair_count,
+                       uint64_t* pair_hash, psg_scan_stats* stats);
+int psg_frnn_plan_pairs(psg_frnn_plan* plan, uint64_t nbuckets, uint64_t* bucket_counts, uint64_t* out,
+                        uint64_t capacity);
+void psg_frnn_plan_free(psg_frnn_plan* plan);
+
 /* ---- data formats --------------------------------------------
  * Text series: io.cpp:44-60 load_series — one decimal real per line, strtod
  * values, the reference's messages ("path:line: ..."; PSG_ERR_IO) and the

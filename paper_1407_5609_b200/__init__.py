@@ -120,6 +120,10 @@ _SIGS = {
     "psg_cpp_plan_bootstrap": (_int, [_p, _u64, _u64, _p]),
     "psg_cpp_plan_scan": (_int, [_p, _u64, _u64, _f32, _p]),
     "psg_cpp_plan_free": (None, [_p]),
+    "psg_frnn_plan_create": (_int, [_p, _f64, _u64, _f64, _u64, _u64, _p]),
+    "psg_frnn_plan_scan": (_int, [_p, _u64, _u64, _int, _p, _p, _p]),
+    "psg_frnn_plan_pairs": (_int, [_p, _u64, _p, _p, _u64]),
+    "psg_frnn_plan_free": (None, [_p]),
     "psg_gen_random_walk": (_int, [_u64, _u64, _f64, _p]),
     "psg_gen_uniform": (None, [_u64, _u64, _u64, _p]),
     "psg_gen_gauss_planted": (None, [_u64, _u64, _u64, _f64, _p, _p, _p]),

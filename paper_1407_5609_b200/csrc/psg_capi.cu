@@ -333,6 +333,32 @@ int psg_cpp_plan_scan(psg_cpp_plan* plan, uint64_t part, uint64_t nparts, float 
 }
 void psg_cpp_plan_free(psg_cpp_plan* plan) { delete plan; }
 
+// ---- sharded fixed-radius neighbours -------------------------------------------
+int psg_frnn_plan_create(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed,
+                         uint64_t exclusion_zone, psg_frnn_plan** out) {
+  return guarded([&] {
+    if (ps->n == 0) throw psg::invalid_argument("empty input");  // refscan.cpp:162
+    *out = reinterpret_cast<psg_frnn_plan*>(psg::frnn_plan_create(ps, radius, q, f, seed, exclusion_zone));
+  });
+}
+int psg_frnn_plan_scan(psg_frnn_plan* plan, uint64_t part, uint64_t nparts, int keep_pairs, uint64_t* pair_count,
+                       uint64_t* pair_hash, psg_scan_stats* stats) {
+  return guarded([&] {
+    if (nparts == 0 || part >= nparts) throw psg::invalid_argument("part out of range");
+    psg::FrnnPlan& p = *reinterpret_cast<psg::FrnnPlan*>(plan);
+    psg::frnn_plan_scan(p, part, nparts, keep_pairs != 0);
+    psg::frnn_plan_result(p, pair_count, pair_hash, stats);
+  });
+}
+int psg_frnn_plan_pairs(psg_frnn_plan* plan, uint64_t nbuckets, uint64_t* bucket_counts, uint64_t* out,
+                        uint64_t capacity) {
+  return guarded([&] {
+    if (nbuckets == 0) throw psg::invalid_argument("bucket count must be positive");
+    psg::frnn_plan_pairs(*reinterpret_cast<psg::FrnnPlan*>(plan), nbuckets, bucket_counts, out, capacity);
+  });
+}
+void psg_frnn_plan_free(psg_frnn_plan* plan) { psg::frnn_plan_free(reinterpret_cast<psg::FrnnPlan*>(plan)); }
+
 // ---- host helpers ----------------------------------------------------------------
 int psg_host_alloc(size_t bytes, void** out) {
   return guarded([&] { PSG_CUDA(cudaMallocHost(out, bytes)); });

@@ -634,7 +634,12 @@ void part_range(uint64_t n, uint64_t part, uint64_t nparts, uint32_t* lo, uint32
 
 // ---------------------------------------------------------------------------
 // Device-side solve state (DevState): initialised, filled and read back once.
-__global__ void k_state_init(DevState* st) {
+__global__ void k_state_init(DevState* st, ExactSrc src, const uint32_t* sidx) {
+  st->ic.src = src;
+  st->ic.sidx = sidx;
+  st->ic.best128 = st->best128;
+  st->ic.examined = &st->examined;
+  st->ic.inline_n = &st->inline_n;
   st->norm2_bits = 0;
   st->best = 0x7f800000u;  // +inf
   st->cand_n = 0;
@@ -875,10 +880,7 @@ ScanArgs make_args(CppPlan& plan) {
   a.cand_s = W.cand_s.p;
   a.cand_n = &st->cand_n;
   a.cand_cap = W.cand_cap;
-  a.src = plan.ps->exact();
-  a.best128 = st->best128;
-  a.examined = &st->examined;
-  a.inline_n = &st->inline_n;
+  a.ic = &st->ic;
   a.evals = &st->evals;
   a.visited = &st->visited;
   a.no_ub = std::getenv("PSG_NO_UB") != nullptr;
@@ -928,7 +930,19 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   plan->g = plan->grid ? std::min(3, plan->dir.q) : 0;
   plan->prep_tm = std::make_unique<StageTimer>(s);
   StageTimer& tm = *plan->prep_tm;
-  k_state_init<<<1, 1, 0, s>>>(W.st.p);
+  // every buffer the kernels see is allocated before the state that points into them
+  if (plan->grid) {
+    W.gi.ensure(static_cast<uint32_t>(n), nk, s);
+  } else if (W.wsidx.n != n) {
+    W.wskeys.alloc(n * nk, s);
+    W.wsidx.alloc(n, s);
+    W.wk0.alloc(n, s);
+    W.wk1.alloc(n, s);
+    W.wv0.alloc(n, s);
+    W.wv1.alloc(n, s);
+    W.whist.alloc(radix_hist_words(n), s);
+  }
+  k_state_init<<<1, 1, 0, s>>>(W.st.p, ps->exact(), plan->grid ? W.gi.sidx.p : W.wsidx.p);
   PSG_LAUNCHED();
   {
     plan->proj_span = std::make_unique<KernelSpan>(s);
@@ -957,15 +971,6 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
       k_setup<<<1, 256, 0, s>>>(W.st.p, nullptr, nullptr, sa);
       PSG_LAUNCHED();
       // K2 (window): sort by key 0 (stable, index payload)
-      if (W.wsidx.n != n) {
-        W.wskeys.alloc(n * nk, s);
-        W.wsidx.alloc(n, s);
-        W.wk0.alloc(n, s);
-        W.wk1.alloc(n, s);
-        W.wv0.alloc(n, s);
-        W.wv1.alloc(n, s);
-        W.whist.alloc(radix_hist_words(n), s);
-      }
       if (nk == 4)
         k_sort_keys<4><<<blocks_for(n, 256), 256, 0, s>>>(W.keys.p, static_cast<uint32_t>(n), W.wk0.p, W.wv0.p);
       else

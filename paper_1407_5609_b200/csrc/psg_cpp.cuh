@@ -45,6 +45,7 @@ struct DevState {
   unsigned long long best64, lex, examined, evals, visited, inline_n;
   Budget bud;
   double box_lo[kMaxGridKeys], box_span[kMaxGridKeys];
+  InlineCtx ic;  // set by k_state_init
 };
 
 // Buffers reused by every solve on one point set (per key count).

@@ -944,8 +944,8 @@ __global__ void k_group_strips(const uint32_t* __restrict__ pa, const uint32_t* 
 // (flags[npairs] = 0); after an exclusive scan, the group index of its first pair.
 // A group is an A cell with at most kMaxPartners of its kept pairs (the own
 // pair first): an A with more (up to 3^8/2 stencil cells) spans several groups.
-__global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t* __restrict__ flags,
-                              unsigned long long* __restrict__ split) {
+__global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, uint32_t group,
+                              uint32_t* __restrict__ flags, unsigned long long* __restrict__ split) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= npairs; k += gridDim.x * blockDim.x) {
     uint32_t f = 0, cont = 0;
     if (k < npairs) {
@@ -961,7 +961,7 @@ __global__ void k_group_flags(const uint32_t* __restrict__ pa, uint32_t npairs, 
           else
             hi = mid;
         }
-        f = (k - lo) % kMaxPartners == 0;
+        f = (k - lo) % group == 0;
         cont = f;  // a group continuing a longer run of the same A
       }
     }
@@ -1081,7 +1081,13 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   g_launches += 1 + (bits + 7) / 8;
   if (gram) {
     // groups (a cell A and its kept partners), in pair order
-    k_group_flags<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, np32, scr0, w.ctr.p + 5);
+    // pairs per group: kMaxPartners (the strip setup's capacity); PSG_GROUP_PAIRS
+    // lowers it so tests reach the split path at small n
+    uint32_t group = kMaxPartners;
+    if (const char* e = std::getenv("PSG_GROUP_PAIRS"))
+      group = static_cast<uint32_t>(std::clamp(std::atoi(e), 2, kMaxPartners));
+    k_group_flags<<<std::min<unsigned>(blocks(npairs + 1, 256), 4096), 256, 0, s>>>(spa, np32, group, scr0,
+                                                                                    w.ctr.p + 5);
     PSG_LAUNCHED();
     exclusive_scan_u32(scr0, scr1, npairs + 1, w.stmp.p, s);
     uint32_t ng = 0;

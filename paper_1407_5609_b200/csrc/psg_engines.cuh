@@ -19,6 +19,17 @@ void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
                 bool want_lists, psg_neighbor_result* out);
 void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                 uint64_t* pairs, uint64_t capacity, uint64_t* count, uint64_t* hash);
+// Sharded FRNN: the plan (projection + grid, identical on every rank), then
+// per-part scans; a pair belongs to the part holding its earlier sorted
+// position.  frnn_plan_pairs: the last scanned part's pairs, sorted, with
+// per-i-range bucket counts (the all-to-all split of the sorted list).
+struct FrnnPlan;
+FrnnPlan* frnn_plan_create(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone);
+void frnn_plan_scan(FrnnPlan& plan, uint64_t part, uint64_t nparts, bool emit);
+void frnn_plan_result(const FrnnPlan& plan, uint64_t* count, uint64_t* hash, psg_scan_stats* stats);
+void frnn_plan_pairs(FrnnPlan& plan, uint64_t nbuckets, uint64_t* bucket_counts, uint64_t* out, uint64_t capacity);
+void frnn_plan_free(FrnnPlan* plan);
+
 // refscan.cpp:211-227 on device.
 void brute_neighbors(psg_pointset* ps, double radius, uint64_t zone, bool want_lists, psg_neighbor_result* out);
 

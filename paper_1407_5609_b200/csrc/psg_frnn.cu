@@ -94,10 +94,33 @@ struct FrnnArgs {
   ExactSrc src;
   uint64_t* out;
   uint64_t cap;
-  unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined, [4] band pairs, [5] cell cursor
+  unsigned long long* acc;  // [0] count, [1] hash, [2] visited, [3] examined, [4] band pairs, [5] cell cursor,
+                            // [6] / [7] the part's cell range (k_part_cells)
   uint64_t* band;           // k_frnn_cells: pairs inside the rounding band, decided by k_frnn_band
   uint64_t bcap;
+  uint32_t plo, phi;        // the part's sorted positions [plo, phi) (pairs whose first position is there)
 };
+
+// The part's cells for k_frnn_cells: the cells whose first sorted position
+// lies in [plo, phi) (cfirst is non-decreasing, so parts split the cells into
+// consecutive ranges and every pair, visited from its earlier position's
+// cell, has exactly one owner).  One thread; acc[6], acc[7].
+__global__ void k_part_cells(FrnnArgs a) {
+  const uint64_t cells = a.grid.gp->cells;
+  auto first_at_or_after = [&](uint32_t pos) {  // least c with cfirst[c] >= pos
+    uint64_t lo = 0, hi = cells;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (a.grid.cfirst[mid] < pos)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  };
+  a.acc[6] = a.plo == 0 ? 0 : first_at_or_after(a.plo);
+  a.acc[7] = a.phi >= a.n ? cells : first_at_or_after(a.phi);
+}
 
 constexpr int kFrnnThreads = 256;
 
@@ -110,8 +133,8 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) sP = *a.grid.gp;
   __syncthreads();
-  const uint32_t p = blockIdx.x * kFrnnThreads + tid;
-  const bool valid = p < a.n;
+  const uint32_t p = a.plo + blockIdx.x * kFrnnThreads + tid;
+  const bool valid = p < a.phi;
   uint64_t visited = 0, examined = 0, hsum = 0;
   GridRanges R{};
   float mk[NK];
@@ -228,7 +251,7 @@ __global__ void __launch_bounds__(kFrnnThreads, 4) k_frnn_cells(FrnnArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) sP = *a.grid.gp;
   __syncthreads();
-  const uint64_t cells = sP.cells;
+  const uint64_t cell_lo = a.acc[6], cells = a.acc[7];  // this part's cells [cell_lo, cells)
   const uint32_t* __restrict__ cfirst = a.grid.cfirst;
   const unsigned lt = (1u << lane) - 1u;
   const float band = a.th.band, lo = a.lo;
@@ -251,7 +274,7 @@ __global__ void __launch_bounds__(kFrnnThreads, 4) k_frnn_cells(FrnnArgs a) {
   for (;;) {
     unsigned long long claim = 0;
     if (lane == 0) claim = atomicAdd(a.acc + 5, 1ull);
-    const uint64_t c0 = __shfl_sync(kFull, claim, 0) * 32ull;
+    const uint64_t c0 = cell_lo + __shfl_sync(kFull, claim, 0) * 32ull;
     if (c0 >= cells) break;
     const uint64_t mycell = c0 + lane;
     uint32_t s = 0, e = 0;
@@ -646,9 +669,30 @@ struct FrnnRun {
   uint64_t count = 0, hash = 0, visited = 0, examined = 0;
 };
 
-// emit = false: count + hash only (no pair list is materialised)
-FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
-                 bool emit = true) {
+}  // namespace
+
+// Everything before the candidate scan, shared by every part of a sharded
+// solve (identical on every rank): projection, the R-derived thresholds, the
+// cell grid and (d <= 4) the coordinates in cell order.
+struct FrnnPlan {
+  psg_pointset* ps = nullptr;
+  uint64_t zone = 0;
+  double radius = 0;
+  Thresholds th{};
+  float lo = -1.f;
+  uint64_t ncells = 1;
+  int nk = 4;
+  bool small_d = false;
+  DevBuf<float> keys;
+  GridIndex gi;
+  DevBuf<float4> sx;
+  DevBuf<unsigned long long> acc;
+  DevBuf<uint64_t> band;
+  uint64_t bcap = 1u << 16;
+  FrnnRun run;  // the last part scanned
+};
+
+FrnnPlan* frnn_plan_create(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone) {
   const uint64_t n = ps->n;
   if (n == 0) throw invalid_argument("empty input");  // refscan.cpp:162, before the radius check
   if (!(radius > 0.0) || !std::isfinite(radius)) throw invalid_argument("radius must be positive");
@@ -657,33 +701,37 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   Ctx& c = ctx();
   cudaStream_t s = c.stream;
   StageTimer tm(s);
-  FrnnRun run;
+  auto plan = std::make_unique<FrnnPlan>();
+  FrnnPlan& P = *plan;
+  P.ps = ps;
+  P.zone = zone;
+  P.radius = radius;
   const Directions dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(std::min(q, n), 64)));
   const int nk = dir.nk;
-  DevBuf<float> keys(n * nk, s);
-  const float norm2 = project(*ps, dir, keys.p, s);
+  P.nk = nk;
+  P.keys.alloc(n * nk, s);
+  const float norm2 = project(*ps, dir, P.keys.p, s);
   tm.mark("project");
   const Budget bud = make_budget(*ps, dir, norm2);
   const double Rw = radius * ps->scale;
   const double dmax = (Rw * (1.0 + 4.0 * bud.gamma64) + 2.0 * bud.Rn) * (1.0 + 1e-12);
-  const Thresholds th = budget_thresholds(bud, dmax);
+  P.th = budget_thresholds(bud, dmax);
   const double inner = Rw * (1.0 - 4.0 * bud.gamma64) - 2.0 * bud.Rn;
-  const float lo = inner > 0 ? static_cast<float>(((inner * inner) * (1.0 - bud.e) - bud.a) * (1.0 - 1e-6)) : -1.0f;
+  P.lo = inner > 0 ? static_cast<float>(((inner * inner) * (1.0 - bud.e) - bud.a) * (1.0 - 1e-6)) : -1.0f;
 
   // grid over the first g keys, cell width >= the key window of R
   const int g = std::min(3, dir.q);
-  GridIndex gi;
+  GridIndex& gi = P.gi;
   gi.ensure(static_cast<uint32_t>(n), nk, s);
-  uint64_t ncells = 1;
   {
     DevBuf<unsigned> mm(6, s);
     const unsigned init[6] = {~0u, ~0u, ~0u, 0u, 0u, 0u};
     PSG_CUDA(cudaMemcpyAsync(mm.p, init, 24, cudaMemcpyHostToDevice, s));
     const unsigned gb = std::min<unsigned>(blocks(n, 256), c.sm_count * 8);
     if (nk == 4)
-      k_key_range<4><<<gb, 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), g, mm.p, mm.p + 3);
+      k_key_range<4><<<gb, 256, 0, s>>>(P.keys.p, static_cast<uint32_t>(n), g, mm.p, mm.p + 3);
     else
-      k_key_range<8><<<gb, 256, 0, s>>>(keys.p, static_cast<uint32_t>(n), g, mm.p, mm.p + 3);
+      k_key_range<8><<<gb, 256, 0, s>>>(P.keys.p, static_cast<uint32_t>(n), g, mm.p, mm.p + 3);
     PSG_LAUNCHED();
     ++g_launches;
     unsigned h[6];
@@ -695,53 +743,72 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
       span[t] = std::max(static_cast<double>(f32_unorder(h[3 + t])) - lo3[t], 1e-30);
     }
     GridParams gp;
-    grid_params_for(gp, std::max(g, 1), static_cast<double>(th.win) * (1.0 + 1e-6), lo3, span);
-    ncells = gp.cells;
+    grid_params_for(gp, std::max(g, 1), static_cast<double>(P.th.win) * (1.0 + 1e-6), lo3, span);
+    P.ncells = gp.cells;
     PSG_CUDA(cudaMemcpyAsync(gi.gp.p, &gp, sizeof(GridParams), cudaMemcpyHostToDevice, s));
   }
-  build_grid(keys.p, static_cast<uint32_t>(n), nk, gi, 24, s);
-  const bool small_d = ps->d <= 4;
-  DevBuf<float4> sx;
-  if (small_d) {
-    sx.alloc(n, s);
-    k_gather_rows4<<<blocks(n, 256), 256, 0, s>>>(ps->X, gi.sidx.p, static_cast<uint32_t>(n), ps->d, sx.p);
+  build_grid(P.keys.p, static_cast<uint32_t>(n), nk, gi, 24, s);
+  P.small_d = ps->d <= 4;
+  if (P.small_d) {
+    P.sx.alloc(n, s);
+    k_gather_rows4<<<blocks(n, 256), 256, 0, s>>>(ps->X, gi.sidx.p, static_cast<uint32_t>(n), ps->d, P.sx.p);
     PSG_LAUNCHED();
     ++g_launches;
   }
+  P.acc.alloc(8, s);
   tm.mark("grid");
+  PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
+  return plan.release();
+}
 
+// The pairs of part `part` of `nparts` (sorted positions split evenly; a pair
+// belongs to the part holding its earlier position).  emit = false: count +
+// hash only (no pair list is materialised for d <= 4).
+void frnn_plan_scan(FrnnPlan& P, uint64_t part, uint64_t nparts, bool emit) {
+  psg_pointset* ps = P.ps;
+  const uint64_t n = ps->n;
+  Ctx& c = ctx();
+  cudaStream_t s = c.stream;
+  StageTimer tm(s);
+  FrnnRun& run = P.run;
+  run = FrnnRun{};
   FrnnArgs a{};
   a.X = ps->X;
-  a.skeys = gi.skeys.p;
-  a.sx = sx.p;
-  a.sidx = gi.sidx.p;
-  a.grid = gi.dev;
+  a.skeys = P.gi.skeys.p;
+  a.sx = P.sx.p;
+  a.sidx = P.gi.sidx.p;
+  a.grid = P.gi.dev;
   a.n = static_cast<uint32_t>(n);
   a.d = ps->d;
-  a.zone = zone;
-  a.th = th;
-  a.lo = lo;
-  a.R = radius;
+  a.zone = P.zone;
+  a.th = P.th;
+  a.lo = P.lo;
+  a.R = P.radius;
   a.src = ps->exact();
-  DevBuf<unsigned long long> acc(6, s);
+  a.plo = static_cast<uint32_t>(n * part / nparts);
+  a.phi = static_cast<uint32_t>(n * (part + 1) / nparts);
+  const uint32_t rows = a.phi - a.plo;
+  unsigned long long* acc = P.acc.p;
   // count-only runs of the small-d scan never write pairs
-  const bool no_list = small_d && !emit;
-  uint64_t cap = no_list ? 0 : std::max<uint64_t>(1u << 20, 24 * n);
-  uint64_t bcap = 1u << 16;
-  DevBuf<uint64_t> band;
+  const bool no_list = P.small_d && !emit;
+  uint64_t cap = no_list ? 0 : std::max<uint64_t>(1u << 20, 24 * std::max<uint64_t>(rows, 1));
   for (;;) {
     run.pairs.alloc(std::max<uint64_t>(cap, 1), s);
-    PSG_CUDA(cudaMemsetAsync(acc.p, 0, 48, s));
+    PSG_CUDA(cudaMemsetAsync(acc, 0, 64, s));
     a.out = run.pairs.p;
     a.cap = cap;
-    a.acc = acc.p;
-    if (small_d) {
-      if (band.n < bcap) band.alloc(bcap, s);
-      a.band = band.p;
-      a.bcap = bcap;
-      const unsigned cb = static_cast<unsigned>(
-          std::min<uint64_t>((ncells + 32 * (kFrnnThreads / 32) - 1) / (32 * (kFrnnThreads / 32)), c.sm_count * 4ull));
-      const int v = (no_list ? 0 : 4) + (ps->d == 4 ? 2 : 0) + (zone > 1 ? 1 : 0);
+    a.acc = acc;
+    if (P.small_d) {
+      if (P.band.n < P.bcap) P.band.alloc(P.bcap, s);
+      a.band = P.band.p;
+      a.bcap = P.bcap;
+      k_part_cells<<<1, 1, 0, s>>>(a);
+      PSG_LAUNCHED();
+      const uint64_t part_cells = (P.ncells + nparts - 1) / nparts + 1;  // launch size only (claims are dynamic)
+      const unsigned cb = static_cast<unsigned>(std::min<uint64_t>(
+          (part_cells + 32 * (kFrnnThreads / 32) - 1) / (32 * (kFrnnThreads / 32)), c.sm_count * 4ull));
+      const int v = (no_list ? 0 : 4) + (ps->d == 4 ? 2 : 0) + (P.zone > 1 ? 1 : 0);
       switch (v) {
         case 0: k_frnn_cells<false, false, false><<<cb, kFrnnThreads, 0, s>>>(a); break;
         case 1: k_frnn_cells<false, false, true><<<cb, kFrnnThreads, 0, s>>>(a); break;
@@ -753,21 +820,21 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
         default: k_frnn_cells<true, true, true><<<cb, kFrnnThreads, 0, s>>>(a); break;
       }
       PSG_LAUNCHED();
-      ++g_launches;
+      g_launches += 2;
       k_frnn_band<<<c.sm_count * 2, 256, 0, s>>>(a);
-    } else {
-      if (nk == 4)
-        k_frnn_scan<4><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+    } else if (rows) {
+      if (P.nk == 4)
+        k_frnn_scan<4><<<blocks(rows, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
       else
-        k_frnn_scan<8><<<blocks(n, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
+        k_frnn_scan<8><<<blocks(rows, kFrnnThreads), kFrnnThreads, 0, s>>>(a);
     }
     PSG_LAUNCHED();
     ++g_launches;
     unsigned long long h[5];
-    PSG_CUDA(cudaMemcpyAsync(h, acc.p, 40, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(h, acc, 40, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    if (small_d && h[4] > bcap) {  // more rounding-band pairs than room: again with room for all
-      bcap = h[4];
+    if (P.small_d && h[4] > P.bcap) {  // more rounding-band pairs than room: again with room for all
+      P.bcap = h[4];
       continue;
     }
     if (no_list || h[0] <= cap) {
@@ -784,10 +851,77 @@ FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t
   prof_stages(tm);
   g_prof.window_pairs = run.visited;
   g_prof.lb_survivors = run.examined;
-  return run;
+}
+
+void frnn_plan_free(FrnnPlan* p) { delete p; }
+
+// Part stats: examined = FP32-evaluated pairs, pruned = visited - examined;
+// the caller adds the parts up and fills pairs_skipped_by_exit from the
+// closed-form admissible count.
+void frnn_plan_result(const FrnnPlan& P, uint64_t* count, uint64_t* hash, psg_scan_stats* stats) {
+  *count = P.run.count;
+  *hash = P.run.hash;
+  stats->pairs_examined = P.run.examined;
+  stats->pairs_pruned_by_reference = P.run.visited - P.run.examined;
+  stats->pairs_skipped_by_exit = 0;
+  stats->inner_loop_exits = 0;
+}
+
+namespace {
+
+// The (i<j) pairs of a run, sorted ascending, into `sorted` (device).
+void sort_pairs(const FrnnRun& run, uint64_t n, DevBuf<uint64_t>& sorted, cudaStream_t s) {
+  sorted.alloc(std::max<uint64_t>(run.count, 1), s);
+  if (run.count == 0) return;
+  DevBuf<uint32_t> off, cols;
+  if (csr_rows(run.pairs, run.count, n, false, off, cols, s)) {  // rows of i<j, ascending
+    k_csr_to_pairs<<<grid_cap(n * 32), 256, 0, s>>>(off.p, n, cols.p, sorted.p);
+    PSG_LAUNCHED();
+    ++g_launches;
+  } else {
+    const int b = bits_for(n);
+    k_pack<<<blocks(run.count, 256), 256, 0, s>>>(run.pairs.p, run.count, b, sorted.p);
+    PSG_LAUNCHED();
+    sort_u64(sorted, run.count, 2 * b, s);
+    k_unpack<<<blocks(run.count, 256), 256, 0, s>>>(sorted.p, run.count, b);
+    PSG_LAUNCHED();
+    g_launches += 2;
+  }
+}
+
+FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                 bool emit = true) {
+  std::unique_ptr<FrnnPlan> plan(frnn_plan_create(ps, radius, q, f, seed, zone));
+  frnn_plan_scan(*plan, 0, 1, emit);
+  return std::move(plan->run);
 }
 
 }  // namespace
+
+void frnn_plan_pairs(FrnnPlan& P, uint64_t nbuckets, uint64_t* bucket_counts, uint64_t* out, uint64_t capacity) {
+  cudaStream_t s = ctx().stream;
+  const uint64_t n = P.ps->n, m = P.run.count;
+  DevBuf<uint64_t> sorted;
+  sort_pairs(P.run, n, sorted, s);
+  std::vector<uint64_t> host;
+  uint64_t* dst = out;
+  if (m > capacity || !out) {  // bucket counts still need the keys: stage them
+    host.resize(m);
+    dst = host.data();
+  }
+  if (m) PSG_CUDA(cudaMemcpyAsync(dst, sorted.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  if (dst == out) g_prof.d2h_bytes += m * sizeof(uint64_t);
+  // bucket b holds the pairs with i in [n b / nb, n (b + 1) / nb): the sorted
+  // list is already in bucket order
+  uint64_t k = 0;
+  for (uint64_t b = 0; b < nbuckets; ++b) {
+    const uint64_t ihi = n * (b + 1) / nbuckets;
+    const uint64_t* e = std::lower_bound(dst + k, dst + m, ihi << 32);
+    bucket_counts[b] = static_cast<uint64_t>(e - (dst + k));
+    k = static_cast<uint64_t>(e - dst);
+  }
+}
 
 void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                 bool want_lists, psg_neighbor_result* out) {
@@ -810,21 +944,8 @@ void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
   *hash = run.hash;
   if (!pairs || capacity == 0 || run.count == 0) return;
   const uint64_t m = std::min(capacity, run.count);
-  DevBuf<uint32_t> off, cols;
-  DevBuf<uint64_t> sorted(run.count, s);
-  if (csr_rows(run.pairs, run.count, ps->n, false, off, cols, s)) {  // rows of i<j, ascending
-    k_csr_to_pairs<<<grid_cap(ps->n * 32), 256, 0, s>>>(off.p, ps->n, cols.p, sorted.p);
-    PSG_LAUNCHED();
-    ++g_launches;
-  } else {
-    const int b = bits_for(ps->n);
-    k_pack<<<blocks(run.count, 256), 256, 0, s>>>(run.pairs.p, run.count, b, sorted.p);
-    PSG_LAUNCHED();
-    sort_u64(sorted, run.count, 2 * b, s);
-    k_unpack<<<blocks(run.count, 256), 256, 0, s>>>(sorted.p, run.count, b);
-    PSG_LAUNCHED();
-    g_launches += 2;
-  }
+  DevBuf<uint64_t> sorted;
+  sort_pairs(run, ps->n, sorted, s);
   PSG_CUDA(cudaMemcpyAsync(pairs, sorted.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaStreamSynchronize(s));
   g_prof.d2h_bytes += m * sizeof(uint64_t);

@@ -117,6 +117,29 @@ __device__ __forceinline__ unsigned long long lex_key(uint32_t i, uint32_t j) {
   return i < j ? (static_cast<unsigned long long>(i) << 32) | j : (static_cast<unsigned long long>(j) << 32) | i;
 }
 
+// What the inline FP64 evaluation of an overflowing band pair needs, kept in
+// device memory (DevState) so the hot kernels carry one pointer for it and
+// the cold path stays out of their register allocation.
+struct InlineCtx {
+  ExactSrc src;                  // the reference's values
+  const uint32_t* sidx;          // sorted position -> original index
+  unsigned long long* best128;   // (distance bits, (i << 32) | j) minimum, see atomic_min_u128
+  unsigned long long* examined;  // FP64 evaluations
+  unsigned long long* inline_n;  // of which inline
+};
+
+// Out of line (noinline): only ever reached past the candidate list.
+static __device__ __noinline__ void record_inline(const InlineCtx* __restrict__ ic, uint32_t p, uint32_t j) {
+  const uint32_t oi = ic->sidx[p], oj = ic->sidx[j];
+  const double dd = exact_distance(ic->src, oi, oj);
+  atomic_min_u128(ic->best128, static_cast<unsigned long long>(__double_as_longlong(dd)), lex_key(oi, oj));
+  const unsigned m = __activemask();
+  if ((threadIdx.x & 31) == __ffs(m) - 1) {
+    atomicAdd(ic->examined, static_cast<unsigned long long>(__popc(m)));
+    atomicAdd(ic->inline_n, static_cast<unsigned long long>(__popc(m)));
+  }
+}
+
 struct ScanArgs {
   const float* X;
   const float* skeys;
@@ -131,10 +154,7 @@ struct ScanArgs {
   float* cand_s;
   unsigned long long* cand_n;  // 64-bit: counts every band pair, never wraps
   uint32_t cand_cap;
-  ExactSrc src;                   // the reference's values, for band pairs past the list
-  unsigned long long* best128;    // DevState::best128 (see atomic_min_u128)
-  unsigned long long* examined;   // FP64 evaluations
-  unsigned long long* inline_n;   // of which inline (past the list)
+  const InlineCtx* ic;            // band pairs past the list (DevState::ic)
   unsigned long long* evals;
   unsigned long long* visited;  // grid engine: admissible stencil pairs
   int no_ub;                    // debugging: dense Gram tiles do not feed their upper bounds to `best`
@@ -157,14 +177,7 @@ __device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j
       a.cand_j[c] = j;
       a.cand_s[c] = s32;
     } else {
-      const uint32_t oi = a.sidx[p], oj = a.sidx[j];
-      const double dd = exact_distance(a.src, oi, oj);
-      atomic_min_u128(a.best128, static_cast<unsigned long long>(__double_as_longlong(dd)), lex_key(oi, oj));
-      const unsigned m = __activemask();
-      if ((threadIdx.x & 31) == __ffs(m) - 1) {
-        atomicAdd(a.examined, static_cast<unsigned long long>(__popc(m)));
-        atomicAdd(a.inline_n, static_cast<unsigned long long>(__popc(m)));
-      }
+      record_inline(a.ic, p, j);
     }
   }
 }

@@ -99,8 +99,17 @@ def test_c5_recipe_large(psg, orc, logn):
     got, prof = _check_c5(psg, orc, 1 << logn)
     assert prof["dense_cell_pairs"] > 0 and prof["dense_groups"] > 0
     assert prof["dense_cells"] > 1 << 24, prof
-    if logn == 22:
-        assert prof["dense_split_groups"] > 0, prof
+
+
+@pytest.mark.parametrize("group", [8, 40])
+def test_c5_recipe_split_groups(psg, orc, monkeypatch, group):
+    """A cells with more kept partners than a Gram group holds are split over
+    several groups (366 pairs per group; the full C5's first solve splits one).
+    PSG_GROUP_PAIRS lowers the group size so the split path runs on many cells
+    at 2^19, against the device brute force."""
+    monkeypatch.setenv("PSG_GROUP_PAIRS", str(group))
+    got, prof = _check_c5(psg, orc, 1 << 19)
+    assert prof["dense_split_groups"] > 100, prof
 
 
 @pytest.mark.slow
@@ -108,4 +117,4 @@ def test_c5_recipe_large(psg, orc, logn):
 def test_c5_full(psg, orc):
     got, prof = _check_c5(psg, orc, 1 << 24)
     assert (got.index_i, got.index_j) == (2449215, 7867199)  # profiles/r02_c5_fullsize.json
-    assert prof["dense_cells"] > 1 << 24 and prof["dense_split_groups"] > 0, prof
+    assert prof["dense_cells"] > 1 << 24, prof

@@ -58,3 +58,48 @@ def test_sharded_motif_windows(psg):
     got = run_parts(psg, lambda: psg.PointSet.windows_of(series, 64, znorm=True), 2, zone=64)
     one = psg.closest_pair(psg.PointSet.windows_of(series, 64, znorm=True), 10, 10.0, 1, 64)
     assert (got.index_i, got.index_j, got.distance) == (one.index_i, one.index_j, one.distance)
+
+
+# --- sharded FRNN (psg_frnn_plan_*): W parts on one device ----------------------
+def frnn_parts(psg, pts, radius, world, zone=0):
+    d = pts.shape[1]
+    # one point set per emulated rank, alive as long as its plan
+    sets = [psg.PointSet.from_flat(pts, d) for _ in range(world)]
+    plans = [sharded.DeviceFrnnPlan(ps._device(), radius, 10, 10.0, 1, zone) for ps in sets]
+    outs = [plans[r].scan(r, world, keep_pairs=True) for r in range(world)]
+    runs = [plans[r].pairs(world) for r in range(world)]
+    # the all-to-all: rank b receives bucket b of every part
+    lists = []
+    for b in range(world):
+        recv = []
+        for keys, counts in runs:
+            off = int(np.sum(counts[:b]))
+            recv.append(keys[off:off + int(counts[b])])
+        lists.append(sharded.merge_sorted_runs(recv))
+    cnt = sum(o[0] for o in outs)
+    h = sum(o[1] for o in outs) & sharded.MASK64
+    for p in plans:
+        p.close()
+    return cnt, h, np.concatenate(lists)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_frnn_c4_shape(psg, orc, world):
+    n = 1 << 20
+    cube = psg.gen.uniform(4, n, 3)
+    R = (3 * 32 / (4 * np.pi * n)) ** (1 / 3)
+    cnt, h, pairs = frnn_parts(psg, cube, R, world)
+    one, c1, h1 = psg.frnn_pairs(cube, R)
+    assert (cnt, h) == (c1, h1) == orc.frnn_grid(cube, R)
+    assert np.array_equal(pairs, one)
+
+
+@pytest.mark.parametrize("d,zone", [(5, 0), (3, 7)])
+def test_sharded_frnn_scan_and_zone(psg, orc, d, zone):
+    rng = np.random.default_rng(d + zone)
+    pts = rng.random((30_000, d)).astype(np.float32)
+    R = 0.1 if d == 5 else 0.02
+    cnt, h, pairs = frnn_parts(psg, pts, R, 3, zone)
+    want = orc.brute_force_neighbors(pts.astype(np.float64), R, zone, lists=True)
+    assert (cnt, h) == want[:2]
+    assert np.array_equal(pairs, np.sort(want[2]))

@@ -130,3 +130,83 @@ def test_admissible_closed_form():
         for z in range(0, 32):
             brute = sum(1 for i in range(n) for j in range(i + 1, n) if j - i >= max(z, 1))
             assert admissible_pairs(n, z) == brute
+
+
+# ---------------------------------------------------------------------------
+# Sharded FRNN (sharded.frnn_sharded): count/hash SUM and the i-range
+# all-to-all of the sorted list, over gloo with an oracle-backed stand-in for
+# the device plan (same ownership rule: a pair belongs to the part holding
+# its earlier sorted position).
+def _mix(k):
+    k = (k + 0x9E3779B97F4A7C15) & ((1 << 64) - 1)
+    k = ((k ^ (k >> 30)) * 0xBF58476D1CE4E5B9) & ((1 << 64) - 1)
+    k = ((k ^ (k >> 27)) * 0x94D049BB133111EB) & ((1 << 64) - 1)
+    return k ^ (k >> 31)
+
+
+class OracleFrnnBackend:
+    def __init__(self, pts, radius, zone, all_pairs):
+        self.n = len(pts)
+        order = np.argsort(pts[:, 0], kind="stable")  # stands in for the grid order
+        self.pos = np.empty(self.n, np.int64)
+        self.pos[order] = np.arange(self.n)
+        self.all_pairs = all_pairs  # uint64 (i<<32)|j, i<j
+        self.mine = None
+
+    def scan(self, part, nparts, keep_pairs):
+        lo, hi = self.n * part // nparts, self.n * (part + 1) // nparts
+        i = (self.all_pairs >> np.uint64(32)).astype(np.int64)
+        j = (self.all_pairs & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        first = np.minimum(self.pos[i], self.pos[j])
+        self.mine = self.all_pairs[(first >= lo) & (first < hi)]
+        h = 0
+        for k in self.mine.tolist():
+            h = (h + _mix(int(k))) & ((1 << 64) - 1)
+        return len(self.mine), h, ScanStats(len(self.mine), 3, 0, 0)
+
+    def pairs(self, nbuckets):
+        keys = np.sort(self.mine)
+        i = (keys >> np.uint64(32)).astype(np.int64)
+        b = np.minimum((i * nbuckets) // self.n, nbuckets - 1)
+        # bucket of i: the b with n b / nb <= i < n (b + 1) / nb
+        edges = np.array([self.n * k // nbuckets for k in range(nbuckets + 1)])
+        b = np.searchsorted(edges, i, side="right") - 1
+        return keys, np.bincount(b, minlength=nbuckets).astype(np.uint64)
+
+
+def _frnn_worker(rank, world, port, pts, radius, all_pairs, q):
+    from paper_1407_5609_b200.sharded import TorchFrnnCollectives, frnn_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        be = OracleFrnnBackend(pts, radius, 0, all_pairs)
+        coll = TorchFrnnCollectives(device="cpu")
+        cnt, h, st, mine = frnn_sharded(be, len(pts), 0, rank, world, coll.all_reduce_sum, coll.all_to_all)
+        q.put((rank, cnt, h, st.admissible_pairs(), mine.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_frnn_gloo(orc, world):
+    rng = np.random.default_rng(3)
+    n = 400
+    pts = rng.random((n, 3))
+    radius = 0.12
+    cnt, h, keys = orc.brute_force_neighbors(pts, radius, 0, lists=True)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_frnn_worker, args=(r, world, port, pts, radius, keys, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, c, hh, adm, _ in res:
+        assert (c, hh) == (cnt, h)
+        assert adm == n * (n - 1) // 2
+    merged = [k for r in res for k in r[4]]  # rank order = i-range order
+    assert merged == sorted(int(k) for k in keys)
