@@ -22,7 +22,7 @@ constexpr int kPad = 132;
 enum Mode : int { kMin = 0, kCollect = 1, kFrnn = 2 };
 
 struct BruteArgs {
-  const float* X;
+  Rows X;  // the working rows (materialised or virtual windows)
   uint32_t n;
   int d;
   uint64_t zone;
@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(256) k_brute(BruteArgs a, uint64_t base) {
       const int r = idx >> 4, c = idx & 15;
       const int t = k0 + c;
       const uint32_t gi = i0 + r, gj = j0 + r;
-      As[c][r] = (t < a.d && gi < a.n) ? __ldg(a.X + static_cast<size_t>(gi) * a.d + t) : 0.f;
-      Bs[c][r] = (t < a.d && gj < a.n) ? __ldg(a.X + static_cast<size_t>(gj) * a.d + t) : 0.f;
+      As[c][r] = (t < a.d && gi < a.n) ? row_at(a.X, gi, t) : 0.f;
+      Bs[c][r] = (t < a.d && gj < a.n) ? row_at(a.X, gj, t) : 0.f;
     }
     __syncthreads();
     const int kend = min(kDK, a.d - k0);
@@ -198,7 +198,7 @@ psg_pair_result brute_solve(psg_pointset* ps, uint64_t zone, double upper) {
   cudaStream_t s = c.stream;
   StageTimer tm(s);
   BruteArgs a{};
-  a.X = ps->X;
+  a.X = ps->rows();
   a.n = static_cast<uint32_t>(n);
   a.d = ps->d;
   a.zone = zone;
@@ -284,7 +284,7 @@ uint64_t brute_emit_pairs(psg_pointset* ps, double radius, uint64_t zone, DevBuf
                           cudaStream_t s) {
   const uint64_t n = ps->n;
   BruteArgs a{};
-  a.X = ps->X;
+  a.X = ps->rows();
   a.n = static_cast<uint32_t>(n);
   a.d = ps->d;
   a.zone = zone;

@@ -127,6 +127,62 @@ __global__ void __launch_bounds__(256) k_project_thread(const float* __restrict_
   if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
 }
 
+// Window sets (virtual rows, psg_points.cuh Rows): one thread per window.
+// A block stages the series segment its 128 windows span (128 + d - 1
+// values) and, when it fits, U transposed (d x NK: one broadcast per tap and
+// key quad); each thread then forms its row on the fly — the same FP32
+// values every other reader sees — and accumulates the NK keys and the row's
+// sum of squares in coordinate order.  No n_w x d buffer is read or written:
+// the C3 projection reads the 4 MiB series instead of 1 GiB of rows.
+constexpr int kWinRows = 128;
+template <int NK>
+__global__ void __launch_bounds__(kWinRows) k_project_windows(Rows R, uint32_t n, const float* __restrict__ Ut,
+                                                              float* __restrict__ keys, unsigned* __restrict__ norm2_bits,
+                                                              int u_smem, int seg_smem) {
+  extern __shared__ float4 sh4[];
+  float* sh = reinterpret_cast<float*>(sh4);
+  const int d = R.d;
+  const uint32_t i0 = blockIdx.x * kWinRows;
+  const uint32_t cnt = min(static_cast<uint32_t>(kWinRows), n - i0);
+  float* su = sh;  // d x NK (16-byte aligned)
+  float* seg = sh + (u_smem ? d * NK : 0);
+  if (u_smem)
+    for (int k = threadIdx.x; k < d * NK; k += kWinRows) su[k] = Ut[k];
+  if (seg_smem)
+    for (uint32_t k = threadIdx.x; k < cnt + d - 1; k += kWinRows) seg[k] = R.s32[i0 + k];
+  __syncthreads();
+  const int r = threadIdx.x;
+  float nn = 0.f;
+  if (r < static_cast<int>(cnt)) {
+    const float* Us = u_smem ? su : Ut;
+    const float* x = seg_smem ? seg + r : R.s32 + i0 + r;
+    const bool z = R.m32 != nullptr;
+    const float m = z ? R.m32[i0 + r] : 0.f, rr = z ? R.r32[i0 + r] : 1.f;
+    float acc[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
+    for (int t = 0; t < d; ++t) {
+      float v = x[t];
+      if (z) v = __fmul_rn(__fsub_rn(v, m), rr);
+      nn = fmaf(v, v, nn);
+      const float4* u4 = reinterpret_cast<const float4*>(Us + t * NK);
+#pragma unroll
+      for (int q = 0; q < NK / 4; ++q) {
+        const float4 u = u4[q];
+        acc[4 * q + 0] = fmaf(u.x, v, acc[4 * q + 0]);
+        acc[4 * q + 1] = fmaf(u.y, v, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(u.z, v, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(u.w, v, acc[4 * q + 3]);
+      }
+    }
+    float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(i0 + r) * NK);
+#pragma unroll
+    for (int q = 0; q < NK / 4; ++q) out[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+  }
+  nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
+  if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
+}
+
 template <int NK>
 __global__ void k_sort_keys(const float* __restrict__ keys, uint32_t n, uint32_t* __restrict__ k_out,
                             uint32_t* __restrict__ v_out) {
@@ -153,8 +209,7 @@ __global__ void k_gather(const float* __restrict__ keys, const uint32_t* __restr
 // is finite from the start.
 __global__ void k_seed_pair(ScanArgs a, uint32_t z) {
   const int lane = threadIdx.x & 31;
-  const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(a.X, a.X + static_cast<size_t>(z) * a.d, a.d) : 0.f)
-                                  : warp_sqdist(a.X, a.X + static_cast<size_t>(z) * a.d, a.d, lane);
+  const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(a.rows, 0, z) : 0.f) : warp_sqdist(a.rows, 0, z, lane);
   if (lane == 0) atomicMin(a.best, __float_as_uint(s));
 }
 
@@ -230,18 +285,17 @@ __global__ void __launch_bounds__(kThreads) k_bootstrap(ScanArgs a, uint32_t lo,
   if (wj == 0xffffffffu) return;
   const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
   if (!(wlb <= th.lb2)) return;
-  const float* xi = a.X + static_cast<size_t>(a.sidx[wp]) * a.d;
-  const float* xj = a.X + static_cast<size_t>(a.sidx[wj]) * a.d;
+  const uint32_t xi = a.sidx[wp], xj = a.sidx[wj];
   float s;
   if (a.d <= kInlineD)
-    s = lane == 0 ? thread_sqdist(xi, xj, a.d) : 0.f;
+    s = lane == 0 ? thread_sqdist(a.rows, xi, xj) : 0.f;
   else
-    s = warp_sqdist(xi, xj, a.d, lane);
+    s = warp_sqdist(a.rows, xi, xj, lane);
   if (lane == 0) atomicMin(a.best, __float_as_uint(s));
 }
 
 // K3b: the windowed candidate scan.
-template <int NK>
+template <int NK, bool kExact>
 __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint32_t hi) {
   __shared__ __align__(16) float sk[kChunk * NK];
   __shared__ uint32_t so[kChunk];
@@ -307,8 +361,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
           qp[slot] = p;
           qj[slot] = j;
         } else {  // queue full: evaluate here (canonical order, bounded memory)
-          record(a, p, j, thread_sqdist(a.X + static_cast<size_t>(mo) * a.d, a.X + static_cast<size_t>(so[jj]) * a.d, a.d),
-                 th.band);
+          record_scan<kExact>(a, p, j, thread_sqdist(a.rows, mo, so[jj]), th.band);
         }
       }
     }
@@ -318,9 +371,8 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
       const float band = th.band;
       for (int i = tid; i < nq; i += kThreads) {  // one queued pair per thread
         const uint32_t pi = qp[i], pj = qj[i];
-        const float s = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                      a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
-        record(a, pi, pj, s, band);
+        const float s = thread_sqdist(a.rows, a.sidx[pi], a.sidx[pj]);
+        record_scan<kExact>(a, pi, pj, s, band);
       }
     }
     __syncthreads();
@@ -353,8 +405,7 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
     }
   }
   if (j == 0xffffffffu) return;
-  const float* xi = a.X + static_cast<size_t>(a.sidx[p]) * a.d;
-  const float* xj = a.X + static_cast<size_t>(a.sidx[j]) * a.d;
+  const uint32_t xi = a.sidx[p], xj = a.sidx[j];
   // Warp-parallel sum (not the canonical order), rounded up by (2d+8) ulps
   // relative: two FP32 orders of a sum of d non-negative terms differ by at
   // most 2d*2^-24 relative, so this stays >= the canonical value the scan
@@ -362,7 +413,7 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
   // and any value >= a computed one is a valid bound for the thresholds.
   float s = 0.f;
   for (int t = lane; t < a.d; t += 32) {
-    const float g = __ldg(xi + t) - __ldg(xj + t);
+    const float g = row_at(a.rows, xi, t) - row_at(a.rows, xj, t);
     s = fmaf(g, g, s);
   }
 #pragma unroll
@@ -436,7 +487,7 @@ __global__ void k_check_grid(unsigned* best, const Budget* bud, const GridParams
 // bound only tightens, so a stale threshold only admits more); survivors go to
 // a shared-memory queue (global spill list when full) and whole warps evaluate
 // them as exact FP32 distances at the end of the block.
-template <int NK>
+template <int NK, bool kExact>
 __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi,
                                                          const unsigned* __restrict__ regrid,
                                                          const Thresholds* __restrict__ th0) {
@@ -507,9 +558,7 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
           qp[slot] = p;
           qj[slot] = j;
         } else {  // queue full: evaluate here (canonical order, bounded memory)
-          record(a, p, j,
-                 thread_sqdist(a.X + static_cast<size_t>(mo) * a.d, a.X + static_cast<size_t>(a.sidx[j]) * a.d, a.d),
-                 th0->band);
+          record_scan<kExact>(a, p, j, thread_sqdist(a.rows, mo, a.sidx[j]), th0->band);
           ++inline_evals;
         }
       }
@@ -521,9 +570,8 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
     const float band = th0->band;  // >= the band of any tighter bound: a superset, refiltered by k_recheck
     for (int i = tid; i < nq; i += kThreads) {  // one queued pair per thread
       const uint32_t pi = qp[i], pj = qj[i];
-      const float sd = thread_sqdist(a.X + static_cast<size_t>(a.sidx[pi]) * a.d,
-                                     a.X + static_cast<size_t>(a.sidx[pj]) * a.d, a.d);
-      record(a, pi, pj, sd, band);
+      const float sd = thread_sqdist(a.rows, a.sidx[pi], a.sidx[pj]);
+      record_scan<kExact>(a, pi, pj, sd, band);
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -662,6 +710,7 @@ struct SetupArgs {
   double unorm, sigma, Rn, occupancy, box_sd;
   double min_w;        // cell width learned by an earlier regrid on this point set (0: none)
   uint32_t n, m;
+  int tc;              // keys from the tensor-core projection (key_gamma)
 };
 static_assert(kMaxGridKeys <= 8, "k_setup: one warp per boxed key");
 
@@ -680,7 +729,7 @@ __global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, con
     b.a = (2.0 * sa.d + 2.0) * 0x1.0p-149;
     const double nn = static_cast<double>(__uint_as_float(st->norm2_bits));
     const double maxnorm = sqrt(nn * (1.0 + (sa.d + 4) * u)) * (1.0 + 1e-7);
-    b.E = key_gamma(sa.d, sa.n) * sa.unorm * maxnorm * 1.0001 + key_abs(sa.d, sa.n);
+    b.E = key_gamma(sa.d, sa.tc) * sa.unorm * maxnorm * 1.0001 + key_abs(sa.d, sa.tc);
     b.Rn = sa.Rn;
     b.sigma = sa.sigma;
     b.unorm = sa.unorm;
@@ -763,7 +812,9 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
   const uint32_t n = static_cast<uint32_t>(ps.n);
   const int d = ps.d;
   const int sms = ctx().sm_count;
-  if (tc_projection(d, ps.n)) {
+  if (!ps.X) {
+    project_windows(ps, dir, keys, norm2_bits, s);  // virtual window rows (Rows)
+  } else if (tc_projection(d, ps.n)) {
     project_tc(ps, dir, keys, norm2_bits, s);  // psg_project_tc.cu
   } else if (d < 32) {
     USmall u{};
@@ -791,6 +842,46 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
   ++g_launches;
 }
 
+// Window sets: U transposed (d x nk), kept on the point set and uploaded
+// when the directions change (solve_graph primes it before a capture, so a
+// captured solve holds no host buffer).
+const float* window_directions(const psg_pointset& ps, const Directions& dir, cudaStream_t s) {
+  const int d = ps.d, nk = dir.nk;
+  std::vector<float> ut(static_cast<size_t>(d) * nk);
+  for (int k = 0; k < nk; ++k)
+    for (int t = 0; t < d; ++t) ut[static_cast<size_t>(t) * nk + k] = dir.U[static_cast<size_t>(k) * d + t];
+  if (ut != ps.win_ut_host || !ps.win_ut.p) {
+    if (g_capturing) throw std::runtime_error("window directions changed inside a graph capture");
+    ps.win_ut_host = std::move(ut);
+    ps.win_ut.alloc(ps.win_ut_host.size(), s);
+    PSG_CUDA(cudaMemcpyAsync(ps.win_ut.p, ps.win_ut_host.data(), ps.win_ut_host.size() * 4, cudaMemcpyHostToDevice, s));
+  }
+  return ps.win_ut.p;
+}
+
+void project_windows(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
+                     cudaStream_t s) {
+  const uint32_t n = static_cast<uint32_t>(ps.n);
+  const int d = ps.d, nk = dir.nk;
+  const float* Ut = window_directions(ps, dir, s);
+  const size_t ubytes = static_cast<size_t>(d) * nk * 4, sbytes = (static_cast<size_t>(kWinRows) + d) * 4;
+  constexpr size_t kMaxSmem = 200 * 1024;
+  const int u_smem = ubytes <= kMaxSmem - std::min(sbytes, kMaxSmem / 2) ? 1 : 0;
+  const int seg_smem = (u_smem ? ubytes : 0) + sbytes <= kMaxSmem ? 1 : 0;
+  const size_t smem = (u_smem ? ubytes : 0) + (seg_smem ? sbytes : 0);
+  if (nk == 4) {
+    if (smem > 48 * 1024)
+      PSG_CUDA(cudaFuncSetAttribute(k_project_windows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_project_windows<4><<<blocks_for(n, kWinRows), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, norm2_bits, u_smem,
+                                                                         seg_smem);
+  } else {
+    if (smem > 48 * 1024)
+      PSG_CUDA(cudaFuncSetAttribute(k_project_windows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_project_windows<8><<<blocks_for(n, kWinRows), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, norm2_bits, u_smem,
+                                                                         seg_smem);
+  }
+}
+
 float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s) {
   DevBuf<unsigned> nb(1, s);
   PSG_CUDA(cudaMemsetAsync(nb.p, 0, 4, s));
@@ -810,7 +901,8 @@ Budget make_budget(const psg_pointset& ps, const Directions& dir, float max_norm
   b.e = (d + 4) * u * 1.01;
   b.a = (2.0 * d + 2.0) * 0x1.0p-149;
   const double maxnorm = std::sqrt(static_cast<double>(max_norm2) * (1.0 + (d + 4) * u)) * (1.0 + 1e-7);
-  b.E = key_gamma(d, ps.n) * dir.unorm * maxnorm * 1.0001 + key_abs(d, ps.n);
+  const bool tc = tc_projection(d, ps.n) && ps.X;
+  b.E = key_gamma(d, tc) * dir.unorm * maxnorm * 1.0001 + key_abs(d, tc);
   b.Rn = ps.Rn;
   b.sigma = dir.sigma;
   b.unorm = dir.unorm;
@@ -866,7 +958,7 @@ float bits_to_float(unsigned b) {
 ScanArgs make_args(CppPlan& plan) {
   CppWork& W = *plan.work;
   ScanArgs a{};
-  a.X = plan.ps->X;
+  a.rows = plan.ps->rows();
   a.skeys = plan.grid ? W.gi.skeys.p : W.wskeys.p;
   a.sidx = plan.grid ? W.gi.sidx.p : W.wsidx.p;
   a.n = static_cast<uint32_t>(plan.ps->n);
@@ -954,7 +1046,7 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
     static const double box_sd = std::getenv("PSG_BOXSD") ? std::atof(std::getenv("PSG_BOXSD")) : kGridBoxSd;
     const double min_w = W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone ? W.learned_w : 0.0;
     SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy, box_sd, min_w,
-                 static_cast<uint32_t>(n), 0};
+                 static_cast<uint32_t>(n), 0, tc_projection(ps->d, n) && ps->X != nullptr};
     if (plan->grid) {
       // K2 (grid): cells over the first g keys at the occupancy width, sorted;
       // parameters computed on device, no host round trip
@@ -1118,18 +1210,21 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
     PSG_CUDA(cudaMemcpyAsync(&regrid, &st->regrid, 4, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
     if (!regrid)
-      dense_scan(a, W.gi, plan.gp.cells, plan.ps->X, static_cast<uint32_t>(plan.ps->n), plan.ps->d, plan.dir.nk,
+      dense_scan(a, W.gi, plan.gp.cells, plan.ps->rows(), static_cast<uint32_t>(plan.ps->n), plan.ps->d, plan.dir.nk,
                  &st->th, W.dense, part, nparts, s);
   } else if (hi > lo) {
-    if (plan.grid) {
-      if (plan.dir.nk == 4)
-        k_grid_scan2<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th);
-      else
-        k_grid_scan2<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th);
-    } else if (plan.dir.nk == 4)
-      k_scan<4><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
-    else
-      k_scan<8><<<blocks_for(hi - lo, kThreads), kThreads, 0, s>>>(a, lo, hi);
+    const unsigned nb = blocks_for(hi - lo, kThreads);
+    const int v = (plan.grid ? 4 : 0) + (plan.dir.nk == 8 ? 2 : 0) + (plan.exact_scan ? 1 : 0);
+    switch (v) {
+      case 0: k_scan<4, false><<<nb, kThreads, 0, s>>>(a, lo, hi); break;
+      case 1: k_scan<4, true><<<nb, kThreads, 0, s>>>(a, lo, hi); break;
+      case 2: k_scan<8, false><<<nb, kThreads, 0, s>>>(a, lo, hi); break;
+      case 3: k_scan<8, true><<<nb, kThreads, 0, s>>>(a, lo, hi); break;
+      case 4: k_grid_scan2<4, false><<<nb, kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th); break;
+      case 5: k_grid_scan2<4, true><<<nb, kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th); break;
+      case 6: k_grid_scan2<8, false><<<nb, kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th); break;
+      default: k_grid_scan2<8, true><<<nb, kThreads, 0, s>>>(a, W.gi.dev, lo, hi, &st->regrid, &st->th); break;
+    }
     PSG_LAUNCHED();
     ++g_prof.scan_launches;
   }
@@ -1291,6 +1386,13 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       }
       continue;
     }
+    if (!plan.dense && !plan.exact_scan && h.cand_n > W.cand_cap) {
+      // the band outgrew the list: grow it for later solves and rescan this
+      // part with every band pair evaluated inline (the bound only tightened)
+      grow_after_overflow(W, h);
+      plan.exact_scan = true;
+      continue;
+    }
     grow_after_overflow(W, h);
     break;
   }
@@ -1339,12 +1441,13 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   const char* eng = std::getenv("PSG_ENGINE");
   if (dir.q < 2 || (eng && std::string(eng) == "window")) return false;
   const int d = ps->d;
-  if (!(d < 32 || d == 32 || d == 64 || d == 128 || d == 256)) return false;  // projection needs a host buffer
+  if (ps->X && !(d < 32 || d == 32 || d == 64 || d == 128 || d == 256)) return false;  // projection needs a host buffer
   std::shared_ptr<CppWork> work = get_work(ps, dir.nk, s);
   CppWork& W = *work;
   if (W.learned_dense && W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone) return false;
   // every allocation happens before capture (and drops a graph that holds
   // buffers it replaces)
+  if (!ps->X) window_directions(*ps, dir, s);
   W.gi.ensure(static_cast<uint32_t>(ps->n), dir.nk, s);
   ensure_candidates(W, s);
   if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone || W.gcap != W.cand_cap) {
@@ -1388,8 +1491,12 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   PSG_CUDA(cudaStreamSynchronize(s));
   g_launches += W.glaunches;
   const DevState h = *W.host_st;
-  if (h.regrid) return false;  // cells narrower than the bound's window: the regular path rebuilds them
-  grow_after_overflow(W, h);    // exact regardless; the next capture gets a longer list
+  // cells narrower than the bound's window, or a band longer than the list:
+  // the regular path rebuilds the cells / rescans exactly
+  if (h.regrid || h.cand_n > W.cand_cap) {
+    grow_after_overflow(W, h);
+    return false;
+  }
   float ms = 0.f;
   PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[0], W.gev[1]));
   g_prof.project_kernel_ms += ms;

@@ -24,6 +24,9 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
                    cudaStream_t s);
 // The tensor-core projection (psg_project_tc.cu): tc_projection(d, n) shapes.
 void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s);
+// Window sets (virtual rows): CUDA-core projection from the series.
+void project_windows(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s);
+const float* window_directions(const psg_pointset& ps, const Directions& dir, cudaStream_t s);
 // Host-synchronous variant: returns max ||X_i||^2.
 float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s);
 // Error budget for the keys of `ps` under `dir` (host).
@@ -91,6 +94,7 @@ struct CppPlan {
   // engine "grid":   keys sorted by cell of the first g keys (psg_grid.cuh)
   bool grid = false;
   bool dense = false;      // grid engine: cell-pair tiles instead of per-point candidates
+  bool exact_scan = false; // sparse engines: rescan with inline FP64 for every band pair (list overflow)
   int g = 0;
   std::shared_ptr<CppWork> work;
   uint32_t width = 0;      // window engine: bootstrap width (sorted neighbours)

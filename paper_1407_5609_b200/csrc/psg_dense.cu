@@ -104,15 +104,16 @@ __global__ void k_estimate(const uint32_t* __restrict__ cfirst, const GridParams
   if ((threadIdx.x & 31) == 0 && total) atomicAdd(est, total);
 }
 
-__global__ void k_gather_rows(const float* __restrict__ X, const uint32_t* __restrict__ sidx, uint32_t n, int d,
-                              float* __restrict__ Xs) {
+// Rows in grid order (materialised here also for window sets: the tiles
+// stream them with TMA / wide loads).
+__global__ void k_gather_rows(Rows R, const uint32_t* __restrict__ sidx, uint32_t n, int d, float* __restrict__ Xs) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t p = warp; p < n; p += nwarps) {
-    const float* src = X + static_cast<size_t>(sidx[p]) * d;
+    const uint32_t i = sidx[p];
     float* dst = Xs + static_cast<size_t>(p) * d;
-    for (int t = lane; t < d; t += 32) dst[t] = __ldg(src + t);
+    for (int t = lane; t < d; t += 32) dst[t] = row_at(R, i, t);
   }
 }
 
@@ -1005,7 +1006,7 @@ uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s)
   return h;
 }
 
-uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, const float* X, uint32_t n, int d,
+uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, const Rows& X, uint32_t n, int d,
                     int nk, const Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s) {
   const int sms = ctx().sm_count;
   // tensor-core Gram tiles for d in {32, 64}; CUDA-core canonical tiles otherwise

@@ -69,18 +69,18 @@ __global__ void k_key_range(const float* __restrict__ keys, uint32_t n, int g, u
 }
 
 // d <= 4: the coordinates in cell order, one float4 per sorted position
-__global__ void k_gather_rows4(const float* __restrict__ X, const uint32_t* __restrict__ sidx, uint32_t n, int d,
+__global__ void k_gather_rows4(Rows X, const uint32_t* __restrict__ sidx, uint32_t n, int d,
                                float4* __restrict__ sx) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const float* r = X + static_cast<size_t>(sidx[p]) * d;
+  const uint32_t i = sidx[p];
   float v[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int t = 0; t < d; ++t) v[t] = r[t];
+  for (int t = 0; t < d; ++t) v[t] = row_at(X, i, t);
   sx[p] = make_float4(v[0], v[1], v[2], v[3]);
 }
 
 struct FrnnArgs {
-  const float* X;
+  Rows X;  // the working rows (materialised or virtual windows)
   const float* skeys;
   const float4* sx;  // d <= 4
   const uint32_t* sidx;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
   };
   skip_empty();
   bool active = valid && j < e;
-  const float* xi = a.X + static_cast<size_t>(mi) * a.d;
+
   const unsigned lt = (1u << lane) - 1u;
   const bool zoned = a.zone > 1;
   int c = 0;  // warp-uniform fill of wbuf[w]
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kFrnnThreads) k_frnn_scan(FrnnArgs a) {
         float kj[NK];
         load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
         const bool pass = lb2_full<NK>(mk, kj) <= a.th.lb2;
-        const float s32 = pass ? thread_sqdist(xi, a.X + static_cast<size_t>(mj) * a.d, a.d) : INFINITY;
+        const float s32 = pass ? thread_sqdist(a.X, mi, mj) : INFINITY;
         if (pass) {
           ++examined;
           if (s32 <= a.th.band) {
@@ -751,7 +751,7 @@ FrnnPlan* frnn_plan_create(psg_pointset* ps, double radius, uint64_t q, double f
   P.small_d = ps->d <= 4;
   if (P.small_d) {
     P.sx.alloc(n, s);
-    k_gather_rows4<<<blocks(n, 256), 256, 0, s>>>(ps->X, gi.sidx.p, static_cast<uint32_t>(n), ps->d, P.sx.p);
+    k_gather_rows4<<<blocks(n, 256), 256, 0, s>>>(ps->rows(), gi.sidx.p, static_cast<uint32_t>(n), ps->d, P.sx.p);
     PSG_LAUNCHED();
     ++g_launches;
   }
@@ -774,7 +774,7 @@ void frnn_plan_scan(FrnnPlan& P, uint64_t part, uint64_t nparts, bool emit) {
   FrnnRun& run = P.run;
   run = FrnnRun{};
   FrnnArgs a{};
-  a.X = ps->X;
+  a.X = ps->rows();
   a.skeys = P.gi.skeys.p;
   a.sx = P.sx.p;
   a.sidx = P.gi.sidx.p;

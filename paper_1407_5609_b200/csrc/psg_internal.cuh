@@ -266,12 +266,14 @@ __host__ __device__ inline bool tc_projection(int d, uint64_t n) {
 //   every-addition-truncates model, plus 2^-19 for lo.  tests/test_gpu_keys.py
 //   measures the realised error against FP64 projections.  Values the tensor
 //   core may flush (|x| < 2^-126) add at most d 2^-126 (key_abs).
-__host__ __device__ inline double key_gamma(int d, uint64_t n) {
+//   `tc` = the keys came from the tensor-core projection (materialised rows of
+//   a tc_projection shape; window sets are projected on CUDA cores).
+__host__ __device__ inline double key_gamma(int d, bool tc) {
   const double u = 0x1.0p-24;
-  if (tc_projection(d, n)) return (0x1.0p-19 + 2.0 * d * 0x1.0p-22) * 1.01;
+  if (tc) return (0x1.0p-19 + 2.0 * d * 0x1.0p-22) * 1.01;
   return d * u / (1.0 - d * u);
 }
-__host__ __device__ inline double key_abs(int d, uint64_t n) { return tc_projection(d, n) ? d * 0x1.0p-120 : 0.0; }
+__host__ __device__ inline double key_abs(int d, bool tc) { return tc ? d * 0x1.0p-120 : 0.0; }
 
 // Thresholds derived from an upper bound `dmax` (working units) on the real
 // distance of any pair that may still matter.

@@ -87,7 +87,7 @@ void h2d_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
     PSG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
-  static const unsigned threads = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  static const unsigned threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   const char* in = static_cast<const char*>(src);
   h2d_staged(dst, bytes, [&](char* stage, uint64_t off, size_t len) {
     // memcpy fan-out: one host thread moves ~10 GB/s, the PCIe link ~50
@@ -233,9 +233,11 @@ __global__ void k_narrow_rows(const T* __restrict__ src, uint64_t n, int d, doub
   if (lane == 0) atomic_max_nonneg(r2max_bits, worst);
 }
 
-// Per-window FP64 statistics, two-pass and sequential like the oracle.
+// Per-window FP64 statistics, two-pass and sequential like the oracle
+// (the FP64 recheck reads them: exact_coord), plus the virtual rows' FP32
+// mean and inverse sigma (psg_points.cuh Rows).
 __global__ void k_window_stats(const double* __restrict__ s, uint64_t nw, int len, double* __restrict__ mu,
-                               double* __restrict__ sigma) {
+                               double* __restrict__ sigma, float* __restrict__ m32, float* __restrict__ r32) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= nw) return;
   const double* w = s + i;
@@ -247,39 +249,51 @@ __global__ void k_window_stats(const double* __restrict__ s, uint64_t nw, int le
     const double c = __dsub_rn(w[t], m);
     v = __dadd_rn(v, __dmul_rn(c, c));
   }
+  const double sg = __dsqrt_rn(__ddiv_rn(v, static_cast<double>(len)));
   mu[i] = m;
-  sigma[i] = __dsqrt_rn(__ddiv_rn(v, static_cast<double>(len)));
+  sigma[i] = sg;
+  m32[i] = __double2float_rn(m);
+  r32[i] = sg == 0.0 ? 0.f : __double2float_rn(__drcp_rn(sg));
 }
 
-// Window rows (raw or z-normalised) -> scaled FP32 rows + narrowing radius.
-__global__ void k_narrow_windows(const double* __restrict__ s, uint64_t nw, int len, const double* __restrict__ mu,
-                                 const double* __restrict__ sigma, double scale, float* __restrict__ X,
-                                 unsigned long long* __restrict__ r2max_bits) {
+// The FP32 series of a window set: fl(scale * s) (raw windows; scale is a
+// power of two) or fl(s) (z-normalised: the scale-free values are O(sqrt(len))).
+__global__ void k_series_f32(const double* __restrict__ s, uint64_t len, double scale, float* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = __double2float_rn(s[i] * scale);
+}
+
+// One warp per window: the narrowing radius of the virtual FP32 row against
+// the reference's FP64 window values (exact_coord order, times scale), in
+// FP64, and the row's FP32 sum of squares; both max-reduced.
+__global__ void k_window_check(Rows R, ExactSrc src, uint64_t nw, double scale,
+                               unsigned long long* __restrict__ r2max_bits, unsigned* __restrict__ norm2_bits) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   double worst = 0.0;
+  float wn = 0.f;
   for (uint64_t r = warp; r < nw; r += nwarps) {
-    double m = 0.0, sg = 1.0;
-    const bool z = mu != nullptr;
-    if (z) {
-      m = mu[r];
-      sg = sigma[r];
-    }
     double acc = 0.0;
-    for (int t = lane; t < len; t += 32) {
-      double v = s[r + t];
-      if (z) v = sg == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(v, m), sg);
-      v *= scale;
-      const float f = static_cast<float>(v);
-      X[r * len + t] = f;
-      const double e = v - static_cast<double>(f);
-      acc += e * e;
+    float nn = 0.f;
+    for (int t = lane; t < R.d; t += 32) {
+      const float x = row_at(R, r, t);
+      const double e = exact_coord(src, r, t) * scale - static_cast<double>(x);
+      acc = fma(e, e, acc);
+      nn = fmaf(x, x, nn);
     }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      nn += __shfl_xor_sync(0xffffffffu, nn, o);
+    }
     worst = fmax(worst, acc);
+    wn = fmaxf(wn, nn);
   }
-  if (lane == 0) atomic_max_nonneg(r2max_bits, worst);
+  if (lane == 0) {
+    atomic_max_nonneg(r2max_bits, worst);
+    atomicMax(norm2_bits, __float_as_uint(wn));
+  }
 }
 
 __global__ void k_widen(const float* __restrict__ in, uint64_t count, double* __restrict__ out) {
@@ -468,26 +482,33 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
   if (hb) throw invalid_argument("series value must be finite");
   double maxabs;
   std::memcpy(&maxabs, &hm, 8);
+  ps->scale = znorm ? 1.0 : choose_scale(maxabs);  // z-normalised: |x| <= sqrt(len)
   if (znorm) {
     ps->mu.alloc(nw, s);
     ps->sigma.alloc(nw, s);
-    k_window_stats<<<static_cast<int>((nw + 255) / 256), 256, 0, s>>>(ps->src64.p, nw, ps->d, ps->mu.p, ps->sigma.p);
+    ps->m32.alloc(nw, s);
+    ps->r32.alloc(nw, s);
+    k_window_stats<<<static_cast<int>((nw + 255) / 256), 256, 0, s>>>(ps->src64.p, nw, ps->d, ps->mu.p, ps->sigma.p,
+                                                                       ps->m32.p, ps->r32.p);
     PSG_LAUNCHED();
     ++g_launches;
-    ps->scale = 1.0;  // |z| <= sqrt(len)
     maxabs = std::sqrt(static_cast<double>(len));
-  } else {
-    ps->scale = choose_scale(maxabs);
   }
-  ps->work.alloc(nw * len, s);
-  k_narrow_windows<<<grid_for(nw * 32, 256, c.sm_count), 256, 0, s>>>(ps->src64.p, nw, ps->d, ps->mu.p, ps->sigma.p,
-                                                                       ps->scale, ps->work.p, mx.p + 1);
+  ps->s32.alloc(length, s);
+  k_series_f32<<<grid_for(length, 256 * 4, c.sm_count), 256, 0, s>>>(ps->src64.p, length, ps->scale, ps->s32.p);
   PSG_LAUNCHED();
-  ++g_launches;
+  DevBuf<unsigned> nb(1, s);
+  PSG_CUDA(cudaMemsetAsync(nb.p, 0, 4, s));
+  k_window_check<<<grid_for(nw * 32, 256, c.sm_count), 256, 0, s>>>(ps->rows(), ps->exact(), nw, ps->scale,
+                                                                     mx.p + 1, nb.p);
+  PSG_LAUNCHED();
+  g_launches += 2;
   ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d);
-  ps->X = ps->work.p;
+  unsigned hn = 0;
+  PSG_CUDA(cudaMemcpy(&hn, nb.p, 4, cudaMemcpyDeviceToHost));
+  std::memcpy(&ps->norm2max, &hn, 4);
+  ps->X = nullptr;  // virtual rows (Rows): no n_w x len buffer
   ps->maxabs = maxabs * ps->scale;
-  ps->norm2max = row_norm2max(ps->X, ps->n, ps->d, s, c.sm_count);
   return ps.release();
 }
 

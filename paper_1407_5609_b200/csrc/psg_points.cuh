@@ -11,6 +11,7 @@
 
 #include <functional>
 #include <memory>
+#include <vector>
 
 #include "psg_internal.cuh"
 
@@ -52,6 +53,31 @@ __device__ __forceinline__ double exact_distance(const ExactSrc& s, uint64_t i, 
   return __dsqrt_rn(acc);
 }
 
+// The FP32 working rows every filter reads.  Row sets: X, n x d row-major.
+// Window sets (windows_of, series.cpp:34-42) are virtual, as the reference's
+// are: row i is computed where it is read from the FP32 series in working
+// units (4 MiB at C3, L2-resident), so no n_w x len buffer exists:
+//   raw          x_t = s32[i + t]
+//   z-normalised x_t = fl(fl(s32[i + t] - m32[i]) * r32[i])
+// (m32 = fl(mu), r32 = fl(scale / sigma), 0 when sigma == 0).  Rn and the row
+// norms are measured on exactly these values (psg_points.cu), so the error
+// budget covers them like materialised rows.
+struct Rows {
+  const float* X = nullptr;    // materialised rows, or nullptr for a window set
+  const float* s32 = nullptr;  // window sets: the series
+  const float* m32 = nullptr;  // z-normalised windows: per-window mean / inverse sigma
+  const float* r32 = nullptr;
+  int d = 0;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ float row_at(const Rows& R, uint64_t i, int t) {
+  if (R.X) return __ldg(R.X + i * R.d + t);
+  const float v = __ldg(R.s32 + i + t);
+  return R.m32 ? __fmul_rn(__fsub_rn(v, __ldg(R.m32 + i)), __ldg(R.r32 + i)) : v;
+}
+#endif
+
 }  // namespace psg
 
 struct psg_pointset {
@@ -63,7 +89,10 @@ struct psg_pointset {
   psg::DevBuf<double> src64;   // kRowsF64 rows / window series
   psg::DevBuf<double> mu, sigma;
   psg::DevBuf<float> work;     // FP32 working copy when X != src32
-  const float* X = nullptr;
+  psg::DevBuf<float> s32, m32, r32;  // window sets: virtual rows (psg::Rows)
+  mutable psg::DevBuf<float> win_ut;      // window sets: the last directions used, transposed (d x nk)
+  mutable std::vector<float> win_ut_host;
+  const float* X = nullptr;    // nullptr for window sets
   double scale = 1.0;          // X = fl(scale * src)
   double Rn = 0.0;             // max narrowing radius, working units
   double maxabs = 0.0;         // max |X|
@@ -73,6 +102,15 @@ struct psg_pointset {
   // type-erased here, owned by the closest-pair engine (psg_cpp.cu)
   std::shared_ptr<void> cpp_work[2];
 
+  psg::Rows rows() const {
+    psg::Rows r;
+    r.X = X;
+    r.s32 = s32.p;
+    r.m32 = m32.p;
+    r.r32 = r32.p;
+    r.d = d;
+    return r;
+  }
   psg::ExactSrc exact() const {
     psg::ExactSrc s;
     s.kind = kind;

@@ -71,11 +71,40 @@ __device__ __forceinline__ float thread_sqdist(const float* __restrict__ a, cons
   return s;
 }
 
+// The same canonical distance between rows i and j of a row set, materialised
+// or virtual (window sets: psg_points.cuh Rows): coordinate order, one fmaf
+// per coordinate, identical bits for a pair on every path.
+__device__ __forceinline__ float thread_sqdist(const Rows& R, uint64_t i, uint64_t j) {
+  if (R.X) return thread_sqdist(R.X + i * R.d, R.X + j * R.d, R.d);
+  const float* a = R.s32 + i;
+  const float* b = R.s32 + j;
+  float s = 0.f;
+  if (R.m32) {
+    const float ma = __ldg(R.m32 + i), ra = __ldg(R.r32 + i), mb = __ldg(R.m32 + j), rb = __ldg(R.r32 + j);
+    for (int t = 0; t < R.d; ++t) {
+      const float g = __fsub_rn(__fmul_rn(__fsub_rn(__ldg(a + t), ma), ra), __fmul_rn(__fsub_rn(__ldg(b + t), mb), rb));
+      s = fmaf(g, g, s);
+    }
+  } else {
+    for (int t = 0; t < R.d; ++t) {
+      const float g = __ldg(a + t) - __ldg(b + t);
+      s = fmaf(g, g, s);
+    }
+  }
+  return s;
+}
+
 // Warp-level call site of the canonical distance (lane 0 computes, broadcast).
 __device__ __forceinline__ float warp_sqdist(const float* __restrict__ a, const float* __restrict__ b, int d,
                                              int lane) {
   float s = 0.f;
   if (lane == 0) s = thread_sqdist(a, b, d);
+  return __shfl_sync(kFull, s, 0);
+}
+
+__device__ __forceinline__ float warp_sqdist(const Rows& R, uint64_t i, uint64_t j, int lane) {
+  float s = 0.f;
+  if (lane == 0) s = thread_sqdist(R, i, j);
   return __shfl_sync(kFull, s, 0);
 }
 
@@ -141,7 +170,7 @@ static __device__ __noinline__ void record_inline(const InlineCtx* __restrict__ 
 }
 
 struct ScanArgs {
-  const float* X;
+  Rows rows;  // the FP32 working rows (X or virtual windows)
   const float* skeys;
   const uint32_t* sidx;
   uint32_t n;
@@ -178,6 +207,28 @@ __device__ __forceinline__ void record(const ScanArgs& a, uint32_t p, uint32_t j
       a.cand_s[c] = s32;
     } else {
       record_inline(a.ic, p, j);
+    }
+  }
+}
+
+// The sparse scans' two variants (no function call in the list variant: the
+// call's ABI would cost their candidate loops registers).  kExact = false: the
+// list only, every band pair counted (cand_n > cand_cap tells the host the
+// list lost pairs); kExact = true, the rescan after such an overflow: every
+// band pair evaluated inline in FP64 into the 128-bit minimum, nothing listed.
+template <bool kExact>
+__device__ __forceinline__ void record_scan(const ScanArgs& a, uint32_t p, uint32_t j, float s32, float band) {
+  atomicMin(a.best, __float_as_uint(s32));
+  if (s32 <= band) {
+    if constexpr (kExact) {
+      record_inline(a.ic, p, j);
+    } else {
+      const unsigned long long c = atomicAdd(a.cand_n, 1ull);
+      if (c < a.cand_cap) {
+        a.cand_p[c] = p;
+        a.cand_j[c] = j;
+        a.cand_s[c] = s32;
+      }
     }
   }
 }

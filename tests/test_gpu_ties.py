@@ -101,3 +101,16 @@ def test_duplicates_near_not_exact(psg, orc):
     want = orc.brute_force_closest_pair(sub, 0)
     assert got.distance == want.distance
     assert (got.index_i, got.index_j) == (int(idx[want.index_i]), int(idx[want.index_j]))
+
+
+@pytest.mark.parametrize("q", [1, 10])
+def test_sparse_engine_exact_rescan(psg, q):
+    """10k duplicates among 120k points: ~5e7 band pairs, more than the
+    sparse engines' longest candidate list (2^24), so the scan is redone with
+    every band pair evaluated inline in FP64 (k_grid_scan2 / k_scan <kExact>)."""
+    pts, idx = planted_duplicates(120_000, 10_000, 8, 21)
+    ps = psg.PointSet.from_flat(pts, 8)
+    for _ in range(2):
+        got = psg.closest_pair(ps, q, 10.0, 1, 3)
+        assert (got.index_i, got.index_j, got.distance) == (*first_admissible(idx, 3), 0.0)
+        assert psg.last_profile()["inline_fp64"] > 1 << 24
