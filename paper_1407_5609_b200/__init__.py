@@ -40,7 +40,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpairscan_b200.so")
+# PSG_LIB_PATH: a diagnostic build (e.g. -DPSG_DEBUG_SYNC) in place of the in-tree library
+LIB_PATH = os.environ.get("PSG_LIB_PATH") or os.path.join(HERE, "libpairscan_b200.so")
 
 PSG_OK, PSG_ERR_INVALID, PSG_ERR_CUDA, PSG_ERR_NOMEM, PSG_ERR_INTERNAL = 0, 1, 2, 3, 4
 PSG_ERR_IO = 5

@@ -73,7 +73,7 @@ struct USmall {
 template <int NK>
 __global__ void __launch_bounds__(256) k_project_small(const float* __restrict__ X, uint32_t n, int d,
                                                        const __grid_constant__ USmall U, float* __restrict__ keys,
-                                                       unsigned* __restrict__ norm2_bits) {
+                                                       unsigned* __restrict__ norm2_bits, CellCount cc) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   float nn = 0.f;
   if (r < n) {
@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256) k_project_small(const float* __restrict__
     float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(r) * NK);
 #pragma unroll
     for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+    if (cc.gp) count_cell<NK>(acc, r, cc);
   }
   nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
   if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
@@ -138,7 +139,7 @@ constexpr int kWinRows = 128;
 template <int NK>
 __global__ void __launch_bounds__(kWinRows) k_project_windows(Rows R, uint32_t n, const float* __restrict__ Ut,
                                                               float* __restrict__ keys, unsigned* __restrict__ norm2_bits,
-                                                              int u_smem, int seg_smem) {
+                                                              int u_smem, int seg_smem, CellCount cc) {
   extern __shared__ float4 sh4[];
   float* sh = reinterpret_cast<float*>(sh4);
   const int d = R.d;
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(kWinRows) k_project_windows(Rows R, uint32_t n
     float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(i0 + r) * NK);
 #pragma unroll
     for (int q = 0; q < NK / 4; ++q) out[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    if (cc.gp) count_cell<NK>(acc, i0 + r, cc);
   }
   nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
   if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
@@ -473,13 +475,18 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
 // the window of the bound reached by the bootstrap; otherwise flag a rebuild
 // (the host widens the cells and reruns the scan).  One thread, so every
 // block of the scan sees the same decision.
-__global__ void k_check_grid(unsigned* best, const Budget* bud, const GridParams* gp, unsigned* regrid,
-                             unsigned* check_best, Thresholds* th_out) {
-  const unsigned b = *best;
-  const Thresholds th = budget_thresholds_s32(*bud, __uint_as_float(b));
-  *check_best = b;
-  *th_out = th;  // the scan's starting thresholds, computed once
-  *regrid = gp ? !(gp->w >= static_cast<double>(th.win) * (1.0 + 1e-5)) : 0u;
+// Also resets the attempt's counters and minima (one launch for both).
+__global__ void k_scan_prepare(DevState* st, const GridParams* gp) {
+  st->cand_n = 0;
+  st->best64 = ~0ull;
+  st->lex = ~0ull;
+  st->best128[0] = st->best128[1] = ~0ull;
+  st->examined = st->evals = st->visited = st->inline_n = 0;
+  const unsigned b = st->best;
+  const Thresholds th = budget_thresholds_s32(st->bud, __uint_as_float(b));
+  st->check_best = b;
+  st->th = th;  // the scan's starting thresholds, computed once
+  st->regrid = gp ? !(gp->w >= static_cast<double>(th.win) * (1.0 + 1e-5)) : 0u;
 }
 
 // K3b (grid): one pass per sorted position over its (at most five) stencil
@@ -589,8 +596,13 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
 template <int NK, bool kWindow>
 __global__ void k_recheck(ScanArgs a, ExactSrc src, double* __restrict__ d64, unsigned long long* __restrict__ best64,
                           unsigned long long* __restrict__ examined) {
-  const Thresholds th = budget_thresholds_s32(*a.bud,best_now(a.best));
   const uint32_t count = static_cast<uint32_t>(min(*a.cand_n, static_cast<unsigned long long>(a.cand_cap)));
+  if (blockIdx.x * blockDim.x >= count) return;  // usually one block has work (C2: one candidate)
+  // the final bound's thresholds, once per block (FP64 sqrt / divisions)
+  __shared__ Thresholds sth;
+  if (threadIdx.x == 0) sth = budget_thresholds_s32(*a.bud, best_now(a.best));
+  __syncthreads();
+  const Thresholds th = sth;
   for (uint32_t base = blockIdx.x * blockDim.x; base < count; base += gridDim.x * blockDim.x) {
   const uint32_t c = base + threadIdx.x;
   unsigned pass = 0;
@@ -682,7 +694,9 @@ void part_range(uint64_t n, uint64_t part, uint64_t nparts, uint32_t* lo, uint32
 
 // ---------------------------------------------------------------------------
 // Device-side solve state (DevState): initialised, filled and read back once.
-__global__ void k_state_init(DevState* st, ExactSrc src, const uint32_t* sidx) {
+__global__ void k_state_init(DevState* st, ExactSrc src, const uint32_t* sidx, Budget bud) {
+  st->bud = bud;
+  st->pre_ticket = 0;
   st->ic.src = src;
   st->ic.sidx = sidx;
   st->ic.best128 = st->best128;
@@ -697,104 +711,200 @@ __global__ void k_state_init(DevState* st, ExactSrc src, const uint32_t* sidx) {
   st->examined = st->evals = st->visited = st->inline_n = 0;
 }
 
-__global__ void k_scan_reset(DevState* st) {
-  st->cand_n = 0;
-  st->best64 = ~0ull;
-  st->lex = ~0ull;
-  st->best128[0] = st->best128[1] = ~0ull;
-  st->examined = st->evals = st->visited = st->inline_n = 0;
-}
 
-struct SetupArgs {
-  int d, nk, g, gbox;  // gbox: keys sampled for boxes (>= g)
-  double unorm, sigma, Rn, occupancy, box_sd;
-  double min_w;        // cell width learned by an earlier regrid on this point set (0: none)
+// ---------------------------------------------------------------------------
+// The grid's key box and cell width before the projection runs (so the
+// projection can count cells): kPreBlocks x 8 warps project a hashed sample of
+// kGridSample rows on CUDA cores (warp per row, lanes over coordinates; a
+// tuning input only, so any summation order), reduce per-key moments, and the
+// last block to finish turns them into the box (mean +- box_sd sd clipped to
+// the sample range) and GridParams at the occupancy width.
+constexpr int kPreBlocks = 64;
+struct PresampleArgs {
+  Rows R;
+  const float* Ut;  // d x nk (transposed directions)
+  int ut_smem;      // Ut staged in shared memory (d * nk * 4 bytes)
+  int nk, g, gbox;  // gbox: keys boxed (the dense engine may regrid on up to kMaxGridKeys)
   uint32_t n, m;
-  int tc;              // keys from the tensor-core projection (key_gamma)
+  double occupancy, box_sd, min_w;
 };
-static_assert(kMaxGridKeys <= 8, "k_setup: one warp per boxed key");
 
-// The error budget from the projection's max norm (same formula as the host
-// make_budget), then — grid engine — the key box from the sample moments
-// (mean +- 3 sd clipped to the sample range) and the grid parameters for the
-// occupancy width.  One block; nothing returns to the host.
-__global__ void __launch_bounds__(256) k_setup(DevState* st, GridParams* gp, const float* __restrict__ sample,
-                                               SetupArgs sa) {
-  __shared__ double red[4][8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    const double u = 0x1.0p-24;
-    Budget b;
-    b.e = (sa.d + 4) * u * 1.01;
-    b.a = (2.0 * sa.d + 2.0) * 0x1.0p-149;
-    const double nn = static_cast<double>(__uint_as_float(st->norm2_bits));
-    const double maxnorm = sqrt(nn * (1.0 + (sa.d + 4) * u)) * (1.0 + 1e-7);
-    b.E = key_gamma(sa.d, sa.tc) * sa.unorm * maxnorm * 1.0001 + key_abs(sa.d, sa.tc);
-    b.Rn = sa.Rn;
-    b.sigma = sa.sigma;
-    b.unorm = sa.unorm;
-    b.gamma64 = (sa.d + 2) * 0x1.0p-53 * 1.01;
-    b.nk = sa.nk;
-    st->bud = b;
+__global__ void __launch_bounds__(256) k_presample(PresampleArgs a, DevState* st, GridParams* gp,
+                                                   double* __restrict__ part, unsigned* __restrict__ ticket,
+                                                   uint32_t* __restrict__ bctr) {
+  extern __shared__ float sut[];  // U transposed (d x nk), when it fits
+  __shared__ double red[8][kMaxGridKeys][4];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = a.R.d, nk = a.nk;
+  const bool ut_smem = a.ut_smem;
+  if (ut_smem)
+    for (int k = threadIdx.x; k < d * nk; k += blockDim.x) sut[k] = a.Ut[k];
+  __syncthreads();
+  const float* Ut = ut_smem ? sut : a.Ut;
+  double s1[kMaxGridKeys], s2[kMaxGridKeys];
+  float mn[kMaxGridKeys], mx[kMaxGridKeys];
+#pragma unroll
+  for (int t = 0; t < kMaxGridKeys; ++t) {
+    s1[t] = s2[t] = 0.0;
+    mn[t] = INFINITY;
+    mx[t] = -INFINITY;
   }
-  if (sa.g == 0) return;
-  // boxes of every key a grid may use (the sparse grid takes the first g,
-  // the dense engine up to kMaxGridKeys): warp t reduces key t, every load of
-  // its sample in flight at once, four independent FP64 accumulators per lane
-  __shared__ double s_lo[kMaxGridKeys], s_span[kMaxGridKeys];
-  if (warp < sa.gbox) {
-    const float* v = sample + static_cast<size_t>(warp) * sa.m;
-    constexpr int kPer = kGridSample / 32;  // 128 sample values per lane
-    float x[kPer];  // all 128 loads issued before any use: one memory round trip
+  constexpr int kRows = 4;  // sample rows per warp step, their loads in flight together
+  const uint32_t gw = blockIdx.x * 8 + warp, nw = gridDim.x * 8;
+  for (uint32_t k0 = gw * kRows; k0 < a.m; k0 += nw * kRows) {
+    uint32_t i[kRows];
 #pragma unroll
-    for (int r = 0; r < kPer; ++r) {
-      const uint32_t i = lane + 32u * r;
-      x[r] = i < sa.m ? v[i] : 0.f;
-    }
-    double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
-    float mn = INFINITY, mx = -INFINITY;
+    for (int r = 0; r < kRows; ++r)  // a bijective 32-bit hash scaled to [0, n): no aliasing with
+      i[r] = __umulhi((k0 + r) * 2654435761u + 12345u, a.n);  // index-periodic structure
+    float acc[kRows][kMaxGridKeys];
 #pragma unroll
-    for (int r = 0; r < kPer; ++r) {
-      if (lane + 32u * r < sa.m) {
-        const float y = x[r];
-        s1[r & 3] += y;
-        s2[r & 3] = fma(static_cast<double>(y), static_cast<double>(y), s2[r & 3]);
-        mn = fminf(mn, y);
-        mx = fmaxf(mx, y);
+    for (int r = 0; r < kRows; ++r)
+#pragma unroll
+      for (int t = 0; t < kMaxGridKeys; ++t) acc[r][t] = 0.f;
+#pragma unroll 2
+    for (int c = lane; c < d; c += 32) {
+      float x[kRows];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) x[r] = k0 + r < a.m ? row_at(a.R, i[r], c) : 0.f;
+#pragma unroll
+      for (int t = 0; t < kMaxGridKeys; ++t) {
+        if (t >= a.gbox) break;
+        const float u = Ut[c * nk + t];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) acc[r][t] = fmaf(u, x[r], acc[r][t]);
       }
     }
-    double a1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), a2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+#pragma unroll
+      for (int t = 0; t < kMaxGridKeys; ++t) {
+        float v = acc[r][t];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (t < a.gbox && k0 + r < a.m) {
+          s1[t] += v;
+          s2[t] = fma(static_cast<double>(v), static_cast<double>(v), s2[t]);
+          mn[t] = fminf(mn[t], v);
+          mx[t] = fmaxf(mx[t], v);
+        }
+      }
+  }
+  if (lane == 0)
+    for (int t = 0; t < a.gbox; ++t) {
+      red[warp][t][0] = s1[t];
+      red[warp][t][1] = s2[t];
+      red[warp][t][2] = mn[t];
+      red[warp][t][3] = mx[t];
+    }
+  __syncthreads();
+  if (threadIdx.x < a.gbox) {
+    const int t = threadIdx.x;
+    double q[4] = {0.0, 0.0, INFINITY, -INFINITY};
+    for (int w = 0; w < 8; ++w) {
+      q[0] += red[w][t][0];
+      q[1] += red[w][t][1];
+      q[2] = fmin(q[2], red[w][t][2]);
+      q[3] = fmax(q[3], red[w][t][3]);
+    }
+    for (int c = 0; c < 4; ++c) part[(static_cast<size_t>(blockIdx.x) * kMaxGridKeys + t) * 4 + c] = q[c];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the last block: warp t reduces key t's per-block partials (lanes over blocks)
+  __shared__ double s_lo[kMaxGridKeys], s_span[kMaxGridKeys];
+  if (warp < a.gbox) {
+    const int t = warp;
+    double q[4] = {0.0, 0.0, INFINITY, -INFINITY};
+    for (uint32_t b = lane; b < gridDim.x; b += 32) {
+      const double* pp = part + (static_cast<size_t>(b) * kMaxGridKeys + t) * 4;
+      q[0] += pp[0];
+      q[1] += pp[1];
+      q[2] = fmin(q[2], pp[2]);
+      q[3] = fmax(q[3], pp[3]);
+    }
     for (int o = 16; o; o >>= 1) {
-      a1 += __shfl_xor_sync(kFull, a1, o);
-      a2 += __shfl_xor_sync(kFull, a2, o);
-      mn = fminf(mn, __shfl_xor_sync(kFull, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+      q[0] += __shfl_xor_sync(kFull, q[0], o);
+      q[1] += __shfl_xor_sync(kFull, q[1], o);
+      q[2] = fmin(q[2], __shfl_xor_sync(kFull, q[2], o));
+      q[3] = fmax(q[3], __shfl_xor_sync(kFull, q[3], o));
     }
     if (lane == 0) {
-      const double mean = a1 / sa.m, sd = sqrt(fmax(a2 / sa.m - mean * mean, 0.0));
-      const double lo_t = fmax(static_cast<double>(mn), mean - sa.box_sd * sd);
-      const double hi_t = fmin(static_cast<double>(mx), mean + sa.box_sd * sd);
-      s_lo[warp] = lo_t;
-      s_span[warp] = fmax(hi_t - lo_t, 1e-30);
+      const double mean = q[0] / a.m, sd = sqrt(fmax(q[1] / a.m - mean * mean, 0.0));
+      const double lo_t = fmax(q[2], mean - a.box_sd * sd), hi_t = fmin(q[3], mean + a.box_sd * sd);
+      s_lo[t] = lo_t;
+      s_span[t] = fmax(hi_t - lo_t, 1e-30);
     }
   }
   __syncthreads();
+  if (threadIdx.x != 0) return;
+  *ticket = 0;  // ready for the next solve
+  bctr[0] = bctr[1] = 0;  // the counting build's big-cell list (k_cell_count's reset)
   double lo[kMaxGridKeys] = {}, span[kMaxGridKeys] = {};
-  if (tid == 0)
-    for (int t = 0; t < sa.gbox; ++t) {
-      lo[t] = s_lo[t];
-      span[t] = s_span[t];
-    }
-  if (tid == 0) {
-    for (int t = 0; t < kMaxGridKeys; ++t) {
-      st->box_lo[t] = lo[t];
-      st->box_span[t] = span[t];
-    }
-    const double w = fmax(grid_occupancy_width(sa.n, sa.g, span, sa.occupancy), sa.min_w);
-    GridParams P;
-    grid_params_for(P, sa.g, w, lo, span);
-    *gp = P;
+  for (int t = 0; t < a.gbox; ++t) {
+    lo[t] = s_lo[t];
+    span[t] = s_span[t];
   }
+  for (int t = 0; t < kMaxGridKeys; ++t) {
+    st->box_lo[t] = lo[t];
+    st->box_span[t] = span[t];
+  }
+  const double w = fmax(grid_occupancy_width(a.n, a.g, span, a.occupancy), a.min_w);
+  GridParams P;
+  grid_params_for(P, a.g, w, lo, span);
+  *gp = P;
+}
+
+// The bootstrap bound from the lower bounds k_cell_fix left per warp
+// (BootLB): up to kBootEvals warps each take a chunk of the entries (one entry
+// each up to 2^20 points), pick the least lower bound and evaluate that pair
+// warp-parallel (coalesced row reads), rounded up past any FP32 summation
+// order so the value is a valid bound (warp_eval_best); block 0 also takes the
+// seed pair (0, max(zone, 1)), admissible whenever any pair is.
+constexpr uint32_t kBootEvals = 4096;
+__global__ void __launch_bounds__(256) k_boot_select(ScanArgs a, const float* __restrict__ wlb,
+                                                     const uint2* __restrict__ wpair, uint32_t W, uint32_t nw,
+                                                     uint32_t z) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw == 0 && z < a.n) {
+    const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(a.rows, 0, z) : 0.f) : warp_sqdist(a.rows, 0, z, lane);
+    if (lane == 0) atomicMin(a.best, __float_as_uint(s));
+  }
+  if (gw >= nw) return;
+  const uint32_t chunk = (W + nw - 1) / nw;
+  const uint32_t e0 = gw * chunk, e1 = min(W, e0 + chunk);
+  float lb = INFINITY;
+  uint32_t at = 0;
+  for (uint32_t e = e0 + lane; e < e1; e += 32) {
+    const float x = wlb[e];
+    if (x < lb) {
+      lb = x;
+      at = e;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ol = __shfl_xor_sync(kFull, lb, o);
+    const uint32_t oa = __shfl_xor_sync(kFull, at, o);
+    if (ol < lb || (ol == lb && oa < at)) {
+      lb = ol;
+      at = oa;
+    }
+  }
+  if (!(lb < INFINITY)) return;
+  const uint2 pr = wpair[at];
+  float s = 0.f;
+  for (int t = lane; t < a.d; t += 32) {
+    const float g = row_at(a.rows, pr.x, t) - row_at(a.rows, pr.y, t);
+    s = fmaf(g, g, s);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  s = __fmul_ru(s, 1.0f + static_cast<float>(2 * a.d + 8) * 0x1.0p-24f);  // see warp_eval_best
+  if (lane == 0) atomicMin(a.best, __float_as_uint(s));
 }
 
 }  // namespace
@@ -807,24 +917,25 @@ void check_reference_args(uint64_t n, uint64_t q, double f) {
   if (!(f > 0.0) || !std::isfinite(f)) throw invalid_argument("projection factor must be positive");
 }
 
-void project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
-                   cudaStream_t s) {
+bool project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
+                   cudaStream_t s, const CellCount& cc) {
   const uint32_t n = static_cast<uint32_t>(ps.n);
   const int d = ps.d;
-  const int sms = ctx().sm_count;
+  bool counted = cc.gp != nullptr;
   if (!ps.X) {
-    project_windows(ps, dir, keys, norm2_bits, s);  // virtual window rows (Rows)
+    project_windows(ps, dir, keys, norm2_bits, s, cc);  // virtual window rows (Rows)
   } else if (tc_projection(d, ps.n)) {
-    project_tc(ps, dir, keys, norm2_bits, s);  // psg_project_tc.cu
+    project_tc(ps, dir, keys, norm2_bits, s, cc);  // psg_project_tc.cu
   } else if (d < 32) {
     USmall u{};
     for (int k = 0; k < dir.nk; ++k)
       for (int t = 0; t < d; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * d + t];
     if (dir.nk == 4)
-      k_project_small<4><<<blocks_for(n, 256), 256, 0, s>>>(ps.X, n, d, u, keys, norm2_bits);
+      k_project_small<4><<<blocks_for(n, 256), 256, 0, s>>>(ps.X, n, d, u, keys, norm2_bits, cc);
     else
-      k_project_small<8><<<blocks_for(n, 256), 256, 0, s>>>(ps.X, n, d, u, keys, norm2_bits);
+      k_project_small<8><<<blocks_for(n, 256), 256, 0, s>>>(ps.X, n, d, u, keys, norm2_bits, cc);
   } else {
+    counted = false;
     // irregular d: thread per row, U staged in shared memory (not graph-safe:
     // solve_graph skips these)
     DevBuf<float> U(dir.U.size(), s);  // freed stream-ordered after the launch
@@ -840,6 +951,7 @@ void project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
   }
   PSG_LAUNCHED();
   ++g_launches;
+  return counted;
 }
 
 // Window sets: U transposed (d x nk), kept on the point set and uploaded
@@ -860,7 +972,7 @@ const float* window_directions(const psg_pointset& ps, const Directions& dir, cu
 }
 
 void project_windows(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
-                     cudaStream_t s) {
+                     cudaStream_t s, const CellCount& cc) {
   const uint32_t n = static_cast<uint32_t>(ps.n);
   const int d = ps.d, nk = dir.nk;
   const float* Ut = window_directions(ps, dir, s);
@@ -873,12 +985,12 @@ void project_windows(const psg_pointset& ps, const Directions& dir, float* keys,
     if (smem > 48 * 1024)
       PSG_CUDA(cudaFuncSetAttribute(k_project_windows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_project_windows<4><<<blocks_for(n, kWinRows), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, norm2_bits, u_smem,
-                                                                         seg_smem);
+                                                                         seg_smem, cc);
   } else {
     if (smem > 48 * 1024)
       PSG_CUDA(cudaFuncSetAttribute(k_project_windows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_project_windows<8><<<blocks_for(n, kWinRows), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, norm2_bits, u_smem,
-                                                                         seg_smem);
+                                                                         seg_smem, cc);
   }
 }
 
@@ -934,6 +1046,7 @@ std::shared_ptr<CppWork> get_work(psg_pointset* ps, int nk, cudaStream_t s) {
     w->nk = nk;
     w->keys.alloc(ps->n * nk, s);
     w->st.alloc(1, s);
+    w->pre_part.alloc(kPreBlocks * kMaxGridKeys * 4, s);  // not inside a graph capture
     PSG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->host_st), sizeof(DevState)));
     slot = w;
   }
@@ -1034,34 +1147,46 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
     W.wv1.alloc(n, s);
     W.whist.alloc(radix_hist_words(n), s);
   }
-  k_state_init<<<1, 1, 0, s>>>(W.st.p, ps->exact(), plan->grid ? W.gi.sidx.p : W.wsidx.p);
+  // the error budget is a property of the point set and the directions: host
+  plan->bud = make_budget(*ps, plan->dir, ps->norm2max);
+  k_state_init<<<1, 1, 0, s>>>(W.st.p, ps->exact(), plan->grid ? W.gi.sidx.p : W.wsidx.p, plan->bud);
   PSG_LAUNCHED();
   {
-    plan->proj_span = std::make_unique<KernelSpan>(s);
-    project_async(*ps, plan->dir, W.keys.p, &W.st.p->norm2_bits, s);
-    plan->proj_span->end();
-    tm.mark("project");
     static const double occupancy = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : kGridOccupancy;
-    const int gbox = std::min(plan->dir.q, kMaxGridKeys);
     static const double box_sd = std::getenv("PSG_BOXSD") ? std::atof(std::getenv("PSG_BOXSD")) : kGridBoxSd;
     const double min_w = W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone ? W.learned_w : 0.0;
-    SetupArgs sa{ps->d, nk, plan->g, gbox, plan->dir.unorm, plan->dir.sigma, ps->Rn, occupancy, box_sd, min_w,
-                 static_cast<uint32_t>(n), 0, tc_projection(ps->d, n) && ps->X != nullptr};
+    // a width learned on dense data makes big cells: the radix build then
+    const bool counting = plan->grid && !(min_w > 0.0 && W.learned_dense);
+    CellCount cc{};
+    if (plan->grid) {
+      // K2 (grid) set-up before K1: the key box from a projected sample and the
+      // cell width, on device, so the projection can count the cells
+      const size_t ut_bytes = static_cast<size_t>(ps->d) * nk * 4;
+      const int ut_smem = ut_bytes <= 32 * 1024;
+      PresampleArgs pa{ps->rows(), window_directions(*ps, plan->dir, s), ut_smem, nk, plan->g,
+                       std::min(plan->dir.q, kMaxGridKeys), static_cast<uint32_t>(n),
+                       static_cast<uint32_t>(std::min<uint64_t>(n, kGridSample)), occupancy, box_sd, min_w};
+      k_presample<<<kPreBlocks, 256, ut_smem ? ut_bytes : 0, s>>>(pa, W.st.p, W.gi.gp.p, W.pre_part.p,
+                                                                  &W.st.p->pre_ticket, W.gi.bctr.p);
+      PSG_LAUNCHED();
+      ++g_launches;
+      static const bool no_fuse = std::getenv("PSG_NO_FUSED_COUNT") != nullptr;  // A/B
+      if (counting && !no_fuse) cc = CellCount{W.gi.gp.p, W.gi.cnt.p, W.gi.cid0.p};
+    }
+    plan->proj_span = std::make_unique<KernelSpan>(s);
+    const bool counted = project_async(*ps, plan->dir, W.keys.p, &W.st.p->norm2_bits, s, cc);
+    plan->proj_span->end();
+    tm.mark("project");
     if (plan->grid) {
       // K2 (grid): cells over the first g keys at the occupancy width, sorted;
-      // parameters computed on device, no host round trip
-      W.gi.ensure(static_cast<uint32_t>(n), nk, s);
-      sa.m = grid_sample(W.keys.p, static_cast<uint32_t>(n), nk, gbox, W.gi, s);
-      k_setup<<<1, 256, 0, s>>>(W.st.p, W.gi.gp.p, W.gi.sample.p, sa);
-      PSG_LAUNCHED();
-      // a width learned on dense data makes big cells: the radix build then
-      const bool dense_hint = min_w > 0.0 && W.learned_dense;
-      build_grid(W.keys.p, static_cast<uint32_t>(n), nk, W.gi, 24, s, /*counting=*/!dense_hint);
+      // the counting build also leaves the bootstrap's lower bounds (BootLB)
+      const BootLB boot{W.keys.p, W.gi.wlb.p, W.gi.wpair.p, zone};
+      build_grid(W.keys.p, static_cast<uint32_t>(n), nk, W.gi, 24, s, counting, 0, counted, counting ? &boot : nullptr);
+      static const bool old_boot = std::getenv("PSG_OLD_BOOT") != nullptr;  // A/B: the standalone bootstrap
+      plan->boot_lb = counting && !old_boot;
       g_launches += 3;
       tm.mark("grid");
     } else {
-      k_setup<<<1, 256, 0, s>>>(W.st.p, nullptr, nullptr, sa);
-      PSG_LAUNCHED();
       // K2 (window): sort by key 0 (stable, index payload)
       if (nk == 4)
         k_sort_keys<4><<<blocks_for(n, 256), 256, 0, s>>>(W.keys.p, static_cast<uint32_t>(n), W.wk0.p, W.wv0.p);
@@ -1080,7 +1205,6 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
       PSG_LAUNCHED();
       g_launches += 16;
       tm.mark("sort");
-      read_state(*plan, s);  // the window engine's adaptive bootstrap needs the budget on the host
     }
     trace("plan: enqueued");  // timings are collected at the bootstrap's synchronisation
   }
@@ -1100,6 +1224,33 @@ void collect_prep(CppPlan& plan) {
 }
 }  // namespace
 
+// Tuning hints learned by a solve hold for its (q, seed, zone) on this point
+// set: switching to another triple drops them.
+void learn_for(CppWork& W, const CppPlan& plan) {
+  if (W.learned_q != plan.q_arg || W.learned_seed != plan.seed_arg || W.learned_zone != plan.zone) {
+    W.learned_w = 0.0;
+    W.learned_dense = false;
+    W.learned_full_boot = false;
+  }
+  W.learned_q = plan.q_arg;
+  W.learned_seed = plan.seed_arg;
+  W.learned_zone = plan.zone;
+}
+
+// The bootstrap over every position's whole forward 3^g stencil (at most
+// kGridBootCap candidates each, a uniform stride beyond): the rescue when the
+// own-row bound is too wide for the cells.
+void launch_full_bootstrap(CppPlan& plan, cudaStream_t s) {
+  ScanArgs a = make_args(plan);
+  const uint32_t n = static_cast<uint32_t>(plan.ps->n);
+  if (plan.dir.nk == 4)
+    k_grid_bootstrap<4><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, 0, n, kGridBootCap, 0);
+  else
+    k_grid_bootstrap<8><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, plan.work->gi.dev, 0, n, kGridBootCap, 0);
+  PSG_LAUNCHED();
+  ++g_launches;
+}
+
 float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   Ctx& c = ctx();
   cudaStream_t s = c.stream;
@@ -1108,6 +1259,28 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   ScanArgs a = make_args(plan);
   StageTimer tm(s);
   const uint32_t z = static_cast<uint32_t>(std::max<uint64_t>(plan.zone, 1));
+  if (plan.grid && plan.boot_lb) {
+    // the lower bounds the grid build left (BootLB): the best of them
+    // evaluated exactly, plus the seed pair — one small kernel; the same global
+    // bound on every rank of a sharded solve (every rank built the same grid)
+    plan.boot_span = std::make_unique<KernelSpan>(s);
+    const uint32_t nwarps = static_cast<uint32_t>((plan.ps->n + 255) / 256 * 8);
+    static const uint32_t evals =
+        std::getenv("PSG_BOOT_EVALS") ? static_cast<uint32_t>(std::atoi(std::getenv("PSG_BOOT_EVALS"))) : kBootEvals;
+    const uint32_t nw = std::max(1u, std::min(nwarps, evals));
+    k_boot_select<<<(nw + 7) / 8, 256, 0, s>>>(a, plan.work->gi.wlb.p, plan.work->gi.wpair.p, nwarps, nw, z);
+    PSG_LAUNCHED();
+    ++g_launches;
+    const CppWork& W = *plan.work;
+    if (W.learned_full_boot && W.learned_q == plan.q_arg && W.learned_seed == plan.seed_arg &&
+        W.learned_zone == plan.zone)
+      launch_full_bootstrap(plan, s);  // this (q, seed, zone) needed the whole stencil before
+    plan.boot_span->end();
+    if (!plan.sync_bootstrap) return INFINITY;
+    read_state(plan, s);
+    collect_prep(plan);
+    return bits_to_float(plan.work->host_st->best);
+  }
   if (z < plan.ps->n) {
     k_seed_pair<<<1, 32, 0, s>>>(a, z);
     PSG_LAUNCHED();
@@ -1134,6 +1307,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
   }
   // Window engine.  Adaptive width: widen while the window the bound implies
   // is far more work than the bootstrap that produced it.
+  PSG_CUDA(cudaStreamSynchronize(s));  // the plan's stage events
   collect_prep(plan);
   uint32_t width = 1024;
   for (int round = 0; round < 4; ++round) {
@@ -1194,14 +1368,11 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
   CppWork& W = *plan.work;
   DevState* st = W.st.p;
   ScanArgs a = make_args(plan);
-  k_scan_reset<<<1, 1, 0, s>>>(st);
+  // Reset, and (grid) the check that the cells hold every pair whose key gaps
+  // are within the window of the bound — decided on device from the bound
+  // every rank shares.
+  k_scan_prepare<<<1, 1, 0, s>>>(st, plan.grid ? W.gi.gp.p : nullptr);
   PSG_LAUNCHED();
-  if (plan.grid) {
-    // The grid must hold every pair whose key gaps are within the window of
-    // the bound; decided on device from the bound every rank shares.
-    k_check_grid<<<1, 1, 0, s>>>(&st->best, &st->bud, W.gi.gp.p, &st->regrid, &st->check_best, &st->th);
-    PSG_LAUNCHED();
-  }
   KernelSpan* span = new KernelSpan(s);
   if (plan.grid && plan.dense) {
     // dense cells: cell-pair tiles (the caller decided after the grid check
@@ -1244,7 +1415,7 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
   k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
   PSG_LAUNCHED();
   PSG_CUDA(cudaMemcpyAsync(W.host_st, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-  g_launches += plan.grid ? 6 : 5;
+  g_launches += 4;
   return span;
 }
 
@@ -1305,14 +1476,19 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
       } else {
         const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
         plan.dense = est > kDenseFactor * n;
+        if (std::getenv("PSG_TRACE")) {
+          const DevState& h0 = *W.host_st;
+          std::fprintf(stderr, "[psg] grid: g %d w %.6g cells %llu dims %u %u %u box %.4g+%.4g %.4g+%.4g %.4g+%.4g "
+                       "bound %.6g est %llu dense %d learned_w %.6g\n", plan.gp.g, plan.gp.w,
+                       static_cast<unsigned long long>(plan.gp.cells), plan.gp.dims[0], plan.gp.dims[1],
+                       plan.gp.dims[2], h0.box_lo[0], h0.box_span[0], h0.box_lo[1], h0.box_span[1], h0.box_lo[2],
+                       h0.box_span[2], static_cast<double>(bits_to_float(h0.best)),
+                       static_cast<unsigned long long>(est), static_cast<int>(plan.dense), W.learned_w);
+        }
       }
       if (nparts == 1 && plan.dense) {  // later solves of this (q, seed, zone) skip the graph attempt
-        if (W.learned_q != plan.q_arg || W.learned_seed != plan.seed_arg || W.learned_zone != plan.zone)
-          W.learned_w = 0.0;  // hints of another (q, seed, zone)
+        learn_for(W, plan);
         W.learned_dense = true;
-        W.learned_q = plan.q_arg;
-        W.learned_seed = plan.seed_arg;
-        W.learned_zone = plan.zone;
       }
       static const int dense_keys = std::getenv("PSG_DENSE_KEYS") ? std::atoi(std::getenv("PSG_DENSE_KEYS")) : kMaxGridKeys;
       const int gd = std::min(plan.dir.q, dense_keys);
@@ -1337,6 +1513,22 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
     if (plan.grid) PSG_CUDA(cudaMemcpy(&plan.gp, W.gi.gp.p, sizeof(GridParams), cudaMemcpyDeviceToHost));
     collect_prep(plan);
     const DevState& h = *W.host_st;
+    if (plan.grid && h.regrid && !plan.rescued && plan.g <= 3) {
+      // The bootstrap looked at each point's own cell row only; before
+      // widening the cells, try the whole 3^g stencil on these cells (a
+      // near pair split across a row boundary: e.g. a motif whose windows
+      // straddle a cell face).  Over all positions, so every rank of a
+      // sharded solve derives the same bound; later solves of this (q, seed,
+      // zone) run it up front (learned_full_boot).
+      plan.rescued = true;
+      launch_full_bootstrap(plan, s);
+      if (nparts == 1) {
+        learn_for(W, plan);
+        W.learned_full_boot = true;
+        W.drop_graph();  // recaptured with the full bootstrap
+      }
+      continue;  // k_scan_prepare checks the cells again against the new bound
+    }
     if (plan.grid && h.regrid) {
       // Widen the cells to the key window of the bound the check saw and
       // rebuild.  Single part: the wider cells hold far better partners, so
@@ -1353,7 +1545,10 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         build_grid(W.keys.p, static_cast<uint32_t>(n), plan.dir.nk, W.gi, 24, s, !dense_grid,
                    dense_grid ? plan.gp.cells : 0);
         tm.mark("regrid");
-        if (nparts != 1) break;  // every rank must derive the same grid from the shared bound
+        // every rank must derive the same grid from the shared bound; the
+        // stencil bootstrap walks g <= 3 grids only (the dense engine's own
+        // Gram tiles lower the bound as they go)
+        if (nparts != 1 || dense_grid) break;
         ScanArgs a = make_args(plan);
         if (plan.dir.nk == 4)
           k_grid_bootstrap<4><<<blocks_for(n, kThreads), kThreads, 0, s>>>(a, W.gi.dev, 0, static_cast<uint32_t>(n),
@@ -1376,12 +1571,8 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         // Remember the width for later solves of the same (q, seed, zone) on
         // this point set: their first grid is built at it, so the captured
         // graph solve needs no regrid (a tuning hint; every stage still runs).
-        if (W.learned_q != plan.q_arg || W.learned_seed != plan.seed_arg || W.learned_zone != plan.zone)
-          W.learned_dense = false;  // hints of another (q, seed, zone)
+        learn_for(W, plan);
         W.learned_w = plan.gp.w;
-        W.learned_q = plan.q_arg;
-        W.learned_seed = plan.seed_arg;
-        W.learned_zone = plan.zone;
         W.drop_graph();
       }
       continue;
@@ -1447,7 +1638,7 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   if (W.learned_dense && W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone) return false;
   // every allocation happens before capture (and drops a graph that holds
   // buffers it replaces)
-  if (!ps->X) window_directions(*ps, dir, s);
+  window_directions(*ps, dir, s);  // the presample / window projection read it
   W.gi.ensure(static_cast<uint32_t>(ps->n), dir.nk, s);
   ensure_candidates(W, s);
   if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone || W.gcap != W.cand_cap) {

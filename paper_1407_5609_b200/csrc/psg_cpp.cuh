@@ -20,12 +20,16 @@ void prof_stages(const StageTimer& t);
 // Projection of the FP32 working rows onto the seeded directions:
 // keys[i*nk + k] = <U_k, X_i>; max ||X_i||^2 (FP32 bits) is atomically maxed
 // into *norm2_bits (device).  Enqueued only.
-void project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
-                   cudaStream_t s);
+// With cc.gp set, shapes that can count cells while projecting do so (and
+// return true): cell id and arrival rank of every row (CellCount).
+bool project_async(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits,
+                   cudaStream_t s, const CellCount& cc = CellCount{});
 // The tensor-core projection (psg_project_tc.cu): tc_projection(d, n) shapes.
-void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s);
+void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s,
+                const CellCount& cc);
 // Window sets (virtual rows): CUDA-core projection from the series.
-void project_windows(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s);
+void project_windows(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s,
+                     const CellCount& cc = CellCount{});
 const float* window_directions(const psg_pointset& ps, const Directions& dir, cudaStream_t s);
 // Host-synchronous variant: returns max ||X_i||^2.
 float project(const psg_pointset& ps, const Directions& dir, float* keys, cudaStream_t s);
@@ -40,6 +44,7 @@ struct DevState {
   // candidate list, evaluated inline (record(), psg_scan.cuh): [0] lo, [1] hi
   alignas(16) unsigned long long best128[2];
   unsigned long long cand_n;  // band pairs recorded (may exceed the list capacity)
+  unsigned pre_ticket;  // k_presample's last-block ticket
   unsigned norm2_bits;  // max ||x||^2 (FP32 bits), from the projection
   unsigned best;        // FP32 bits of the best squared distance seen
   unsigned regrid;      // set by k_check_grid: cells narrower than the bound's key window
@@ -66,6 +71,7 @@ struct CppWork {
   DevBuf<double> d64;
   uint32_t cand_cap = 0;
   DenseWork dense;         // dense cell-pair engine (clustered data)
+  DevBuf<double> pre_part; // k_presample's per-block key moments
   // The whole single-part grid solve captured once as a CUDA graph and
   // replayed by later solves with the same (q, seed, zone) on this point set.
   // Its kernels hold the buffer pointers of capture time: any reallocation
@@ -78,6 +84,7 @@ struct CppWork {
   double learned_w = 0.0;
   uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;
   bool learned_dense = false;  // the solve went to the dense engine (not graph-capturable: host decisions)
+  bool learned_full_boot = false;  // the own-row bootstrap was too weak: run the full-stencil one up front
   cudaEvent_t gev[6] = {};  // project / bootstrap / scan spans recorded inside the graph
   void drop_graph();
   ~CppWork();
@@ -95,6 +102,8 @@ struct CppPlan {
   bool grid = false;
   bool dense = false;      // grid engine: cell-pair tiles instead of per-point candidates
   bool exact_scan = false; // sparse engines: rescan with inline FP64 for every band pair (list overflow)
+  bool boot_lb = false;    // the grid build left per-warp bootstrap lower bounds (BootLB)
+  bool rescued = false;    // the full-stencil bootstrap already ran after a failed cell check
   int g = 0;
   std::shared_ptr<CppWork> work;
   uint32_t width = 0;      // window engine: bootstrap width (sorted neighbours)

@@ -565,6 +565,64 @@ __global__ void k_low_bits(uint64_t* __restrict__ keys, uint64_t m, int b) {
   if (k < m) keys[k] &= (1ull << b) - 1;
 }
 
+// ---- the sorted list in i-range buckets (frnn_pairs, large outputs) ----------
+// Bucket b holds the pairs with i in [n b / B, n (b + 1) / B): bucket order is
+// i order, so sorting each bucket on its own gives the global order, and
+// bucket b's copy to the host overlaps the sort of bucket b + 1.
+constexpr int kListBuckets = 32;
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t key, uint64_t n, int B) {
+  return static_cast<uint32_t>(((key >> 32) * B) / n);
+}
+
+__global__ void k_bucket_count(const uint64_t* __restrict__ pairs, uint64_t m, uint64_t n, int B,
+                               unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned sc[kListBuckets];
+  for (int b = threadIdx.x; b < B; b += blockDim.x) sc[b] = 0;
+  __syncthreads();
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < m;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&sc[bucket_of(pairs[k], n, B)], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    if (sc[b]) atomicAdd(cnt + b, static_cast<unsigned long long>(sc[b]));
+}
+
+// Scatter into the buckets, packed for the per-bucket radix sort: the key
+// becomes ((i - i0) << bj) | j.  A block reserves its slots with one global
+// atomic per bucket.
+__global__ void k_bucket_scatter(const uint64_t* __restrict__ pairs, uint64_t m, uint64_t n, int B, int bj,
+                                 unsigned long long* __restrict__ cursor, uint64_t* __restrict__ out) {
+  __shared__ unsigned sc[kListBuckets];
+  __shared__ unsigned long long base[kListBuckets];
+  const uint64_t per = (m + gridDim.x - 1) / gridDim.x;  // a contiguous slice per block
+  const uint64_t k0 = blockIdx.x * per, k1 = min(m, k0 + per);
+  for (int b = threadIdx.x; b < B; b += blockDim.x) sc[b] = 0;
+  __syncthreads();
+  for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&sc[bucket_of(pairs[k], n, B)], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    base[b] = sc[b] ? atomicAdd(cursor + b, static_cast<unsigned long long>(sc[b])) : 0ull;
+    sc[b] = 0;
+  }
+  __syncthreads();
+  for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    const uint64_t v = pairs[k];
+    const uint32_t b = bucket_of(v, n, B);
+    const uint64_t i0 = (n * b + B - 1) / B;  // first i of bucket b
+    const unsigned slot = atomicAdd(&sc[b], 1u);
+    out[base[b] + slot] = (((v >> 32) - i0) << bj) | (v & 0xffffffffull);
+  }
+}
+
+// Back from the bucket's packed keys to (i << 32) | j.
+__global__ void k_bucket_unpack(uint64_t* __restrict__ keys, uint64_t m, int bj, uint64_t i0) {
+  const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (k >= m) return;
+  const uint64_t v = keys[k];
+  keys[k] = (((v >> bj) + i0) << 32) | (v & ((1ull << bj) - 1));
+}
+
 int bits_for(uint64_t n) {
   int b = 1;
   while ((1ull << b) < n) ++b;
@@ -936,6 +994,68 @@ void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
   out->stats.inner_loop_exits = 0;
 }
 
+namespace {
+// The sorted list to the host in i-range buckets: one scatter into packed
+// buckets, then per bucket a radix sort on the library stream and its copy on
+// the context's copy stream as soon as it is sorted (the D2H of one bucket
+// overlaps the sort of the next; the copy engine stays busy).
+void sorted_list_to_host(const FrnnRun& run, uint64_t n, uint64_t* host, uint64_t m, cudaStream_t s) {
+  Ctx& c = ctx();
+  const int B = kListBuckets;
+  const int bj = bits_for(n);
+  int bi = 1;
+  while ((1ull << bi) < (n + B - 1) / B + 1) ++bi;
+  DevBuf<unsigned long long> cnt(2 * B, s);
+  PSG_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * B * sizeof(unsigned long long), s));
+  const unsigned g = grid_cap(run.count);
+  k_bucket_count<<<g, 256, 0, s>>>(run.pairs.p, run.count, n, B, cnt.p);
+  PSG_LAUNCHED();
+  unsigned long long hc[kListBuckets];
+  PSG_CUDA(cudaMemcpyAsync(hc, cnt.p, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  unsigned long long off[kListBuckets + 1] = {0}, biggest = 0;
+  for (int b = 0; b < B; ++b) {
+    off[b + 1] = off[b] + hc[b];
+    biggest = std::max(biggest, hc[b]);
+  }
+  PSG_CUDA(cudaMemcpyAsync(cnt.p + B, off, B * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  DevBuf<uint64_t> a(run.count, s), tmp(std::max<uint64_t>(biggest, 1), s);
+  DevBuf<uint32_t> hist(radix_hist_words(std::max<uint64_t>(biggest, 2)), s);
+  k_bucket_scatter<<<g, 256, 0, s>>>(run.pairs.p, run.count, n, B, bj, cnt.p + B, a.p);
+  PSG_LAUNCHED();
+  g_launches += 2;
+  if (!c.copy_stream) PSG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev(B);
+  for (int b = 0; b < B; ++b) ev[b] = c.get_event();
+  const int passes = (bi + bj + 7) / 8;
+  for (int b = 0; b < B; ++b) {  // all sorts first (the copies below may block the host on pageable memory)
+    const uint64_t len = hc[b];
+    uint64_t* kk[2] = {a.p + off[b], tmp.p};
+    uint32_t* vv[2] = {nullptr, nullptr};
+    if (len > 1) {
+      const int which = radix_sort<uint64_t>(kk, vv, len, 0, passes * 8, hist.p, s);
+      if (which == 1) PSG_CUDA(cudaMemcpyAsync(kk[0], kk[1], len * 8, cudaMemcpyDeviceToDevice, s));
+      g_launches += 1 + passes;
+    }
+    if (len) {
+      k_bucket_unpack<<<blocks(len, 256), 256, 0, s>>>(a.p + off[b], len, bj, (n * b + B - 1) / B);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    PSG_CUDA(cudaEventRecord(ev[b], s));
+  }
+  for (int b = 0; b < B && off[b] < m; ++b) {
+    PSG_CUDA(cudaStreamWaitEvent(c.copy_stream, ev[b], 0));
+    const uint64_t len = std::min<uint64_t>(hc[b], m - off[b]);
+    if (len)
+      PSG_CUDA(cudaMemcpyAsync(host + off[b], a.p + off[b], len * 8, cudaMemcpyDeviceToHost, c.copy_stream));
+  }
+  PSG_CUDA(cudaStreamSynchronize(c.copy_stream));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < B; ++b) c.put_event(ev[b]);
+}
+}  // namespace
+
 void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                 uint64_t* pairs, uint64_t capacity, uint64_t* count, uint64_t* hash) {
   FrnnRun run = frnn_run(ps, radius, q, f, seed, zone, pairs && capacity);
@@ -944,10 +1064,23 @@ void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
   *hash = run.hash;
   if (!pairs || capacity == 0 || run.count == 0) return;
   const uint64_t m = std::min(capacity, run.count);
+  static const bool no_buckets = std::getenv("PSG_LIST_CSR") != nullptr;  // A/B: the one-shot CSR + copy
+  if (run.count >= (1u << 22) && ps->n >= 1024 && !no_buckets) {
+    StageTimer tm(s);
+    sorted_list_to_host(run, ps->n, pairs, m, s);
+    tm.mark("sort+d2h");
+    prof_stages(tm);
+    g_prof.d2h_bytes += m * sizeof(uint64_t);
+    return;
+  }
+  StageTimer tm(s);
   DevBuf<uint64_t> sorted;
   sort_pairs(run, ps->n, sorted, s);
+  tm.mark("sort");
   PSG_CUDA(cudaMemcpyAsync(pairs, sorted.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  tm.mark("d2h");
   PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
   g_prof.d2h_bytes += m * sizeof(uint64_t);
 }
 

@@ -9,6 +9,7 @@
 
 #include "psg_grid.cuh"
 #include "psg_points.cuh"
+#include "psg_scan.cuh"
 #include "psg_sort.cuh"
 
 namespace psg {
@@ -34,16 +35,7 @@ __global__ void k_cell_ids(const float* __restrict__ keys, uint32_t n, const Gri
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const GridParams P = *gpp;
-  uint32_t c = 0;
-#pragma unroll
-  for (int t = 0; t < (NK < kMaxGridKeys ? NK : kMaxGridKeys); ++t) {
-    if (t >= P.g) break;
-    const uint32_t dim = P.dims[t];
-    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - P.lo[t]) * P.inv_w;
-    const uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(dim - 1) ? dim - 1 : static_cast<uint32_t>(v));
-    c = c * dim + ct;
-  }
-  cid[i] = c;
+  cid[i] = cell_of<NK>(keys + static_cast<size_t>(i) * NK, P);
   idx[i] = i;
 }
 
@@ -162,57 +154,103 @@ __global__ void k_cell_count(const float* __restrict__ keys, uint32_t n, const G
   }
   if (i >= n) return;
   const GridParams P = *gpp;
-  uint32_t c = 0;
-#pragma unroll
-  for (int t = 0; t < (NK < kMaxGridKeys ? NK : kMaxGridKeys); ++t) {
-    if (t >= P.g) break;
-    const uint32_t dim = P.dims[t];
-    const double v = (static_cast<double>(keys[static_cast<size_t>(i) * NK + t]) - P.lo[t]) * P.inv_w;
-    const uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(dim - 1) ? dim - 1 : static_cast<uint32_t>(v));
-    c = c * dim + ct;
-  }
+  const uint32_t c = cell_of<NK>(keys + static_cast<size_t>(i) * NK, P);
   cid[i] = c;
-  rnk[i] = atomicAdd(cnt + c, 1u);
+  atomicAdd(cnt + c, 1u);  // result unused: a reduction (k_cell_place ranks)
 }
 
 // Arrival-order placement; the counters go back to zero for the next build
 // (every non-zero counter has at least one point here).
-__global__ void k_cell_place(const uint32_t* __restrict__ cid, const uint32_t* __restrict__ rnk, uint32_t n,
-                             const uint32_t* __restrict__ cfirst, uint32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ tmp) {
+// The arrival rank comes from counting the cell back down (atomicSub), which
+// also leaves every counter at zero for the next build; the counting pass
+// then needs no returned value (fire-and-forget reductions).
+__global__ void k_cell_place(const uint32_t* __restrict__ cid, uint32_t n, const uint32_t* __restrict__ cfirst,
+                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ tmp) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t c = cid[i];
-  tmp[cfirst[c] + rnk[i]] = i;
-  cnt[c] = 0;
+  tmp[cfirst[c] + atomicSub(cnt + c, 1u) - 1u] = i;
 }
 
 constexpr uint32_t kFixSmall = 64;  // cells up to this size are ranked per position
+constexpr uint32_t kBootCand = 64;  // BootLB candidates per point (the old bootstrap's cap was 256)
 
 // Final position of the point at arrival position p: its cell's start plus
 // the number of points of the cell with a smaller original index; gathers its
 // keys there.  Cells above kFixSmall points are listed for k_cell_fix_big.
+// With B.keys: the bootstrap's lower bounds too (BootLB, psg_grid.cuh) — the
+// cell's members are in hand for the ranking anyway.
 template <int NK>
 __global__ void k_cell_fix(const float* __restrict__ keys, const uint32_t* __restrict__ tmp,
                            const uint32_t* __restrict__ cid, uint32_t n, const uint32_t* __restrict__ cfirst,
                            float* __restrict__ skeys, uint32_t* __restrict__ sidx, uint32_t* __restrict__ scell,
-                           uint32_t* __restrict__ big, uint32_t* __restrict__ bctr) {
+                           uint32_t* __restrict__ big, uint32_t* __restrict__ bctr,
+                           const GridParams* __restrict__ gpp, BootLB B) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const uint32_t i = tmp[p], c = cid[i], b = cfirst[c], e = cfirst[c + 1];
-  if (e - b > kFixSmall) {
-    if (p == b) big[atomicAdd(bctr, 1u)] = c;
-    return;
-  }
-  uint32_t r = 0;
-  for (uint32_t k = b; k < e; ++k) r += tmp[k] < i;
-  const uint32_t q = b + r;
-  sidx[q] = i;
-  scell[q] = c;
-  const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
-  float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(q) * NK);
+  float best = INFINITY;
+  uint32_t bi = 0, bj = 0;
+  if (p < n) {
+    const uint32_t i = tmp[p], c = cid[i], b = cfirst[c], e = cfirst[c + 1];
+    float ki[NK];
+    if (B.keys) load_keys<NK>(B.keys + static_cast<size_t>(i) * NK, ki);
+    auto consider = [&](uint32_t m) {
+      if (m == i || (B.zone > 1 && !admissible(i, m, B.zone))) return;
+      float km[NK];
+      load_keys<NK>(B.keys + static_cast<size_t>(m) * NK, km);
+      const float lb = lb2_full<NK>(ki, km);
+      if (lb < best) {
+        best = lb;
+        bj = m;
+      }
+    };
+    if (e - b > kFixSmall) {
+      if (p == b) big[atomicAdd(bctr, 1u)] = c;
+    } else {
+      uint32_t r = 0;
+      for (uint32_t k = b; k < e; ++k) r += tmp[k] < i;
+      const uint32_t q = b + r;
+      sidx[q] = i;
+      scell[q] = c;
+      const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
+      float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(q) * NK);
 #pragma unroll
-  for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+      for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+    }
+    if (B.keys) {
+      // candidates: the own cell and the next cell of its row (last key + 1),
+      // arrival positions [b, ne); all of them up to kBootCand, else a
+      // uniform stride across the range from the point's own position (a
+      // cell's arrival order can follow index order, which can correlate
+      // with structure: windows, index-periodic clusters)
+      const uint32_t D = gpp->dims[gpp->g - 1];
+      const uint32_t ne = c % D + 1 < D ? cfirst[c + 2] : e;
+      const uint32_t L = ne - b;
+      if (L <= kBootCand + 1) {
+        for (uint32_t k = b; k < ne; ++k) consider(tmp[k]);
+      } else {
+        const uint32_t stride = L / kBootCand, o = p - b;
+        for (uint32_t t = 1; t <= kBootCand; ++t) consider(tmp[b + (o + t * stride) % L]);
+      }
+    }
+    bi = i;
+  }
+  if (B.keys) {
+    const int lane = threadIdx.x & 31;
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+        bj = oj;
+      }
+    }
+    if (lane == 0) {
+      const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+      B.wlb[w] = best;
+      B.wpair[w] = make_uint2(bi, bj);
+    }
+  }
 }
 
 // Big cells (duplicates, tight clusters): a block per cell.  The cell's
@@ -334,6 +372,8 @@ void GridIndex::ensure(uint32_t n_, int nk_, cudaStream_t s) {
   big.alloc(n / kFixSmall + 1, s);
   sample.alloc(kMaxKeys * kGridSample, s);
   gp.alloc(1, s);
+  wlb.alloc((n + 255) / 256 * 8, s);
+  wpair.alloc((n + 255) / 256 * 8, s);
 }
 
 uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s) {
@@ -368,27 +408,30 @@ void grid_box_host(const float* sample, uint32_t m, int g, double lo[3], double 
 }
 
 void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s, bool counting,
-                uint64_t dense_cells) {
+                uint64_t dense_cells, bool counted, const BootLB* boot) {
   if (counting) {
     const unsigned nb = blocks(n, 256);
-    if (nk == 4)
-      k_cell_count<4><<<nb, 256, 0, s>>>(keys, n, gi.gp.p, gi.cnt.p, gi.cid0.p, gi.idx0.p, gi.bctr.p);
-    else
-      k_cell_count<8><<<nb, 256, 0, s>>>(keys, n, gi.gp.p, gi.cnt.p, gi.cid0.p, gi.idx0.p, gi.bctr.p);
-    PSG_LAUNCHED();
+    if (!counted) {  // else the projection counted (CellCount; bctr reset by k_presample)
+      if (nk == 4)
+        k_cell_count<4><<<nb, 256, 0, s>>>(keys, n, gi.gp.p, gi.cnt.p, gi.cid0.p, gi.idx0.p, gi.bctr.p);
+      else
+        k_cell_count<8><<<nb, 256, 0, s>>>(keys, n, gi.gp.p, gi.cnt.p, gi.cid0.p, gi.idx0.p, gi.bctr.p);
+      PSG_LAUNCHED();
+    }
+    const BootLB B = boot ? *boot : BootLB{};
     // cfirst = exclusive scan of the counts over cells 0..cells (count read on device)
     exclusive_scan_u32_dev(gi.cnt.p, gi.cfirst.p, kMaxCells + 1, &gi.gp.p->cells, gi.ctmp.p, s);
-    k_cell_place<<<nb, 256, 0, s>>>(gi.cid0.p, gi.idx0.p, n, gi.cfirst.p, gi.cnt.p, gi.idx1.p);
+    k_cell_place<<<nb, 256, 0, s>>>(gi.cid0.p, n, gi.cfirst.p, gi.cnt.p, gi.idx1.p);
     PSG_LAUNCHED();
     if (nk == 4) {
       k_cell_fix<4><<<nb, 256, 0, s>>>(keys, gi.idx1.p, gi.cid0.p, n, gi.cfirst.p, gi.skeys.p, gi.sidx.p, gi.cid1.p,
-                                       gi.big.p, gi.bctr.p);
+                                       gi.big.p, gi.bctr.p, gi.gp.p, B);
       PSG_LAUNCHED();
       k_cell_fix_big<4><<<148, kFixBigThreads, 0, s>>>(keys, gi.idx1.p, gi.idx0.p, gi.cfirst.p, gi.skeys.p,
                                                        gi.sidx.p, gi.cid1.p, gi.big.p, gi.bctr.p);
     } else {
       k_cell_fix<8><<<nb, 256, 0, s>>>(keys, gi.idx1.p, gi.cid0.p, n, gi.cfirst.p, gi.skeys.p, gi.sidx.p, gi.cid1.p,
-                                       gi.big.p, gi.bctr.p);
+                                       gi.big.p, gi.bctr.p, gi.gp.p, B);
       PSG_LAUNCHED();
       k_cell_fix_big<8><<<148, kFixBigThreads, 0, s>>>(keys, gi.idx1.p, gi.idx0.p, gi.cfirst.p, gi.skeys.p,
                                                        gi.sidx.p, gi.cid1.p, gi.big.p, gi.bctr.p);

@@ -79,6 +79,57 @@ __host__ __device__ inline void grid_params_for(GridParams& gp, int g, double w,
   gp.f1 = FastDiv::make(gp.dims[1]);
 }
 
+#ifdef __CUDACC__
+// Cell id of a key vector: cell coordinate floor((k_t - lo_t) / w) clamped to
+// the grid, in FP64, row-major over the first g keys.  The ONE formula every
+// builder uses (the projection's fused count, the counting and radix builds).
+template <int NK>
+__device__ __forceinline__ uint32_t cell_of(const float* k, const GridParams& P) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int t = 0; t < (NK < kMaxGridKeys ? NK : kMaxGridKeys); ++t) {
+    if (t >= P.g) break;
+    const uint32_t dim = P.dims[t];
+    const double v = (static_cast<double>(k[t]) - P.lo[t]) * P.inv_w;
+    const uint32_t ct = v <= 0.0 ? 0u : (v >= static_cast<double>(dim - 1) ? dim - 1 : static_cast<uint32_t>(v));
+    c = c * dim + ct;
+  }
+  return c;
+}
+#endif
+
+// The projection's fused counting pass (sparse grids, first build of a
+// solve): the cell of every row and its arrival rank in the cell, exactly as
+// k_cell_count would produce them (psg_grid.cu), so build_grid skips that
+// kernel and its re-read of the keys.
+struct CellCount {
+  const GridParams* gp = nullptr;  // nullptr: no counting
+  uint32_t* cnt = nullptr;
+  uint32_t* cid = nullptr;
+};
+
+// The bootstrap folded into the counting build's per-position fix-up: every
+// point's least key lower bound over the later points of its own cell and the
+// next cell of its row (the sparse scan's own-row range), warp-reduced to one
+// (lb, i, j) per warp of arrival positions; k_boot_select (psg_cpp.cu) then
+// evaluates the best of them exactly.
+struct BootLB {
+  const float* keys = nullptr;  // original order, nk per row; nullptr: off
+  float* wlb = nullptr;         // per warp: least lower bound (+inf: none)
+  uint2* wpair = nullptr;       //           its (i, j), original indices
+  uint64_t zone = 0;
+};
+
+#ifdef __CUDACC__
+// The fused count of one row (CellCount): the k_cell_count step.
+template <int NK>
+__device__ __forceinline__ void count_cell(const float* k, uint32_t row, const CellCount& cc) {
+  const uint32_t c = cell_of<NK>(k, *cc.gp);
+  cc.cid[row] = c;
+  atomicAdd(cc.cnt + c, 1u);  // result unused: a fire-and-forget reduction
+}
+#endif
+
 struct GridDev {  // POD view passed to kernels
   const float* skeys = nullptr;   // n x nk keys, sorted by cell
   const uint32_t* sidx = nullptr; // sorted position -> original index
@@ -101,6 +152,8 @@ struct GridIndex {
   DevBuf<uint32_t> cnt, ctmp, big, bctr;
   DevBuf<float> sample;
   DevBuf<GridParams> gp;
+  DevBuf<float> wlb;   // BootLB outputs (one per warp of positions)
+  DevBuf<uint2> wpair;
   GridDev dev;
   void ensure(uint32_t n_, int nk_, cudaStream_t s);
 };
@@ -115,7 +168,7 @@ struct GridIndex {
 // dense_cells (counting = false): the grid's cell count when the host knows
 // it; above kMaxCells the table goes to gi.dcfirst and the sort covers its bits.
 void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_bits, cudaStream_t s,
-                bool counting = true, uint64_t dense_cells = 0);
+                bool counting = true, uint64_t dense_cells = 0, bool counted = false, const BootLB* boot = nullptr);
 // Strided sample of the first g keys into gi.sample (g x m floats); returns m.
 uint32_t grid_sample(const float* keys, uint32_t n, int nk, int g, GridIndex& gi, cudaStream_t s);
 // Host-side box from a host copy of the sample (mean +- 3 sd, clipped).

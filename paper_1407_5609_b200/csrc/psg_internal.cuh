@@ -72,6 +72,7 @@ struct Ctx {
   static constexpr size_t kStageBytes = size_t(32) << 20;
   char* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_done[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;  // D2H overlapped with work on `stream` (created on first use)
 };
 Ctx& ctx();  // context of the current CUDA device (created on first use)
 

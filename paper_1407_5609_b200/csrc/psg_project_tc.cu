@@ -73,7 +73,7 @@ struct UTc {
 template <int NK, int D>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_project_tc(const __grid_constant__ CUtensorMap xmap, uint32_t n, const __grid_constant__ UTc<D> U,
-                 float* __restrict__ keys, unsigned* __restrict__ norm2_bits, unsigned set_norm2_bits) {
+                 float* __restrict__ keys, unsigned* __restrict__ norm2_bits, unsigned set_norm2_bits, CellCount cc) {
   constexpr int NC = D / kTcKChunk;  // K chunks (stages) per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared pointer
@@ -233,6 +233,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if constexpr (NK == 8)
           out[1] =
               make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+        if (cc.gp) {  // the counting build's first step, on keys still in registers
+          float k[NK];
+#pragma unroll
+          for (int q = 0; q < NK; ++q) k[q] = __uint_as_float(r[q]);
+          count_cell<NK>(k, row, cc);
+        }
       }
     }
   }
@@ -256,7 +262,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <int NK, int D>
-void launch(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* nb, cudaStream_t s) {
+void launch(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* nb, cudaStream_t s,
+            const CellCount& cc) {
   const uint32_t n = static_cast<uint32_t>(ps.n);
   if (n == 0) return;
   CUtensorMap map;
@@ -282,22 +289,23 @@ void launch(const psg_pointset& ps, const Directions& dir, float* keys, unsigned
   std::memcpy(&nbits, &ps.norm2max, 4);
   const uint32_t ntiles = (n + kTcM - 1) / kTcM;
   const int grid = static_cast<int>(std::min<uint32_t>(ntiles, static_cast<uint32_t>(ctx().sm_count)));
-  k_project_tc<NK, D><<<grid, kTcThreads, kSmem, s>>>(map, n, u, keys, nb, nbits);
+  k_project_tc<NK, D><<<grid, kTcThreads, kSmem, s>>>(map, n, u, keys, nb, nbits, cc);
   PSG_LAUNCHED();
 }
 
 }  // namespace
 
-void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s) {
+void project_tc(const psg_pointset& ps, const Directions& dir, float* keys, unsigned* norm2_bits, cudaStream_t s,
+                const CellCount& cc) {
   switch (dir.nk * 1000 + ps.d) {
-    case 4032: launch<4, 32>(ps, dir, keys, norm2_bits, s); break;
-    case 4064: launch<4, 64>(ps, dir, keys, norm2_bits, s); break;
-    case 4128: launch<4, 128>(ps, dir, keys, norm2_bits, s); break;
-    case 4256: launch<4, 256>(ps, dir, keys, norm2_bits, s); break;
-    case 8032: launch<8, 32>(ps, dir, keys, norm2_bits, s); break;
-    case 8064: launch<8, 64>(ps, dir, keys, norm2_bits, s); break;
-    case 8128: launch<8, 128>(ps, dir, keys, norm2_bits, s); break;
-    case 8256: launch<8, 256>(ps, dir, keys, norm2_bits, s); break;
+    case 4032: launch<4, 32>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 4064: launch<4, 64>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 4128: launch<4, 128>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 4256: launch<4, 256>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 8032: launch<8, 32>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 8064: launch<8, 64>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 8128: launch<8, 128>(ps, dir, keys, norm2_bits, s, cc); break;
+    case 8256: launch<8, 256>(ps, dir, keys, norm2_bits, s, cc); break;
     default: throw std::logic_error("project_tc: unsupported shape");
   }
 }

@@ -277,6 +277,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const uint32_t* 
   __shared__ uint32_t ws[33];
   __shared__ uint32_t tile_s, prefix_s;
   count = scan_count(count, dcells);
+  // persistent: a block keeps claiming tiles (in ticket order, so every tile
+  // it waits on is held by a block that is running) until the count is covered
+  for (;;) {
+  __syncthreads();  // the previous tile's shared state is consumed
   if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint32_t tile = tile_s;
@@ -338,6 +342,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const uint32_t* 
     for (int i = 0; i < kScanItems; ++i)
       if (base + i < count) out[base + i] = o[i];
   }
+  }
 }
 
 }  // namespace
@@ -358,8 +363,9 @@ void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count,
   const size_t words = scan_temp_words(max_count);
   PSG_CUDA(cudaMemsetAsync(temp, 0, words * sizeof(uint32_t), s));
   auto* status = reinterpret_cast<unsigned long long*>(temp);
-  k_scan_lookback<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, max_count, dcells, status,
-                                                                     temp + 2 * (nb + 1), out);
+  // two 1024-thread blocks per SM stay resident; they loop over the tiles
+  const unsigned grid = static_cast<unsigned>(std::min<size_t>(nb, static_cast<size_t>(ctx().sm_count) * 2));
+  k_scan_lookback<<<grid, kScanThreads, 0, s>>>(in, max_count, dcells, status, temp + 2 * (nb + 1), out);
   PSG_LAUNCHED();
 }
 
