@@ -1635,6 +1635,10 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   if (ps->X && !(d < 32 || d == 32 || d == 64 || d == 128 || d == 256)) return false;  // projection needs a host buffer
   std::shared_ptr<CppWork> work = get_work(ps, dir.nk, s);
   CppWork& W = *work;
+  // a point set's first solve runs uncaptured (it also learns the width and
+  // the engine): a graph pays off only once the set is solved again (the
+  // one-shot entries build a fresh set per call)
+  if (W.solves++ == 0) return false;
   if (W.learned_dense && W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone) return false;
   // every allocation happens before capture (and drops a graph that holds
   // buffers it replaces)

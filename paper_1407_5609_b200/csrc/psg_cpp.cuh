@@ -80,6 +80,7 @@ struct CppWork {
   uint64_t gq = 0, gseed = 0, gzone = 0;
   uint32_t gcap = 0;  // cand_cap at capture
   uint64_t glaunches = 0;
+  uint64_t solves = 0;  // closest-pair solves on this point set (the first one is not captured)
   // cell width a regrid converged to, for the same (q, seed, zone)
   double learned_w = 0.0;
   uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) k_cell_pairs_list(const uint32_t* __restr
                                                          const Thresholds* __restrict__ th, uint32_t* __restrict__ pa,
                                                          uint32_t* __restrict__ pb, uint32_t* __restrict__ pt,
                                                          uint32_t cap, unsigned long long* __restrict__ count,
-                                                         bool strips) {
+                                                         bool strips, int mode) {
   __shared__ GridParams sP;
   if (threadIdx.x == 0) sP = *gpp;
   __syncthreads();
@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(256) k_cell_pairs_list(const uint32_t* __restr
       const int s = s0 + lane;
       bool keep = false;
       uint32_t B = A, nb = 0;
-      if (s <= fc && (s == 0 || cell_forward(sP, cc, s, &B))) {
+      // mode 1: own cells only; mode 2: every stencil cell but the own one
+      const bool in_mode = mode == 0 || (mode == 1 ? s == 0 : s > 0);
+      if (in_mode && s <= fc && (s == 0 || cell_forward(sP, cc, s, &B))) {
         nb = cfirst[B + 1] - cfirst[B];
         keep = nb != 0 && !(s == 0 && na < 2);
         if (keep && s > 0) {
@@ -791,6 +793,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     unsigned band_bits = 0xffffffffu;
     float band_c = 0.f;
     unsigned next_best = lane == 0 ? ld_relaxed_u32(a.best) : 0u;
+    float known = INFINITY;  // a bound at least as large as the global one (read every 16th tile)
     for (;;) {
       const uint32_t bb = bcount % kGBB, acc = tcount & 1, tph = (tcount >> 1) & 1;
       mbar_wait(&sm.tfull[acc], tph);
@@ -802,6 +805,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       // the next read is issued now and lands while tiles are filtered
       {
         const unsigned cur = __shfl_sync(kFull, next_best, 0);
+        known = fminf(known, __uint_as_float(cur));
         // (re-read every 16th tile: the read itself waits behind every SM's atomicMin traffic)
         if (lane == 0 && (tcount & 15) == 0) next_best = ld_relaxed_u32(a.best);
         // hysteresis: a band up to ~3 % wider than the current bound's is
@@ -878,7 +882,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
       ub = __fmul_ru(fmaxf(ub, 0.f), 1.0f + 0x1.0p-16f);
 #pragma unroll
       for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(kFull, ub, o));
-      if (lane == 0 && ub < INFINITY && !a.no_ub) atomicMin(a.best, __float_as_uint(ub));
+      // only a value below the last bound read can lower the global one: the
+      // other tiles' atomics (one per warp per tile, all on one word) were the
+      // epilogue's main cost
+      if (lane == 0 && ub < known && !a.no_ub) {
+        atomicMin(a.best, __float_as_uint(ub));
+        known = ub;
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -1006,8 +1016,18 @@ uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s)
   return h;
 }
 
+uint64_t dense_pass(const ScanArgs& a, const GridIndex& gi, uint64_t cells, int d, int nk, Thresholds* th,
+                    DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s, bool gram, unsigned lb, uint32_t ne,
+                    int mode);
+
+// The starting thresholds from the bound reached so far (between the two
+// passes of a single-part Gram solve).
+__global__ void k_refresh_th(const Budget* bud, const unsigned* best, Thresholds* th) {
+  *th = budget_thresholds_s32(*bud, __uint_as_float(*best));
+}
+
 uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, const Rows& X, uint32_t n, int d,
-                    int nk, const Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s) {
+                    int nk, Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s) {
   const int sms = ctx().sm_count;
   // tensor-core Gram tiles for d in {32, 64}; CUDA-core canonical tiles otherwise
   static const bool no_gram = std::getenv("PSG_NO_GRAM") != nullptr;
@@ -1036,6 +1056,31 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
   g_launches += 3;
   if (w.pair_cap == 0) w.pair_cap = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(cells * 14, 1024),
                                                                              1u << 26));
+  // Single-part Gram solves run in two passes: the own-cell tiles first (where
+  // a clustered set's closest pairs usually are), whose tile upper bounds
+  // tighten the bound; then every other kept cell pair, chosen under that
+  // tighter bound.  Sharded solves keep one pass: every rank must enumerate
+  // the same work list, so the list is chosen under the shared bound only.
+  static const bool one_pass = std::getenv("PSG_DENSE_ONE_PASS") != nullptr;
+  const bool two = gram && nparts == 1 && !one_pass;
+  uint64_t kept = 0;
+  for (int pass = two ? 1 : 0; pass <= (two ? 2 : 0); ++pass) {
+    if (pass == 2) {
+      k_refresh_th<<<1, 1, 0, s>>>(a.bud, a.best, th);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    kept += dense_pass(a, gi, cells, d, nk, th, w, part, nparts, s, gram, lb, ne, pass);
+  }
+  return kept;
+}
+
+// One pass of dense_scan over the kept cell pairs of `mode` (0 all, 1 own
+// cells, 2 all but own): list, sort by A, groups / tile prefix, launch.
+uint64_t dense_pass(const ScanArgs& a, const GridIndex& gi, uint64_t cells, int d, int nk, Thresholds* th,
+                    DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s, bool gram, unsigned lb, uint32_t ne,
+                    int mode) {
+  const int sms = ctx().sm_count;
   unsigned long long npairs = 0;
   for (;;) {
     if (w.pa.n < w.pair_cap) {
@@ -1049,10 +1094,10 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     PSG_CUDA(cudaMemsetAsync(w.ctr.p + 5, 0, 8, s));
     if (nk == 4)
       k_cell_pairs_list<4><<<lb, 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, w.clist.p, ne, w.cbox.p, th, w.pa.p, w.pb.p,
-                                             w.ptiles.p, w.pair_cap, w.ctr.p, gram);
+                                             w.ptiles.p, w.pair_cap, w.ctr.p, gram, mode);
     else
       k_cell_pairs_list<8><<<lb, 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, w.clist.p, ne, w.cbox.p, th, w.pa.p, w.pb.p,
-                                             w.ptiles.p, w.pair_cap, w.ctr.p, gram);
+                                             w.ptiles.p, w.pair_cap, w.ctr.p, gram, mode);
     PSG_LAUNCHED();
     ++g_launches;
     PSG_CUDA(cudaMemcpyAsync(&npairs, w.ctr.p, 8, cudaMemcpyDeviceToHost, s));
@@ -1061,7 +1106,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     w.pair_cap = static_cast<uint32_t>(npairs);
   }
   g_prof.dense_cells = cells;
-  g_prof.dense_cell_pairs = npairs;
+  g_prof.dense_cell_pairs += npairs;
   if (npairs == 0) return 0;
   const uint32_t np32 = static_cast<uint32_t>(npairs);
   // Deterministic work order: every rank of a sharded solve enumerates the
@@ -1112,9 +1157,9 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
     unsigned long long t[6] = {};
     PSG_CUDA(cudaMemcpyAsync(t, w.ctr.p, 48, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    g_prof.dense_groups = ng;
-    g_prof.dense_split_groups = t[5];
-    g_prof.dense_tiles = t[2];
+    g_prof.dense_groups += ng;
+    g_prof.dense_split_groups += t[5];
+    g_prof.dense_tiles += t[2];
     if (std::getenv("PSG_TRACE"))
       std::fprintf(stderr, "[psg] gram: %llu kept cell pairs, %u groups (%llu split), %llu tiles\n",
                    static_cast<unsigned long long>(npairs), ng, t[5], t[2]);

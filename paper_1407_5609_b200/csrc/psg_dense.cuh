@@ -31,6 +31,6 @@ uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s)
 // in the sparse scan.  Tiles are split round-robin over `nparts` parts.
 // Returns the number of cell pairs kept.  Synchronises.
 uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, const Rows& X, uint32_t n, int d,
-                    int nk, const Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s);
+                    int nk, Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s);
 
 }  // namespace psg

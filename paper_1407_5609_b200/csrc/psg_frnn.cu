@@ -1069,6 +1069,7 @@ void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
     StageTimer tm(s);
     sorted_list_to_host(run, ps->n, pairs, m, s);
     tm.mark("sort+d2h");
+    PSG_CUDA(cudaStreamSynchronize(s));
     prof_stages(tm);
     g_prof.d2h_bytes += m * sizeof(uint64_t);
     return;

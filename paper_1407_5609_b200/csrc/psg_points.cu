@@ -277,9 +277,16 @@ __global__ void k_window_check(Rows R, ExactSrc src, uint64_t nw, double scale,
   for (uint64_t r = warp; r < nw; r += nwarps) {
     double acc = 0.0;
     float nn = 0.f;
+    // z-normalised: the reference's (s - mu) / sigma as (s - mu) * (1 / sigma),
+    // within 2^-51 |x| of it (one FP64 division per window instead of one per
+    // value; the host adds len * 2^-50 to Rn for it)
+    const bool z = src.kind == kWindowsZ;
+    const double mu = z ? src.mu[r] : 0.0, sg = z ? src.sigma[r] : 1.0;
+    const double inv = sg == 0.0 ? 0.0 : 1.0 / sg;
     for (int t = lane; t < R.d; t += 32) {
       const float x = row_at(R, r, t);
-      const double e = exact_coord(src, r, t) * scale - static_cast<double>(x);
+      const double xe = z ? (src.f64[r + t] - mu) * inv : exact_coord(src, r, t);
+      const double e = xe * scale - static_cast<double>(x);
       acc = fma(e, e, acc);
       nn = fmaf(x, x, nn);
     }
@@ -503,7 +510,7 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
                                                                      mx.p + 1, nb.p);
   PSG_LAUNCHED();
   g_launches += 2;
-  ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d);
+  ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d) + (znorm ? static_cast<double>(len) * 0x1.0p-50 : 0.0);
   unsigned hn = 0;
   PSG_CUDA(cudaMemcpy(&hn, nb.p, 4, cudaMemcpyDeviceToHost));
   std::memcpy(&ps->norm2max, &hn, 4);
