@@ -437,6 +437,19 @@ struct GramSmem {
   uint32_t tmem;
 };
 
+#ifdef PSG_GRAM_TIMELINE
+// Diagnostic build only: per-role clock64 stamps of CTA 0's first tiles.
+//   0 loader: B buffer acquired     7 loader: B tile published (bfull)
+//   1 MMA: B tile ready             2 MMA: accumulator free (tempty)
+//   3 MMA: MMAs + commit issued     4 epilogue: accumulator full (tfull)
+//   5 epilogue: tile released
+constexpr int kTlTiles = 96;
+__device__ long long g_tl[kTlTiles][8];
+__device__ __forceinline__ void tl_mark(int ev, uint32_t tile) {
+  if (blockIdx.x == 0 && tile < kTlTiles) g_tl[tile][ev] = clock64();
+}
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(kGThreads, 1)
     k_dense_gram(ScanArgs a, const float* __restrict__ Xs, const uint32_t* __restrict__ cfirst,
@@ -558,6 +571,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         constexpr int kLpr = D / 4, kRpi = 32 / kLpr, kNi = 32 / kRpi;
         const int sub = lane % kLpr, rsel = lane / kLpr;
         const float4 mu4 = *reinterpret_cast<const float4*>(mu + 4 * sub);
+        const unsigned long long mu_a = pk2(mu4.x, mu4.y), mu_b = pk2(mu4.z, mu4.w);
         // lane l resolves the grid position of tile row 32 w + l; tile tj+1's
         // positions are resolved while tile tj's loads are in flight
         auto resolve = [&](uint32_t tj, uint32_t& pos, bool& mine) -> bool {
@@ -600,41 +614,61 @@ __global__ void __launch_bounds__(kGThreads, 1)
         auto split_half = [&](const float4 (&v)[kNh], int h, unsigned vmask, uint32_t bb, float& wm) {
           float* hi_tile = sm.B[bb][0];
           float* lo_tile = sm.B[bb][1];
+          static_assert(kNh * 2 == kLpr, "one butterfly level per halving of the row slots");
+          float part[kNh];  // this lane's partial norm of each row slot
 #pragma unroll
           for (int i = 0; i < kNh; ++i) {
             const int src = (h * kNh + i) * kRpi + rsel;
             const int rr = 32 * warp + src;
-            float4 x = v[i];
+            // shift, norm and the lo part in packed pairs (FADD2 / FMUL2 /
+            // FFMA2, exact per lane like the scalar ops; the norm's summation
+            // order is any FP32 order, which gram_slack charges)
+            unsigned long long xa = 0ull, xb = 0ull;
             if ((vmask >> src) & 1u) {
-              x.x -= mu4.x;
-              x.y -= mu4.y;
-              x.z -= mu4.z;
-              x.w -= mu4.w;
-            } else {
-              x = make_float4(0.f, 0.f, 0.f, 0.f);
+              xa = sub2(pk2(v[i].x, v[i].y), mu_a);
+              xb = sub2(pk2(v[i].z, v[i].w), mu_b);
             }
-            float nrm = x.x * x.x;
-            nrm = fmaf(x.y, x.y, nrm);
-            nrm = fmaf(x.z, x.z, nrm);
-            nrm = fmaf(x.w, x.w, nrm);
-#pragma unroll
-            for (int o = kLpr / 2; o; o >>= 1) nrm += __shfl_xor_sync(kFull, nrm, o);
+            const float2 n2 = up2(fma2(xb, xb, mul2(xa, xa)));
+            part[i] = n2.x + n2.y;
+            const float2 xlo = up2(xa), xhi = up2(xb);
+            const float4 x = make_float4(xlo.x, xlo.y, xhi.x, xhi.y);
             const float4 hh = make_float4(__uint_as_float(__float_as_uint(x.x) & ~0x1fffu),
                                           __uint_as_float(__float_as_uint(x.y) & ~0x1fffu),
                                           __uint_as_float(__float_as_uint(x.z) & ~0x1fffu),
                                           __uint_as_float(__float_as_uint(x.w) & ~0x1fffu));
-            const float4 l = make_float4(x.x - hh.x, x.y - hh.y, x.z - hh.z, x.w - hh.w);  // exact
+            const float2 la = up2(sub2(xa, pk2(hh.x, hh.y))), lb = up2(sub2(xb, pk2(hh.z, hh.w)));  // exact
+            const float4 l = make_float4(la.x, la.y, lb.x, lb.y);
             const int c = sub >> 3, u = sub & 7;  // 32-float chunk, 16 B unit inside the 128 B row
             const int off = c * (kGN * 32) + rr * 32 + ((u ^ (rr & 7)) << 2);
             *reinterpret_cast<float4*>(hi_tile + off) = hh;
             *reinterpret_cast<float4*>(lo_tile + off) = l;
-            if (sub == 0) {
-              const bool ok = (vmask >> src) & 1u;
-              sm.nb[bb][rr] = nrm;
-              sm.cnb[bb][rr] = ok ? (1.f - 2.f * gram_slack<D>()) * nrm : INFINITY;
-            }
-            wm = fmaxf(wm, nrm);
           }
+          // the kNh row norms over the row's kLpr lanes by a transposing
+          // butterfly: each level sends half of the remaining slots to the
+          // partner lane and adds what comes back (kNh + ... + 1 shuffles
+          // instead of kNh log2(kLpr)); lane pair (slot, slot') ends with row
+          // slot idx's total
+          int idx = 0;
+#pragma unroll
+          for (int m = kLpr / 2, cnt = kNh; m >= 2; m >>= 1, cnt >>= 1) {
+            const bool up = (sub & m) != 0;
+#pragma unroll
+            for (int k = 0; k < cnt / 2; ++k) {
+              const float send = up ? part[k] : part[k + cnt / 2];
+              const float keep = up ? part[k + cnt / 2] : part[k];
+              part[k] = keep + __shfl_xor_sync(kFull, send, m);
+            }
+            idx += up ? m / 2 : 0;
+          }
+          const float nrm = part[0] + __shfl_xor_sync(kFull, part[0], 1);
+          if ((sub & 1) == 0) {
+            const int src = (h * kNh + idx) * kRpi + rsel;
+            const int rr = 32 * warp + src;
+            const bool ok = (vmask >> src) & 1u;
+            sm.nb[bb][rr] = nrm;
+            sm.cnb[bb][rr] = ok ? (1.f - 2.f * gram_slack<D>()) * nrm : INFINITY;
+          }
+          wm = fmaxf(wm, nrm);
         };
         uint32_t pos = 0;
         bool mine = false;
@@ -650,6 +684,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
           load_half(vn, pos, 1);  // this tile's second half
           if (tj + 1 < tb) valid = resolve(tj + 1, pos, mine);  // the next tile's rows
           mbar_wait(&sm.bfree[bb], bph ^ 1);
+#ifdef PSG_GRAM_TIMELINE
+          if (warp == 0 && lane == 0) tl_mark(0, bcount - 1);
+#endif
           float wm = 0.f;
           split_half(vc, 0, vmask, bb, wm);
           if (tj + 1 < tb) load_half(vc, pos, 0);  // the next tile's first half
@@ -658,10 +695,16 @@ __global__ void __launch_bounds__(kGThreads, 1)
           sm.jpos[bb][r] = jpos_c;
           wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(wm)));  // norms >= 0
           if (lane == 0) sm.wmaxnb[bb][warp] = wm;
-          if (r == 0) sm.meta[bb] = GramMeta{a0, alen, 0u, blen, ab, npar, tj * kGN < own_len, tj + 1 == tb, 0u};
+          // only the strip's first B tile can hold pairs with j <= i (own-cell
+          // rows start at the strip's first row, so tile tj >= 1 has every B
+          // row past every A row): the other tiles take the epilogue's fast path
+          if (r == 0) sm.meta[bb] = GramMeta{a0, alen, 0u, blen, ab, npar, tj == 0 && own_len > 0, tj + 1 == tb, 0u};
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.bfull[bb]);
+#ifdef PSG_GRAM_TIMELINE
+          if (warp == 0 && lane == 0) tl_mark(7, bcount - 1);
+#endif
         }
       }
       __syncwarp();
@@ -746,8 +789,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
     for (;;) {
       const uint32_t bb = bcount % kGBB, bph = (bcount / kGBB) & 1;
       mbar_wait(&sm.bfull[bb], bph);
+#ifdef PSG_GRAM_TIMELINE
+      if (lane == 0) tl_mark(1, tcount);
+#endif
       const uint32_t acc = tcount & 1, tph = (tcount >> 1) & 1;
       mbar_wait(&sm.tempty[acc], tph ^ 1);
+#ifdef PSG_GRAM_TIMELINE
+      if (lane == 0) tl_mark(2, tcount);
+#endif
       const GramMeta m = sm.meta[bb];  // published before the barrier arrive
       if (m.done) {
         if (lane == 0) {
@@ -773,6 +822,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
           umma_tf32_ts_3x_chunk32(dcol, ah, al, bh, bl, idesc, c != 0);
         }
         umma_commit(&sm.tfull[acc]);
+#ifdef PSG_GRAM_TIMELINE
+        tl_mark(3, tcount);
+#endif
         if (m.last) umma_commit(&sm.afree[m.abuf]);  // the strip's A tile is free once these MMAs have read it
       }
       __syncwarp();
@@ -797,6 +849,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
     for (;;) {
       const uint32_t bb = bcount % kGBB, acc = tcount & 1, tph = (tcount >> 1) & 1;
       mbar_wait(&sm.tfull[acc], tph);
+#ifdef PSG_GRAM_TIMELINE
+      if (lane == 0 && warp == 8) tl_mark(4, tcount);
+#endif
       tc_fence_after();
       const GramMeta m = sm.meta[bb];
       if (m.done) break;
@@ -837,19 +892,25 @@ __global__ void __launch_bounds__(kGThreads, 1)
         const uint32_t c0 = half * (kGN / 2) + q * 32;
         const uint32_t (&v)[32] = vv[q];
         if (!vr || c0 >= m.blen) continue;
-        bool hit = false;
+        if (!general) {
+          // fast path: x = -2 g + cnb in packed pairs (FFMA2, the scalar fmaf's
+          // rounding per lane) and a 3-input running min; the chunk hits iff
+          // its min is <= R.  Every column is a valid pair here.
+          const unsigned long long m2 = pk2(-2.f, -2.f);
+          float vc = INFINITY;
 #pragma unroll
-        for (int jj = 0; jj < 32; jj += 4) {
-          const float4 cn = *reinterpret_cast<const float4*>(&sm.cnb[bb][c0 + jj]);
-          const float x0 = fmaf(-2.f, __uint_as_float(v[jj]), cn.x);
-          const float x1 = fmaf(-2.f, __uint_as_float(v[jj + 1]), cn.y);
-          const float x2 = fmaf(-2.f, __uint_as_float(v[jj + 2]), cn.z);
-          const float x3 = fmaf(-2.f, __uint_as_float(v[jj + 3]), cn.w);
-          hit |= (x0 <= R) | (x1 <= R) | (x2 <= R) | (x3 <= R);
-          if (!general) vmin = fminf(vmin, fminf(fminf(x0, x1), fminf(x2, x3)));  // every column is a valid pair
+          for (int jj = 0; jj < 32; jj += 4) {
+            const float4 cn = *reinterpret_cast<const float4*>(&sm.cnb[bb][c0 + jj]);
+            const float2 x01 = up2(fma2(pk2(__uint_as_float(v[jj]), __uint_as_float(v[jj + 1])), m2, pk2(cn.x, cn.y)));
+            const float2 x23 =
+                up2(fma2(pk2(__uint_as_float(v[jj + 2]), __uint_as_float(v[jj + 3])), m2, pk2(cn.z, cn.w)));
+            vc = fmin3(vc, x01.x, x01.y);
+            vc = fmin3(vc, x23.x, x23.y);
+          }
+          vmin = fminf(vmin, vc);
+          visited += min(32u, m.blen - c0);
+          if (!(vc <= R)) continue;
         }
-        if (!general) visited += min(32u, m.blen - c0);
-        if (!(hit || general)) continue;
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {  // slow path: every check, the exact slack test
           const uint32_t jl = c0 + jj;
@@ -893,6 +954,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&sm.tempty[acc]);
+#ifdef PSG_GRAM_TIMELINE
+        if (warp == 8) tl_mark(5, tcount);
+#endif
         mbar_arrive(&sm.bfree[bb]);
       }
       ++bcount;
@@ -913,6 +977,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
     tc_fence_after();
     tmem_free(tmem, kGTmemCols);
   }
+#ifdef PSG_GRAM_TIMELINE
+  if (blockIdx.x == 0 && tid == 0) {
+    const long long t0 = g_tl[0][0];
+    for (int t = 0; t < kTlTiles; ++t)
+      printf("TL %d %lld %lld %lld %lld %lld %lld %lld\n", t, g_tl[t][0] - t0, g_tl[t][7] - t0, g_tl[t][1] - t0,
+             g_tl[t][2] - t0, g_tl[t][3] - t0, g_tl[t][4] - t0, g_tl[t][5] - t0);
+  }
+#endif
 }
 
 template <int D>
