@@ -42,6 +42,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+CDEV = None  # collectives' tensor device override (PSG_BENCH_GLOO test mode)
 METRIC = "closest-pair solve time & candidate dist-evals/s at n=2^20,d=128 vs roofline"
 UNIT = "pairs/s"
 N_C2, D_C2, Q, F, SEED = 1 << 20, 128, 10, 10.0, 1
@@ -393,7 +394,7 @@ def c5_scaling(psg, L, rank, world, local_rank, coll, barrier):
     e1.record(stream)
     barrier()
     wall = time.perf_counter() - t0
-    t = torch.tensor([wall, e0.elapsed_time(e1) / 1e3], device=f"cuda:{local_rank}", dtype=torch.float64)
+    t = torch.tensor([wall, e0.elapsed_time(e1) / 1e3], device=CDEV or f"cuda:{local_rank}", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ps.release()
     return {"workload": "C5 CPP n=2^24 d=64 mixture, key-range parts (replicated points)", "n_gpus": world,
@@ -426,7 +427,7 @@ def run_ours(args, rank, world, local_rank):
     planted = tuple(sorted((pi.value, pj.value)))
     stream = torch.cuda.ExternalStream(L.psg_stream())
     adm = sharded.admissible_pairs(n, 0)
-    coll = sharded.TorchCollectives(device=f"cuda:{local_rank}") if world > 1 else None
+    coll = sharded.TorchCollectives(device=CDEV or f"cuda:{local_rank}") if world > 1 else None
 
     def barrier():
         if dist is not None:
@@ -487,7 +488,7 @@ def run_ours(args, rank, world, local_rank):
                 agg["stages"][k] = agg["stages"].get(k, 0.0) + v
     t_ms = ev0.elapsed_time(ev1)
     if dist is not None:
-        t = torch.tensor([t_ms], device=f"cuda:{local_rank}")
+        t = torch.tensor([t_ms], device=CDEV or f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
     ok = all((r.index_i, r.index_j) == planted for r in results)
@@ -515,7 +516,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e_ms = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([e_ms], device=f"cuda:{local_rank}")
+        t = torch.tensor([e_ms], device=CDEV or f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
     e2e_value = e2e_steps * adm / (e_ms / 1000.0)
@@ -648,8 +649,17 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        global CDEV
+        if os.environ.get("PSG_BENCH_GLOO") == "1":
+            # test mode: every rank on the one visible GPU, host collectives
+            # (the ranks never wait on each other inside a kernel)
+            CDEV = "cpu"
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     try:
         return run_ours(args, rank, world, local)
     finally:

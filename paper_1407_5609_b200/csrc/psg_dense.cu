@@ -84,12 +84,18 @@ __device__ __forceinline__ bool cell_forward(const GridParams& P, const int (&cc
 
 __device__ __forceinline__ int forward_count(int g) { return (pow3(g) - 1) / 2; }
 
+// Estimate of the stencil pairs the sparse scan would visit (the dense /
+// sparse decision, a heuristic against 512 n): every kEstStride-th cell,
+// scaled back up; GridParams once per block in shared memory.
+constexpr uint32_t kEstStride = 8;
 __global__ void k_estimate(const uint32_t* __restrict__ cfirst, const GridParams* __restrict__ gpp, uint64_t cells,
                            unsigned long long* __restrict__ est) {
-  const GridParams P = *gpp;
+  __shared__ GridParams P;
+  if (threadIdx.x == 0) P = *gpp;
+  __syncthreads();
   unsigned long long total = 0;
-  for (uint64_t A = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; A < cells;
-       A += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  for (uint64_t A = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kEstStride; A < cells;
+       A += static_cast<uint64_t>(gridDim.x) * blockDim.x * kEstStride) {
     const unsigned long long na = cfirst[A + 1] - cfirst[A];
     if (na == 0) continue;
     total += na * (na - 1) / 2;
@@ -101,7 +107,7 @@ __global__ void k_estimate(const uint32_t* __restrict__ cfirst, const GridParams
     }
   }
   for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
-  if ((threadIdx.x & 31) == 0 && total) atomicAdd(est, total);
+  if ((threadIdx.x & 31) == 0 && total) atomicAdd(est, total * kEstStride);
 }
 
 // Rows in grid order (materialised here also for window sets: the tiles
@@ -1079,7 +1085,8 @@ bool gram_shape(int d) { return d == 32 || d == 64; }
 uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s) {
   DevBuf<unsigned long long> est(1, s);
   PSG_CUDA(cudaMemsetAsync(est.p, 0, 8, s));
-  k_estimate<<<std::min<unsigned>(blocks(cells, 256), 4096), 256, 0, s>>>(gi.dev.cfirst, gi.gp.p, cells, est.p);
+  k_estimate<<<std::min<unsigned>(blocks((cells + kEstStride - 1) / kEstStride, 256), 4096), 256, 0, s>>>(
+      gi.dev.cfirst, gi.gp.p, cells, est.p);
   PSG_LAUNCHED();
   ++g_launches;
   unsigned long long h = 0;
