@@ -315,7 +315,7 @@ int psg_cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, u
                         psg_cpp_plan** out) {
   return guarded([&] {
     auto p = std::make_unique<psg_cpp_plan>();
-    p->plan.reset(psg::cpp_plan_create(ps, q, f, seed, exclusion_zone));
+    p->plan.reset(psg::cpp_plan_create(ps, q, f, seed, exclusion_zone, /*sharded=*/true));
     *out = p.release();
   });
 }

@@ -958,16 +958,17 @@ bool project_async(const psg_pointset& ps, const Directions& dir, float* keys, u
 // when the directions change (solve_graph primes it before a capture, so a
 // captured solve holds no host buffer).
 const float* window_directions(const psg_pointset& ps, const Directions& dir, cudaStream_t s) {
+  if (ps.win_ut.p && ps.win_ut_seed == dir.seed && ps.win_ut_q == dir.q) return ps.win_ut.p;  // same (seed, q)
   const int d = ps.d, nk = dir.nk;
   std::vector<float> ut(static_cast<size_t>(d) * nk);
   for (int k = 0; k < nk; ++k)
     for (int t = 0; t < d; ++t) ut[static_cast<size_t>(t) * nk + k] = dir.U[static_cast<size_t>(k) * d + t];
-  if (ut != ps.win_ut_host || !ps.win_ut.p) {
-    if (g_capturing) throw std::runtime_error("window directions changed inside a graph capture");
-    ps.win_ut_host = std::move(ut);
-    ps.win_ut.alloc(ps.win_ut_host.size(), s);
-    PSG_CUDA(cudaMemcpyAsync(ps.win_ut.p, ps.win_ut_host.data(), ps.win_ut_host.size() * 4, cudaMemcpyHostToDevice, s));
-  }
+  if (g_capturing) throw std::runtime_error("window directions changed inside a graph capture");
+  ps.win_ut_host = std::move(ut);
+  ps.win_ut.alloc(ps.win_ut_host.size(), s);
+  PSG_CUDA(cudaMemcpyAsync(ps.win_ut.p, ps.win_ut_host.data(), ps.win_ut_host.size() * 4, cudaMemcpyHostToDevice, s));
+  ps.win_ut_seed = dir.seed;
+  ps.win_ut_q = dir.q;
   return ps.win_ut.p;
 }
 
@@ -1113,7 +1114,7 @@ uint64_t window_pairs(CppPlan& plan, uint32_t lo, uint32_t hi, float win, uint64
 
 }  // namespace
 
-CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone) {
+CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone, bool sharded) {
   const uint64_t n = ps->n;
   if (n < 2) throw invalid_argument("closest_pair needs at least 2 points");  // refscan.cpp:70
   check_reference_args(n, q, f);
@@ -1126,6 +1127,7 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   plan->zone = zone;
   plan->q_arg = q;
   plan->seed_arg = seed;
+  plan->sharded = sharded;
   plan->dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
   const int nk = plan->dir.nk;
   plan->work = get_work(ps, nk, s);
@@ -1154,7 +1156,11 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   {
     static const double occupancy = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : kGridOccupancy;
     static const double box_sd = std::getenv("PSG_BOXSD") ? std::atof(std::getenv("PSG_BOXSD")) : kGridBoxSd;
-    const double min_w = W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone ? W.learned_w : 0.0;
+    // Learned hints (a width, the engine, the bootstrap mode) come from this
+    // process's earlier solves; a sharded plan must not use them: every rank
+    // has to build the same grid, whatever each rank solved before.
+    const bool hints = !sharded && W.learned_q == q && W.learned_seed == seed && W.learned_zone == zone;
+    const double min_w = hints ? W.learned_w : 0.0;
     // a width learned on dense data makes big cells: the radix build then
     const bool counting = plan->grid && !(min_w > 0.0 && W.learned_dense);
     CellCount cc{};
@@ -1272,7 +1278,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
     PSG_LAUNCHED();
     ++g_launches;
     const CppWork& W = *plan.work;
-    if (W.learned_full_boot && W.learned_q == plan.q_arg && W.learned_seed == plan.seed_arg &&
+    if (!plan.sharded && W.learned_full_boot && W.learned_q == plan.q_arg && W.learned_seed == plan.seed_arg &&
         W.learned_zone == plan.zone)
       launch_full_bootstrap(plan, s);  // this (q, seed, zone) needed the whole stencil before
     plan.boot_span->end();

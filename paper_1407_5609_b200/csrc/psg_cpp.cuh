@@ -105,6 +105,7 @@ struct CppPlan {
   bool exact_scan = false; // sparse engines: rescan with inline FP64 for every band pair (list overflow)
   bool boot_lb = false;    // the grid build left per-warp bootstrap lower bounds (BootLB)
   bool rescued = false;    // the full-stencil bootstrap already ran after a failed cell check
+  bool sharded = false;    // a part plan: no learned hints (cpp_plan_create)
   int g = 0;
   std::shared_ptr<CppWork> work;
   uint32_t width = 0;      // window engine: bootstrap width (sorted neighbours)
@@ -113,7 +114,10 @@ struct CppPlan {
   bool sync_bootstrap = true;  // false inside cpp_solve: bootstrap -> scan without a host round trip
 };
 
-CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone);
+// sharded = a key-range part plan (psg_cpp_plan_*): ignores the hints learned
+// by earlier solves on this point set, so every rank builds the same grid.
+CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                         bool sharded = false);
 float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts);
 // Result: index_i == UINT64_MAX when the part has no admissible pair.
 psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, float bound_s32);

@@ -321,6 +321,7 @@ constexpr int kMaxKeys = 8;
 
 // Host-built orthonormal projection directions (random, seeded), in FP32.
 struct Directions {
+  uint64_t seed = 0;          // make_directions(seed, d, q) is a pure function of these
   int d = 0, q = 0, nk = 0;   // q used rows, nk = padded rows (power of 2)
   std::vector<float> U;       // nk x d, rows >= q are zero
   double sigma = 1.0, unorm = 1.0;

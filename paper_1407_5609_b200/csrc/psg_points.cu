@@ -546,6 +546,7 @@ Directions make_directions(uint64_t seed, int d, int q) {
 namespace {
 Directions make_directions_uncached(uint64_t seed, int d, int q) {
   Directions dir;
+  dir.seed = seed;
   dir.d = d;
   dir.q = std::max(1, std::min(std::min(q, d), kMaxKeys));
   dir.nk = dir.q <= 4 ? 4 : 8;

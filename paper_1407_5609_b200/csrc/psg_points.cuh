@@ -90,8 +90,10 @@ struct psg_pointset {
   psg::DevBuf<double> mu, sigma;
   psg::DevBuf<float> work;     // FP32 working copy when X != src32
   psg::DevBuf<float> s32, m32, r32;  // window sets: virtual rows (psg::Rows)
-  mutable psg::DevBuf<float> win_ut;      // window sets: the last directions used, transposed (d x nk)
+  mutable psg::DevBuf<float> win_ut;      // the last directions used, transposed (d x nk)
   mutable std::vector<float> win_ut_host;
+  mutable uint64_t win_ut_seed = 0;
+  mutable int win_ut_q = -1;
   const float* X = nullptr;    // nullptr for window sets
   double scale = 1.0;          // X = fl(scale * src)
   double Rn = 0.0;             // max narrowing radius, working units

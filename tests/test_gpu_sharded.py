@@ -103,3 +103,29 @@ def test_sharded_frnn_scan_and_zone(psg, orc, d, zone):
     want = orc.brute_force_neighbors(pts.astype(np.float64), R, zone, lists=True)
     assert (cnt, h) == want[:2]
     assert np.array_equal(pairs, np.sort(want[2]))
+
+
+@pytest.mark.parametrize("recipe", ["mixture", "motif"])
+def test_sharded_ranks_with_different_histories(psg, recipe):
+    """Rank 0's point set has been solved before (it learned a cell width /
+    engine / bootstrap mode), rank 1's has not: the part plans must still
+    build the same grid on both (learned hints are not used by part plans),
+    or pairs fall between the ranks' work lists."""
+    if recipe == "mixture":
+        pts = psg.gen.mixture(5, 1 << 18, 64, 1024, 0.05)
+        make = lambda: psg.PointSet.from_flat(pts, 64)  # noqa: E731
+        zone = 0
+    else:
+        s, _ = psg.gen.walk_motif(3, 1 << 18, 128)
+        series = s.astype(np.float64)
+        make = lambda: psg.PointSet.windows_of(series, 128, znorm=True)  # noqa: E731
+        zone = 128
+    sets = [make() for _ in range(2)]
+    for _ in range(2):
+        psg.closest_pair(sets[0], 10, 10.0, 1, zone)  # history on rank 0 only
+    plans = [sharded.DevicePlan(ps._device(), 10, 10.0, 1, zone) for ps in sets]
+    bound = min(plans[r].bootstrap(r, 2) for r in range(2))
+    parts = [plans[r].scan(r, 2, bound) for r in range(2)]
+    got = sharded.combine(parts, sharded.admissible_pairs(sets[0].size(), zone))
+    one = psg.closest_pair(make(), 10, 10.0, 1, zone)
+    assert (got.index_i, got.index_j, got.distance) == (one.index_i, one.index_j, one.distance)
