@@ -715,11 +715,12 @@ __global__ void k_state_init(DevState* st, ExactSrc src, const uint32_t* sidx, B
 // ---------------------------------------------------------------------------
 // The grid's key box and cell width before the projection runs (so the
 // projection can count cells): kPreBlocks x 8 warps project a hashed sample of
-// kGridSample rows on CUDA cores (warp per row, lanes over coordinates; a
+// kPreRows rows on CUDA cores (warp per row, lanes over coordinates; a
 // tuning input only, so any summation order), reduce per-key moments, and the
 // last block to finish turns them into the box (mean +- box_sd sd clipped to
 // the sample range) and GridParams at the occupancy width.
-constexpr int kPreBlocks = 64;
+constexpr int kPreBlocks = 128;
+constexpr uint32_t kPreRows = 1024;  // one sample row per warp: the box is a tuning input
 struct PresampleArgs {
   Rows R;
   const float* Ut;  // d x nk (transposed directions)
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(256) k_presample(PresampleArgs a, DevState* st
     mn[t] = INFINITY;
     mx[t] = -INFINITY;
   }
-  constexpr int kRows = 4;  // sample rows per warp step, their loads in flight together
+  constexpr int kRows = 1;  // sample rows per warp step (kPreRows = one per warp)
   const uint32_t gw = blockIdx.x * 8 + warp, nw = gridDim.x * 8;
   for (uint32_t k0 = gw * kRows; k0 < a.m; k0 += nw * kRows) {
     uint32_t i[kRows];
@@ -1171,7 +1172,7 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
       const int ut_smem = ut_bytes <= 32 * 1024;
       PresampleArgs pa{ps->rows(), window_directions(*ps, plan->dir, s), ut_smem, nk, plan->g,
                        std::min(plan->dir.q, kMaxGridKeys), static_cast<uint32_t>(n),
-                       static_cast<uint32_t>(std::min<uint64_t>(n, kGridSample)), occupancy, box_sd, min_w};
+                       static_cast<uint32_t>(std::min<uint64_t>(n, kPreRows)), occupancy, box_sd, min_w};
       k_presample<<<kPreBlocks, 256, ut_smem ? ut_bytes : 0, s>>>(pa, W.st.p, W.gi.gp.p, W.pre_part.p,
                                                                   &W.st.p->pre_ticket, W.gi.bctr.p);
       PSG_LAUNCHED();
