@@ -11,6 +11,7 @@
 #include <thread>
 #include <tuple>
 
+#include "host_pool.hpp"
 #include "host_rng.hpp"
 #include "psg_points.cuh"
 
@@ -87,16 +88,17 @@ void h2d_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
     PSG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
-  static const unsigned threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  // memcpy fan-out over a persistent pool: one host thread moves ~10 GB/s,
+  // the PCIe link ~50
+  static HostPool pool(std::max(1u, std::min(16u, std::thread::hardware_concurrency())) - 1);
   const char* in = static_cast<const char*>(src);
   h2d_staged(dst, bytes, [&](char* stage, uint64_t off, size_t len) {
-    // memcpy fan-out: one host thread moves ~10 GB/s, the PCIe link ~50
-    const size_t per = (len / threads + 4095) & ~size_t(4095);
-    std::vector<std::thread> th;
-    for (size_t a = per; a < len; a += per)
-      th.emplace_back([=] { std::memcpy(stage + a, in + off + a, std::min(per, len - a)); });
-    std::memcpy(stage, in + off, std::min(per, len));
-    for (std::thread& t : th) t.join();
+    const size_t per = ((len + pool.size() - 1) / pool.size() + 4095) & ~size_t(4095);
+    const unsigned tasks = static_cast<unsigned>((len + per - 1) / per);
+    pool.run(tasks, [&](unsigned k) {
+      const size_t a = static_cast<size_t>(k) * per;
+      std::memcpy(stage + a, in + off + a, std::min(per, len - a));
+    });
     return len;
   }, s);
 }
