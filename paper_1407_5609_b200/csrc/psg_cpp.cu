@@ -503,22 +503,25 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
   __shared__ GridParams sP;  // one copy per block, not per thread (registers)
   if (*regrid) return;
   const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t p = lo + blockIdx.x * kThreads + tid;
+  // the position's own loads go out before the block barrier (they do not
+  // need the shared grid parameters)
+  const uint32_t pc = p < hi ? p : lo;
+  float mk[NK];
+  load_keys<NK>(a.skeys + static_cast<size_t>(pc) * NK, mk);
+  const uint32_t mo = a.sidx[pc], mcell = G.scell[pc];
+  const float lb2 = th0->lb2;
   if (tid == 0) {
     qn = 0;
     sP = *G.gp;
   }
   __syncthreads();
-  const uint32_t p = lo + blockIdx.x * kThreads + tid;
   unsigned long long visited = 0, inline_evals = 0;
   if (p < hi) {
-    float mk[NK];
-    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, mk);
-    const uint32_t mo = a.sidx[p];
-    const float lb2 = th0->lb2;
     // rows the point is too far from to hold a passing pair are skipped
     // (margin: cell faces are computed in FP64 like the cell ids, keys are FP32)
     const double win = sqrt(static_cast<double>(lb2)) * (1.0 + 0x1.0p-20) + 1e-6 * sP.w;
-    const GridFlat F = grid_flat(grid_ranges_pruned(G.cfirst, sP, p, G.scell[p], mk, win));
+    const GridFlat F = grid_flat(grid_ranges_pruned(G.cfirst, sP, p, mcell, mk, win));
     const bool zoned = a.zone > 1;
     // four candidates per step: all loads in flight before any math
     constexpr int B = 2;  // candidates in flight per step (registers vs latency)
