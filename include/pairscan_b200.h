@@ -105,6 +105,12 @@ void* psg_stream(void);
 /* Select the CUDA device for this thread's subsequent calls (one process per
  * GPU: pass LOCAL_RANK). */
 int psg_set_device(int device);
+/* Timing inside the captured solves that repeated calls on a point set
+ * replay: 0 (default) none — the fastest replay; 1 the projection, bootstrap
+ * and scan spans (psg_profile.*_kernel_ms); 2 also every stage
+ * (psg_profile.stage_*).  Each event node costs ~5 us of device time per
+ * solve.  Graphs captured at another level are recaptured on their next use. */
+int psg_set_graph_profiling(int level);
 
 /* ---- one-shot entries (host buffers in, result out) --------------------- */
 int psg_closest_pair_f64(const double* points, uint64_t n, uint64_t dim, uint64_t q, double f,

@@ -93,6 +93,7 @@ _SIGS = {
     "psg_device_ok": (_int, [_int]),
     "psg_stream": (_p, []),
     "psg_set_device": (_int, [_int]),
+    "psg_set_graph_profiling": (_int, [_int]),
     "psg_closest_pair_f64": (_int, [_p, _u64, _u64, _u64, _f64, _u64, _u64, _p]),
     "psg_closest_pair_f32": (_int, [_p, _u64, _u64, _u64, _f64, _u64, _u64, _p]),
     "psg_brute_force_closest_pair_f64": (_int, [_p, _u64, _u64, _u64, _p]),
@@ -178,6 +179,13 @@ def _check(rc: int) -> None:
 
 def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
+
+
+def set_graph_profiling(level: int) -> None:
+    """Event timing inside the CUDA graphs that repeated solves on a point set
+    replay: 0 (default) none, 1 projection / bootstrap / scan kernel times,
+    2 also the per-stage times.  Each event node costs ~5 us per solve."""
+    _check(lib().psg_set_graph_profiling(int(level)))
 
 
 def last_profile() -> dict:

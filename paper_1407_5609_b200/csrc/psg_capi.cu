@@ -119,6 +119,11 @@ int psg_last_profile(psg_profile* out) {
   return PSG_OK;
 }
 
+int psg_set_graph_profiling(int level) {
+  psg::set_graph_profiling(level);
+  return PSG_OK;
+}
+
 int psg_set_device(int device) {
   const cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {

@@ -36,7 +36,7 @@ void prof_begin() {
 }
 
 void prof_stages(const StageTimer& t) {
-  if (!t.on) return;
+  if (!t.on || t.capture) return;  // a captured timer is read per replay (solve_graph)
   for (int i = 0; i < t.count && g_prof.stages < 16; ++i) {
     float ms = 0.f;
     PSG_CUDA(cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]));
@@ -1183,7 +1183,8 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
       static const bool no_fuse = std::getenv("PSG_NO_FUSED_COUNT") != nullptr;  // A/B
       if (counting && !no_fuse) cc = CellCount{W.gi.gp.p, W.gi.cnt.p, W.gi.cid0.p};
     }
-    plan->proj_span = std::make_unique<KernelSpan>(s);
+    tm.mark("presample");
+    plan->proj_span = std::make_unique<KernelSpan>(s, "project");
     const bool counted = project_async(*ps, plan->dir, W.keys.p, &W.st.p->norm2_bits, s, cc);
     plan->proj_span->end();
     tm.mark("project");
@@ -1273,7 +1274,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
     // the lower bounds the grid build left (BootLB): the best of them
     // evaluated exactly, plus the seed pair — one small kernel; the same global
     // bound on every rank of a sharded solve (every rank built the same grid)
-    plan.boot_span = std::make_unique<KernelSpan>(s);
+    plan.boot_span = std::make_unique<KernelSpan>(s, "bootstrap");
     const uint32_t nwarps = static_cast<uint32_t>((plan.ps->n + 255) / 256 * 8);
     static const uint32_t evals =
         std::getenv("PSG_BOOT_EVALS") ? static_cast<uint32_t>(std::atoi(std::getenv("PSG_BOOT_EVALS"))) : kBootEvals;
@@ -1286,6 +1287,7 @@ float cpp_plan_bootstrap(CppPlan& plan, uint64_t part, uint64_t nparts) {
         W.learned_zone == plan.zone)
       launch_full_bootstrap(plan, s);  // this (q, seed, zone) needed the whole stencil before
     plan.boot_span->end();
+    tm.mark("bootstrap");
     if (!plan.sync_bootstrap) return INFINITY;
     read_state(plan, s);
     collect_prep(plan);
@@ -1381,9 +1383,11 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
   // Reset, and (grid) the check that the cells hold every pair whose key gaps
   // are within the window of the bound — decided on device from the bound
   // every rank shares.
+  StageTimer tm(s, g_capturing);  // stage marks inside a captured solve (replays report them)
   k_scan_prepare<<<1, 1, 0, s>>>(st, plan.grid ? W.gi.gp.p : nullptr);
   PSG_LAUNCHED();
-  KernelSpan* span = new KernelSpan(s);
+  tm.mark("prepare");
+  KernelSpan* span = new KernelSpan(s, "scan");
   if (plan.grid && plan.dense) {
     // dense cells: cell-pair tiles (the caller decided after the grid check
     // passed on the host, so the cells are wide enough for the bound)
@@ -1410,6 +1414,7 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
     ++g_prof.scan_launches;
   }
   span->end();
+  tm.mark("scan");
   const ExactSrc ex = plan.ps->exact();
   const int nb = c.sm_count * 2;
   if (plan.grid) {
@@ -1424,6 +1429,7 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
   PSG_LAUNCHED();
   k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
   PSG_LAUNCHED();
+  tm.mark("recheck");
   PSG_CUDA(cudaMemcpyAsync(W.host_st, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   g_launches += 4;
   return span;
@@ -1655,7 +1661,8 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
   window_directions(*ps, dir, s);  // the presample / window projection read it
   W.gi.ensure(static_cast<uint32_t>(ps->n), dir.nk, s);
   ensure_candidates(W, s);
-  if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone || W.gcap != W.cand_cap) {
+  if (!W.gexec || W.gq != q || W.gseed != seed || W.gzone != zone || W.gcap != W.cand_cap ||
+      W.glevel != graph_profiling()) {
     W.drop_graph();
     for (cudaEvent_t& e : W.gev)
       if (!e) PSG_CUDA(cudaEventCreate(&e));
@@ -1666,7 +1673,12 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
     g_capturing = true;
     g_cap_ev = W.gev;
     g_cap_next = 0;
-    g_cap_max = 6;
+    g_cap_max = static_cast<int>(std::size(W.gev));
+    g_cap_spans.clear();
+    g_cap_stages.clear();
+    W.glevel = graph_profiling();
+    g_cap_span_marks = W.glevel >= 1;
+    g_cap_stage_marks = W.glevel >= 2;
     try {
       std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));
       plan->sync_bootstrap = false;
@@ -1688,6 +1700,8 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
     W.gq = q;
     W.gseed = seed;
     W.gzone = zone;
+    W.gspans = g_cap_spans;
+    W.gstages = g_cap_stages;
     W.gcap = W.cand_cap;
     W.glaunches = g_launches - launches0;
     g_launches = launches0;
@@ -1702,13 +1716,22 @@ bool solve_graph(psg_pointset* ps, uint64_t q, double f, uint64_t seed, uint64_t
     grow_after_overflow(W, h);
     return false;
   }
-  float ms = 0.f;
-  PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[0], W.gev[1]));
-  g_prof.project_kernel_ms += ms;
-  PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[2], W.gev[3]));
-  g_prof.bootstrap_kernel_ms += ms;
-  PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[4], W.gev[5]));
-  g_prof.scan_kernel_ms += ms;
+  // the captured spans and stages, read from this replay's event nodes
+  for (const CapMark& m : W.gspans) {
+    float ms = 0.f;
+    PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[m.a], W.gev[m.b]));
+    const std::string nm = m.name;
+    if (nm == "project") g_prof.project_kernel_ms += ms;
+    else if (nm == "bootstrap") g_prof.bootstrap_kernel_ms += ms;
+    else if (nm == "scan") g_prof.scan_kernel_ms += ms;
+  }
+  for (const CapMark& m : W.gstages) {
+    if (g_prof.stages >= 16) break;
+    float ms = 0.f;
+    PSG_CUDA(cudaEventElapsedTime(&ms, W.gev[m.a], W.gev[m.b]));
+    std::strncpy(g_prof.stage_name[g_prof.stages], m.name, 23);
+    g_prof.stage_ms[g_prof.stages++] = ms;
+  }
   ++g_prof.scan_launches;
   *out = result_from(h, h.visited, 0);
   return true;

@@ -79,6 +79,7 @@ struct CppWork {
   cudaGraphExec_t gexec = nullptr;
   uint64_t gq = 0, gseed = 0, gzone = 0;
   uint32_t gcap = 0;  // cand_cap at capture
+  int glevel = -1;    // graph_profiling() at capture
   uint64_t glaunches = 0;
   uint64_t solves = 0;  // closest-pair solves on this point set (the first one is not captured)
   // cell width a regrid converged to, for the same (q, seed, zone)
@@ -86,7 +87,8 @@ struct CppWork {
   uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;
   bool learned_dense = false;  // the solve went to the dense engine (not graph-capturable: host decisions)
   bool learned_full_boot = false;  // the own-row bootstrap was too weak: run the full-stencil one up front
-  cudaEvent_t gev[6] = {};  // project / bootstrap / scan spans recorded inside the graph
+  cudaEvent_t gev[32] = {};  // event nodes recorded inside the graph (spans and stages)
+  std::vector<CapMark> gspans, gstages;  // which gev pairs time which span / stage
   void drop_graph();
   ~CppWork();
 };

@@ -116,22 +116,59 @@ struct DevBuf {
 extern thread_local bool g_capturing;
 extern thread_local cudaEvent_t* g_cap_ev;
 extern thread_local int g_cap_next, g_cap_max;
+// What a capture recorded: named spans (KernelSpan) and stages (StageTimer)
+// as indices into g_cap_ev, so a replay can read each one's device time.
+struct CapMark {
+  const char* name;
+  int a, b;  // event indices
+};
+extern thread_local std::vector<CapMark> g_cap_spans, g_cap_stages;
+// Event nodes inside a captured solve cost ~5 us of graph time each, so the
+// graphs carry them only on request (psg_set_graph_profiling): level 0 none,
+// 1 the named spans (project / bootstrap / scan), 2 spans and stage marks.
+// PSG_GRAPH_STAGES=1 starts at level 2.
+extern thread_local bool g_cap_stage_marks, g_cap_span_marks;
+int graph_profiling();
+void set_graph_profiling(int level);
+// next capture event (external record node), or -1 when the pool is used up
+inline int cap_event() { return g_cap_ev && g_cap_next < g_cap_max ? g_cap_next++ : -1; }
 
 // Stage timer: CUDA events on the library stream; read after the final sync.
+// Inside a graph capture it records external event nodes from g_cap_ev and
+// logs its stages in g_cap_stages (read after each replay, solve_graph).
 struct StageTimer {
   static constexpr int kMax = 16;
   cudaEvent_t ev[kMax + 1] = {};
+  int cap[kMax + 1] = {};
   const char* name[kMax] = {};
   int count = 0;
   cudaStream_t s = nullptr;
-  bool on = true;
-  explicit StageTimer(cudaStream_t st, bool enabled = true) : s(st), on(enabled && !g_capturing) {
+  bool on = true, capture = false;
+  explicit StageTimer(cudaStream_t st, bool enabled = true)
+      : s(st), on(enabled && (!g_capturing || g_cap_stage_marks)), capture(g_capturing) {
     if (!on) return;
+    if (capture) {
+      cap[0] = cap_event();
+      if (cap[0] < 0) {
+        on = false;
+        return;
+      }
+      PSG_CUDA(cudaEventRecordWithFlags(g_cap_ev[cap[0]], s, cudaEventRecordExternal));
+      return;
+    }
     ev[0] = ctx().get_event();
     PSG_CUDA(cudaEventRecord(ev[0], s));
   }
   void mark(const char* stage) {
     if (!on || count >= kMax) return;
+    if (capture) {
+      const int e = cap_event();
+      if (e < 0) return;
+      name[count] = stage;
+      cap[++count] = e;
+      PSG_CUDA(cudaEventRecordWithFlags(g_cap_ev[e], s, cudaEventRecordExternal));
+      return;
+    }
     name[count] = stage;
     ++count;
     ev[count] = ctx().get_event();
@@ -139,6 +176,10 @@ struct StageTimer {
   }
   ~StageTimer() {
     if (!on) return;
+    if (capture) {
+      for (int i = 0; i < count; ++i) g_cap_stages.push_back(CapMark{name[i], cap[i], cap[i + 1]});
+      return;
+    }
     Ctx& c = ctx();
     for (int i = 0; i <= count; ++i) c.put_event(ev[i]);
   }
@@ -147,17 +188,23 @@ struct StageTimer {
 // Host-side trace (PSG_TRACE=1): wall time since the previous mark, stderr.
 void trace(const char* what);
 
-// Device time of one kernel (or a short launch sequence) on a stream.
+// Device time of one kernel (or a short launch sequence) on a stream.  A
+// named span inside a capture is logged in g_cap_spans.
 struct KernelSpan {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s = nullptr;
   bool pooled = true;
-  explicit KernelSpan(cudaStream_t st) : s(st) {
+  const char* name = nullptr;
+  int ia = -1, ib = -1;
+  explicit KernelSpan(cudaStream_t st, const char* nm = nullptr) : s(st), name(nm) {
     if (g_capturing) {
       pooled = false;
-      if (!g_cap_ev || g_cap_next + 1 >= g_cap_max) return;
-      a = g_cap_ev[g_cap_next++];
-      b = g_cap_ev[g_cap_next++];
+      if (!g_cap_span_marks) return;
+      ia = cap_event();
+      ib = cap_event();
+      if (ia < 0 || ib < 0) return;
+      a = g_cap_ev[ia];
+      b = g_cap_ev[ib];
     } else {
       a = ctx().get_event();
       b = ctx().get_event();
@@ -178,6 +225,7 @@ struct KernelSpan {
   // Deferred form: end() now, ms() after a later stream synchronisation.
   void end() {
     if (b) record(b);
+    if (!pooled && name && b) g_cap_spans.push_back(CapMark{name, ia, ib});
   }
   double ms() const {
     if (!a || !b) return 0.0;

@@ -2,6 +2,7 @@
 // narrowing to the FP32 working copy, z-normalised windows), and the seeded
 // projection directions.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -21,6 +22,13 @@ thread_local uint64_t g_launches = 0;
 thread_local bool g_capturing = false;
 thread_local cudaEvent_t* g_cap_ev = nullptr;
 thread_local int g_cap_next = 0, g_cap_max = 0;
+thread_local std::vector<CapMark> g_cap_spans, g_cap_stages;
+thread_local bool g_cap_stage_marks = false, g_cap_span_marks = false;
+namespace {
+std::atomic<int> g_graph_prof{std::getenv("PSG_GRAPH_STAGES") ? 2 : 0};
+}
+int graph_profiling() { return g_graph_prof.load(); }
+void set_graph_profiling(int level) { g_graph_prof.store(std::clamp(level, 0, 2)); }
 
 void trace(const char* what) {
   static const bool on = std::getenv("PSG_TRACE") != nullptr;

@@ -1,5 +1,5 @@
-"""Per-stage device times of one config (stage events need PSG_NO_GRAPH=1),
-then the graph-mode total.  python tools/stage_probe.py c2|c5|c3|c1 [reps]"""
+"""Per-stage device times of one config: graph replays carry event nodes at
+level PSG_GRAPH_PROF (default 2; 0 gives the graph's own total only).  python tools/stage_probe.py c2|c5|c3|c1 [reps]"""
 import json
 import os
 import sys
@@ -23,6 +23,7 @@ elif which == "c3":
     zone = 256
 else:
     ps = psg.PointSet.from_flat(psg.gen.mixture(5, 1 << 24, 64, 1024, 0.05), 64)
+psg.set_graph_profiling(int(os.environ.get("PSG_GRAPH_PROF", "2")))
 out = []
 for k in range(reps + 1):
     r = psg.closest_pair(ps, 10, 10.0, 1, zone)
