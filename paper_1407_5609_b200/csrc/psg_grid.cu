@@ -178,78 +178,93 @@ constexpr uint32_t kBootCand = 64;  // BootLB candidates per point (the old boot
 // Final position of the point at arrival position p: its cell's start plus
 // the number of points of the cell with a smaller original index; gathers its
 // keys there.  Cells above kFixSmall points are listed for k_cell_fix_big.
-// With B.keys: the bootstrap's lower bounds too (BootLB, psg_grid.cuh) — the
-// cell's members are in hand for the ranking anyway.
 template <int NK>
 __global__ void k_cell_fix(const float* __restrict__ keys, const uint32_t* __restrict__ tmp,
                            const uint32_t* __restrict__ cid, uint32_t n, const uint32_t* __restrict__ cfirst,
                            float* __restrict__ skeys, uint32_t* __restrict__ sidx, uint32_t* __restrict__ scell,
-                           uint32_t* __restrict__ big, uint32_t* __restrict__ bctr,
-                           const GridParams* __restrict__ gpp, BootLB B) {
+                           uint32_t* __restrict__ big, uint32_t* __restrict__ bctr) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t i = tmp[p], c = cid[i], b = cfirst[c], e = cfirst[c + 1];
+  if (e - b > kFixSmall) {
+    if (p == b) big[atomicAdd(bctr, 1u)] = c;
+    return;
+  }
+  uint32_t r = 0;
+  for (uint32_t k = b; k < e; ++k) r += tmp[k] < i;
+  const uint32_t q = b + r;
+  sidx[q] = i;
+  scell[q] = c;
+  const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
+  float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(q) * NK);
+#pragma unroll
+  for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+}
+
+// (lb, i, j) order: the least lower bound, ties to the least (i, j).
+__device__ __forceinline__ bool boot_less(float lb, uint32_t i, uint32_t j, float ob, uint32_t oi, uint32_t oj) {
+  return lb < ob || (lb == ob && (i < oi || (i == oi && j < oj)));
+}
+
+// BootLB on the finished grid: the point at sorted position p against the
+// other points of its cell and of the next cell of its row (all of them up to
+// kBootCand, else a uniform stride from p), keys read by position (a warp's
+// candidates are its neighbours: coalesced, mostly L1 hits); the least (lb,
+// i, j) per warp of positions.
+template <int NK>
+__global__ void k_boot_lb(const float* __restrict__ skeys, const uint32_t* __restrict__ sidx,
+                          const uint32_t* __restrict__ scell, const uint32_t* __restrict__ cfirst, uint32_t n,
+                          const GridParams* __restrict__ gpp, BootLB B) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   float best = INFINITY;
-  uint32_t bi = 0, bj = 0;
+  uint32_t bi = 0xffffffffu, bj = 0xffffffffu;
   if (p < n) {
-    const uint32_t i = tmp[p], c = cid[i], b = cfirst[c], e = cfirst[c + 1];
-    float ki[NK];
-    if (B.keys) load_keys<NK>(B.keys + static_cast<size_t>(i) * NK, ki);
+    const uint32_t c = scell[p];
+    const uint32_t D = gpp->dims[gpp->g - 1];
+    const FastDiv fD = gpp->fD;
+    const uint32_t cs = cfirst[c];
+    const uint32_t c1 = c + 1;
+    const uint32_t ne = fD.div(c1) * D != c1 ? cfirst[c + 2] : cfirst[c1];  // the row's next cell when there is one
+    const uint32_t L = ne - cs;
+    float mk[NK];
+    load_keys<NK>(skeys + static_cast<size_t>(p) * NK, mk);
+    const uint32_t mi = sidx[p];
     auto consider = [&](uint32_t m) {
-      if (m == i || (B.zone > 1 && !admissible(i, m, B.zone))) return;
+      if (m == p) return;
       float km[NK];
-      load_keys<NK>(B.keys + static_cast<size_t>(m) * NK, km);
-      const float lb = lb2_full<NK>(ki, km);
-      if (lb < best) {
+      load_keys<NK>(skeys + static_cast<size_t>(m) * NK, km);
+      const float lb = lb2_full<NK>(mk, km);
+      if (lb > best) return;
+      const uint32_t mj = sidx[m];
+      if (B.zone > 1 && !admissible(mi, mj, B.zone)) return;
+      const uint32_t a = min(mi, mj), z = max(mi, mj);
+      if (boot_less(lb, a, z, best, bi, bj)) {
         best = lb;
-        bj = m;
+        bi = a;
+        bj = z;
       }
     };
-    if (e - b > kFixSmall) {
-      if (p == b) big[atomicAdd(bctr, 1u)] = c;
+    if (L <= kBootCand + 1) {
+      for (uint32_t m = cs; m < ne; ++m) consider(m);
     } else {
-      uint32_t r = 0;
-      for (uint32_t k = b; k < e; ++k) r += tmp[k] < i;
-      const uint32_t q = b + r;
-      sidx[q] = i;
-      scell[q] = c;
-      const float4* src = reinterpret_cast<const float4*>(keys + static_cast<size_t>(i) * NK);
-      float4* dst = reinterpret_cast<float4*>(skeys + static_cast<size_t>(q) * NK);
-#pragma unroll
-      for (int v = 0; v < NK / 4; ++v) dst[v] = src[v];
+      const uint32_t stride = L / kBootCand, o = p - cs;
+      for (uint32_t t = 1; t <= kBootCand; ++t) consider(cs + (o + t * stride) % L);
     }
-    if (B.keys) {
-      // candidates: the own cell and the next cell of its row (last key + 1),
-      // arrival positions [b, ne); all of them up to kBootCand, else a
-      // uniform stride across the range from the point's own position (a
-      // cell's arrival order can follow index order, which can correlate
-      // with structure: windows, index-periodic clusters)
-      const uint32_t D = gpp->dims[gpp->g - 1];
-      const uint32_t ne = c % D + 1 < D ? cfirst[c + 2] : e;
-      const uint32_t L = ne - b;
-      if (L <= kBootCand + 1) {
-        for (uint32_t k = b; k < ne; ++k) consider(tmp[k]);
-      } else {
-        const uint32_t stride = L / kBootCand, o = p - b;
-        for (uint32_t t = 1; t <= kBootCand; ++t) consider(tmp[b + (o + t * stride) % L]);
-      }
-    }
-    bi = i;
   }
-  if (B.keys) {
-    const int lane = threadIdx.x & 31;
-    for (int o = 16; o; o >>= 1) {
-      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
-      if (ob < best || (ob == best && oi < bi)) {
-        best = ob;
-        bi = oi;
-        bj = oj;
-      }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ob = __shfl_xor_sync(kGridFull, best, o);
+    const uint32_t oi = __shfl_xor_sync(kGridFull, bi, o), oj = __shfl_xor_sync(kGridFull, bj, o);
+    if (boot_less(ob, oi, oj, best, bi, bj)) {
+      best = ob;
+      bi = oi;
+      bj = oj;
     }
-    if (lane == 0) {
-      const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-      B.wlb[w] = best;
-      B.wpair[w] = make_uint2(bi, bj);
-    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    B.wlb[w] = best;
+    B.wpair[w] = make_uint2(bi, bj);
   }
 }
 
@@ -425,18 +440,25 @@ void build_grid(const float* keys, uint32_t n, int nk, GridIndex& gi, int sort_b
     PSG_LAUNCHED();
     if (nk == 4) {
       k_cell_fix<4><<<nb, 256, 0, s>>>(keys, gi.idx1.p, gi.cid0.p, n, gi.cfirst.p, gi.skeys.p, gi.sidx.p, gi.cid1.p,
-                                       gi.big.p, gi.bctr.p, gi.gp.p, B);
+                                       gi.big.p, gi.bctr.p);
       PSG_LAUNCHED();
       k_cell_fix_big<4><<<148, kFixBigThreads, 0, s>>>(keys, gi.idx1.p, gi.idx0.p, gi.cfirst.p, gi.skeys.p,
                                                        gi.sidx.p, gi.cid1.p, gi.big.p, gi.bctr.p);
+      PSG_LAUNCHED();
+      if (B.keys) k_boot_lb<4><<<nb, 256, 0, s>>>(gi.skeys.p, gi.sidx.p, gi.cid1.p, gi.cfirst.p, n, gi.gp.p, B);
     } else {
       k_cell_fix<8><<<nb, 256, 0, s>>>(keys, gi.idx1.p, gi.cid0.p, n, gi.cfirst.p, gi.skeys.p, gi.sidx.p, gi.cid1.p,
-                                       gi.big.p, gi.bctr.p, gi.gp.p, B);
+                                       gi.big.p, gi.bctr.p);
       PSG_LAUNCHED();
       k_cell_fix_big<8><<<148, kFixBigThreads, 0, s>>>(keys, gi.idx1.p, gi.idx0.p, gi.cfirst.p, gi.skeys.p,
                                                        gi.sidx.p, gi.cid1.p, gi.big.p, gi.bctr.p);
+      PSG_LAUNCHED();
+      if (B.keys) k_boot_lb<8><<<nb, 256, 0, s>>>(gi.skeys.p, gi.sidx.p, gi.cid1.p, gi.cfirst.p, n, gi.gp.p, B);
     }
-    PSG_LAUNCHED();
+    if (B.keys) {
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
 #ifdef PSG_DEBUG_SYNC
     k_verify_cfirst<<<1024, 256, 0, s>>>(gi.cid1.p, n, gi.gp.p, gi.cfirst.p);
     PSG_LAUNCHED();
