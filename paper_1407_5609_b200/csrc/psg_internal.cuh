@@ -10,6 +10,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace psg {
@@ -45,6 +46,34 @@ struct cuda_error : std::runtime_error {
 #else
 #define PSG_LAUNCHED() PSG_CUDA(cudaGetLastError())
 #endif
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  A kernel enqueued by launch_pdl may be
+// scheduled while its predecessor on the stream is still draining; it calls
+// pdl_wait() before touching anything the predecessor writes (the wait also
+// makes the predecessor's writes visible) and pdl_trigger() right after, so
+// its own successor can be scheduled in turn.  Because every kernel triggers
+// only after its wait, a kernel's pre-wait prologue may read whatever the
+// kernel two back wrote.  Outside a PDL chain both are no-ops.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+bool pdl_enabled();  // PSG_NO_PDL=1: plain launches (A/B)
+template <class... P, class... A>
+void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PSG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
+}
 
 // ---------------------------------------------------------------------------
 // Per-device context: one stream, a stream-ordered pool that keeps freed

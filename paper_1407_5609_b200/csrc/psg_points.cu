@@ -40,6 +40,11 @@ void trace(const char* what) {
   last = now;
 }
 
+bool pdl_enabled() {
+  static const bool off = std::getenv("PSG_NO_PDL") != nullptr;
+  return !off;
+}
+
 Ctx& ctx() {
   static std::mutex mu;
   static std::map<int, std::unique_ptr<Ctx>> all;

@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // PDL: the set-up above (B operand, barriers, TMEM) overlaps the
+  // predecessor's tail; the grid parameters it wrote are read below
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem = *tmem_slot;
   const uint32_t ntiles = (n + kTcM - 1) / kTcM;
 
@@ -289,7 +293,7 @@ void launch(const psg_pointset& ps, const Directions& dir, float* keys, unsigned
   std::memcpy(&nbits, &ps.norm2max, 4);
   const uint32_t ntiles = (n + kTcM - 1) / kTcM;
   const int grid = static_cast<int>(std::min<uint32_t>(ntiles, static_cast<uint32_t>(ctx().sm_count)));
-  k_project_tc<NK, D><<<grid, kTcThreads, kSmem, s>>>(map, n, u, keys, nb, nbits, cc);
+  launch_pdl(k_project_tc<NK, D>, grid, kTcThreads, kSmem, s, map, n, u, keys, nb, nbits, cc);
   PSG_LAUNCHED();
 }
 

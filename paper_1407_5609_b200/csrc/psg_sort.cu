@@ -226,8 +226,8 @@ int sort_impl(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bi
 
 // ---- exclusive scan ---------------------------------------------------------
 constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 16384
 
 // Block-wide exclusive scan of one value per thread; returns the block total.
 __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* warp_sums, uint32_t& total) {
@@ -261,8 +261,8 @@ __device__ __forceinline__ size_t scan_count(size_t count, const uint64_t* dcell
   return dcells ? static_cast<size_t>(*dcells) + 1 : count;
 }
 
-// Single pass (decoupled look-back): each block claims the next tile from a
-// ticket, scans its 4096 values (one 16-byte load per thread), publishes its
+// Single pass (decoupled look-back): each block takes tiles in order, scans
+// a tile's 16384 values (four 16-byte loads per thread), publishes its
 // aggregate, then one warp looks back over its predecessors' status words
 // (flag in the top bits, value in the low 32; zeroed before the launch) until
 // it reaches an inclusive prefix.  Reads the input once and writes the output
@@ -274,30 +274,37 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const uint32_t* 
                                                                 unsigned long long* __restrict__ status,
                                                                 uint32_t* __restrict__ ticket,
                                                                 uint32_t* __restrict__ out) {
+  pdl_wait();  // PDL: the predecessor's writes are visible from here
+  pdl_trigger();
   __shared__ uint32_t ws[33];
   __shared__ uint32_t tile_s, prefix_s;
   count = scan_count(count, dcells);
-  // persistent: a block keeps claiming tiles (in ticket order, so every tile
-  // it waits on is held by a block that is running) until the count is covered
-  for (;;) {
+  (void)ticket;
+  // persistent, static striding: block b scans tiles b, b + grid, ... in
+  // order; every tile a block waits on is held by a block that started (all
+  // blocks are resident: the grid is sized by the occupancy), so no ticket (a
+  // shared ticket serialises every tile on one L2 address)
+  for (uint32_t tile = blockIdx.x;; tile += gridDim.x) {
   __syncthreads();  // the previous tile's shared state is consumed
-  if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint32_t tile = tile_s;
   if (static_cast<size_t>(tile) * kScanTile >= count) return;
   const size_t base = static_cast<size_t>(tile) * kScanTile + static_cast<size_t>(threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
   if (base + kScanItems <= count) {
-    const uint4 q = *reinterpret_cast<const uint4*>(in + base);
-    v[0] = q.x;
-    v[1] = q.y;
-    v[2] = q.z;
-    v[3] = q.w;
+#pragma unroll
+    for (int q4 = 0; q4 < kScanItems / 4; ++q4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(in + base + 4 * q4);
+      v[4 * q4] = q.x;
+      v[4 * q4 + 1] = q.y;
+      v[4 * q4 + 2] = q.z;
+      v[4 * q4 + 3] = q.w;
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) v[i] = base + i < count ? in[base + i] : 0u;
   }
-  const uint32_t sum = v[0] + v[1] + v[2] + v[3];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) sum += v[i];
   uint32_t total;
   const uint32_t excl = block_exclusive(sum, ws, total);
   if (threadIdx.x < 32) {
@@ -336,7 +343,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const uint32_t* 
     run += v[i];
   }
   if (base + kScanItems <= count) {
-    *reinterpret_cast<uint4*>(out + base) = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int q4 = 0; q4 < kScanItems / 4; ++q4)
+      *reinterpret_cast<uint4*>(out + base + 4 * q4) = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
   } else {
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i)
@@ -355,17 +364,23 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_
 }
 
 void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count, const uint64_t* dcells,
-                            uint32_t* temp, cudaStream_t s) {
+                            uint32_t* temp, cudaStream_t s, bool zeroed) {
   if (max_count == 0) return;
   const size_t nb = (max_count + kScanTile - 1) / kScanTile;
   if (reinterpret_cast<uintptr_t>(in) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
     throw std::runtime_error("exclusive_scan_u32: buffers must be 16-byte aligned");
   const size_t words = scan_temp_words(max_count);
-  PSG_CUDA(cudaMemsetAsync(temp, 0, words * sizeof(uint32_t), s));
+  if (!zeroed) PSG_CUDA(cudaMemsetAsync(temp, 0, words * sizeof(uint32_t), s));
   auto* status = reinterpret_cast<unsigned long long*>(temp);
-  // two 1024-thread blocks per SM stay resident; they loop over the tiles
-  const unsigned grid = static_cast<unsigned>(std::min<size_t>(nb, static_cast<size_t>(ctx().sm_count) * 2));
-  k_scan_lookback<<<grid, kScanThreads, 0, s>>>(in, max_count, dcells, status, temp + 2 * (nb + 1), out);
+  // every block resident at once (the static tile striding waits on blocks
+  // that must be running); they loop over the tiles
+  static const int per_sm = [] {
+    int per = 0;
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan_lookback, kScanThreads, 0));
+    return std::max(per, 1);
+  }();
+  const unsigned grid = static_cast<unsigned>(std::min<size_t>(nb, static_cast<size_t>(ctx().sm_count) * per_sm));
+  launch_pdl(k_scan_lookback, grid, kScanThreads, 0, s, in, max_count, dcells, status, temp + 2 * (nb + 1), out);
   PSG_LAUNCHED();
 }
 

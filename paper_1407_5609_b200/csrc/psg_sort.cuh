@@ -22,8 +22,9 @@ size_t radix_hist_words(size_t n);
 size_t scan_temp_words(size_t count);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t count, uint32_t* temp, cudaStream_t s);
 // Same with the length read on device: count = *dcells + 1 (<= max_count).
+// zeroed: the caller already zeroed the temp (no memset node between kernels).
 void exclusive_scan_u32_dev(const uint32_t* in, uint32_t* out, size_t max_count, const uint64_t* dcells,
-                            uint32_t* temp, cudaStream_t s);
+                            uint32_t* temp, cudaStream_t s, bool zeroed = false);
 template <class K>
 int radix_sort(K* keys[2], uint32_t* vals[2], size_t n, int begin_bit, int end_bit, uint32_t* hist,
                cudaStream_t s);
