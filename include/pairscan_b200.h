@@ -146,6 +146,13 @@ int psg_brute_force_neighbors_f64(const double* points, uint64_t n, uint64_t dim
 int psg_frnn_pairs_f32(const float* points, uint64_t n, uint64_t dim, double radius, uint64_t q,
                        double f, uint64_t seed, uint64_t exclusion_zone, uint64_t* pairs,
                        uint64_t capacity, uint64_t* pair_count, uint64_t* pair_hash);
+/* The same sorted list as upper-triangular CSR (12 bytes per pair less 4 on
+ * the wire): row i = offsets[i] .. offsets[i+1] of cols, every j > i with
+ * d(i,j) <= R, ascending (main.cpp:465-478 --pairs-out order).  offsets holds
+ * n+1 entries (always complete); cols receives the first `capacity` columns. */
+int psg_frnn_pairs_csr_f32(const float* points, uint64_t n, uint64_t dim, double radius, uint64_t q,
+                           double f, uint64_t seed, uint64_t exclusion_zone, uint64_t* offsets,
+                           uint32_t* cols, uint64_t capacity, uint64_t* pair_count, uint64_t* pair_hash);
 void psg_neighbor_result_free(psg_neighbor_result* r);
 
 /* build_reference_set (refscan.cpp:30-65), bit-exact: ref_indices[q],

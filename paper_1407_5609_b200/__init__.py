@@ -105,6 +105,7 @@ _SIGS = {
     "psg_fixed_radius_neighbors_f32": (_int, [_p, _u64, _u64, _f64, _u64, _f64, _u64, _u64, _int, _p]),
     "psg_brute_force_neighbors_f64": (_int, [_p, _u64, _u64, _f64, _u64, _int, _p]),
     "psg_frnn_pairs_f32": (_int, [_p, _u64, _u64, _f64, _u64, _f64, _u64, _u64, _p, _u64, _p, _p]),
+    "psg_frnn_pairs_csr_f32": (_int, [_p, _u64, _u64, _f64, _u64, _f64, _u64, _u64, _p, _p, _u64, _p, _p]),
     "psg_neighbor_result_free": (None, [_p]),
     "psg_build_reference_set_f64": (_int, [_p, _u64, _u64, _u64, _f64, _u64, _p, _p, _p, _p]),
     "psg_reference_bound": (_int, [_p, _p, _p, _u64, _p]),
@@ -468,6 +469,32 @@ def frnn_pairs(points: np.ndarray, radius: float, q: int = 10, f: float = 10.0, 
         if cnt.value <= cap:
             return buf[: cnt.value], cnt.value, h.value
         cap = cnt.value
+
+
+def frnn_pairs_csr(points: np.ndarray, radius: float, q: int = 10, f: float = 10.0, seed: int = 1,
+                   exclusion_zone: int = 0, offsets: np.ndarray | None = None, cols: np.ndarray | None = None):
+    """The sorted i<j list as upper-triangular CSR: (offsets[n+1] uint64,
+    cols uint32, count, hash); row i is cols[offsets[i]:offsets[i+1]].
+
+    `offsets` / `cols` (optional, e.g. pinned arrays) receive the output; when
+    `cols` is too small only the offsets, count and hash are complete."""
+    pts = np.ascontiguousarray(points, dtype=np.float32)
+    n, d = pts.shape
+    cnt, h = _u64(), _u64()
+    if offsets is None:
+        offsets = np.empty(n + 1, np.uint64)
+    if cols is None:
+        cap = max(40 * n, 1 << 16)
+        while True:
+            cols = np.empty(cap, np.uint32)
+            _check(lib().psg_frnn_pairs_csr_f32(_ptr(pts), n, d, radius, q, f, seed, exclusion_zone, _ptr(offsets),
+                                                _ptr(cols), cap, C.byref(cnt), C.byref(h)))
+            if cnt.value <= cap:
+                return offsets, cols[: cnt.value], cnt.value, h.value
+            cap = cnt.value
+    _check(lib().psg_frnn_pairs_csr_f32(_ptr(pts), n, d, radius, q, f, seed, exclusion_zone, _ptr(offsets),
+                                        _ptr(cols), cols.size, C.byref(cnt), C.byref(h)))
+    return offsets, (cols[: cnt.value] if cnt.value <= cols.size else None), cnt.value, h.value
 
 
 def build_reference_set(points: PointSet, q: int, f: float, seed: int) -> ReferenceSet:

@@ -246,6 +246,19 @@ int psg_frnn_pairs_f32(const float* points, uint64_t n, uint64_t dim, double rad
     account_io(*ps, 0);
   });
 }
+int psg_frnn_pairs_csr_f32(const float* points, uint64_t n, uint64_t dim, double radius, uint64_t q, double f,
+                           uint64_t seed, uint64_t exclusion_zone, uint64_t* offsets, uint32_t* cols,
+                           uint64_t capacity, uint64_t* pair_count, uint64_t* pair_hash) {
+  return guarded([&] {
+    if (n == 0) throw psg::invalid_argument("empty input");
+    psg::trace("csr: enter");
+    auto ps = rows32(points, n, dim);
+    psg::trace("csr: point set");
+    psg::frnn_pairs_csr(ps.get(), radius, q, f, seed, exclusion_zone, offsets, cols, capacity, pair_count,
+                        pair_hash);
+    account_io(*ps, 0);
+  });
+}
 void psg_neighbor_result_free(psg_neighbor_result* r) {
   if (!r) return;
   std::free(r->offsets);

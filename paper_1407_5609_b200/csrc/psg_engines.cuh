@@ -19,6 +19,10 @@ void frnn_solve(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
                 bool want_lists, psg_neighbor_result* out);
 void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                 uint64_t* pairs, uint64_t capacity, uint64_t* count, uint64_t* hash);
+// The same list as upper-triangular CSR: offsets[n + 1] (row i = j > i,
+// ascending) and the first `capacity` columns.
+void frnn_pairs_csr(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                    uint64_t* offsets, uint32_t* cols, uint64_t capacity, uint64_t* count, uint64_t* hash);
 // Sharded FRNN: the plan (projection + grid, identical on every rank), then
 // per-part scans; a pair belongs to the part holding its earlier sorted
 // position.  frnn_plan_pairs: the last scanned part's pairs, sorted, with

@@ -623,6 +623,28 @@ __global__ void k_bucket_unpack(uint64_t* __restrict__ keys, uint64_t m, int bj,
   keys[k] = (((v >> bj) + i0) << 32) | (v & ((1ull << bj) - 1));
 }
 
+// A bucket's sorted packed keys as upper-triangular CSR: cols[k] = j, and
+// offs[i] = the bucket's first slot plus the first k whose row is >= i, for
+// every row i of the bucket's range [i0, i1) (each row written once, by the
+// pair that starts it or by the bucket's last pair for trailing empty rows).
+__global__ void k_bucket_csr(const uint64_t* __restrict__ keys, uint64_t len, int bj, uint64_t i0, uint64_t i1,
+                             uint64_t slot0, uint32_t* __restrict__ cols, uint64_t* __restrict__ offs) {
+  const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (k >= len) return;
+  const uint64_t v = keys[k];
+  const uint64_t r = v >> bj;
+  cols[k] = static_cast<uint32_t>(v & ((1ull << bj) - 1));
+  const uint64_t first = k == 0 ? 0 : (keys[k - 1] >> bj) + 1;  // rows (prev, r] start here
+  for (uint64_t rr = first; rr <= r; ++rr) offs[i0 + rr] = slot0 + k;
+  if (k == len - 1)
+    for (uint64_t rr = r + 1; rr < i1 - i0; ++rr) offs[i0 + rr] = slot0 + len;
+}
+
+__global__ void k_fill_u64(uint64_t* __restrict__ out, uint64_t count, uint64_t v) {
+  const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (k < count) out[k] = v;
+}
+
 int bits_for(uint64_t n) {
   int b = 1;
   while ((1ull << b) < n) ++b;
@@ -949,8 +971,11 @@ void sort_pairs(const FrnnRun& run, uint64_t n, DevBuf<uint64_t>& sorted, cudaSt
 
 FrnnRun frnn_run(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
                  bool emit = true) {
+  trace("frnn: enter");
   std::unique_ptr<FrnnPlan> plan(frnn_plan_create(ps, radius, q, f, seed, zone));
+  trace("frnn: plan");
   frnn_plan_scan(*plan, 0, 1, emit);
+  trace("frnn: scan");
   return std::move(plan->run);
 }
 
@@ -1054,6 +1079,83 @@ void sorted_list_to_host(const FrnnRun& run, uint64_t n, uint64_t* host, uint64_
   PSG_CUDA(cudaStreamSynchronize(s));
   for (int b = 0; b < B; ++b) c.put_event(ev[b]);
 }
+
+// The sorted (i<j) lists as upper-triangular CSR on the host: offs[n + 1]
+// (u64) and cols (u32, the first `cap` of them), in i-range buckets like
+// sorted_list_to_host — each bucket sorted on the library stream, turned into
+// its columns and row offsets, and copied on the copy stream while the next
+// bucket sorts.  12 bytes per pair less 4: the 530 MB of C4's packed pairs
+// become 265 MB of columns + 32 MB of offsets.
+void sorted_csr_to_host(const FrnnRun& run, uint64_t n, uint64_t* offs, uint32_t* cols, uint64_t cap,
+                        cudaStream_t s) {
+  Ctx& c = ctx();
+  const uint64_t m = run.count;
+  const int B = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kListBuckets, m >> 17)));
+  const int bj = bits_for(n);
+  int bi = 1;
+  while ((1ull << bi) < (n + B - 1) / B + 1) ++bi;
+  DevBuf<unsigned long long> cnt(2 * kListBuckets, s);
+  PSG_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * kListBuckets * sizeof(unsigned long long), s));
+  unsigned long long hc[kListBuckets] = {0};
+  const unsigned g = grid_cap(std::max<uint64_t>(m, 1));
+  if (m) {
+    k_bucket_count<<<g, 256, 0, s>>>(run.pairs.p, m, n, B, cnt.p);
+    PSG_LAUNCHED();
+    PSG_CUDA(cudaMemcpyAsync(hc, cnt.p, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+  }
+  unsigned long long off[kListBuckets + 1] = {0}, biggest = 0;
+  for (int b = 0; b < B; ++b) {
+    off[b + 1] = off[b] + hc[b];
+    biggest = std::max(biggest, hc[b]);
+  }
+  PSG_CUDA(cudaMemcpyAsync(cnt.p + B, off, B * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  DevBuf<uint64_t> a(std::max<uint64_t>(m, 1), s), tmp(std::max<uint64_t>(biggest, 1), s), doffs(n + 1, s);
+  DevBuf<uint32_t> dcols(std::max<uint64_t>(m, 1), s);
+  DevBuf<uint32_t> hist(radix_hist_words(std::max<uint64_t>(biggest, 2)), s);
+  if (m) {
+    k_bucket_scatter<<<g, 256, 0, s>>>(run.pairs.p, m, n, B, bj, cnt.p + B, a.p);
+    PSG_LAUNCHED();
+    g_launches += 2;
+  }
+  if (!c.copy_stream) PSG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev(B);
+  for (int b = 0; b < B; ++b) ev[b] = c.get_event();
+  const int passes = (bi + bj + 7) / 8;
+  for (int b = 0; b < B; ++b) {
+    const uint64_t len = hc[b], i0 = (n * b + B - 1) / B, i1 = (n * (b + 1) + B - 1) / B;
+    uint64_t* kk[2] = {a.p + off[b], tmp.p};
+    uint32_t* vv[2] = {nullptr, nullptr};
+    if (len > 1) {
+      const int which = radix_sort<uint64_t>(kk, vv, len, 0, passes * 8, hist.p, s);
+      g_launches += 1 + passes;
+      kk[0] = kk[which];
+    }
+    if (len) {
+      k_bucket_csr<<<blocks(len, 256), 256, 0, s>>>(kk[0], len, bj, i0, i1, off[b], dcols.p + off[b], doffs.p);
+    } else if (i1 > i0) {
+      k_fill_u64<<<blocks(i1 - i0, 256), 256, 0, s>>>(doffs.p + i0, i1 - i0, off[b]);
+    }
+    PSG_LAUNCHED();
+    ++g_launches;
+    PSG_CUDA(cudaEventRecord(ev[b], s));
+  }
+  for (int b = 0; b < B; ++b) {
+    PSG_CUDA(cudaStreamWaitEvent(c.copy_stream, ev[b], 0));
+    const uint64_t i0 = (n * b + B - 1) / B, i1 = (n * (b + 1) + B - 1) / B;
+    if (i1 > i0)
+      PSG_CUDA(cudaMemcpyAsync(offs + i0, doffs.p + i0, (i1 - i0) * 8, cudaMemcpyDeviceToHost, c.copy_stream));
+    if (off[b] < cap) {
+      const uint64_t len = std::min<uint64_t>(hc[b], cap - off[b]);
+      if (len)
+        PSG_CUDA(cudaMemcpyAsync(cols + off[b], dcols.p + off[b], len * 4, cudaMemcpyDeviceToHost, c.copy_stream));
+    }
+  }
+  PSG_CUDA(cudaStreamSynchronize(c.copy_stream));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  offs[n] = m;
+  for (int b = 0; b < B; ++b) c.put_event(ev[b]);
+}
 }  // namespace
 
 void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
@@ -1083,6 +1185,22 @@ void frnn_pairs(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t 
   PSG_CUDA(cudaStreamSynchronize(s));
   prof_stages(tm);
   g_prof.d2h_bytes += m * sizeof(uint64_t);
+}
+
+void frnn_pairs_csr(psg_pointset* ps, double radius, uint64_t q, double f, uint64_t seed, uint64_t zone,
+                    uint64_t* offsets, uint32_t* cols, uint64_t capacity, uint64_t* count, uint64_t* hash) {
+  FrnnRun run = frnn_run(ps, radius, q, f, seed, zone, true);
+  cudaStream_t s = ctx().stream;
+  *count = run.count;
+  *hash = run.hash;
+  if (!offsets) return;
+  StageTimer tm(s);
+  sorted_csr_to_host(run, ps->n, offsets, cols, cols ? capacity : 0, s);
+  tm.mark("sort+d2h");
+  trace("frnn: csr to host");
+  PSG_CUDA(cudaStreamSynchronize(s));
+  prof_stages(tm);
+  g_prof.d2h_bytes += (ps->n + 1) * 8 + std::min(capacity, run.count) * 4;
 }
 
 void brute_neighbors(psg_pointset* ps, double radius, uint64_t zone, bool want_lists, psg_neighbor_result* out) {

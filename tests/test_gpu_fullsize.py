@@ -61,6 +61,12 @@ def test_c4_full(psg, orc):
     assert 60_000_000 < cnt < 72_000_000  # ~32 expected neighbours per point
     assert np.all(pairs[1:] > pairs[:-1])
     assert np.all((pairs >> np.uint64(32)) < (pairs & np.uint64(0xFFFFFFFF)))
+    # the same list as upper-triangular CSR (32 buckets at this size)
+    off, cols, c2, h2 = psg.frnn_pairs_csr(cube, oracle.R_C4)
+    assert (c2, h2) == (cnt, h)
+    assert np.array_equal(np.diff(off.astype(np.int64)), np.bincount((pairs >> np.uint64(32)).astype(np.int64),
+                                                                        minlength=n))
+    assert np.array_equal(cols, (pairs & np.uint64(0xFFFFFFFF)).astype(np.uint32))
 
 
 @pytest.mark.parametrize("logn", [17, 19])

@@ -223,6 +223,34 @@ def test_c4_recipe_small(psg, orc):
     assert np.all(i < j)
 
 
+def _csr_from_pairs(pairs, n):
+    i = (pairs >> np.uint64(32)).astype(np.int64)
+    off = np.zeros(n + 1, np.uint64)
+    np.cumsum(np.bincount(i, minlength=n), out=off[1:])
+    return off, (pairs & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+@pytest.mark.parametrize("n,k", [(1 << 12, 32), (1 << 16, 32), (1 << 16, 0.01), (3000, 200)])
+def test_frnn_csr_matches_sorted_pairs(psg, orc, n, k):
+    """The upper-triangular CSR output (psg_frnn_pairs_csr_f32) is the sorted
+    pair list re-encoded: same count and hash, offsets = row starts, columns =
+    the j's in order (one bucket, several buckets, almost no pairs, dense rows)."""
+    cube = orc.gen_uniform(6, n, 3)
+    R = (3 * k / (4 * np.pi * n)) ** (1 / 3)
+    pairs, cnt, h = psg.frnn_pairs(cube, R)
+    off, cols, c2, h2 = psg.frnn_pairs_csr(cube, R)
+    assert (c2, h2) == (cnt, h)
+    woff, wcols = _csr_from_pairs(pairs, n)
+    assert np.array_equal(off, woff)
+    assert np.array_equal(cols, wcols)
+    if cnt > 10:  # a short column buffer: offsets complete, columns cut at capacity
+        short = np.zeros(cnt // 3, np.uint32)
+        off2, cols2, c3, _ = psg.frnn_pairs_csr(cube, R, cols=short)
+        assert c3 == cnt and cols2 is None
+        assert np.array_equal(off2, woff)
+        assert np.array_equal(short, wcols[: short.size])
+
+
 def test_c5_recipe_small(psg, orc):
     pts = orc.gen_mixture(5, 8192, 64, 1024, 0.05)
     want = orc.brute_force_closest_pair(pts, 0)
