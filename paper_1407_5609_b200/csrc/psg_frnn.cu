@@ -645,6 +645,153 @@ __global__ void k_fill_u64(uint64_t* __restrict__ out, uint64_t count, uint64_t 
   if (k < count) out[k] = v;
 }
 
+// ---- the (i<j) lists as CSR by row groups (frnn_pairs_csr) -------------------
+// Group g = rows [256 g, 256 g + 256).  One histogram pass and one scatter
+// (both block-aggregated in shared memory: one global atomic per block and
+// group) put every pair in its group's slice; then one CTA per group orders
+// the slice in shared memory — rows counted, scanned and placed, each row's
+// columns sorted by a warp — and writes its columns and row offsets
+// coalesced.  No global sort: about three passes over the 8-byte pairs.
+constexpr int kGroupShift = 8;
+constexpr uint32_t kGroupRows = 1u << kGroupShift;
+constexpr int kGroupHistThreads = 1024;
+constexpr uint32_t kMaxGroups = 16384;  // shared-memory histogram (n <= 2^22 rows)
+constexpr uint32_t kGroupCap = 16384;   // pairs a group CTA sorts in shared memory (64 KiB)
+
+__global__ void __launch_bounds__(kGroupHistThreads) k_group_hist(const uint64_t* __restrict__ pairs, uint64_t m,
+                                                                  uint32_t ng, unsigned* __restrict__ cnt) {
+  extern __shared__ unsigned sh[];
+  for (uint32_t g = threadIdx.x; g < ng; g += blockDim.x) sh[g] = 0;
+  __syncthreads();
+  const uint64_t per = (m + gridDim.x - 1) / gridDim.x;
+  const uint64_t k0 = blockIdx.x * per, k1 = min(m, k0 + per);
+  for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&sh[pairs[k] >> (32 + kGroupShift)], 1u);
+  __syncthreads();
+  for (uint32_t g = threadIdx.x; g < ng; g += blockDim.x)
+    if (sh[g]) atomicAdd(cnt + g, sh[g]);
+}
+
+// Scatter by digit v >> (32 + shift) (nbins of them; cur[b] starts at bin
+// b's first slot), block-aggregated: a block histograms its tile in shared
+// memory, reserves each bin's run with one global atomic and writes the run.
+// tile = 0: one contiguous slice per block (few bins: long runs); a pass
+// over input already grouped by a coarser digit uses small tiles, so each
+// tile touches few bins and its runs stay long.
+__global__ void __launch_bounds__(kGroupHistThreads) k_group_scatter(const uint64_t* __restrict__ pairs, uint64_t m,
+                                                                     int shift, uint32_t nbins, uint64_t tile,
+                                                                     unsigned* __restrict__ cur,
+                                                                     uint64_t* __restrict__ out) {
+  extern __shared__ unsigned sh[];  // nbins counters, then nbins bases
+  unsigned* base = sh + nbins;
+  const uint64_t per = tile ? tile : (m + gridDim.x - 1) / gridDim.x;
+  for (uint64_t k0 = blockIdx.x * per; k0 < m; k0 += gridDim.x * per) {
+    const uint64_t k1 = min(m, k0 + per);
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < nbins; g += blockDim.x) sh[g] = 0;
+    __syncthreads();
+    for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&sh[pairs[k] >> (32 + shift)], 1u);
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < nbins; g += blockDim.x) {
+      base[g] = sh[g] ? atomicAdd(cur + g, sh[g]) : 0u;
+      sh[g] = 0;
+    }
+    __syncthreads();
+    for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      const uint64_t v = pairs[k];
+      const uint32_t g = static_cast<uint32_t>(v >> (32 + shift));
+      out[base[g] + atomicAdd(&sh[g], 1u)] = v;
+    }
+  }
+}
+
+// A row longer than 1024 (rare: a dense cluster), straight to its final
+// place: each column's rank among the row's (distinct) columns.
+__device__ void block_rank_row(const uint32_t* __restrict__ row, uint32_t len, uint32_t* __restrict__ out) {
+  for (uint32_t k = threadIdx.x; k < len; k += blockDim.x) {
+    const uint32_t v = row[k];
+    uint32_t r = 0;
+    for (uint32_t t = 0; t < len; ++t) r += row[t] < v;
+    out[r] = v;
+  }
+}
+
+// One CTA per group g0 + blockIdx.x (at most kGroupCap pairs): columns in
+// row order, each row ascending, to cols[gstart[g] ..]; row offsets to offs.
+constexpr int kGroupSortThreads = 512;
+__global__ void __launch_bounds__(kGroupSortThreads) k_group_sort(const uint64_t* __restrict__ grouped,
+                                                                  const uint32_t* __restrict__ gstart, uint32_t g0,
+                                                                  uint64_t n, uint32_t* __restrict__ cols,
+                                                                  uint64_t* __restrict__ offs) {
+  __shared__ uint32_t rs[kGroupRows + 1];  // row counts, then row starts
+  __shared__ uint32_t cur[kGroupRows];
+  extern __shared__ uint32_t sc[];         // the group's columns, by row (kGroupCap)
+  const uint32_t g = g0 + blockIdx.x;
+  const uint32_t b = gstart[g], len = gstart[g + 1] - b;
+  const uint64_t r0 = static_cast<uint64_t>(g) << kGroupShift;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t r = tid; r <= kGroupRows; r += blockDim.x) rs[r] = 0;
+  __syncthreads();
+  for (uint32_t k = tid; k < len; k += blockDim.x)
+    atomicAdd(&rs[static_cast<uint32_t>(grouped[b + k] >> 32) & (kGroupRows - 1)], 1u);
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of 256 counts: 8 per lane
+    uint32_t v[kGroupRows / 32], sum = 0;
+#pragma unroll
+    for (int t = 0; t < static_cast<int>(kGroupRows / 32); ++t) {
+      v[t] = rs[lane * (kGroupRows / 32) + t];
+      sum += v[t];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(kFull, inc, o);
+      if (lane >= static_cast<uint32_t>(o)) inc += x;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int t = 0; t < static_cast<int>(kGroupRows / 32); ++t) {
+      rs[lane * (kGroupRows / 32) + t] = run;
+      cur[lane * (kGroupRows / 32) + t] = run;
+      run += v[t];
+    }
+    if (lane == 31) rs[kGroupRows] = run;
+  }
+  __syncthreads();
+  for (uint32_t k = tid; k < len; k += blockDim.x) {
+    const uint64_t v = grouped[b + k];
+    sc[atomicAdd(&cur[static_cast<uint32_t>(v >> 32) & (kGroupRows - 1)], 1u)] = static_cast<uint32_t>(v);
+  }
+  __syncthreads();
+  const uint32_t nw = blockDim.x >> 5;
+  for (uint32_t r = warp; r < kGroupRows; r += nw) {
+    const uint32_t a = rs[r], l = rs[r + 1] - a;
+    if (l <= 1) continue;
+    uint32_t* row = sc + a;
+    if (l <= 32) sort_row<1>(row, l, lane);
+    else if (l <= 64) sort_row<2>(row, l, lane);
+    else if (l <= 128) sort_row<4>(row, l, lane);
+    else if (l <= 256) sort_row<8>(row, l, lane);
+    else if (l <= 512) sort_row<16>(row, l, lane);
+    else if (l <= 1024) sort_row<32>(row, l, lane);
+  }
+  // rows over 1024 (rare; at most kGroupCap / 1025 of them) go straight to cols
+  uint32_t big_lo[kGroupCap / 1025], big_hi[kGroupCap / 1025], nbig = 0;
+  for (uint32_t r = 0; r < kGroupRows; ++r)
+    if (rs[r + 1] - rs[r] > 1024) {
+      block_rank_row(sc + rs[r], rs[r + 1] - rs[r], cols + b + rs[r]);
+      big_lo[nbig] = rs[r];
+      big_hi[nbig++] = rs[r + 1];
+    }
+  __syncthreads();
+  for (uint32_t k = tid; k < len; k += blockDim.x) {
+    bool in_big = false;
+    for (uint32_t t = 0; t < nbig; ++t) in_big |= k >= big_lo[t] && k < big_hi[t];
+    if (!in_big) cols[b + k] = sc[k];
+  }
+  for (uint32_t r = tid; r < kGroupRows; r += blockDim.x)
+    if (r0 + r < n) offs[r0 + r] = static_cast<uint64_t>(b) + rs[r];
+}
+
 int bits_for(uint64_t n) {
   int b = 1;
   while ((1ull << b) < n) ++b;
@@ -1086,6 +1233,86 @@ void sorted_list_to_host(const FrnnRun& run, uint64_t n, uint64_t* host, uint64_
 // its columns and row offsets, and copied on the copy stream while the next
 // bucket sorts.  12 bytes per pair less 4: the 530 MB of C4's packed pairs
 // become 265 MB of columns + 32 MB of offsets.
+// The (i<j) lists as CSR through the row-group kernels (k_group_*), the
+// group sorts in chunks so the copies overlap them.  Returns false (nothing
+// written) when the shape is outside their limits: more than kMaxGroups
+// groups, a group over kGroupCap pairs, or 2^32 pairs.
+bool sorted_csr_groups(const FrnnRun& run, uint64_t n, uint64_t* offs, uint32_t* cols, uint64_t cap,
+                       cudaStream_t s) {
+  Ctx& c = ctx();
+  const uint64_t m = run.count;
+  const uint32_t ng = static_cast<uint32_t>((n + kGroupRows - 1) >> kGroupShift);
+  if (ng > kMaxGroups || m >= 0xffffffffull || m == 0) return false;
+  static const bool configured = [] {
+    PSG_CUDA(cudaFuncSetAttribute(k_group_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxGroups * 4));
+    PSG_CUDA(cudaFuncSetAttribute(k_group_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxGroups * 8));
+    PSG_CUDA(cudaFuncSetAttribute(k_group_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kGroupCap * 4));
+    return true;
+  }();
+  (void)configured;
+  DevBuf<unsigned> gcnt(ng + 1, s);
+  PSG_CUDA(cudaMemsetAsync(gcnt.p, 0, (ng + 1) * 4, s));
+  k_group_hist<<<c.sm_count, kGroupHistThreads, ng * 4, s>>>(run.pairs.p, m, ng, gcnt.p);
+  PSG_LAUNCHED();
+  std::vector<uint32_t> gs(ng + 1);
+  PSG_CUDA(cudaMemcpyAsync(gs.data(), gcnt.p, ng * 4, cudaMemcpyDeviceToHost, s));
+  PSG_CUDA(cudaStreamSynchronize(s));
+  uint32_t run_sum = 0, biggest = 0;
+  for (uint32_t g = 0; g < ng; ++g) {
+    const uint32_t v = gs[g];
+    biggest = std::max(biggest, v);
+    gs[g] = run_sum;
+    run_sum += v;
+  }
+  gs[ng] = run_sum;
+  trace("csr groups: histogram");
+  if (biggest > kGroupCap) return false;
+  DevBuf<uint32_t> gstart(ng + 1, s);
+  DevBuf<uint64_t> grouped(m, s), doffs(n + 1, s);
+  DevBuf<uint32_t> dcols(m, s);
+  PSG_CUDA(cudaMemcpyAsync(gstart.p, gs.data(), (ng + 1) * 4, cudaMemcpyHostToDevice, s));
+  PSG_CUDA(cudaMemcpyAsync(gcnt.p, gstart.p, ng * 4, cudaMemcpyDeviceToDevice, s));  // cursors
+  // one pass by group, a contiguous slice per block (a coarse pass first to
+  // lengthen the runs measured the same: ~0.57 ms per pass over C4's 66M pairs)
+  k_group_scatter<<<c.sm_count, kGroupHistThreads, ng * 8, s>>>(run.pairs.p, m, kGroupShift, ng, 0, gcnt.p,
+                                                                 grouped.p);
+  PSG_LAUNCHED();
+  g_launches += 2;
+  if (!c.copy_stream) PSG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+  const uint32_t chunks = std::min<uint32_t>(ng, 16);
+  std::vector<cudaEvent_t> ev(chunks);
+  for (auto& e : ev) e = c.get_event();
+  for (uint32_t k = 0; k < chunks; ++k) {
+    const uint32_t ga = static_cast<uint32_t>(static_cast<uint64_t>(ng) * k / chunks);
+    const uint32_t gb = static_cast<uint32_t>(static_cast<uint64_t>(ng) * (k + 1) / chunks);
+    if (gb > ga) {
+      k_group_sort<<<gb - ga, kGroupSortThreads, kGroupCap * 4, s>>>(grouped.p, gstart.p, ga, n, dcols.p, doffs.p);
+      PSG_LAUNCHED();
+      ++g_launches;
+    }
+    PSG_CUDA(cudaEventRecord(ev[k], s));
+  }
+  trace("csr groups: enqueued");
+  for (uint32_t k = 0; k < chunks; ++k) {
+    const uint32_t ga = static_cast<uint32_t>(static_cast<uint64_t>(ng) * k / chunks);
+    const uint32_t gb = static_cast<uint32_t>(static_cast<uint64_t>(ng) * (k + 1) / chunks);
+    PSG_CUDA(cudaStreamWaitEvent(c.copy_stream, ev[k], 0));
+    const uint64_t ra = static_cast<uint64_t>(ga) << kGroupShift, rb = std::min<uint64_t>(n, uint64_t(gb) << kGroupShift);
+    if (rb > ra)
+      PSG_CUDA(cudaMemcpyAsync(offs + ra, doffs.p + ra, (rb - ra) * 8, cudaMemcpyDeviceToHost, c.copy_stream));
+    const uint64_t ca = gs[ga], cb = std::min<uint64_t>(gs[gb], cap);
+    if (cb > ca)
+      PSG_CUDA(cudaMemcpyAsync(cols + ca, dcols.p + ca, (cb - ca) * 4, cudaMemcpyDeviceToHost, c.copy_stream));
+  }
+  PSG_CUDA(cudaStreamSynchronize(s));
+  trace("csr groups: sorted");
+  PSG_CUDA(cudaStreamSynchronize(c.copy_stream));
+  trace("csr groups: copied");
+  offs[n] = m;
+  for (auto& e : ev) c.put_event(e);
+  return true;
+}
+
 void sorted_csr_to_host(const FrnnRun& run, uint64_t n, uint64_t* offs, uint32_t* cols, uint64_t cap,
                         cudaStream_t s) {
   Ctx& c = ctx();
@@ -1195,7 +1422,9 @@ void frnn_pairs_csr(psg_pointset* ps, double radius, uint64_t q, double f, uint6
   *hash = run.hash;
   if (!offsets) return;
   StageTimer tm(s);
-  sorted_csr_to_host(run, ps->n, offsets, cols, cols ? capacity : 0, s);
+  static const bool radix = std::getenv("PSG_CSR_RADIX") != nullptr;  // A/B: the i-range radix buckets
+  if (radix || !sorted_csr_groups(run, ps->n, offsets, cols, cols ? capacity : 0, s))
+    sorted_csr_to_host(run, ps->n, offsets, cols, cols ? capacity : 0, s);
   tm.mark("sort+d2h");
   trace("frnn: csr to host");
   PSG_CUDA(cudaStreamSynchronize(s));

@@ -79,14 +79,17 @@ void h2d_staged(void* dst, uint64_t bytes, const std::function<size_t(char*, uin
     if (!c.stage_done[k]) PSG_CUDA(cudaEventCreateWithFlags(&c.stage_done[k], cudaEventDisableTiming));
   }
   char* out = static_cast<char*>(dst);
+  const uint64_t chunk = Ctx::kStageBytes;
   int k = 0;
-  for (uint64_t off = 0; off < bytes; off += Ctx::kStageBytes, k ^= 1) {
-    const size_t len = static_cast<size_t>(std::min<uint64_t>(Ctx::kStageBytes, bytes - off));
+  for (uint64_t off = 0; off < bytes; off += chunk, k ^= 1) {
+    const size_t len = static_cast<size_t>(std::min<uint64_t>(chunk, bytes - off));
     PSG_CUDA(cudaEventSynchronize(c.stage_done[k]));  // chunk k's previous upload has left it
+    trace("h2d: buffer free");
     if (fill(c.stage[k], off, len) != len) {
       cudaStreamSynchronize(s);
       throw std::runtime_error("short read while staging host input");
     }
+    trace("h2d: filled");
     PSG_CUDA(cudaMemcpyAsync(out + off, c.stage[k], len, cudaMemcpyHostToDevice, s));
     PSG_CUDA(cudaEventRecord(c.stage_done[k], s));
   }
@@ -390,7 +393,9 @@ psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev
   ps->d = static_cast<int>(d);
   ps->kind = kRowsF32;
   ps->device = c.device;
+  trace("rows32: enter");
   upload(ps->src32, p, n * d, dev_src, s, &ps->h2d_bytes);
+  trace("rows32: upload enqueued");
   DevBuf<unsigned> flags(3, s);
   PSG_CUDA(cudaMemsetAsync(flags.p, 0, 12, s));
   if (n * d) {
@@ -402,6 +407,7 @@ psg_pointset* pointset_rows_f32(const float* p, uint64_t n, uint64_t d, bool dev
   unsigned h[3];
   PSG_CUDA(cudaMemcpyAsync(h, flags.p, 12, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaStreamSynchronize(s));
+  trace("rows32: checked");
   if (h[0]) throw invalid_argument("point coordinate must be finite");
   float mx;
   std::memcpy(&mx, &h[1], 4);

@@ -251,6 +251,24 @@ def test_frnn_csr_matches_sorted_pairs(psg, orc, n, k):
         assert np.array_equal(short, wcols[: short.size])
 
 
+def test_frnn_csr_long_row(psg):
+    """A row of 1100 columns inside a row group under the group capacity: the
+    block-wide sort path of the group CSR kernel."""
+    rng = np.random.default_rng(7)
+    R = 1.0
+    pts = np.zeros((1356, 64), np.float32)
+    far = rng.normal(size=(255, 64)).astype(np.float32)
+    pts[1:256] = 50.0 * far / np.linalg.norm(far, axis=1, keepdims=True) * (1 + np.arange(255)[:, None])
+    ring = rng.normal(size=(1100, 64))
+    pts[256:] = (0.9 * R * ring / np.linalg.norm(ring, axis=1, keepdims=True)).astype(np.float32)
+    pairs, cnt, h = psg.frnn_pairs(pts, R)
+    off, cols, c2, h2 = psg.frnn_pairs_csr(pts, R)
+    assert (c2, h2) == (cnt, h)
+    assert int(off[1] - off[0]) >= 1100
+    woff, wcols = _csr_from_pairs(pairs, pts.shape[0])
+    assert np.array_equal(off, woff) and np.array_equal(cols, wcols)
+
+
 def test_c5_recipe_small(psg, orc):
     pts = orc.gen_mixture(5, 8192, 64, 1024, 0.05)
     want = orc.brute_force_closest_pair(pts, 0)
