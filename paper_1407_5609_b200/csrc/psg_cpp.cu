@@ -92,8 +92,7 @@ __global__ void __launch_bounds__(256) k_project_small(const float* __restrict__
     for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
     if (cc.gp) count_cell<NK>(acc, r, cc);
   }
-  nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
-  if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
+  block_max_to(norm2_bits, __float_as_uint(nn));
 }
 
 // Small or irregular d: one thread per row, U staged in shared memory.
@@ -124,8 +123,7 @@ __global__ void __launch_bounds__(256) k_project_thread(const float* __restrict_
 #pragma unroll
     for (int v = 0; v < NK / 4; ++v) out[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
   }
-  nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
-  if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
+  block_max_to(norm2_bits, __float_as_uint(nn));
 }
 
 // Window sets (virtual rows, psg_points.cuh Rows): one thread per window.
@@ -181,8 +179,7 @@ __global__ void __launch_bounds__(kWinRows) k_project_windows(Rows R, uint32_t n
     for (int q = 0; q < NK / 4; ++q) out[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
     if (cc.gp) count_cell<NK>(acc, i0 + r, cc);
   }
-  nn = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(nn)));
-  if ((threadIdx.x & 31) == 0) atomicMax(norm2_bits, __float_as_uint(nn));
+  block_max_to(norm2_bits, __float_as_uint(nn));
 }
 
 template <int NK>
@@ -584,13 +581,27 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
       record_scan<kExact>(a, pi, pj, sd, band);
     }
   }
+  // the block's counts in one atomic each (per-warp atomics on one address
+  // serialise at the L2: 32K warps at C2)
+  __shared__ unsigned long long wv[kThreads / 32], we[kThreads / 32];
   for (int o = 16; o; o >>= 1) {
     visited += __shfl_xor_sync(kFull, visited, o);
     inline_evals += __shfl_xor_sync(kFull, inline_evals, o);
   }
-  if (lane == 0 && visited) atomicAdd(a.visited, visited);
-  if (lane == 0 && inline_evals) atomicAdd(a.evals, inline_evals);
-  if (tid == 0 && nq) atomicAdd(a.evals, static_cast<unsigned long long>(nq));
+  if (lane == 0) {
+    wv[tid >> 5] = visited;
+    we[tid >> 5] = inline_evals;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long v = 0, e = static_cast<unsigned long long>(nq);
+    for (int w = 0; w < kThreads / 32; ++w) {
+      v += wv[w];
+      e += we[w];
+    }
+    if (v) atomicAdd(a.visited, v);
+    if (e) atomicAdd(a.evals, e);
+  }
 }
 
 // K6: deterministic final filter + FP64 recheck in the reference's order.
@@ -878,9 +889,10 @@ __global__ void __launch_bounds__(256) k_boot_select(ScanArgs a, const float* __
     const float s = a.d <= kInlineD ? (lane == 0 ? thread_sqdist(a.rows, 0, z) : 0.f) : warp_sqdist(a.rows, 0, z, lane);
     if (lane == 0) atomicMin(a.best, __float_as_uint(s));
   }
-  if (gw >= nw) return;
+  // every warp of the block reaches the block minimum below (one atomic per
+  // block: per-warp atomics on one address serialise at the L2)
   const uint32_t chunk = (W + nw - 1) / nw;
-  const uint32_t e0 = gw * chunk, e1 = min(W, e0 + chunk);
+  const uint32_t e0 = gw < nw ? gw * chunk : W, e1 = min(W, e0 + chunk);
   float lb = INFINITY;
   uint32_t at = 0;
   for (uint32_t e = e0 + lane; e < e1; e += 32) {
@@ -898,17 +910,26 @@ __global__ void __launch_bounds__(256) k_boot_select(ScanArgs a, const float* __
       at = oa;
     }
   }
-  if (!(lb < INFINITY)) return;
-  const uint2 pr = wpair[at];
-  float s = 0.f;
-  for (int t = lane; t < a.d; t += 32) {
-    const float g = row_at(a.rows, pr.x, t) - row_at(a.rows, pr.y, t);
-    s = fmaf(g, g, s);
-  }
+  float s = INFINITY;
+  if (lb < INFINITY) {
+    const uint2 pr = wpair[at];
+    s = 0.f;
+    for (int t = lane; t < a.d; t += 32) {
+      const float g = row_at(a.rows, pr.x, t) - row_at(a.rows, pr.y, t);
+      s = fmaf(g, g, s);
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  s = __fmul_ru(s, 1.0f + static_cast<float>(2 * a.d + 8) * 0x1.0p-24f);  // see warp_eval_best
-  if (lane == 0) atomicMin(a.best, __float_as_uint(s));
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    s = __fmul_ru(s, 1.0f + static_cast<float>(2 * a.d + 8) * 0x1.0p-24f);  // see warp_eval_best
+  }
+  __shared__ float wmin[8];
+  if (lane == 0) wmin[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = wmin[0];
+    for (int w = 1; w < 8; ++w) m = fminf(m, wmin[w]);
+    if (m < INFINITY) atomicMin(a.best, __float_as_uint(m));
+  }
 }
 
 }  // namespace

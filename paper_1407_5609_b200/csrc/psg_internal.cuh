@@ -58,6 +58,24 @@ struct cuda_error : std::runtime_error {
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// The block's maximum of v into *dst: one atomic per block, and none when
+// the current value is already as large (after the first blocks it usually
+// is; every warp hitting one address serialises at the L2).  Every thread
+// of the block calls it.
+__device__ __forceinline__ void block_max_to(unsigned* dst, unsigned v) {
+  __shared__ unsigned wmax[32];
+  __syncthreads();  // a previous call's readers are done with wmax
+  v = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned nw = (blockDim.x + 31) >> 5;
+    unsigned m = threadIdx.x < nw ? wmax[threadIdx.x] : 0u;
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (threadIdx.x == 0 && m > *reinterpret_cast<volatile unsigned*>(dst)) atomicMax(dst, m);
+  }
+}
+
 #endif
 bool pdl_enabled();  // PSG_NO_PDL=1: plain launches (A/B)
 template <class... P, class... A>

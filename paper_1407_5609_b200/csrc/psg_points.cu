@@ -170,11 +170,9 @@ __global__ void __launch_bounds__(256) k_check_rows_f32(const float* __restrict_
   m = __reduce_max_sync(0xffffffffu, m);
   nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
   const unsigned wb = __reduce_max_sync(0xffffffffu, __float_as_uint(worst));
-  if ((threadIdx.x & 31) == 0) {
-    if (nonfinite) atomicOr(flags, 1u);
-    atomicMax(flags + 1, m);
-    atomicMax(flags + 2, wb);
-  }
+  if ((threadIdx.x & 31) == 0 && nonfinite) atomicOr(flags, 1u);
+  block_max_to(flags + 1, m);
+  block_max_to(flags + 2, wb);
 }
 
 // max over rows of the FP32 sum of squares of a row (a per-set invariant the
