@@ -283,39 +283,55 @@ __global__ void k_series_f32(const double* __restrict__ s, uint64_t len, double 
 // One warp per window: the narrowing radius of the virtual FP32 row against
 // the reference's FP64 window values (exact_coord order, times scale), in
 // FP64, and the row's FP32 sum of squares; both max-reduced.
-__global__ void k_window_check(Rows R, ExactSrc src, uint64_t nw, double scale,
-                               unsigned long long* __restrict__ r2max_bits, unsigned* __restrict__ norm2_bits) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+__global__ void __launch_bounds__(256) k_window_check(Rows R, ExactSrc src, uint64_t nw, double scale,
+                                                      unsigned long long* __restrict__ r2max_bits,
+                                                      unsigned* __restrict__ norm2_bits) {
+  // one thread per window, coordinates in order: a warp's 32 windows read the
+  // same 32 + t series values per step (coalesced, L1), and the per-value work
+  // is a handful of instructions (a warp per window spent ~55 per value on
+  // lane bookkeeping and shuffles: 1.5 ms at C3)
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   double worst = 0.0;
   float wn = 0.f;
-  for (uint64_t r = warp; r < nw; r += nwarps) {
+  if (i < nw) {
+    // z-normalised: the reference's (s - mu) / sigma as (s - mu) * (1 / sigma),
+    // within 2^-51 |x| of it (one FP64 division per window; the host adds
+    // len * 2^-50 to Rn for it)
+    const bool z = src.kind == kWindowsZ;
+    float m = 0.f, rr = 1.f;
+    double mu = 0.0, inv = scale;
+    if (z) {
+      m = R.m32[i];
+      rr = R.r32[i];
+      mu = src.mu[i];
+      const double sg = src.sigma[i];
+      inv = sg == 0.0 ? 0.0 : 1.0 / sg;
+    }
+    const float* sp = R.s32 + i;
+    const double* dp = src.f64 + i;
     double acc = 0.0;
     float nn = 0.f;
-    // z-normalised: the reference's (s - mu) / sigma as (s - mu) * (1 / sigma),
-    // within 2^-51 |x| of it (one FP64 division per window instead of one per
-    // value; the host adds len * 2^-50 to Rn for it)
-    const bool z = src.kind == kWindowsZ;
-    const double mu = z ? src.mu[r] : 0.0, sg = z ? src.sigma[r] : 1.0;
-    const double inv = sg == 0.0 ? 0.0 : 1.0 / sg;
-    for (int t = lane; t < R.d; t += 32) {
-      const float x = row_at(R, r, t);
-      const double xe = z ? (src.f64[r + t] - mu) * inv : exact_coord(src, r, t);
-      const double e = xe * scale - static_cast<double>(x);
+    for (int t = 0; t < R.d; ++t) {
+      const float v = sp[t];
+      const float x = z ? __fmul_rn(__fsub_rn(v, m), rr) : v;  // row_at, virtual window row
+      const double xe = (dp[t] - mu) * inv;                     // raw: mu = 0, inv = scale
+      const double e = xe - static_cast<double>(x);
       acc = fma(e, e, acc);
       nn = fmaf(x, x, nn);
     }
-    for (int o = 16; o; o >>= 1) {
-      acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      nn += __shfl_xor_sync(0xffffffffu, nn, o);
-    }
-    worst = fmax(worst, acc);
-    wn = fmaxf(wn, nn);
+    worst = acc;
+    wn = nn;
   }
-  if (lane == 0) {
-    atomic_max_nonneg(r2max_bits, worst);
-    atomicMax(norm2_bits, __float_as_uint(wn));
+  // one atomic per block for each maximum (non-negative doubles order as their bits)
+  __shared__ unsigned long long wr[32];
+  unsigned long long wm = static_cast<unsigned long long>(__double_as_longlong(worst));
+  for (int o = 16; o; o >>= 1) wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+  if ((threadIdx.x & 31) == 0) wr[threadIdx.x >> 5] = wm;
+  block_max_to(norm2_bits, __float_as_uint(wn));  // its barrier also publishes wr
+  if (threadIdx.x == 0) {
+    unsigned long long mx = 0;
+    for (unsigned w = 0; w < (blockDim.x + 31) / 32; ++w) mx = max(mx, wr[w]);
+    if (mx) atomicMax(r2max_bits, mx);
   }
 }
 
@@ -525,8 +541,8 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
   PSG_LAUNCHED();
   DevBuf<unsigned> nb(1, s);
   PSG_CUDA(cudaMemsetAsync(nb.p, 0, 4, s));
-  k_window_check<<<grid_for(nw * 32, 256, c.sm_count), 256, 0, s>>>(ps->rows(), ps->exact(), nw, ps->scale,
-                                                                     mx.p + 1, nb.p);
+  k_window_check<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, s>>>(ps->rows(), ps->exact(), nw, ps->scale,
+                                                                          mx.p + 1, nb.p);
   PSG_LAUNCHED();
   g_launches += 2;
   ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d) + (znorm ? static_cast<double>(len) * 0x1.0p-50 : 0.0);
