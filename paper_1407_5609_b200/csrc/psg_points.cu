@@ -280,9 +280,9 @@ __global__ void k_series_f32(const double* __restrict__ s, uint64_t len, double 
     out[i] = __double2float_rn(s[i] * scale);
 }
 
-// One warp per window: the narrowing radius of the virtual FP32 row against
-// the reference's FP64 window values (exact_coord order, times scale), in
-// FP64, and the row's FP32 sum of squares; both max-reduced.
+// The narrowing radius of each virtual FP32 window row against the
+// reference's FP64 window values (exact_coord order, times scale), in FP64,
+// and the row's FP32 sum of squares; both max-reduced.
 __global__ void __launch_bounds__(256) k_window_check(Rows R, ExactSrc src, uint64_t nw, double scale,
                                                       unsigned long long* __restrict__ r2max_bits,
                                                       unsigned* __restrict__ norm2_bits) {
