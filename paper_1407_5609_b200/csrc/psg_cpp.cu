@@ -126,23 +126,27 @@ __global__ void __launch_bounds__(256) k_project_thread(const float* __restrict_
   block_max_to(norm2_bits, __float_as_uint(nn));
 }
 
-// Window sets (virtual rows, psg_points.cuh Rows): one thread per window.
-// A block stages the series segment its 128 windows span (128 + d - 1
-// values) and, when it fits, U transposed (d x NK: one broadcast per tap and
-// key quad); each thread then forms its row on the fly — the same FP32
-// values every other reader sees — and accumulates the NK keys and the row's
-// sum of squares in coordinate order.  No n_w x d buffer is read or written:
-// the C3 projection reads the 4 MiB series instead of 1 GiB of rows.
+// Window sets (virtual rows, psg_points.cuh Rows): kWinW consecutive windows
+// per thread.  A block stages the series segment its kWinRows * kWinW windows
+// span and, when it fits, U transposed (d x NK: one broadcast per tap and key
+// quad); each thread slides a register window of kWinW series values along
+// the taps, forms its rows on the fly — the same FP32 values every other
+// reader sees — and accumulates each window's NK keys in coordinate order.
+// Per tap the series value and U are loaded once for kWinW windows.  No
+// n_w x d buffer is read or written: the C3 projection reads the 4 MiB series
+// instead of 1 GiB of rows.  (The window rows' norms are measured once, when
+// the set is built: k_window_check.)
 constexpr int kWinRows = 128;
+constexpr int kWinW = 4;
 template <int NK>
 __global__ void __launch_bounds__(kWinRows) k_project_windows(Rows R, uint32_t n, const float* __restrict__ Ut,
-                                                              float* __restrict__ keys, unsigned* __restrict__ norm2_bits,
-                                                              int u_smem, int seg_smem, CellCount cc) {
+                                                              float* __restrict__ keys, int u_smem, int seg_smem,
+                                                              CellCount cc) {
   extern __shared__ float4 sh4[];
   float* sh = reinterpret_cast<float*>(sh4);
   const int d = R.d;
-  const uint32_t i0 = blockIdx.x * kWinRows;
-  const uint32_t cnt = min(static_cast<uint32_t>(kWinRows), n - i0);
+  const uint32_t i0 = blockIdx.x * (kWinRows * kWinW);
+  const uint32_t cnt = min(static_cast<uint32_t>(kWinRows * kWinW), n - i0);
   float* su = sh;  // d x NK (16-byte aligned)
   float* seg = sh + (u_smem ? d * NK : 0);
   if (u_smem)
@@ -150,36 +154,55 @@ __global__ void __launch_bounds__(kWinRows) k_project_windows(Rows R, uint32_t n
   if (seg_smem)
     for (uint32_t k = threadIdx.x; k < cnt + d - 1; k += kWinRows) seg[k] = R.s32[i0 + k];
   __syncthreads();
-  const int r = threadIdx.x;
-  float nn = 0.f;
-  if (r < static_cast<int>(cnt)) {
-    const float* Us = u_smem ? su : Ut;
-    const float* x = seg_smem ? seg + r : R.s32 + i0 + r;
-    const bool z = R.m32 != nullptr;
-    const float m = z ? R.m32[i0 + r] : 0.f, rr = z ? R.r32[i0 + r] : 1.f;
-    float acc[NK];
+  const uint32_t r0 = threadIdx.x * kWinW;  // this thread's first window, block-relative
+  if (r0 >= cnt) return;
+  const float* Us = u_smem ? su : Ut;
+  const float* x = seg_smem ? seg + r0 : R.s32 + i0 + r0;
+  const bool z = R.m32 != nullptr;
+  float m[kWinW], rr[kWinW], acc[kWinW][NK], ring[kWinW];
 #pragma unroll
-    for (int k = 0; k < NK; ++k) acc[k] = 0.f;
-    for (int t = 0; t < d; ++t) {
-      float v = x[t];
-      if (z) v = __fmul_rn(__fsub_rn(v, m), rr);
-      nn = fmaf(v, v, nn);
-      const float4* u4 = reinterpret_cast<const float4*>(Us + t * NK);
+  for (int w = 0; w < kWinW; ++w) {
+    const uint32_t i = min(i0 + r0 + w, n - 1);  // past the end: a duplicate, not stored
+    m[w] = z ? R.m32[i] : 0.f;
+    rr[w] = z ? R.r32[i] : 1.f;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) acc[w][k] = 0.f;
+  }
+  // ring[w] = series value at tap t of window r0 + w = x[t + w]; offsets past
+  // the last valid one (windows beyond the set's end, never stored) are
+  // clamped so no read leaves the segment / series
+  const uint32_t last = cnt - r0 - 1 + d - 1;
+#pragma unroll
+  for (int w = 0; w < kWinW - 1; ++w) ring[w] = x[min(static_cast<uint32_t>(w), last)];
+  for (int t = 0; t < d; ++t) {
+    ring[kWinW - 1] = x[min(static_cast<uint32_t>(t + kWinW - 1), last)];
+    float4 u[NK / 4];
+    const float4* u4 = reinterpret_cast<const float4*>(Us + t * NK);
+#pragma unroll
+    for (int q = 0; q < NK / 4; ++q) u[q] = u4[q];
+#pragma unroll
+    for (int w = 0; w < kWinW; ++w) {
+      const float v = z ? __fmul_rn(__fsub_rn(ring[w], m[w]), rr[w]) : ring[w];
 #pragma unroll
       for (int q = 0; q < NK / 4; ++q) {
-        const float4 u = u4[q];
-        acc[4 * q + 0] = fmaf(u.x, v, acc[4 * q + 0]);
-        acc[4 * q + 1] = fmaf(u.y, v, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(u.z, v, acc[4 * q + 2]);
-        acc[4 * q + 3] = fmaf(u.w, v, acc[4 * q + 3]);
+        acc[w][4 * q + 0] = fmaf(u[q].x, v, acc[w][4 * q + 0]);
+        acc[w][4 * q + 1] = fmaf(u[q].y, v, acc[w][4 * q + 1]);
+        acc[w][4 * q + 2] = fmaf(u[q].z, v, acc[w][4 * q + 2]);
+        acc[w][4 * q + 3] = fmaf(u[q].w, v, acc[w][4 * q + 3]);
       }
     }
-    float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(i0 + r) * NK);
 #pragma unroll
-    for (int q = 0; q < NK / 4; ++q) out[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-    if (cc.gp) count_cell<NK>(acc, i0 + r, cc);
+    for (int w = 0; w < kWinW - 1; ++w) ring[w] = ring[w + 1];
   }
-  block_max_to(norm2_bits, __float_as_uint(nn));
+#pragma unroll
+  for (int w = 0; w < kWinW; ++w) {
+    if (r0 + w >= cnt) break;
+    float4* out = reinterpret_cast<float4*>(keys + static_cast<size_t>(i0 + r0 + w) * NK);
+#pragma unroll
+    for (int q = 0; q < NK / 4; ++q)
+      out[q] = make_float4(acc[w][4 * q], acc[w][4 * q + 1], acc[w][4 * q + 2], acc[w][4 * q + 3]);
+    if (cc.gp) count_cell<NK>(acc[w], i0 + r0 + w, cc);
+  }
 }
 
 template <int NK>
@@ -391,7 +414,9 @@ __global__ void __launch_bounds__(kThreads) k_scan(ScanArgs a, uint32_t lo, uint
 // 3^g cell stencil, so each unordered pair is visited exactly once.
 
 // Warp argmin of (lb, p) and one exact FP32 evaluation of the winner.
-__device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint32_t j, uint32_t p, int lane) {
+// Returns the (rounded-up) FP32 squared distance of the warp's winner, +inf
+// when the warp has none; the caller min-reduces it per block.
+__device__ __forceinline__ float warp_eval_best(const ScanArgs& a, float lb, uint32_t j, uint32_t p, int lane) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     const float olb = __shfl_xor_sync(kFull, lb, o);
@@ -403,7 +428,7 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
       p = op;
     }
   }
-  if (j == 0xffffffffu) return;
+  if (j == 0xffffffffu) return INFINITY;
   const uint32_t xi = a.sidx[p], xj = a.sidx[j];
   // Warp-parallel sum (not the canonical order), rounded up by (2d+8) ulps
   // relative: two FP32 orders of a sum of d non-negative terms differ by at
@@ -417,8 +442,7 @@ __device__ __forceinline__ void warp_eval_best(const ScanArgs& a, float lb, uint
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  s = __fmul_ru(s, 1.0f + static_cast<float>(2 * a.d + 8) * 0x1.0p-24f);
-  if (lane == 0) atomicMin(a.best, __float_as_uint(s));
+  return __fmul_ru(s, 1.0f + static_cast<float>(2 * a.d + 8) * 0x1.0p-24f);
 }
 
 // K3a (grid): per position, the stencil candidate with the least key lower
@@ -465,7 +489,16 @@ __global__ void __launch_bounds__(kThreads) k_grid_bootstrap(ScanArgs a, GridDev
       }
     }
   }
-  warp_eval_best(a, best_lb, best_j, p, lane);
+  const float s = warp_eval_best(a, best_lb, best_j, p, lane);
+  // one atomic per block (per-warp atomics on one address serialise at the L2)
+  __shared__ float wmin[kThreads / 32];
+  if (lane == 0) wmin[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = wmin[0];
+    for (int w = 1; w < kThreads / 32; ++w) m = fminf(m, wmin[w]);
+    if (m < INFINITY) atomicMin(a.best, __float_as_uint(m));
+  }
 }
 
 // Before the scan: the grid must hold every pair whose key gaps are within
@@ -1002,7 +1035,8 @@ void project_windows(const psg_pointset& ps, const Directions& dir, float* keys,
   const uint32_t n = static_cast<uint32_t>(ps.n);
   const int d = ps.d, nk = dir.nk;
   const float* Ut = window_directions(ps, dir, s);
-  const size_t ubytes = static_cast<size_t>(d) * nk * 4, sbytes = (static_cast<size_t>(kWinRows) + d) * 4;
+  const size_t ubytes = static_cast<size_t>(d) * nk * 4,
+               sbytes = (static_cast<size_t>(kWinRows) * kWinW + d + kWinW) * 4;
   constexpr size_t kMaxSmem = 200 * 1024;
   const int u_smem = ubytes <= kMaxSmem - std::min(sbytes, kMaxSmem / 2) ? 1 : 0;
   const int seg_smem = (u_smem ? ubytes : 0) + sbytes <= kMaxSmem ? 1 : 0;
@@ -1010,13 +1044,13 @@ void project_windows(const psg_pointset& ps, const Directions& dir, float* keys,
   if (nk == 4) {
     if (smem > 48 * 1024)
       PSG_CUDA(cudaFuncSetAttribute(k_project_windows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k_project_windows<4><<<blocks_for(n, kWinRows), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, norm2_bits, u_smem,
-                                                                         seg_smem, cc);
+    k_project_windows<4><<<blocks_for(n, kWinRows * kWinW), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, u_smem,
+                                                                                  seg_smem, cc);
   } else {
     if (smem > 48 * 1024)
       PSG_CUDA(cudaFuncSetAttribute(k_project_windows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k_project_windows<8><<<blocks_for(n, kWinRows), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, norm2_bits, u_smem,
-                                                                         seg_smem, cc);
+    k_project_windows<8><<<blocks_for(n, kWinRows * kWinW), kWinRows, smem, s>>>(ps.rows(), n, Ut, keys, u_smem,
+                                                                                  seg_smem, cc);
   }
 }
 
