@@ -522,17 +522,25 @@ __global__ void k_scan_prepare(DevState* st, const GridParams* gp) {
 // K3b (grid): one pass per sorted position over its (at most five) stencil
 // ranges with the key lower bound at the threshold it read at start (the
 // bound only tightens, so a stale threshold only admits more); survivors go to
-// a shared-memory queue (global spill list when full) and whole warps evaluate
-// them as exact FP32 distances at the end of the block.
+// the warp's shared-memory queue (evaluated in place when full) and the warp's
+// lanes evaluate them as exact FP32 distances after its own loop — no block
+// barrier after the candidate loops, so a warp never waits for the block's
+// slowest position.  The block's counts reach global memory through the last
+// warp to finish (a shared-memory ticket): one atomic per block and counter.
+constexpr int kScanWarps = kThreads / 32;
+constexpr int kWarpQueue = kQueue / kScanWarps;
 template <int NK, bool kExact>
 __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, uint32_t lo, uint32_t hi,
                                                          const unsigned* __restrict__ regrid,
                                                          const Thresholds* __restrict__ th0) {
-  __shared__ uint32_t qp[kQueue], qj[kQueue];
-  __shared__ int qn;
+  __shared__ uint32_t qp[kScanWarps][kWarpQueue], qj[kScanWarps][kWarpQueue];
+  __shared__ int qn[kScanWarps];
+  __shared__ unsigned long long s_visited, s_evals;
+  __shared__ unsigned s_done;
+  __shared__ double s_win;
   __shared__ GridParams sP;  // one copy per block, not per thread (registers)
   if (*regrid) return;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t p = lo + blockIdx.x * kThreads + tid;
   // the position's own loads go out before the block barrier (they do not
   // need the shared grid parameters)
@@ -541,19 +549,22 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
   load_keys<NK>(a.skeys + static_cast<size_t>(pc) * NK, mk);
   const uint32_t mo = a.sidx[pc], mcell = G.scell[pc];
   const float lb2 = th0->lb2;
+  if (tid < kScanWarps) qn[tid] = 0;
   if (tid == 0) {
-    qn = 0;
     sP = *G.gp;
+    s_visited = s_evals = 0;
+    s_done = 0;
+    // rows the point is too far from to hold a passing pair are skipped
+    // (margin: cell faces are computed in FP64 like the cell ids, keys are
+    // FP32); one FP64 square root per block
+    s_win = sqrt(static_cast<double>(lb2)) * (1.0 + 0x1.0p-20) + 1e-6 * sP.w;
   }
   __syncthreads();
   unsigned long long visited = 0, inline_evals = 0;
   if (p < hi) {
-    // rows the point is too far from to hold a passing pair are skipped
-    // (margin: cell faces are computed in FP64 like the cell ids, keys are FP32)
-    const double win = sqrt(static_cast<double>(lb2)) * (1.0 + 0x1.0p-20) + 1e-6 * sP.w;
-    const GridFlat F = grid_flat(grid_ranges_pruned(G.cfirst, sP, p, mcell, mk, win));
+    const GridFlat F = grid_flat(grid_ranges_pruned(G.cfirst, sP, p, mcell, mk, s_win));
     const bool zoned = a.zone > 1;
-    // four candidates per step: all loads in flight before any math
+    // two candidates per step: all loads in flight before any math
     constexpr int B = 2;  // candidates in flight per step (registers vs latency)
     for (uint32_t t0 = 0; t0 < F.total; t0 += B) {
       uint32_t jj[B], oo[B];
@@ -593,10 +604,10 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
           sl = fmaf(g, g, sl);
           if (sl > lb2) continue;
         }
-        const int slot = atomicAdd(&qn, 1);
-        if (slot < kQueue) {
-          qp[slot] = p;
-          qj[slot] = j;
+        const int slot = atomicAdd(&qn[warp], 1);
+        if (slot < kWarpQueue) {
+          qp[warp][slot] = p;
+          qj[warp][slot] = j;
         } else {  // queue full: evaluate here (canonical order, bounded memory)
           record_scan<kExact>(a, p, j, thread_sqdist(a.rows, mo, a.sidx[j]), th0->band);
           ++inline_evals;
@@ -604,36 +615,31 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
       }
     }
   }
-  __syncthreads();
-  const int nq = min(qn, kQueue);
+  __syncwarp();
+  const int nq = min(qn[warp], kWarpQueue);
   if (nq > 0) {
     const float band = th0->band;  // >= the band of any tighter bound: a superset, refiltered by k_recheck
-    for (int i = tid; i < nq; i += kThreads) {  // one queued pair per thread
-      const uint32_t pi = qp[i], pj = qj[i];
+    for (int i = lane; i < nq; i += 32) {  // one queued pair per lane
+      const uint32_t pi = qp[warp][i], pj = qj[warp][i];
       const float sd = thread_sqdist(a.rows, a.sidx[pi], a.sidx[pj]);
       record_scan<kExact>(a, pi, pj, sd, band);
     }
   }
-  // the block's counts in one atomic each (per-warp atomics on one address
-  // serialise at the L2: 32K warps at C2)
-  __shared__ unsigned long long wv[kThreads / 32], we[kThreads / 32];
   for (int o = 16; o; o >>= 1) {
     visited += __shfl_xor_sync(kFull, visited, o);
     inline_evals += __shfl_xor_sync(kFull, inline_evals, o);
   }
   if (lane == 0) {
-    wv[tid >> 5] = visited;
-    we[tid >> 5] = inline_evals;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long v = 0, e = static_cast<unsigned long long>(nq);
-    for (int w = 0; w < kThreads / 32; ++w) {
-      v += wv[w];
-      e += we[w];
+    if (visited) atomicAdd(&s_visited, visited);
+    const unsigned long long e = inline_evals + static_cast<unsigned long long>(nq);
+    if (e) atomicAdd(&s_evals, e);
+    __threadfence_block();
+    if (atomicAdd(&s_done, 1u) == kScanWarps - 1) {  // the block's last warp
+      __threadfence_block();
+      const unsigned long long v = atomicAdd(&s_visited, 0ull), ev = atomicAdd(&s_evals, 0ull);
+      if (v) atomicAdd(a.visited, v);
+      if (ev) atomicAdd(a.evals, ev);
     }
-    if (v) atomicAdd(a.visited, v);
-    if (e) atomicAdd(a.evals, e);
   }
 }
 
