@@ -269,6 +269,27 @@ def test_frnn_csr_long_row(psg):
     assert np.array_equal(off, woff) and np.array_equal(cols, wcols)
 
 
+def test_frnn_csr_edge_cases(psg, orc):
+    """No pairs at all, two points, an exclusion zone, and the empty input
+    (the reference's message)."""
+    far = np.arange(40, dtype=np.float32).reshape(20, 2) * 100
+    off, cols, cnt, h = psg.frnn_pairs_csr(far, 1.0)
+    assert cnt == 0 and h == 0 and np.all(off == 0) and cols.size == 0
+    two = np.array([[0, 0], [0.5, 0]], np.float32)
+    off, cols, cnt, _ = psg.frnn_pairs_csr(two, 1.0)
+    assert cnt == 1 and list(off) == [0, 1, 1] and list(cols) == [1]
+    walk = orc.gen_random_walk(3000, 5)
+    win = np.lib.stride_tricks.sliding_window_view(walk, 8).astype(np.float32)
+    for zone in (0, 8):
+        pairs, c1, h1 = psg.frnn_pairs(win, 2.0, exclusion_zone=zone)
+        off, cols, c2, h2 = psg.frnn_pairs_csr(win, 2.0, exclusion_zone=zone)
+        assert (c2, h2) == (c1, h1)
+        woff, wcols = _csr_from_pairs(pairs, win.shape[0])
+        assert np.array_equal(off, woff) and np.array_equal(cols, wcols)
+    with pytest.raises(psg.InvalidArgument, match="empty input"):
+        psg.frnn_pairs_csr(np.zeros((0, 3), np.float32), 1.0)
+
+
 def test_c5_recipe_small(psg, orc):
     pts = orc.gen_mixture(5, 8192, 64, 1024, 0.05)
     want = orc.brute_force_closest_pair(pts, 0)
