@@ -53,6 +53,10 @@ constexpr int kChunk = 256;
 constexpr int kQueue = 1024;
 constexpr int kInlineD = 16;  // d <= 16: one thread per exact evaluation
 constexpr double kGridOccupancy = 0.25;   // mean points per cell over the key box (sweep: tools/occ_sweep.sh)
+// window sets (motifs): near-duplicate windows straddle cell faces far more
+// often; wider cells cost less than the regrid / full-stencil bootstrap the
+// narrow ones trigger (C3 graph solve 0.77 -> 0.67 ms; tools/gpu_r2s2_ac2.sh)
+constexpr double kGridOccupancyWindows = 1.5;
 constexpr double kGridBoxSd = 2.5;        // key box: mean +- kGridBoxSd sd (clipped to the sample range)
 constexpr int kGridBootCap = 256;         // candidates per point in the grid bootstrap
 int boot_own_row() {  // the first bootstrap looks at the own cell row only (one cfirst lookup)
@@ -1219,7 +1223,9 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   k_state_init<<<1, 1, 0, s>>>(W.st.p, ps->exact(), plan->grid ? W.gi.sidx.p : W.wsidx.p, plan->bud);
   PSG_LAUNCHED();
   {
-    static const double occupancy = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : kGridOccupancy;
+    static const double occ_env = std::getenv("PSG_OCC") ? std::atof(std::getenv("PSG_OCC")) : 0.0;
+    const bool windows = ps->kind == kWindowsZ || ps->kind == kWindowsRaw;
+    const double occupancy = occ_env > 0.0 ? occ_env : windows ? kGridOccupancyWindows : kGridOccupancy;
     static const double box_sd = std::getenv("PSG_BOXSD") ? std::atof(std::getenv("PSG_BOXSD")) : kGridBoxSd;
     // Learned hints (a width, the engine, the bootstrap mode) come from this
     // process's earlier solves; a sharded plan must not use them: every rank
