@@ -650,37 +650,56 @@ __global__ void __launch_bounds__(kThreads) k_grid_scan2(ScanArgs a, GridDev G, 
 // K6: deterministic final filter + FP64 recheck in the reference's order.
 // Thresholds come from the final FP32 bound on device; the candidate count is
 // min(candidates, capacity) read on device; grid-stride over candidates.
-template <int NK, bool kWindow>
+// kWarp: one warp per candidate, the exact distance's terms in parallel
+// (warp_exact_distance) — for d >= 32, where one thread per candidate is
+// latency-bound (a z-normalised window term costs two FP64 divisions: one
+// thread spent 76 us on C3's single candidate); else one thread per candidate.
+template <int NK, bool kWindow, bool kWarp>
 __global__ void k_recheck(ScanArgs a, ExactSrc src, double* __restrict__ d64, unsigned long long* __restrict__ best64,
                           unsigned long long* __restrict__ examined) {
   const uint32_t count = static_cast<uint32_t>(min(*a.cand_n, static_cast<unsigned long long>(a.cand_cap)));
-  if (blockIdx.x * blockDim.x >= count) return;  // usually one block has work (C2: one candidate)
+  constexpr uint32_t kPer = kWarp ? 32 : 1;  // threads per candidate
+  const uint32_t per_block = blockDim.x / kPer;
+  if (blockIdx.x * per_block >= count) return;  // usually one block has work (C2: one candidate)
   // the final bound's thresholds, once per block (FP64 sqrt / divisions)
   __shared__ Thresholds sth;
   if (threadIdx.x == 0) sth = budget_thresholds_s32(*a.bud, best_now(a.best));
   __syncthreads();
   const Thresholds th = sth;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < count; base += gridDim.x * blockDim.x) {
-  const uint32_t c = base + threadIdx.x;
-  unsigned pass = 0;
-  if (c < count) {
-    const uint32_t p = a.cand_p[c], j = a.cand_j[c];
-    float kp[NK], kj[NK];
-    load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, kp);
-    load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
-    const bool keep = (!kWindow || kj[0] - kp[0] <= th.win) && (lb2_full<NK>(kp, kj) <= th.lb2) &&
-                      (a.cand_s[c] <= th.band);
-    double dd = -1.0;
-    if (keep) {
-      dd = exact_distance(src, a.sidx[p], a.sidx[j]);
-      atomicMin(best64, static_cast<unsigned long long>(__double_as_longlong(dd)));
-      pass = 1;
+  const int lane = threadIdx.x & 31;
+  const uint32_t u0 = (blockIdx.x * blockDim.x + threadIdx.x) / kPer, nu = gridDim.x * per_block;
+  unsigned long long pass = 0;
+  for (uint32_t base = (u0 / per_block) * per_block; base < count; base += nu) {
+    const uint32_t c = base + (threadIdx.x / kPer);
+    bool keep = false;
+    uint32_t p = 0, j = 0;
+    if (c < count) {
+      p = a.cand_p[c];
+      j = a.cand_j[c];
+      float kp[NK], kj[NK];
+      load_keys<NK>(a.skeys + static_cast<size_t>(p) * NK, kp);
+      load_keys<NK>(a.skeys + static_cast<size_t>(j) * NK, kj);
+      keep = (!kWindow || kj[0] - kp[0] <= th.win) && (lb2_full<NK>(kp, kj) <= th.lb2) && (a.cand_s[c] <= th.band);
     }
-    d64[c] = dd;
+    double dd = -1.0;
+    if constexpr (kWarp) {
+      if (keep) {  // warp-uniform: every lane read the same candidate
+        dd = warp_exact_distance(src, a.sidx[p], a.sidx[j], lane);
+        if (lane == 0) atomicMin(best64, static_cast<unsigned long long>(__double_as_longlong(dd)));
+        ++pass;
+      }
+      if (c < count && lane == 0) d64[c] = dd;
+    } else {
+      if (keep) {
+        dd = exact_distance(src, a.sidx[p], a.sidx[j]);
+        atomicMin(best64, static_cast<unsigned long long>(__double_as_longlong(dd)));
+        ++pass;
+      }
+      if (c < count) d64[c] = dd;
+    }
   }
-  const unsigned wsum = __reduce_add_sync(kFull, pass);
-  if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(examined, static_cast<unsigned long long>(wsum));
-  }
+  if constexpr (!kWarp) pass = __reduce_add_sync(kFull, static_cast<unsigned>(pass));
+  if (lane == 0 && pass) atomicAdd(examined, pass);
 }
 
 __global__ void k_pick(const ScanArgs a, const double* __restrict__ d64, const unsigned long long* __restrict__ best64,
@@ -1484,15 +1503,18 @@ KernelSpan* scan_enqueue(CppPlan& plan, uint32_t lo, uint32_t hi, uint32_t part,
   tm.mark("scan");
   const ExactSrc ex = plan.ps->exact();
   const int nb = c.sm_count * 2;
-  if (plan.grid) {
-    if (plan.dir.nk == 4)
-      k_recheck<4, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
-    else
-      k_recheck<8, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
-  } else if (plan.dir.nk == 4)
-    k_recheck<4, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
-  else
-    k_recheck<8, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined);
+  const bool wide = plan.ps->d >= 32;  // a warp per candidate (k_recheck)
+  const int v = (plan.grid ? 0 : 4) + (plan.dir.nk == 8 ? 2 : 0) + (wide ? 1 : 0);
+  switch (v) {
+    case 0: k_recheck<4, false, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    case 1: k_recheck<4, false, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    case 2: k_recheck<8, false, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    case 3: k_recheck<8, false, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    case 4: k_recheck<4, true, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    case 5: k_recheck<4, true, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    case 6: k_recheck<8, true, false><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+    default: k_recheck<8, true, true><<<nb, 256, 0, s>>>(a, ex, W.d64.p, &st->best64, &st->examined); break;
+  }
   PSG_LAUNCHED();
   k_pick<<<nb, 256, 0, s>>>(a, W.d64.p, &st->best64, &st->lex);
   PSG_LAUNCHED();

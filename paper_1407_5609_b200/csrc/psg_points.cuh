@@ -53,6 +53,25 @@ __device__ __forceinline__ double exact_distance(const ExactSrc& s, uint64_t i, 
   return __dsqrt_rn(acc);
 }
 
+// exact_distance by a whole warp (every lane returns it): the squared
+// differences — for z-normalised windows two FP64 divisions each, the slow
+// part — are formed 32 at a time in parallel, then every lane adds the same
+// terms in the same index order, so the result is bit-identical.
+__device__ __forceinline__ double warp_exact_distance(const ExactSrc& s, uint64_t i, uint64_t j, int lane) {
+  double acc = 0.0;
+  for (int t0 = 0; t0 < s.d; t0 += 32) {
+    const int t = t0 + lane;
+    double term = 0.0;
+    if (t < s.d) {
+      const double diff = __dsub_rn(exact_coord(s, i, t), exact_coord(s, j, t));
+      term = __dmul_rn(diff, diff);
+    }
+    const int m = s.d - t0 < 32 ? s.d - t0 : 32;
+    for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, term, k));
+  }
+  return __dsqrt_rn(acc);
+}
+
 // The FP32 working rows every filter reads.  Row sets: X, n x d row-major.
 // Window sets (windows_of, series.cpp:34-42) are virtual, as the reference's
 // are: row i is computed where it is read from the FP32 series in working
