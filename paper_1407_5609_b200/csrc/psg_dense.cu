@@ -997,19 +997,7 @@ template <int D>
 void launch_gram(const ScanArgs& a, const DenseWork& w, const GridIndex& gi, const uint32_t* pa, const uint32_t* pb,
                  uint32_t npairs, uint32_t part, uint32_t nparts, cudaStream_t s) {
   constexpr size_t kSmem = sizeof(GramSmem<D>) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(k_dense_gram<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
-    if (e != cudaSuccess) {
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, k_dense_gram<D>);
-      throw cuda_error("k_dense_gram: dynamic smem " + std::to_string(kSmem) + " refused (" + cudaGetErrorString(e) +
-                       "); static " + std::to_string(fa.sharedSizeBytes) + ", regs " + std::to_string(fa.numRegs) +
-                       ", max threads " + std::to_string(fa.maxThreadsPerBlock));
-    }
-    configured = true;
-  }
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k_dense_gram<D>), kSmem);
   k_dense_gram<D><<<ctx().sm_count, kGThreads, kSmem, s>>>(a, w.Xs.p, gi.dev.cfirst, pa, pb, w.gstart.p,
                                                            w.gprefix.p, reinterpret_cast<const uint32_t*>(w.ctr.p + 3),
                                                            npairs, part, nparts, w.ctr.p + 1);

@@ -1243,13 +1243,9 @@ bool sorted_csr_groups(const FrnnRun& run, uint64_t n, uint64_t* offs, uint32_t*
   const uint64_t m = run.count;
   const uint32_t ng = static_cast<uint32_t>((n + kGroupRows - 1) >> kGroupShift);
   if (ng > kMaxGroups || m >= 0xffffffffull || m == 0) return false;
-  static const bool configured = [] {
-    PSG_CUDA(cudaFuncSetAttribute(k_group_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxGroups * 4));
-    PSG_CUDA(cudaFuncSetAttribute(k_group_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxGroups * 8));
-    PSG_CUDA(cudaFuncSetAttribute(k_group_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kGroupCap * 4));
-    return true;
-  }();
-  (void)configured;
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k_group_hist), kMaxGroups * 4);
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k_group_scatter), kMaxGroups * 8);
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k_group_sort), kGroupCap * 4);
   DevBuf<unsigned> gcnt(ng + 1, s);
   PSG_CUDA(cudaMemsetAsync(gcnt.p, 0, (ng + 1) * 4, s));
   k_group_hist<<<c.sm_count, kGroupHistThreads, ng * 4, s>>>(run.pairs.p, m, ng, gcnt.p);

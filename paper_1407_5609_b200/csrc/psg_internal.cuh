@@ -77,6 +77,9 @@ __device__ __forceinline__ void block_max_to(unsigned* dst, unsigned v) {
 }
 
 #endif
+// cudaFuncAttributeMaxDynamicSharedMemorySize once per (kernel, device): the
+// attribute is per device, so a process driving several GPUs sets it on each.
+void set_max_dynamic_smem(const void* kernel, size_t bytes);
 bool pdl_enabled();  // PSG_NO_PDL=1: plain launches (A/B)
 template <class... P, class... A>
 void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <set>
 #include <map>
 #include <memory>
 #include <thread>
@@ -38,6 +39,21 @@ void trace(const char* what) {
   std::fprintf(stderr, "[psg] %-24s %9.1f us\n", what,
                std::chrono::duration<double, std::micro>(now - last).count());
   last = now;
+}
+
+void set_max_dynamic_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  PSG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (!done.insert({kernel, dev}).second) return;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e != cudaSuccess) {
+    done.erase({kernel, dev});
+    throw cuda_error(std::string("dynamic shared memory of ") + std::to_string(bytes) + " bytes refused: " +
+                     cudaGetErrorString(e));
+  }
 }
 
 bool pdl_enabled() {

@@ -283,12 +283,7 @@ void launch(const psg_pointset& ps, const Directions& dir, float* keys, unsigned
   for (int k = 0; k < NK; ++k)
     for (int t = 0; t < D; ++t) u.u[k][t] = dir.U[static_cast<size_t>(k) * D + t];
   constexpr size_t kSmem = 1024 + kTcStages * kStageBytes + (D / kTcKChunk) * kBChunkBytes + 512;
-  static bool configured = false;
-  if (!configured) {
-    PSG_CUDA(cudaFuncSetAttribute(k_project_tc<NK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmem)));
-    configured = true;
-  }
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k_project_tc<NK, D>), kSmem);
   unsigned nbits;
   std::memcpy(&nbits, &ps.norm2max, 4);
   const uint32_t ntiles = (n + kTcM - 1) / kTcM;
