@@ -8,6 +8,8 @@ bit-exact; distances must equal the oracle's FP64 value exactly (the engines
 recheck in the reference's FP64 order), which is stricter than north_star's
 1e-5 relative tolerance.
 """
+import ctypes
+
 import numpy as np
 import pytest
 from numpy.lib.stride_tricks import sliding_window_view
@@ -343,6 +345,20 @@ def test_float32_and_float64_entry_points_agree(psg, orc):
     a = psg.closest_pair(psg.PointSet.from_flat(pts, 3), 10, 10.0, 1, 0)
     b = psg.closest_pair(psg.PointSet.from_flat(pts.astype(np.float64), 3), 10, 10.0, 1, 0)
     assert (a.index_i, a.index_j, a.distance) == (b.index_i, b.index_j, b.distance)
+
+
+@pytest.mark.parametrize("length,znorm", [(8192, True), (8192, False), (3, True)])
+def test_window_projection_shapes(psg, orc, length, znorm):
+    """Window sets whose directions do not fit shared memory (len 8192: the
+    projection reads U from global memory) and tiny windows: the motif equals
+    the device brute force over the same virtual rows."""
+    walk = orc.gen_random_walk(12000 if length > 100 else 4000, 21)
+    zone = 64  # admissible pairs among the 3809 windows of length 8192
+    got = psg.motif(walk, length, znorm=znorm, exclusion_zone=zone)
+    out = psg._Pair()
+    psg._check(psg.lib().psg_brute_force_motif_f64(walk.ctypes.data, walk.size, length, int(znorm), zone,
+                                                   ctypes.byref(out)))
+    assert (got.index_i, got.index_j, got.distance) == (out.index_i, out.index_j, out.distance)
 
 
 def test_raw_windows_motif_matches_reference_engine(psg, orc):
