@@ -1118,7 +1118,7 @@ void CppWork::drop_graph() {
 }
 
 CppWork::~CppWork() {
-  if (host_st) cudaFreeHost(host_st);
+  pinned_small_put(host_st);
   if (gexec) cudaGraphExecDestroy(gexec);
   for (cudaEvent_t e : gev)
     if (e) cudaEventDestroy(e);
@@ -1136,7 +1136,8 @@ std::shared_ptr<CppWork> get_work(psg_pointset* ps, int nk, cudaStream_t s) {
     w->keys.alloc(ps->n * nk, s);
     w->st.alloc(1, s);
     w->pre_part.alloc(kPreBlocks * kMaxGridKeys * 4, s);  // not inside a graph capture
-    PSG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->host_st), sizeof(DevState)));
+    static_assert(sizeof(DevState) <= kPinnedSmall, "DevState mirror outgrew the pinned pool's blocks");
+    w->host_st = static_cast<DevState*>(pinned_small_get());
     slot = w;
   }
   return w;
@@ -1220,6 +1221,7 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   const int nk = plan->dir.nk;
   plan->work = get_work(ps, nk, s);
   CppWork& W = *plan->work;
+  trace("plan: workspace");
   const char* eng = std::getenv("PSG_ENGINE");
   plan->grid = plan->dir.q >= 2 && !(eng && std::string(eng) == "window");
   plan->g = plan->grid ? std::min(3, plan->dir.q) : 0;
@@ -1239,6 +1241,7 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
   }
   // the error budget is a property of the point set and the directions: host
   plan->bud = make_budget(*ps, plan->dir, ps->norm2max);
+  trace_sync("plan: buffers + budget", s);
   k_state_init<<<1, 1, 0, s>>>(W.st.p, ps->exact(), plan->grid ? W.gi.sidx.p : W.wsidx.p, plan->bud);
   PSG_LAUNCHED();
   {
@@ -1270,10 +1273,12 @@ CppPlan* cpp_plan_create(psg_pointset* ps, uint64_t q, double f, uint64_t seed, 
       if (counting && !no_fuse) cc = CellCount{W.gi.gp.p, W.gi.cnt.p, W.gi.cid0.p};
     }
     tm.mark("presample");
+    trace_sync("plan: presample", s);
     plan->proj_span = std::make_unique<KernelSpan>(s, "project");
     const bool counted = project_async(*ps, plan->dir, W.keys.p, &W.st.p->norm2_bits, s, cc);
     plan->proj_span->end();
     tm.mark("project");
+    trace_sync("plan: project", s);
     if (plan->grid) {
       // K2 (grid): cells over the first g keys at the occupancy width, sorted;
       // the counting build also leaves the bootstrap's lower bounds (BootLB)

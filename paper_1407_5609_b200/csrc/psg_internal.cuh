@@ -80,6 +80,12 @@ __device__ __forceinline__ void block_max_to(unsigned* dst, unsigned v) {
 // cudaFuncAttributeMaxDynamicSharedMemorySize once per (kernel, device): the
 // attribute is per device, so a process driving several GPUs sets it on each.
 void set_max_dynamic_smem(const void* kernel, size_t bytes);
+// Small page-locked blocks (kPinnedSmall bytes: per-workspace state mirrors)
+// from a process-wide pool of portable slabs: cudaMallocHost / cudaFreeHost
+// cost milliseconds per call, which a one-shot solve would pay every time.
+constexpr size_t kPinnedSmall = 4096;
+void* pinned_small_get();
+void pinned_small_put(void* p);
 bool pdl_enabled();  // PSG_NO_PDL=1: plain launches (A/B)
 template <class... P, class... A>
 void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
@@ -237,6 +243,7 @@ struct StageTimer {
 
 // Host-side trace (PSG_TRACE=1): wall time since the previous mark, stderr.
 void trace(const char* what);
+void trace_sync(const char* what, cudaStream_t s);
 
 // Device time of one kernel (or a short launch sequence) on a stream.  A
 // named span inside a capture is logged in g_cap_spans.

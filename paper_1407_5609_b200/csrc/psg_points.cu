@@ -41,6 +41,38 @@ void trace(const char* what) {
   last = now;
 }
 
+namespace {
+std::mutex g_pinned_mu;
+std::vector<void*> g_pinned_free;
+}  // namespace
+
+void* pinned_small_get() {
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  if (g_pinned_free.empty()) {
+    constexpr size_t kSlab = 64;
+    void* slab = nullptr;
+    PSG_CUDA(cudaHostAlloc(&slab, kSlab * kPinnedSmall, cudaHostAllocPortable));  // never freed: a pool
+    for (size_t k = 0; k < kSlab; ++k) g_pinned_free.push_back(static_cast<char*>(slab) + k * kPinnedSmall);
+  }
+  void* p = g_pinned_free.back();
+  g_pinned_free.pop_back();
+  return p;
+}
+
+void pinned_small_put(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
+// trace() after draining the stream when PSG_TRACE_SYNC is set too (stage
+// timing of normally asynchronous sequences; diagnostics only)
+void trace_sync(const char* what, cudaStream_t s) {
+  static const bool on = std::getenv("PSG_TRACE") != nullptr && std::getenv("PSG_TRACE_SYNC") != nullptr;
+  if (on) cudaStreamSynchronize(s);
+  trace(what);
+}
+
 void set_max_dynamic_smem(const void* kernel, size_t bytes) {
   static std::mutex mu;
   static std::set<std::pair<const void*, int>> done;
@@ -515,8 +547,10 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
   ps->d = static_cast<int>(len);
   ps->kind = znorm ? kWindowsZ : kWindowsRaw;
   ps->device = c.device;
+  trace("windows: enter");
   if (series64) {
     upload(ps->src64, series64, length, dev_src, s, &ps->h2d_bytes);
+    trace_sync("windows: uploaded", s);
   } else {
     DevBuf<float> tmp;
     upload(tmp, series32, length, dev_src, s, &ps->h2d_bytes);
@@ -537,6 +571,7 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
   PSG_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaMemcpyAsync(&hm, mx.p, 8, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaStreamSynchronize(s));
+  trace("windows: checked");
   if (hb) throw invalid_argument("series value must be finite");
   double maxabs;
   std::memcpy(&maxabs, &hm, 8);
@@ -551,6 +586,7 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
     PSG_LAUNCHED();
     ++g_launches;
     maxabs = std::sqrt(static_cast<double>(len));
+    trace_sync("windows: stats", s);
   }
   ps->s32.alloc(length, s);
   k_series_f32<<<grid_for(length, 256 * 4, c.sm_count), 256, 0, s>>>(ps->src64.p, length, ps->scale, ps->s32.p);
@@ -562,6 +598,7 @@ psg_pointset* pointset_windows(const double* series64, const float* series32, ui
   PSG_LAUNCHED();
   g_launches += 2;
   ps->Rn = radius_bound(read_r2(mx.p + 1, s), ps->d) + (znorm ? static_cast<double>(len) * 0x1.0p-50 : 0.0);
+  trace("windows: error check");
   unsigned hn = 0;
   PSG_CUDA(cudaMemcpy(&hn, nb.p, 4, cudaMemcpyDeviceToHost));
   std::memcpy(&ps->norm2max, &hn, 4);
