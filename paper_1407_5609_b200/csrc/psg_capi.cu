@@ -397,8 +397,8 @@ int psg_debug_projection(psg_pointset* ps, uint64_t q, uint64_t seed, int* nk, f
     *nk = dir.nk;
     cudaStream_t s = psg::ctx().stream;
     psg::DevBuf<float> k(ps->n * dir.nk, s);
-    const float norm2 = psg::project(*ps, dir, k.p, s);
-    const psg::Budget b = psg::make_budget(*ps, dir, norm2);
+    psg::project(*ps, dir, k.p, s);
+    const psg::Budget b = psg::make_budget(*ps, dir, ps->norm2max);  // as the solves charge it
     if (keys) PSG_CUDA(cudaMemcpyAsync(keys, k.p, ps->n * dir.nk * sizeof(float), cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
     if (dirs) std::copy(dir.U.begin(), dir.U.end(), dirs);

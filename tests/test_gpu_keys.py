@@ -49,3 +49,45 @@ def test_tensor_core_directions_are_tf32():
     _, dirs, _, _ = psg.debug_projection(psg.PointSet.from_flat(x, 128), q=10, seed=1)
     bits = dirs.view(np.uint32)
     assert np.all(bits & 0x1FFF == 0), "tensor-core directions must be exact TF32 operands"
+
+
+def _window_rows(series, length, znorm):
+    """The FP32 virtual window rows the device filters read (psg_points.cuh
+    Rows): fl(fl(s32[i+t] - m32[i]) * r32[i]) with the FP64 two-pass window
+    statistics (sequential sums, like k_window_stats), or s32[i+t] raw."""
+    s64 = np.asarray(series, dtype=np.float64)
+    nw = s64.size - length + 1
+    w = np.lib.stride_tricks.sliding_window_view(s64, length)
+    s32 = s64.astype(np.float32)
+    ws = np.lib.stride_tricks.sliding_window_view(s32, length)
+    if not znorm:
+        return ws.astype(np.float64)
+    mu = np.zeros(nw)
+    for t in range(length):  # sequential, as the device sums
+        mu = mu + w[:, t]
+    mu = mu / length
+    var = np.zeros(nw)
+    for t in range(length):
+        c = w[:, t] - mu
+        var = var + c * c
+    sg = np.sqrt(var / length)
+    m32 = mu.astype(np.float32)
+    r32 = np.where(sg == 0, 0.0, 1.0 / sg).astype(np.float32)
+    x = ((ws - m32[:, None]).astype(np.float32) * r32[:, None]).astype(np.float32)
+    return x.astype(np.float64)
+
+
+@pytest.mark.parametrize("length", [32, 64, 128, 256, 24])
+@pytest.mark.parametrize("znorm", [True, False])
+def test_window_keys_within_charged_error(length, znorm):
+    """Window sets (k_project_windows forms the virtual rows from the series,
+    4 windows per thread): the keys stay inside E.  A random walk has large
+    window means against small window spreads."""
+    rng = np.random.default_rng(length + znorm)
+    series = np.cumsum(rng.standard_normal(4099 + length - 1)) + 300.0
+    ps = psg.PointSet.windows_of(series, length, znorm=znorm)
+    keys, dirs, E, scale = psg.debug_projection(ps, q=10, seed=7)
+    x = _window_rows(series * (1.0 if znorm else scale), length, znorm)
+    exact = x @ dirs.astype(np.float64).T
+    err = np.abs(keys.astype(np.float64) - exact).max()
+    assert err <= E, f"key error {err:.3e} exceeds the charged bound {E:.3e}"
