@@ -189,6 +189,10 @@ C4_N, C4_R = 1 << 22, float.fromhex("0x1.902ce9269f6dp-7")
 C4_EXPECT = (66173431, 8231864707796938076)  # oracle cell-grid FRNN (tests/test_gpu_fullsize.py)
 
 
+C4_INSTR_PER_CAND = 868812561 / 420761475  # ncu, k_frnn_cells count+hash at C4 (profiles/r02_ncu_frnn_cells.txt)
+C4_SM_HZ = 1965e6  # clocks.max.sm of the pool's B200s (the bench's clocks sampler reports the run's)
+
+
 def candidate_kernel_c4(hbm_gbs, peak_kind, reps=3):
     """North-star check of the candidate-distance kernel where it is the hot
     spot: C4 (FRNN, n=2^22, d=3, ~32 neighbours), count + hash on a resident
@@ -215,6 +219,13 @@ def candidate_kernel_c4(hbm_gbs, peak_kind, reps=3):
             "roofline_candidates_per_s": roof, "frac": rate / roof, "achieved_gbs": rate * 12 / 1e9,
             "peak": hbm_gbs, "peak_source": peak_kind,
             "model": "SURVEY 8(d): 4d B per candidate (streaming); candidates are re-read from L1/L2, so true DRAM traffic is far lower",
+            # the bound the kernel actually meets: SM instruction issue.  Warp-
+            # instructions per candidate from ncu (profiles/r02_ncu_frnn_cells.txt:
+            # 868.8M executed / 420.8M candidates); peak = 148 SMs x 4 issue/clk
+            "issue_model": {"warp_instr_per_candidate": C4_INSTR_PER_CAND,
+                            "achieved_ginst_per_s": rate * C4_INSTR_PER_CAND / 1e9,
+                            "peak_ginst_per_s": 148 * 4 * C4_SM_HZ / 1e9,
+                            "frac": rate * C4_INSTR_PER_CAND / (148 * 4 * C4_SM_HZ)},
             "pairs": r.pair_count, "correct": ok}
 
 
