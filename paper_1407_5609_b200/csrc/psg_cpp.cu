@@ -23,6 +23,7 @@
 #include <memory>
 
 #include "psg_cpp.cuh"
+#include "psg_engines.cuh"
 #include "psg_scan.cuh"
 #include "psg_sort.cuh"
 
@@ -1333,6 +1334,7 @@ void learn_for(CppWork& W, const CppPlan& plan) {
     W.learned_w = 0.0;
     W.learned_dense = false;
     W.learned_full_boot = false;
+    W.learned_brute = false;
   }
   W.learned_q = plan.q_arg;
   W.learned_seed = plan.seed_arg;
@@ -1571,6 +1573,7 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
   PSG_LAUNCHED();
   ++g_launches;
   KernelSpan* scan_span = nullptr;
+  uint64_t last_est = 0;  // the grid's pair estimate (sparse grids)
   for (int attempt = 0;; ++attempt) {
     if (attempt > 16) throw std::runtime_error("closest_pair: the cell grid did not settle after 16 rebuilds");
     ensure_candidates(W, s);
@@ -1585,6 +1588,7 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
         plan.dense = true;
       } else {
         const uint64_t est = grid_pair_estimate(W.gi, plan.gp.cells, s);  // synchronises
+        last_est = est;
         plan.dense = est > kDenseFactor * n;
         if (std::getenv("PSG_TRACE")) {
           const DevState& h0 = *W.host_st;
@@ -1594,6 +1598,24 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
                        plan.gp.dims[2], h0.box_lo[0], h0.box_span[0], h0.box_lo[1], h0.box_span[1], h0.box_lo[2],
                        h0.box_span[2], static_cast<double>(bits_to_float(h0.best)),
                        static_cast<unsigned long long>(est), static_cast<int>(plan.dense), W.learned_w);
+        }
+      }
+      // Pairs the grid cannot separate (est a sizeable share of all pairs:
+      // uniform data in mid dimensions, where every key gap is small next to
+      // the nearest-neighbour distance) go to the all-pairs engine when the
+      // dense engine would run on CUDA cores (d outside the Gram tiles'
+      // 32 / 64): it evaluates ~100x more pairs per second than the CUDA-core
+      // cell-pair tiles (n = 16384, d = 16 uniform: 35 ms -> 0.7 ms).  Same
+      // exact answer (refscan.cpp:134-157 is the definition it implements).
+      if (nparts == 1 && plan.dense && plan.ps->d != 32 && plan.ps->d != 64 &&
+          plan.g <= 3 && !std::getenv("PSG_NO_BRUTE_SWITCH")) {
+        const double all = 0.5 * static_cast<double>(n) * static_cast<double>(n - 1);
+        if (static_cast<double>(last_est) > all / 64.0) {
+          trace("scan: dense on CUDA cores -> all-pairs engine");
+          learn_for(W, plan);
+          W.learned_brute = true;  // later solves of this (q, seed, zone) go there directly (cpp_solve)
+          delete scan_span;
+          return brute_solve(plan.ps, plan.zone);
         }
       }
       if (nparts == 1 && plan.dense) {  // later solves of this (q, seed, zone) skip the graph attempt
@@ -1839,6 +1861,13 @@ psg_pair_result cpp_solve(psg_pointset* ps, uint64_t q, double f, uint64_t seed,
   check_reference_args(ps->n, q, f);
   if (admissible_pairs(ps->n, zone) == 0) throw invalid_argument("no admissible pair");
   psg_pair_result r;
+  {  // a set this (q, seed, zone) already sent to the all-pairs engine (cpp_plan_scan)
+    const Directions dir = make_directions(seed, ps->d, static_cast<int>(std::min<uint64_t>(q, 1u << 20)));
+    const std::shared_ptr<void>& slot = ps->cpp_work[dir.nk == 8 ? 1 : 0];
+    const auto* W = static_cast<const CppWork*>(slot.get());
+    if (W && W->learned_brute && W->learned_q == q && W->learned_seed == seed && W->learned_zone == zone)
+      return finalize(brute_solve(ps, zone), ps->n, zone);
+  }
   if (graphs_enabled() && ps->n < 0xffffffffull && solve_graph(ps, q, f, seed, zone, &r))
     return finalize(r, ps->n, zone);
   std::unique_ptr<CppPlan> plan(cpp_plan_create(ps, q, f, seed, zone));

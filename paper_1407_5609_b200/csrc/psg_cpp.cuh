@@ -87,6 +87,7 @@ struct CppWork {
   uint64_t learned_q = 0, learned_seed = 0, learned_zone = 0;
   bool learned_dense = false;  // the solve went to the dense engine (not graph-capturable: host decisions)
   bool learned_full_boot = false;  // the own-row bootstrap was too weak: run the full-stencil one up front
+  bool learned_brute = false;  // the grid could not separate the pairs: later solves go to the all-pairs engine
   cudaEvent_t gev[32] = {};  // event nodes recorded inside the graph (spans and stages)
   std::vector<CapMark> gspans, gstages;  // which gev pairs time which span / stage
   void drop_graph();
