@@ -292,6 +292,20 @@ def test_frnn_csr_edge_cases(psg, orc):
         psg.frnn_pairs_csr(np.zeros((0, 3), np.float32), 1.0)
 
 
+@pytest.mark.parametrize("d", [16, 100])
+def test_unseparable_sets_take_the_all_pairs_engine(psg, orc, d):
+    """Uniform data in mid/high dimensions: the grid cannot separate the
+    pairs (the estimate is a large share of all pairs) and the dense engine
+    would run on CUDA cores, so the solve goes to the all-pairs engine —
+    learned for later solves.  Same answer as the oracle every time."""
+    x = orc.gen_uniform(9, 6000, d)
+    want = orc.brute_force_closest_pair(x, 0)
+    ps = psg.PointSet.from_flat(x, d)
+    for _ in range(3):  # first solve (grid, then the switch), then the learned path
+        got = psg.closest_pair(ps, 10, 10.0, 1, 0)
+        assert (got.index_i, got.index_j, got.distance) == (want.index_i, want.index_j, want.distance)
+
+
 def test_c5_recipe_small(psg, orc):
     pts = orc.gen_mixture(5, 8192, 64, 1024, 0.05)
     want = orc.brute_force_closest_pair(pts, 0)
