@@ -1600,18 +1600,19 @@ psg_pair_result cpp_plan_scan(CppPlan& plan, uint64_t part, uint64_t nparts, flo
                        static_cast<unsigned long long>(est), static_cast<int>(plan.dense), W.learned_w);
         }
       }
-      // Pairs the grid cannot separate (est a sizeable share of all pairs:
-      // uniform data in mid dimensions, where every key gap is small next to
-      // the nearest-neighbour distance) go to the all-pairs engine when the
-      // dense engine would run on CUDA cores (d outside the Gram tiles'
-      // 32 / 64): it evaluates ~100x more pairs per second than the CUDA-core
-      // cell-pair tiles (n = 16384, d = 16 uniform: 35 ms -> 0.7 ms).  Same
-      // exact answer (refscan.cpp:134-157 is the definition it implements).
-      if (nparts == 1 && plan.dense && plan.ps->d != 32 && plan.ps->d != 64 &&
-          plan.g <= 3 && !std::getenv("PSG_NO_BRUTE_SWITCH")) {
+      // Small sets the grid cannot separate (a pair estimate over 1/64 of all
+      // pairs, under ~4e9 pair-coordinates: ~0.6 ms all-pairs) go to the
+      // all-pairs engine: the dense engine's set-up (pair lists, sorts, host
+      // synchronisations) costs more than that (4096 x 32 Gaussian: 0.95 ->
+      // 0.18 ms).  Larger ones stay on the dense engine, which beats the
+      // all-pairs kernel at every d measured (tools/cmp_switch.py: 2^16 x 100
+      // Gaussian 20 ms against 47 ms).  Same exact answer either way
+      // (refscan.cpp:134-157 is the definition the all-pairs engine implements).
+      if (nparts == 1 && plan.dense && plan.g <= 3 && !std::getenv("PSG_NO_BRUTE_SWITCH")) {
         const double all = 0.5 * static_cast<double>(n) * static_cast<double>(n - 1);
-        if (static_cast<double>(last_est) > all / 64.0) {
-          trace("scan: dense on CUDA cores -> all-pairs engine");
+        const bool small = all * plan.ps->d < 4e9;
+        if (static_cast<double>(last_est) > all / 64.0 && small) {
+          trace("scan: small unseparable set -> all-pairs engine");
           learn_for(W, plan);
           W.learned_brute = true;  // later solves of this (q, seed, zone) go there directly (cpp_solve)
           delete scan_span;

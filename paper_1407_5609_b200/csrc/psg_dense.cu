@@ -112,14 +112,18 @@ __global__ void k_estimate(const uint32_t* __restrict__ cfirst, const GridParams
 
 // Rows in grid order (materialised here also for window sets: the tiles
 // stream them with TMA / wide loads).
-__global__ void k_gather_rows(Rows R, const uint32_t* __restrict__ sidx, uint32_t n, int d, float* __restrict__ Xs) {
+// Rows in cell order, dx >= d floats each: coordinates past d are zero (the
+// Gram tiles' padded width; a zero coordinate adds fmaf(0, 0, s) == s to a
+// canonical distance and nothing to a norm or a dot product).
+__global__ void k_gather_rows(Rows R, const uint32_t* __restrict__ sidx, uint32_t n, int d, int dx,
+                              float* __restrict__ Xs) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t p = warp; p < n; p += nwarps) {
     const uint32_t i = sidx[p];
-    float* dst = Xs + static_cast<size_t>(p) * d;
-    for (int t = lane; t < d; t += 32) dst[t] = row_at(R, i, t);
+    float* dst = Xs + static_cast<size_t>(p) * dx;
+    for (int t = lane; t < dx; t += 32) dst[t] = t < d ? row_at(R, i, t) : 0.f;
   }
 }
 
@@ -1068,6 +1072,8 @@ __global__ void k_pair_tiles(const uint32_t* __restrict__ pa, const uint32_t* __
 }
 
 bool gram_shape(int d) { return d == 32 || d == 64; }
+// The Gram tiles' width for d coordinates (zero-padded), 0 when d is too wide.
+int gram_width(int d) { return d <= 32 ? 32 : d <= 64 ? 64 : 0; }
 }  // namespace
 
 uint64_t grid_pair_estimate(const GridIndex& gi, uint64_t cells, cudaStream_t s) {
@@ -1096,14 +1102,17 @@ __global__ void k_refresh_th(const Budget* bud, const unsigned* best, Thresholds
 uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, const Rows& X, uint32_t n, int d,
                     int nk, Thresholds* th, DenseWork& w, uint32_t part, uint32_t nparts, cudaStream_t s) {
   const int sms = ctx().sm_count;
-  // tensor-core Gram tiles for d in {32, 64}; CUDA-core canonical tiles otherwise
+  // tensor-core Gram tiles for d <= 64 (rows zero-padded to 32 or 64);
+  // CUDA-core canonical tiles otherwise
   static const bool no_gram = std::getenv("PSG_NO_GRAM") != nullptr;
-  const bool gram = gram_shape(d) && !no_gram;
-  if (w.Xs.n != static_cast<size_t>(n) * d) w.Xs.alloc(static_cast<size_t>(n) * d, s);
+  const int dg = gram_width(d);
+  const bool gram = dg > 0 && !no_gram;
+  const int dx = gram ? dg : d;  // Xs row width
+  if (w.Xs.n != static_cast<size_t>(n) * dx) w.Xs.alloc(static_cast<size_t>(n) * dx, s);
   if (w.cbox.n < cells * 2 * nk) w.cbox.alloc(cells * 2 * nk, s);
   if (w.ctr.n < 6) w.ctr.alloc(6, s);
   if (w.clist.n < n) w.clist.alloc(n, s);
-  k_gather_rows<<<sms * 16, 256, 0, s>>>(X, gi.sidx.p, n, d, w.Xs.p);
+  k_gather_rows<<<sms * 16, 256, 0, s>>>(X, gi.sidx.p, n, d, dx, w.Xs.p);
   PSG_LAUNCHED();
   // the non-empty cells: boxes and pairs are per non-empty cell (a dense grid
   // over 8 keys has up to 2^27 cells, almost all empty)
@@ -1137,7 +1146,7 @@ uint64_t dense_scan(const ScanArgs& a, const GridIndex& gi, uint64_t cells, cons
       PSG_LAUNCHED();
       ++g_launches;
     }
-    kept += dense_pass(a, gi, cells, d, nk, th, w, part, nparts, s, gram, lb, ne, pass);
+    kept += dense_pass(a, gi, cells, dx, nk, th, w, part, nparts, s, gram, lb, ne, pass);
   }
   return kept;
 }

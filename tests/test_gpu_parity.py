@@ -294,10 +294,11 @@ def test_frnn_csr_edge_cases(psg, orc):
 
 @pytest.mark.parametrize("d", [16, 100])
 def test_unseparable_sets_take_the_all_pairs_engine(psg, orc, d):
-    """Uniform data in mid/high dimensions: the grid cannot separate the
-    pairs (the estimate is a large share of all pairs) and the dense engine
-    would run on CUDA cores, so the solve goes to the all-pairs engine —
-    learned for later solves.  Same answer as the oracle every time."""
+    """Uniform data in mid/high dimensions at a small n: the grid cannot
+    separate the pairs (the estimate is a large share of all pairs) and the
+    set is small enough for the all-pairs engine to beat the dense engine's
+    set-up, so the solve goes there — learned for later solves.  Same answer
+    as the oracle every time."""
     x = orc.gen_uniform(9, 6000, d)
     want = orc.brute_force_closest_pair(x, 0)
     ps = psg.PointSet.from_flat(x, d)
