@@ -69,7 +69,11 @@ void pinned_small_put(void* p) {
 // timing of normally asynchronous sequences; diagnostics only)
 void trace_sync(const char* what, cudaStream_t s) {
   static const bool on = std::getenv("PSG_TRACE") != nullptr && std::getenv("PSG_TRACE_SYNC") != nullptr;
-  if (on) cudaStreamSynchronize(s);
+  if (on) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusNone) cudaStreamSynchronize(s);  // never inside a graph capture
+  }
   trace(what);
 }
 
