@@ -152,7 +152,12 @@ void h2d_copy(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
   cudaPointerAttributes at{};
   const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
   cudaGetLastError();  // an unregistered pointer may leave a sticky "invalid value" on old drivers
-  if (pinned || bytes <= (size_t(1) << 20)) {  // small copies: the driver's own staging is as fast
+  // small copies: the driver's own staging is as fast.  Mid-size ones too
+  // until this device's pinned chunks exist: allocating them (64 MiB of
+  // page-locked memory) costs ~30 ms once, which a process making one call
+  // (the CLI) would pay for a copy the driver stages in about a millisecond
+  const bool staged = ctx().stage[0] != nullptr;
+  if (pinned || bytes <= (size_t(1) << 20) || (!staged && bytes <= (size_t(64) << 20))) {
     PSG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
