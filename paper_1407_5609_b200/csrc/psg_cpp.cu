@@ -816,6 +816,10 @@ __global__ void __launch_bounds__(256) k_presample(PresampleArgs a, DevState* st
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = a.R.d, nk = a.nk;
   const bool ut_smem = a.ut_smem;
+  // PDL: the tensor-core projection that follows reads nothing this kernel
+  // writes before its epilogue warps' own wait, so it may be scheduled now
+  // (k_project_tc); any other successor waits at its top or is a plain launch
+  pdl_trigger();
   if (ut_smem)
     for (int k = threadIdx.x; k < d * nk; k += blockDim.x) sut[k] = a.Ut[k];
   __syncthreads();

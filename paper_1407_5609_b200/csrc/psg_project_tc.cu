@@ -123,9 +123,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   // PDL: the set-up above (B operand, barriers, TMEM) overlaps the
-  // predecessor's tail; the grid parameters it wrote are read below
-  pdl_wait();
-  pdl_trigger();
+  // predecessor's tail.  When the epilogue counts cells (cc.gp) the predecessor
+  // is k_presample, which started after everything before it had completed and
+  // writes only what the epilogue reads (GridParams, the box, the big-cell
+  // counters): the TMA producer and the MMA warp then start on X at once and
+  // only the epilogue warps wait, so the mainloop fills the TMEM slots and the
+  // shared-memory ring while the sample is still being reduced.
+  const bool early = cc.gp != nullptr;
+  if (!early) {
+    pdl_wait();
+    pdl_trigger();
+  }
   const uint32_t tmem = *tmem_slot;
   const uint32_t ntiles = (n + kTcM - 1) / kTcM;
 
@@ -211,6 +219,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp >= 8) {  // epilogue: warp (8 + e) owns TMEM lanes 32e .. 32e+31
     const uint32_t e = warp - 8;
     uint32_t it = 0;
+    if (early) {
+      pdl_wait();
+      pdl_trigger();
+    }
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const uint32_t acc = it & 1, aphase = (it >> 1) & 1;
       mbar_wait(tfull + acc, aphase);
